@@ -1,0 +1,136 @@
+"""fp64 CPU oracle for the Hierarchy-Scan + Bind MeshPose path (ctypes binding).
+
+TEST INFRASTRUCTURE ONLY — only tests/, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this.
+The product package ``paper_2505_06703_b200`` never imports it.
+
+The arithmetic lives in ``oracle/oracle.c`` (see its header for the PAPER.md
+passages it follows: §1 steps 2-3, Eq. 1, Alg. 1's parent-left update, Bind
+MeshPose).  This module only marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+STATUS = {0: "ok", 2: "empty", 3: "out_of_range", 4: "cycle", 6: "nomem"}
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with -O2 -ffp-contract=off (no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-shared",
+               "-fPIC", "-pthread", "-o", _SO, _SRC]
+        subprocess.run(cmd, check=True)
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.orc_validate.argtypes = [i32p, ctypes.c_int32]
+        L.orc_validate.restype = ctypes.c_int
+        L.orc_kahn_order.argtypes = [i32p, ctypes.c_int32, i32p]
+        L.orc_kahn_order.restype = ctypes.c_int
+        L.orc_compose.argtypes = [ctypes.c_void_p] * 3
+        L.orc_compose.restype = None
+        L.orc_scan.argtypes = [i32p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_double)]
+        L.orc_scan.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _i32(a):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+class OracleError(ValueError):
+    def __init__(self, status: int):
+        super().__init__(f"oracle: {STATUS.get(status, status)}")
+        self.status = STATUS.get(status, status)
+
+
+def validate(parents) -> str:
+    p, pp = _i32(parents)
+    return STATUS[lib().orc_validate(pp, len(p))]
+
+
+def kahn_order(parents) -> np.ndarray:
+    p, pp = _i32(parents)
+    out = np.empty(len(p), np.int32)
+    st = lib().orc_kahn_order(pp, len(p), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def compose(a, b) -> np.ndarray:
+    """fp64 affine compose of two 3x4 matrices (parent on the left)."""
+    a = np.ascontiguousarray(a, np.float64).reshape(12)
+    b = np.ascontiguousarray(b, np.float64).reshape(12)
+    c = np.empty(12, np.float64)
+    lib().orc_compose(a.ctypes.data, b.ctypes.data, c.ctypes.data)
+    return c.reshape(3, 4)
+
+
+def scan(parents, local, inv_bind=None, nthreads: int | None = None):
+    """Oracle Hierarchy-Scan + bind.
+
+    parents: [J] int (-1 = root, any order); local: [n_chars, J, 3, 4] (or [J,3,4])
+    float32; inv_bind: [J, 3, 4] float32 or None (identity).
+    Returns (global, skin) fp64 arrays of local's shape.
+    """
+    p, pp = _i32(parents)
+    J = len(p)
+    local = np.ascontiguousarray(local, dtype=np.float32)
+    squeeze = local.ndim == 3
+    if squeeze:
+        local = local[None]
+    assert local.shape[1:] == (J, 3, 4), local.shape
+    n_chars = local.shape[0]
+    ib = None
+    if inv_bind is not None:
+        ib = np.ascontiguousarray(inv_bind, dtype=np.float32)
+        assert ib.shape == (J, 3, 4)
+    g = np.empty(local.shape, np.float64)
+    s = np.empty(local.shape, np.float64)
+    st = lib().orc_scan(pp, J, local.ctypes.data, None if ib is None else ib.ctypes.data,
+                        n_chars, g.ctypes.data, s.ctypes.data, nthreads or os.cpu_count() or 1,
+                        None)
+    if st:
+        raise OracleError(st)
+    if squeeze:
+        return g[0], s[0]
+    return g, s
+
+
+def scan_discard(parents, local, inv_bind=None, nthreads: int | None = None) -> float:
+    """Timed-baseline mode: same arithmetic, outputs kept in per-thread scratch only.
+    Returns a checksum of the results so the work is observable."""
+    p, pp = _i32(parents)
+    J = len(p)
+    local = np.ascontiguousarray(local, dtype=np.float32)
+    n_chars = local.shape[0]
+    ib = None if inv_bind is None else np.ascontiguousarray(inv_bind, dtype=np.float32)
+    cs = ctypes.c_double(0.0)
+    st = lib().orc_scan(pp, J, local.ctypes.data, None if ib is None else ib.ctypes.data,
+                        n_chars, None, None, nthreads or os.cpu_count() or 1, ctypes.byref(cs))
+    if st:
+        raise OracleError(st)
+    return cs.value
