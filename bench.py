@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""bench.py — Hierarchy-Scan + fused Bind MeshPose throughput on B200.
+
+Metric (BASELINE.json): joints/s of Hierarchy-Scan + skin, with HBM GB/s against
+the measured peak.  Default workload: config 5 — 1,000,000 mixed characters
+(333,334 hum64 + 333,333 chain256 + 333,333 tree1024; 448 M joints, 64.5 GB of
+algorithmic HBM traffic per step) per GPU (weak scaling: rank r owns global
+characters [r*1M, (r+1)*1M) of an N-million crowd; no collective on the path).
+
+A step = one hs_scan per skeleton type over that rank's characters (3 launches),
+inputs resident in HBM (21.5 GB of local poses, larger than the 126 MB L2, so no
+flush is needed).  Launch (N > 1):
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N
+``--impl reference`` times the fp64 CPU oracle (the reference arm of this tier)
+on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import hsgen  # noqa: E402
+
+BYTES_PER_JOINT = 144  # 48 local in + 48 global out + 48 skin out
+METRIC = "joints/sec (Hierarchy-Scan+skin) and HBM GB/s vs peak at 1/2/4/8 B200"
+WORKLOAD_NAME = {1: "C1 1,000 x hum32 (L=8)", 2: "C2 100,000 x hum64 (L=12)",
+                 3: "C3 50,000 x chain256 (L=256)", 4: "C4 20,000 x tree1024 (L=300)",
+                 5: "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU"}
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--cpu-frac", type=int, default=8,
+                    help="cpu_baseline / reference sample = n_chars // this, per skeleton type")
+    ap.add_argument("--e2e-frac", type=int, default=8,
+                    help="e2e host-buffer slice = n_chars // this, per skeleton type")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--algo", default="auto", help="hs_scan_ex algorithm (comparisons)")
+    ap.add_argument("--tile-ctas", type=int, default=0)
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--tile-joints", type=int, default=0)
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no checks, no e2e, no cpu baseline")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------------------ helpers
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def shard(n_total: int, rank: int, world: int, scaling: str):
+    """(global first character, count) of this rank's characters for one skeleton type."""
+    if scaling == "weak":
+        return rank * n_total, n_total
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_ best of 10)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        if d.get("workload") == workload:
+            return float(d["dram_bytes_per_launch"]), d.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
+class ClockSampler:
+    """NVML SM-clock and clock-event-reason samples while running (every 20 ms)."""
+
+    REASONS = [("gpu_idle", 0x1), ("applications_clocks_setting", 0x2), ("sw_power_cap", 0x4),
+               ("hw_slowdown", 0x8), ("sync_boost", 0x10), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("hw_power_brake_slowdown", 0x80),
+               ("display_clock_setting", 0x100)]
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        names = [n for n, bit in self.REASONS if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The tier's reference arm: the fp64 CPU oracle as it stands, on host cores."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    types = hsgen.CONFIGS[args.config]
+    sample = []
+    for name, n, seed, type_, ib_seed in types:
+        par = hsgen.skeleton(name)
+        m = max(1, n // args.cpu_frac)
+        sample.append((name, par, hsgen.local_poses(seed, len(par), m, type_=type_),
+                       hsgen.inv_bind(ib_seed, len(par))))
+    joints = sum(len(p) * loc.shape[0] for _, p, loc, _ in sample)
+    cores = host_cores()
+
+    def step():
+        for _, par, loc, ib in sample:
+            oracle.scan_discard(par, loc, ib, nthreads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = joints * args.steps / dt
+    desc = ", ".join(f"{loc.shape[0]} x {name}" for name, _, loc, _ in sample)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "joints/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME[args.config] + f" (1/{args.cpu_frac} sample)",
+                       "sample": desc, "joints_per_step": joints},
+            "cpu_baseline": {"value": value, "unit": "joints/s", "cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "joints/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    emit(line, args)
+    return 0
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(s + "\n")
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_06703_b200 as hs
+
+    rank, local_rank, world = dist_env()
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    hs.lib()  # fails loudly when libhs.so is missing: no fallback path exists
+    hsgen.lib_cuda()
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+
+    # ---- workload: one skeleton handle and one resident crowd per skeleton type
+    work = []
+    for name, n_total, seed, type_, ib_seed in hsgen.CONFIGS[args.config]:
+        par = hsgen.skeleton(name)
+        J = len(par)
+        ib = hsgen.inv_bind(ib_seed, J)
+        c0, n = shard(n_total, rank, world, args.scaling)
+        sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints)
+        local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
+        if n:
+            rc = hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, c0, n, local.data_ptr(),
+                                                       stream.cuda_stream)
+            assert rc == 0, f"generator launch failed: {rc}"
+        g = torch.empty_like(local)
+        s = torch.empty_like(local)
+        work.append(dict(name=name, par=par, ib=ib, J=J, c0=c0, n=n, seed=seed, type=type_, sk=sk,
+                         local=local, g=g, s=s))
+    torch.cuda.synchronize()
+    joints_rank = sum(w["n"] * w["J"] for w in work)
+
+    def step(events=None, k=0):
+        for t, w in enumerate(work):
+            if events is not None:
+                events[t][0][k].record(stream)
+            w["sk"].scan_into(w["local"], w["g"], w["s"], stream=stream, algo=args.algo,
+                              tile_ctas=args.tile_ctas)
+            if events is not None:
+                events[t][1][k].record(stream)
+
+    # ---- correctness on sampled characters at full size (outside the timed region)
+    step()
+    torch.cuda.synchronize()
+    check = None
+    if not (args.no_check or args.profile):
+        check = sampled_parity(work, rank)
+
+    # ---- warm-up, then exactly K timed steps between barrier + synchronize
+    for _ in range(args.warmup):
+        step()
+    K = args.steps
+    events = [[[torch.cuda.Event(enable_timing=True) for _ in range(K)] for _ in range(2)]
+              for _ in work]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        start.record(stream)
+        for k in range(K):
+            step(events, k)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_rank = start.elapsed_time(stop)
+    per_type_ms = [statistics.mean(events[t][0][k].elapsed_time(events[t][1][k]) for k in range(K))
+                   for t in range(len(work))]
+    ms = ms_rank
+    joints_total = joints_rank
+    if world > 1:
+        tt = torch.tensor([ms_rank, float(joints_rank)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        ms, joints_total = float(mx[0]), int(tt[1])
+    value = joints_total * K / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (largest byte share: tree1024's launch)
+    dom = max(range(len(work)), key=lambda t: work[t]["n"] * work[t]["J"])
+    dom_bytes = BYTES_PER_JOINT * work[dom]["n"] * work[dom]["J"]
+    achieved = dom_bytes / (per_type_ms[dom] / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    workload = WORKLOAD_NAME[args.config]
+    traffic, traffic_src = ncu_traffic(workload)
+
+    e2e = None
+    cpu = None
+    if not (args.no_e2e or args.profile):
+        e2e = run_e2e(work, args, hs, torch, dist, world)
+    if not (args.no_cpu or args.profile) and rank == 0 and world == 1:
+        cpu = run_cpu_baseline(args)
+
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "joints/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload,
+                   "characters_per_gpu": {w["name"]: w["n"] for w in work},
+                   "joints_total": joints_total, "bytes_per_joint": BYTES_PER_JOINT,
+                   "hbm_gbs": joints_total * BYTES_PER_JOINT * K / (ms / 1e3) / 1e9 / world,
+                   "hbm_gbs_note": "per GPU, algorithmic bytes / step time",
+                   "l2": "inputs larger than L2 (no flush)", "algo": args.algo,
+                   "per_launch_ms": {w["name"]: per_type_ms[t] for t, w in enumerate(work)},
+                   "chunk": work[dom]["sk"].query("chunk"),
+                   "tile_chars": work[dom]["sk"].query("tile_chars")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"chunked_kernel ({work[dom]['name']} launch)",
+                     "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
+                     "traffic_source": traffic_src},
+        "clocks": sampler.summary(),
+        "gpu_launches": len(work) * K,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": check,
+    }
+    emit(line, args)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def sampled_parity(work, rank, per_type=24):
+    """Oracle parity on a deterministic sample of characters (inputs regenerated by the
+    HOST generator; the GPU generator's output for the same characters is compared too)."""
+    import oracle
+    oracle.build()
+    out = {}
+    worst = 0.0
+    for w in work:
+        if w["n"] == 0:
+            continue
+        idx = np.unique(np.linspace(0, w["n"] - 1, per_type).astype(np.int64))
+        host_in = np.concatenate([hsgen.local_poses(w["seed"], w["J"], 1, char0=w["c0"] + int(i),
+                                                    type_=w["type"]) for i in idx])
+        dev_in = w["local"][idx].cpu().numpy()
+        gen_mismatch = int(np.count_nonzero(host_in != dev_in))
+        G, S = oracle.scan(w["par"], host_in, w["ib"])
+        g = w["g"][idx].cpu().numpy().astype(np.float64)
+        s = w["s"][idx].cpu().numpy().astype(np.float64)
+        eg, es = float(np.abs(g - G).max()), float(np.abs(s - S).max())
+        worst = max(worst, eg, es)
+        out[w["name"]] = {"chars": len(idx), "max_err_global": eg, "max_err_skin": es,
+                          "gen_elements_differing": gen_mismatch}
+    out["tolerance"] = 1e-4
+    out["pass"] = worst <= 1e-4
+    if not out["pass"]:
+        print(f"PARITY FAILURE: {out}", file=sys.stderr)
+    return out
+
+
+def run_e2e(work, args, hs, torch, dist, world):
+    """Same metric through the public host-buffer API (hs_scan_host): every step copies
+    that step's local poses H2D from pinned memory and reads global + skin back D2H."""
+    pl = hs.Pipeline(batch_bytes=256 << 20)
+    slices = []
+    h2d = d2h = 0
+    joints = 0
+    for w in work:
+        m = max(1, w["n"] // args.e2e_frac) if w["n"] else 0
+        if m == 0:
+            continue
+        hl = torch.empty((m, w["J"], 3, 4), dtype=torch.float32, pin_memory=True)
+        hl.copy_(w["local"][:m])
+        hg = torch.empty_like(hl, pin_memory=True)
+        hsk = torch.empty_like(hl, pin_memory=True)
+        slices.append((w, hl, hg, hsk))
+        h2d += hl.numel() * 4
+        d2h += 2 * hl.numel() * 4
+        joints += m * w["J"]
+
+    def step():
+        for w, hl, hg, hsk in slices:
+            pl.scan_host(w["sk"], hl, hg, hsk)
+
+    step()  # warm-up
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t)
+        joints *= world
+    # spot-check the e2e output against the device-path result
+    w, hl, hg, hsk = slices[-1]
+    same = bool(torch.equal(hg[:4].cuda(), w["g"][:4]))
+    pl.close()
+    return {"value": joints * args.e2e_steps / dt, "unit": "joints/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "sample": f"1/{args.e2e_frac} of each type's characters per GPU, pinned host buffers, "
+                      f"hs_scan_host (256 MiB batches, 3 streams)",
+            "matches_device_path": same}
+
+
+def run_cpu_baseline(args):
+    import oracle
+    oracle.build()
+    cores = host_cores()
+    sample = []
+    for name, n, seed, type_, ib_seed in hsgen.CONFIGS[args.config]:
+        par = hsgen.skeleton(name)
+        m = max(1, n // args.cpu_frac)
+        sample.append((name, par, hsgen.local_poses(seed, len(par), m, type_=type_),
+                       hsgen.inv_bind(ib_seed, len(par))))
+    joints = sum(len(p) * loc.shape[0] for _, p, loc, _ in sample)
+    best = float("inf")
+    for _ in range(2):
+        t0 = time.perf_counter()
+        for _, par, loc, ib in sample:
+            oracle.scan_discard(par, loc, ib, nthreads=cores)
+        best = min(best, time.perf_counter() - t0)
+    desc = ", ".join(f"{loc.shape[0]} x {name}" for name, _, loc, _ in sample)
+    return {"value": joints / best, "unit": "joints/s", "cores": cores, "kind": "oracle",
+            "sample": f"{desc} (1/{args.cpu_frac} of the workload, best of 2, fp64)"}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.profile:
+        args.no_e2e = args.no_cpu = args.no_check = True
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,200 @@
+/*
+ * hs.h — C ABI of the B200-native Hierarchy-Scan + Bind MeshPose library
+ * (libhs.so, built from paper_2505_06703_b200/csrc/).
+ *
+ * The operation (PAPER.md = arxiv 2505.06703, "A GPU-based solution for
+ * large-scale skeletal animation simulation"):
+ *   - Hierarchy-Scan, §1 step 2 and Eq. 1 (PAPER.md:101-105,
+ *     §3.1): for every character c and joint j, the model-space ("global") pose
+ *          G[c][j] = L[c][j]                    if Parent(j) == -1
+ *          G[c][j] = G[c][Parent(j)] (x) L[c][j] otherwise,
+ *     i.e. the product of the local matrices on j's root path, parent on the
+ *     LEFT as in Algs. 1-4's update M[joint] = M[parent] * M[joint]
+ *     (reading R1).
+ *   - Bind MeshPose, §1 step 3: S[c][j] = G[c][j] (x) IB[j],
+ *     IB = the skeleton's inverse bind pose (reading R4), fused as the
+ *     scan's epilogue.
+ *   - (x) = composition of 3x4 affine transforms [R|t] with an implicit bottom
+ *     row (0,0,0,1): [Ra|ta](x)[Rb|tb] = [Ra Rb | Ra tb + ta] (reading R2).
+ *
+ * Data layout (all pose arrays): float32 [n_chars][n_joints][3][4], row-major,
+ * element (r,c) of joint j of character ch at ((ch*n_joints + j)*12 + 4r + c);
+ * column 3 is the translation.  Joint indices are the USER's labels, in any
+ * order (parents may have larger indices than children); outputs are in the
+ * same user order.  Forests (several roots) are allowed.
+ *
+ * Errors: every function returns hs_status (HS_OK = 0) and never throws or
+ * aborts across the ABI; hs_last_error() returns a thread-local detail string.
+ * CUDA launch errors are reported via cudaGetLastError (no device sync).
+ * NaN/Inf inputs are not validated; they propagate.
+ */
+#ifndef HS_H_
+#define HS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HS_OK = 0,
+    HS_ERR_INVALID_ARG = 1,   /* null pointer, n < 0, misaligned (16 B), size overflow, aliasing */
+    HS_ERR_EMPTY = 2,         /* n_joints == 0                                  (SPEC Empty)      */
+    HS_ERR_OUT_OF_RANGE = 3,  /* parent < -1 or parent >= n_joints              (SPEC OutOfRange) */
+    HS_ERR_CYCLE = 4,         /* a parent chain loops, self-parent included     (SPEC CycleDetected) */
+    HS_ERR_CUDA = 5,          /* CUDA runtime error (detail in hs_last_error)   */
+    HS_ERR_OOM = 6,           /* host or device allocation failed               */
+    HS_ERR_WRONG_DEVICE = 7,  /* handle used on a device other than its own     */
+    HS_ERR_UNSUPPORTED = 8    /* n_joints above HS_MAX_JOINTS, or an option this build lacks */
+} hs_status;
+
+#define HS_MAX_JOINTS (1 << 20)
+
+typedef struct hs_skeleton hs_skeleton;   /* opaque; immutable after create */
+
+/* Build a skeleton handle on the CURRENT CUDA device.
+ *   parents  : host, [n_joints], parents[j] = parent label or -1 (root); any order.
+ *   inv_bind : host, [n_joints][3][4] fp32, or NULL (identity).  Copied.
+ *   out      : receives the handle (unchanged on error).
+ * Runs the host topology preprocessor once (validation, levels, internal
+ * topological order, pointer-jumping schedule, chunk/anchor program;
+ * PAPER.md:126-130 Eq. 2, :146-175 blocks / MaxParentOutBlock, :154 in-order
+ * list) and uploads its tables.  Errors: HS_ERR_EMPTY, HS_ERR_OUT_OF_RANGE,
+ * HS_ERR_CYCLE, HS_ERR_INVALID_ARG (null parents/out, n_joints < 0),
+ * HS_ERR_UNSUPPORTED (n_joints > HS_MAX_JOINTS), HS_ERR_OOM, HS_ERR_CUDA. */
+hs_status hs_skeleton_create(const int32_t* parents, int32_t n_joints, const float* inv_bind,
+                             hs_skeleton** out);
+
+/* Creation options (hs_skeleton_create uses all-zero = automatic). */
+typedef struct {
+    int32_t chunk;        /* K, joints per thread chunk: odd in 3..15; 0 = auto (7)            */
+    int32_t tile_joints;  /* target joints per CTA tile (chars per tile = max(1, this / n));
+                             0 = auto (1024)                                                  */
+    int32_t force_split;  /* 1 = use the multi-CTA program even when one CTA would fit          */
+    int32_t stages;       /* TMA load stages of the chunked kernel (2 or 3); 0 = auto           */
+    int32_t sbufs;        /* skin staging buffers (1 or 2); 0 = auto                            */
+    int32_t reserved[3];  /* must be zero                                                      */
+} hs_create_opts;
+
+/* hs_skeleton_create with explicit options (opts == NULL: automatic).
+ * Extra errors: HS_ERR_INVALID_ARG for an invalid option value. */
+hs_status hs_skeleton_create_ex(const int32_t* parents, int32_t n_joints, const float* inv_bind,
+                                const hs_create_opts* opts, hs_skeleton** out);
+
+/* Hierarchy-Scan + fused Bind MeshPose for n_chars characters sharing `sk`.
+ *   local      : device, [n_chars][n_joints][3][4] fp32, 16-byte aligned, read-only.
+ *   n_chars    : >= 0; 0 is a no-op.
+ *   global_out : device, same shape; receives G.  Must not alias local or skin_out.
+ *   skin_out   : device, same shape; receives S = G (x) IB.  Must not alias.
+ *                NULL skips the Bind MeshPose epilogue (global pose only).
+ *   cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * Asynchronous and stream-ordered: no device synchronisation and no host<->
+ * device copies.  Skeletons beyond one CTA's shared memory (the multi-CTA
+ * path) take a stream-ordered workspace with cudaMallocAsync.  Buffers must
+ * stay valid until the stream work completes.  Errors: HS_ERR_INVALID_ARG,
+ * HS_ERR_WRONG_DEVICE, HS_ERR_CUDA, HS_ERR_OOM. */
+hs_status hs_scan(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,
+                  float* skin_out, void* cuda_stream);
+
+/* Algorithms selectable through hs_scan_ex (tests / comparisons). */
+typedef enum {
+    HS_ALGO_AUTO = 0,       /* = CHUNKED when the skeleton fits one CTA, else SPLIT */
+    HS_ALGO_CHUNKED = 1,    /* persistent TMA tile kernel: per-thread serial chunks + pointer
+                               jumping over chunk anchors                       */
+    HS_ALGO_DOUBLING = 2,   /* Alg. 2: radix-2 pointer jumping, one thread per
+                               joint, ceil(log2 L) rounds; honours max_rounds                    */
+    HS_ALGO_SPLIT = 3,      /* multi-CTA path (PAPER.md:145-175 generalised): phase-1 kernel,
+                               recursive anchor scan, phase-3 kernel.  Available when the
+                               skeleton does not fit one CTA or was created with force_split  */
+    HS_ALGO_GATEAU = 4,     /* Alg. 1: thread per joint walks every ancestor   */
+    HS_ALGO_LEAF = 5        /* KIYA leaf walk: thread per leaf fills its root path */
+} hs_algo;
+
+typedef struct {
+    int32_t algo;        /* hs_algo                                                          */
+    int32_t max_rounds;  /* DOUBLING only: stop after this many rounds (< 0 = all); the
+                            round-induction test                          */
+    int32_t tile_ctas;   /* CHUNKED: CTAs per SM for the persistent grid (0 = occupancy max)  */
+    int32_t reserved[5]; /* must be zero                                                     */
+} hs_scan_opts;
+
+/* hs_scan with explicit options; opts == NULL behaves as hs_scan. */
+hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,
+                     float* skin_out, void* cuda_stream, const hs_scan_opts* opts);
+
+/* Destroy a handle (NULL-safe).  The caller guarantees no hs_scan using it is
+ * still in flight.  Frees its device tables with cudaFree (device-synchronising). */
+hs_status hs_destroy(hs_skeleton* sk);
+
+/* Queries (integer results). */
+typedef enum {
+    HS_Q_N_JOINTS = 0,
+    HS_Q_MAX_LEVEL = 1,      /* L: node count of the longest root path (root level = 1)      */
+    HS_Q_ROUNDS = 2,         /* R = ceil(log2 L): Alg. 2 rounds                               */
+    HS_Q_PATH = 3,           /* algo HS_ALGO_AUTO resolves to (HS_ALGO_CHUNKED or _SPLIT)      */
+    HS_Q_CHUNK = 4,          /* K: joints per thread chunk                                     */
+    HS_Q_TILE_CHARS = 5,     /* characters per CTA tile (chunked path)                         */
+    HS_Q_ANCHORS = 6,        /* anchor slots per tile (chunked) / per character (split)        */
+    HS_Q_ANCHOR_ROUNDS = 7,  /* pointer-jumping rounds over anchors                            */
+    HS_Q_IDENTITY_ORDER = 8, /* 1 if the user order is already topological (no gather)         */
+    HS_Q_SMEM_BYTES = 9,     /* dynamic shared memory per CTA of the chunked kernel            */
+    HS_Q_THREADS = 10,       /* threads per CTA of the chunked kernel (incl. producer warp)    */
+    HS_Q_STAGES = 11,        /* TMA load stages                                                */
+    HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
+    HS_Q_SPLIT_LEVELS = 13   /* recursion depth of the multi-CTA path (0 if single-CTA)         */
+} hs_query;
+
+hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);
+
+const char* hs_status_string(hs_status s);
+const char* hs_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Host-only topology plan (no CUDA calls): the preprocessor hs_skeleton_create
+ * runs, exposed for tests and tools.  Exports are in USER labels unless noted.
+ * ------------------------------------------------------------------------- */
+typedef struct hs_plan hs_plan;
+
+/* parents as in hs_skeleton_create; chunk = K (odd, 3..15; 0 = auto);
+ * block_size = the paper's block size for the MaxParentOutBlock export (0 = 64). */
+hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk,
+                         int32_t block_size, hs_plan** out);
+hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* value);
+
+typedef enum {
+    HS_X_LEVELS = 0,       /* int32 [n]   level of each joint (root = 1)                         */
+    HS_X_ORDER = 1,        /* int32 [n]   internal position -> user label (topological order)     */
+    HS_X_LIFT = 2,         /* int32 [R][n] anc[r][u] = 2^r-th ancestor of u (user labels), -1     */
+    HS_X_BLOCK_OF = 3,     /* int32 [n]   block of each INTERNAL position (position / block_size) */
+    HS_X_MPOB = 4,         /* int32 [n]   MaxParentOutBlock of each INTERNAL position, internal
+                                          position of the nearest ancestor in another block, -1   */
+    HS_X_CHUNK_SRC = 5,    /* int32 [n]   per INTERNAL position: -1 root, -2 previous joint of the
+                                          same chunk, >= 0 anchor = internal position of parent   */
+    HS_X_ANCHOR_LINK = 6   /* int32 [A]   per anchor slot (ascending internal position): link to
+                                          the anchor slot of its segment head's parent, or -1     */
+} hs_plan_export_what;
+
+/* Copy an export into buf (buf_bytes must be >= the export's size). */
+hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_bytes);
+hs_status hs_plan_destroy(hs_plan* p);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer entry point (end-to-end): H2D of local, scan, D2H of global and
+ * skin, pipelined over character batches on the pipeline's own streams.
+ * Synchronous: returns when h_global / h_skin hold the results.  Host buffers
+ * should be page-locked (cudaHostAlloc / torch pin_memory) for full PCIe rate.
+ * ------------------------------------------------------------------------- */
+typedef struct hs_pipeline hs_pipeline;
+
+/* batch_bytes: device staging per buffer set (0 = 256 MiB); created on the
+ * current device with 3 buffer sets and 3 streams. */
+hs_status hs_pipeline_create(int64_t batch_bytes, hs_pipeline** out);
+hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_local,
+                       int64_t n_chars, float* h_global, float* h_skin);
+hs_status hs_pipeline_destroy(hs_pipeline* pl);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_H_ */

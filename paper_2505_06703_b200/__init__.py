@@ -1,0 +1,257 @@
+"""B200-native Hierarchy-Scan + fused Bind MeshPose (arxiv 2505.06703).
+
+Thin ctypes binding over ``libhs.so`` (C ABI in ``include/hs.h``).  Argument
+marshalling only: every step of the path runs in the library's sm_100a kernels.
+PyTorch supplies device memory and streams.  There is NO CPU fallback: if the
+compiled library is missing, importing the bindings raises.
+
+    sk = Skeleton(parents, inv_bind)            # host preprocessor + upload, once
+    g, s = sk.scan(local)                       # local: cuda float32 [N, J, 3, 4]
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "libhs.so")
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu")]
+_DEPS = _SOURCES + [os.path.join(_HERE, "csrc", f) for f in ("plan.hpp", "kernels.cuh")] + [
+    os.path.join(_ROOT, "include", "hs.h")]
+
+NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+# hs_status
+HS_OK, HS_ERR_INVALID_ARG, HS_ERR_EMPTY, HS_ERR_OUT_OF_RANGE, HS_ERR_CYCLE, HS_ERR_CUDA, \
+    HS_ERR_OOM, HS_ERR_WRONG_DEVICE, HS_ERR_UNSUPPORTED = range(9)
+# hs_algo
+ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf": 5}
+# hs_query
+QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "tile_chars": 5,
+         "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
+         "stages": 11, "device": 12, "split_levels": 13}
+# hs_plan_export_what
+EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
+          "anchor_link": 6}
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libhs.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    stale = force or not os.path.exists(LIB_PATH) or any(
+        os.path.getmtime(LIB_PATH) < os.path.getmtime(d) for d in _DEPS)
+    if stale:
+        cmd = ["nvcc", *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *_SOURCES, "-o",
+               LIB_PATH]
+        subprocess.run(cmd, check=True, cwd=_HERE)
+    return LIB_PATH
+
+
+class HSError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.hs_last_error().decode() if _lib is not None else ""
+        name = _lib.hs_status_string(status).decode() if _lib is not None else str(status)
+        super().__init__(f"{where}: {name}: {detail}")
+
+
+class _CreateOpts(ctypes.Structure):
+    _fields_ = [("chunk", ctypes.c_int32), ("tile_joints", ctypes.c_int32),
+                ("force_split", ctypes.c_int32), ("stages", ctypes.c_int32),
+                ("sbufs", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+
+
+class _ScanOpts(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int32), ("max_rounds", ctypes.c_int32),
+                ("tile_ctas", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhs.so.  Raises if it has not been built — no fallback exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.hs_skeleton_create.argtypes = [vp, i32, vp, ctypes.POINTER(vp)]
+    L.hs_skeleton_create_ex.argtypes = [vp, i32, vp, ctypes.POINTER(_CreateOpts), ctypes.POINTER(vp)]
+    L.hs_scan.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.hs_scan_ex.argtypes = [vp, vp, i64, vp, vp, vp, ctypes.POINTER(_ScanOpts)]
+    L.hs_destroy.argtypes = [vp]
+    L.hs_skeleton_query.argtypes = [vp, i32, ctypes.POINTER(i64)]
+    L.hs_status_string.argtypes = [ctypes.c_int]
+    L.hs_status_string.restype = ctypes.c_char_p
+    L.hs_last_error.argtypes = []
+    L.hs_last_error.restype = ctypes.c_char_p
+    L.hs_plan_create.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
+    L.hs_plan_query.argtypes = [vp, i32, ctypes.POINTER(i64)]
+    L.hs_plan_export.argtypes = [vp, i32, vp, i64]
+    L.hs_plan_destroy.argtypes = [vp]
+    L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
+    L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.hs_pipeline_destroy.argtypes = [vp]
+    for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
+              "hs_skeleton_query", "hs_plan_create", "hs_plan_query", "hs_plan_export",
+              "hs_plan_destroy", "hs_pipeline_create", "hs_scan_host", "hs_pipeline_destroy"):
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int, where: str):
+    if status != HS_OK:
+        raise HSError(status, where)
+
+
+class Plan:
+    """Host-only view of the topology preprocessor (no CUDA)."""
+
+    def __init__(self, parents, chunk: int = 0, block_size: int = 0):
+        L = lib()
+        p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
+        self.n = len(p)
+        h = ctypes.c_void_p()
+        _check(L.hs_plan_create(p.ctypes.data if self.n else None, self.n, chunk, block_size,
+                                ctypes.byref(h)), "hs_plan_create")
+        self._h = h
+
+    def query(self, what: str) -> int:
+        v = ctypes.c_int64()
+        _check(lib().hs_plan_query(self._h, QUERY[what], ctypes.byref(v)), "hs_plan_query")
+        return v.value
+
+    def export(self, what: str) -> np.ndarray:
+        if what == "lift":
+            size = self.query("rounds") * self.n
+        elif what == "anchor_link":
+            size = self.query("anchors")
+        else:
+            size = self.n
+        out = np.empty(max(size, 1), np.int32)
+        _check(lib().hs_plan_export(self._h, EXPORT[what], out.ctypes.data, out.nbytes),
+               "hs_plan_export")
+        out = out[:size]
+        return out.reshape(-1, self.n) if what == "lift" else out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hs_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class Skeleton:
+    """A skeleton handle on the current CUDA device (hs_skeleton_create_ex)."""
+
+    def __init__(self, parents, inv_bind=None, *, chunk: int = 0, tile_joints: int = 0,
+                 force_split: bool = False, stages: int = 0, sbufs: int = 0):
+        L = lib()
+        p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
+        self.n_joints = len(p)
+        ib = None
+        if inv_bind is not None:
+            ib = np.ascontiguousarray(np.asarray(inv_bind, dtype=np.float32))
+            if ib.shape != (self.n_joints, 3, 4):
+                raise ValueError(f"inv_bind must be [{self.n_joints}, 3, 4]")
+        o = _CreateOpts(chunk, tile_joints, int(force_split), stages, sbufs)
+        h = ctypes.c_void_p()
+        _check(L.hs_skeleton_create_ex(p.ctypes.data if self.n_joints else None, self.n_joints,
+                                       None if ib is None else ib.ctypes.data, ctypes.byref(o),
+                                       ctypes.byref(h)), "hs_skeleton_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def query(self, what: str) -> int:
+        v = ctypes.c_int64()
+        _check(lib().hs_skeleton_query(self._h, QUERY[what], ctypes.byref(v)), "hs_skeleton_query")
+        return v.value
+
+    def scan_into(self, local, global_out, skin_out=None, *, n_chars: int | None = None,
+                  stream=None, algo: str = "auto", max_rounds: int = -1, tile_ctas: int = 0):
+        """hs_scan_ex on caller-owned CUDA tensors (or raw device pointers as ints)."""
+        import torch
+
+        def ptr(t):
+            return None if t is None else (t if isinstance(t, int) else t.data_ptr())
+
+        if n_chars is None:
+            n_chars = local.shape[0]
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        elif not isinstance(stream, int):
+            stream = stream.cuda_stream
+        opts = _ScanOpts(ALGO[algo], max_rounds, tile_ctas)
+        _check(lib().hs_scan_ex(self._h, ptr(local), n_chars, ptr(global_out), ptr(skin_out),
+                                stream, ctypes.byref(opts)), "hs_scan")
+
+    def scan(self, local, *, skin: bool = True, algo: str = "auto", max_rounds: int = -1,
+             tile_ctas: int = 0):
+        """local: CUDA float32 [N, J, 3, 4] -> (global, skin) (skin None if skin=False)."""
+        import torch
+        if local.dtype != torch.float32 or not local.is_cuda:
+            raise TypeError("local must be a CUDA float32 tensor")
+        local = local.contiguous()
+        squeeze = local.dim() == 3
+        if squeeze:
+            local = local.unsqueeze(0)
+        if tuple(local.shape[1:]) != (self.n_joints, 3, 4):
+            raise ValueError(f"local must be [N, {self.n_joints}, 3, 4]")
+        g = torch.empty_like(local)
+        s = torch.empty_like(local) if skin else None
+        self.scan_into(local, g, s, algo=algo, max_rounds=max_rounds, tile_ctas=tile_ctas)
+        if squeeze:
+            return g[0], (s[0] if s is not None else None)
+        return g, s
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hs_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class Pipeline:
+    """Host-buffer entry point (hs_scan_host): H2D, scan, D2H pipelined over batches."""
+
+    def __init__(self, batch_bytes: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().hs_pipeline_create(batch_bytes, ctypes.byref(h)), "hs_pipeline_create")
+        self._h = h
+
+    def scan_host(self, sk: Skeleton, h_local, h_global, h_skin, n_chars: int | None = None):
+        """Host tensors/arrays (pinned for full PCIe rate) -> fills h_global, h_skin."""
+        def ptr(t):
+            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+
+        if n_chars is None:
+            n_chars = h_local.shape[0]
+        _check(lib().hs_scan_host(self._h, sk.handle, ptr(h_local), n_chars, ptr(h_global),
+                                  ptr(h_skin)), "hs_scan_host")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hs_pipeline_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def exported_symbols() -> list[str]:
+    """Function names declared in include/hs.h (for the ABI export test)."""
+    import re
+    src = open(os.path.join(_ROOT, "include", "hs.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:hs_status|const char\*)\s+(hs_\w+)\s*\(", src, re.M)))

@@ -1,0 +1,526 @@
+// api.cpp — the C ABI (include/hs.h): skeleton handles, scan dispatch, the
+// host-only plan introspection, and the host-buffer pipeline.  DESIGN.md §2.
+#include "../../include/hs.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+hs_status fail(hs_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+hs_status cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? HS_ERR_OOM : HS_ERR_CUDA;
+}
+
+template <typename T>
+cudaError_t upload(T** dptr, const T* host, size_t count) {
+    *dptr = nullptr;
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dptr), count * sizeof(T));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dptr, host, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+bool is_valid_k(int k) { return k >= 3 && k <= 15 && (k & 1); }
+
+}  // namespace
+
+struct hs_plan {
+    hs::Plan plan;
+    int K = 7;
+    int block_size = 64;
+    hs::ChunkDecomp decomp;
+};
+
+struct hs_skeleton {
+    int device = 0;
+    hs::Plan plan;
+    int K = 7;
+    bool chunked = false;          // single-CTA chunked path fits
+    hs::TileProgram tp;
+    int stages = 0, sbufs = 0, threads = 0;
+    int64_t smem = 0;
+    hs::SplitProgram sp;
+    hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
+    int split_levels = 0;
+    // device tables
+    float* d_ib = nullptr;
+    int32_t* d_parents = nullptr;
+    int32_t* d_lift = nullptr;
+    uint64_t* d_meta = nullptr;
+    int32_t* d_p1len = nullptr;
+    int32_t* d_round_off = nullptr;
+    uint64_t* d_rounds = nullptr;
+    int32_t* d_split_meta = nullptr;
+    int32_t* d_path_off = nullptr;
+    int32_t* d_path = nullptr;
+    int32_t n_leaves = 0;
+};
+
+struct hs_pipeline {
+    int device = 0;
+    int64_t batch_bytes = 0;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+    float* d_in[3] = {nullptr, nullptr, nullptr};
+    float* d_g[3] = {nullptr, nullptr, nullptr};
+    float* d_s[3] = {nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+void free_skeleton(hs_skeleton* sk) {
+    if (!sk) return;
+    free_skeleton(sk->sub);
+    cudaFree(sk->d_ib);
+    cudaFree(sk->d_parents);
+    cudaFree(sk->d_lift);
+    cudaFree(sk->d_meta);
+    cudaFree(sk->d_p1len);
+    cudaFree(sk->d_round_off);
+    cudaFree(sk->d_rounds);
+    cudaFree(sk->d_split_meta);
+    cudaFree(sk->d_path_off);
+    cudaFree(sk->d_path);
+    delete sk;
+}
+
+hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
+                      const hs_create_opts& o, hs_skeleton** out, int depth) {
+    if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
+    if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
+        (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
+        o.reserved[0] || o.reserved[1] || o.reserved[2])
+        return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
+    if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
+    hs_skeleton* sk = new (std::nothrow) hs_skeleton();
+    if (!sk) return fail(HS_ERR_OOM, "host allocation failed");
+    std::string err;
+    int st = hs::build_plan(parents, n, sk->plan, err);
+    if (st != 0) { delete sk; return fail((hs_status)st, err); }
+    cudaError_t e = cudaGetDevice(&sk->device);
+    if (e != cudaSuccess) { delete sk; return cuda_fail(e, "cudaGetDevice"); }
+    int smem_optin = 0;
+    e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, sk->device);
+    if (e != cudaSuccess) { delete sk; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+
+    const hs::Plan& P = sk->plan;
+    sk->K = o.chunk ? o.chunk : 7;
+    // --- chunked (single-CTA) program: C characters per tile, ~tile_target joints
+    const int tile_target = o.tile_joints ? o.tile_joints : 1024;
+    int C = std::max(1, tile_target / std::max(1, n));
+    const int max_threads = 224;  // compute threads per CTA (launch bounds 256 incl. producer)
+    while (C > 1 && ((int64_t)C * n + sk->K - 1) / sk->K > max_threads) --C;
+    if (!(o.force_split && depth == 0) && ((int64_t)C * n + sk->K - 1) / sk->K <= max_threads &&
+        (int64_t)C * n <= 65535) {
+        sk->tp = hs::build_tile_program(P, sk->K, C);
+        const int want_stages = o.stages, want_sbufs = o.sbufs;
+        const int cand[][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
+        for (auto& c : cand) {
+            if (want_stages && c[0] != want_stages) continue;
+            if (want_sbufs && c[1] != want_sbufs) continue;
+            int64_t b = hs::tile_smem_bytes(sk->tp, c[0], c[1]);
+            if (b <= smem_optin && 2 * sk->tp.nslots < 32768) {
+                sk->stages = c[0];
+                sk->sbufs = c[1];
+                sk->smem = b;
+                sk->chunked = true;
+                break;
+            }
+        }
+    }
+
+    // --- device tables shared by all paths
+    std::vector<float> ib((size_t)n * 12);
+    if (inv_bind) std::memcpy(ib.data(), inv_bind, ib.size() * sizeof(float));
+    else
+        for (int32_t j = 0; j < n; ++j)
+            for (int k = 0; k < 12; ++k) ib[(size_t)j * 12 + k] = (k == 0 || k == 5 || k == 10) ? 1.f : 0.f;
+    if ((e = upload(&sk->d_ib, ib.data(), ib.size())) != cudaSuccess ||
+        (e = upload(&sk->d_parents, P.parents.data(), P.parents.size())) != cudaSuccess ||
+        (e = upload(&sk->d_lift, P.lift.data(), P.lift.size())) != cudaSuccess) {
+        free_skeleton(sk);
+        return cuda_fail(e, "upload skeleton tables");
+    }
+    // root -> leaf paths for the KIYA leaf kernel (comparison algorithm)
+    {
+        std::vector<int32_t> off{0}, path;
+        size_t total = 0;
+        for (int32_t leaf : P.leaves) total += P.level[leaf];
+        if (total <= (size_t)64 << 20) {
+            std::vector<int32_t> tmp;
+            for (int32_t leaf : P.leaves) {
+                tmp.clear();
+                for (int32_t v = leaf; v >= 0; v = P.parents[v]) tmp.push_back(v);
+                path.insert(path.end(), tmp.rbegin(), tmp.rend());
+                off.push_back((int32_t)path.size());
+            }
+            sk->n_leaves = (int32_t)P.leaves.size();
+            if ((e = upload(&sk->d_path_off, off.data(), off.size())) != cudaSuccess ||
+                (e = upload(&sk->d_path, path.data(), path.size())) != cudaSuccess) {
+                free_skeleton(sk);
+                return cuda_fail(e, "upload leaf paths");
+            }
+        }
+    }
+    if (sk->chunked) {
+        const hs::TileProgram& tp = sk->tp;
+        sk->threads = ((tp.T + 31) / 32) * 32 + 32;
+        if ((e = upload(&sk->d_meta, tp.meta.data(), tp.meta.size())) != cudaSuccess ||
+            (e = upload(&sk->d_p1len, tp.p1len.data(), tp.p1len.size())) != cudaSuccess ||
+            (e = upload(&sk->d_round_off, tp.round_off.data(), tp.round_off.size())) != cudaSuccess ||
+            (e = upload(&sk->d_rounds, tp.rounds.data(), tp.rounds.size())) != cudaSuccess ||
+            (e = hs::prepare_chunked(sk->K, sk->smem)) != cudaSuccess) {
+            free_skeleton(sk);
+            return cuda_fail(e, "chunked program");
+        }
+    } else {
+        sk->sp = hs::build_split_program(P, sk->K);
+        if ((e = upload(&sk->d_split_meta, sk->sp.meta.data(), sk->sp.meta.size())) != cudaSuccess) {
+            free_skeleton(sk);
+            return cuda_fail(e, "split program");
+        }
+        if (sk->sp.nslots > 0) {
+            hs_create_opts so = o;
+            so.force_split = 0;
+            hs_status s2 = create_impl(sk->sp.anchor_parents.data(), sk->sp.nslots, nullptr, so, &sk->sub,
+                                       depth + 1);
+            if (s2 != HS_OK) { free_skeleton(sk); return s2; }
+            sk->split_levels = 1 + sk->sub->split_levels;
+        } else {
+            sk->split_levels = 1;
+        }
+    }
+    *out = sk;
+    return HS_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, float* gout,
+                    float* sout, cudaStream_t st, int algo, int max_rounds, int tile_ctas) {
+    const int32_t J = sk->plan.n;
+    cudaError_t e = cudaSuccess;
+    if (algo == HS_ALGO_AUTO) algo = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT;
+    switch (algo) {
+        case HS_ALGO_CHUNKED: {
+            if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "skeleton does not fit the single-CTA path");
+            hs::ChunkedArgs a;
+            a.local = local; a.gout = gout; a.sout = sout; a.ib = sk->d_ib; a.n_chars = n_chars;
+            a.J = J; a.C = sk->tp.C; a.F = sk->tp.F; a.T = sk->tp.T;
+            a.nslots = sk->tp.nslots; a.R2 = sk->tp.R2;
+            a.meta = sk->d_meta; a.p1len = sk->d_p1len; a.round_off = sk->d_round_off;
+            a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
+            a.smem_bytes = sk->smem; a.threads = sk->threads;
+            a.ctas_per_sm = tile_ctas;
+            e = hs::launch_chunked(sk->K, a, st);
+            break;
+        }
+        case HS_ALGO_DOUBLING:
+            if (J > 1024) return fail(HS_ERR_UNSUPPORTED, "doubling kernel needs n_joints <= 1024");
+            e = hs::launch_doubling(local, gout, sout, sk->d_ib, sk->d_lift, J, sk->plan.R, max_rounds,
+                                    n_chars, st);
+            break;
+        case HS_ALGO_GATEAU:
+            e = hs::launch_gateau(local, gout, sout, sk->d_ib, sk->d_parents, J, n_chars, st);
+            break;
+        case HS_ALGO_LEAF:
+            if (!sk->d_path) return fail(HS_ERR_UNSUPPORTED, "leaf paths too large");
+            e = hs::launch_leaf(local, gout, sout, sk->d_ib, sk->d_path_off, sk->d_path, sk->n_leaves, J,
+                                n_chars, st);
+            break;
+        case HS_ALGO_SPLIT: {
+            if (sk->chunked) {
+                // forced split on a skeleton that fits one CTA: build on the fly is not
+                // allowed (no host work on the hot path) — the handle has no split program.
+                return fail(HS_ERR_UNSUPPORTED, "skeleton has no split program (create with force_split=1)");
+            }
+            const hs::SplitProgram& sp = sk->sp;
+            const int64_t per_char = std::max<int64_t>(1, (int64_t)sp.nslots * 48);
+            int64_t batch = std::max<int64_t>(1, ((int64_t)1 << 30) / per_char);
+            batch = std::min(batch, n_chars);
+            float* ws = nullptr;
+            if (sp.nslots > 0) {
+                e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)(2 * batch * per_char), st);
+                if (e != cudaSuccess) return cuda_fail(e, "split workspace");
+            }
+            float* pg = ws;
+            float* pf = ws ? ws + batch * sp.nslots * 12 : nullptr;
+            for (int64_t c0 = 0; c0 < n_chars && e == cudaSuccess; c0 += batch) {
+                const int64_t nb = std::min(batch, n_chars - c0);
+                const float* lc = local + c0 * J * 12;
+                if (sp.nslots > 0) {
+                    e = hs::launch_split_p1(sk->K, lc, pg, sk->d_split_meta, sp.nchunks, J, sp.nslots, nb, st);
+                    if (e != cudaSuccess) break;
+                    hs_status s2 = scan_impl(sk->sub, pg, nb, pf, nullptr, st, HS_ALGO_AUTO, -1, tile_ctas);
+                    if (s2 != HS_OK) { if (ws) cudaFreeAsync(ws, st); return s2; }
+                }
+                e = hs::launch_split_p3(sk->K, lc, gout + c0 * J * 12, sout ? sout + c0 * J * 12 : nullptr,
+                                        sk->d_ib, pf, sk->d_split_meta, sp.nchunks, J, sp.nslots, nb, st);
+            }
+            if (ws) cudaFreeAsync(ws, st);
+            break;
+        }
+        default:
+            return fail(HS_ERR_INVALID_ARG, "unknown algo");
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hs_status hs_skeleton_create_ex(const int32_t* parents, int32_t n_joints, const float* inv_bind,
+                                const hs_create_opts* opts, hs_skeleton** out) {
+    hs_create_opts o;
+    std::memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    try {
+        return create_impl(parents, n_joints, inv_bind, o, out, 0);
+    } catch (const std::bad_alloc&) {
+        return fail(HS_ERR_OOM, "host allocation failed");
+    } catch (...) {
+        return fail(HS_ERR_INVALID_ARG, "unexpected exception in hs_skeleton_create");
+    }
+}
+
+hs_status hs_skeleton_create(const int32_t* parents, int32_t n_joints, const float* inv_bind,
+                             hs_skeleton** out) {
+    return hs_skeleton_create_ex(parents, n_joints, inv_bind, nullptr, out);
+}
+
+hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,
+                     float* skin_out, void* cuda_stream, const hs_scan_opts* opts) {
+    if (!sk) return fail(HS_ERR_INVALID_ARG, "skeleton is null");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!local || !global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (!aligned16(local) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)))
+        return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+    if (local == global_out || (skin_out && (local == skin_out || global_out == skin_out)))
+        return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
+    if (n_chars > (INT64_MAX / 64) / sk->plan.n) return fail(HS_ERR_INVALID_ARG, "size overflow");
+    int algo = HS_ALGO_AUTO, max_rounds = -1, tile_ctas = 0;
+    if (opts) {
+        algo = opts->algo;
+        max_rounds = opts->max_rounds;
+        tile_ctas = opts->tile_ctas;
+        for (int i = 0; i < 5; ++i)
+            if (opts->reserved[i]) return fail(HS_ERR_INVALID_ARG, "reserved option fields must be zero");
+        if (max_rounds >= 0 && algo != HS_ALGO_DOUBLING)
+            return fail(HS_ERR_INVALID_ARG, "max_rounds applies to HS_ALGO_DOUBLING only");
+    }
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != sk->device) return fail(HS_ERR_WRONG_DEVICE, "handle belongs to another device");
+    return scan_impl(sk, local, n_chars, global_out, skin_out, static_cast<cudaStream_t>(cuda_stream),
+                     algo, max_rounds, tile_ctas);
+}
+
+hs_status hs_scan(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,
+                  float* skin_out, void* cuda_stream) {
+    return hs_scan_ex(sk, local, n_chars, global_out, skin_out, cuda_stream, nullptr);
+}
+
+hs_status hs_destroy(hs_skeleton* sk) {
+    free_skeleton(sk);
+    return HS_OK;
+}
+
+hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
+    if (!sk || !v) return fail(HS_ERR_INVALID_ARG, "null argument");
+    switch (what) {
+        case HS_Q_N_JOINTS: *v = sk->plan.n; break;
+        case HS_Q_MAX_LEVEL: *v = sk->plan.L; break;
+        case HS_Q_ROUNDS: *v = sk->plan.R; break;
+        case HS_Q_PATH: *v = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT; break;
+        case HS_Q_CHUNK: *v = sk->K; break;
+        case HS_Q_TILE_CHARS: *v = sk->chunked ? sk->tp.C : 0; break;
+        case HS_Q_ANCHORS: *v = sk->chunked ? sk->tp.nslots : sk->sp.nslots; break;
+        case HS_Q_ANCHOR_ROUNDS: *v = sk->chunked ? sk->tp.R2 : (sk->sub ? sk->sub->plan.R : 0); break;
+        case HS_Q_IDENTITY_ORDER: *v = sk->plan.identity ? 1 : 0; break;
+        case HS_Q_SMEM_BYTES: *v = sk->smem; break;
+        case HS_Q_THREADS: *v = sk->threads; break;
+        case HS_Q_STAGES: *v = sk->stages; break;
+        case HS_Q_DEVICE: *v = sk->device; break;
+        case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
+        default: return fail(HS_ERR_INVALID_ARG, "unknown query");
+    }
+    return HS_OK;
+}
+
+const char* hs_status_string(hs_status s) {
+    switch (s) {
+        case HS_OK: return "HS_OK";
+        case HS_ERR_INVALID_ARG: return "HS_ERR_INVALID_ARG";
+        case HS_ERR_EMPTY: return "HS_ERR_EMPTY";
+        case HS_ERR_OUT_OF_RANGE: return "HS_ERR_OUT_OF_RANGE";
+        case HS_ERR_CYCLE: return "HS_ERR_CYCLE";
+        case HS_ERR_CUDA: return "HS_ERR_CUDA";
+        case HS_ERR_OOM: return "HS_ERR_OOM";
+        case HS_ERR_WRONG_DEVICE: return "HS_ERR_WRONG_DEVICE";
+        case HS_ERR_UNSUPPORTED: return "HS_ERR_UNSUPPORTED";
+        default: return "HS_ERR_UNKNOWN";
+    }
+}
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ host-only plan
+hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk, int32_t block_size,
+                         hs_plan** out) {
+    if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
+    try {
+        hs_plan* p = new hs_plan();
+        std::string err;
+        int st = hs::build_plan(parents, n_joints, p->plan, err);
+        if (st != 0) { delete p; return fail((hs_status)st, err); }
+        p->K = chunk == 0 ? 7 : chunk;
+        if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..15"); }
+        p->block_size = block_size <= 0 ? 64 : block_size;
+        p->decomp = hs::decompose(p->plan.ipar, p->K);
+        *out = p;
+        return HS_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(HS_ERR_OOM, "host allocation failed");
+    }
+}
+
+hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
+    if (!p || !v) return fail(HS_ERR_INVALID_ARG, "null argument");
+    switch (what) {
+        case HS_Q_N_JOINTS: *v = p->plan.n; break;
+        case HS_Q_MAX_LEVEL: *v = p->plan.L; break;
+        case HS_Q_ROUNDS: *v = p->plan.R; break;
+        case HS_Q_CHUNK: *v = p->K; break;
+        case HS_Q_ANCHORS: *v = (int64_t)p->decomp.slots.size(); break;
+        case HS_Q_IDENTITY_ORDER: *v = p->plan.identity ? 1 : 0; break;
+        case HS_Q_ANCHOR_ROUNDS: {
+            hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1);
+            *v = tp.R2;
+            break;
+        }
+        default: return fail(HS_ERR_INVALID_ARG, "unknown plan query");
+    }
+    return HS_OK;
+}
+
+hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_bytes) {
+    if (!p || !buf) return fail(HS_ERR_INVALID_ARG, "null argument");
+    std::vector<int32_t> tmp;
+    const hs::Plan& P = p->plan;
+    switch (what) {
+        case HS_X_LEVELS: tmp = P.level; break;
+        case HS_X_ORDER: tmp = P.order; break;
+        case HS_X_LIFT: tmp = P.lift; break;
+        case HS_X_BLOCK_OF:
+        case HS_X_MPOB: {
+            std::vector<int32_t> b, m;
+            hs::block_layout(P, p->block_size, b, m);
+            tmp = what == HS_X_BLOCK_OF ? b : m;
+            break;
+        }
+        case HS_X_CHUNK_SRC: tmp = p->decomp.src; break;
+        case HS_X_ANCHOR_LINK: tmp = p->decomp.link0; break;
+        default: return fail(HS_ERR_INVALID_ARG, "unknown export");
+    }
+    if ((int64_t)(tmp.size() * sizeof(int32_t)) > buf_bytes) return fail(HS_ERR_INVALID_ARG, "buffer too small");
+    if (!tmp.empty()) std::memcpy(buf, tmp.data(), tmp.size() * sizeof(int32_t));
+    return HS_OK;
+}
+
+hs_status hs_plan_destroy(hs_plan* p) {
+    delete p;
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------ host pipeline
+hs_status hs_pipeline_create(int64_t batch_bytes, hs_pipeline** out) {
+    if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
+    if (batch_bytes <= 0) batch_bytes = (int64_t)256 << 20;
+    batch_bytes = (batch_bytes + 15) & ~(int64_t)15;
+    hs_pipeline* pl = new (std::nothrow) hs_pipeline();
+    if (!pl) return fail(HS_ERR_OOM, "host allocation failed");
+    pl->batch_bytes = batch_bytes;
+    cudaError_t e = cudaGetDevice(&pl->device);
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+        e = cudaStreamCreateWithFlags(&pl->st[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pl->d_in[i]), (size_t)batch_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pl->d_g[i]), (size_t)batch_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&pl->d_s[i]), (size_t)batch_bytes);
+    }
+    if (e != cudaSuccess) {
+        hs_pipeline_destroy(pl);
+        return cuda_fail(e, "pipeline create");
+    }
+    *out = pl;
+    return HS_OK;
+}
+
+hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_local, int64_t n_chars,
+                       float* h_global, float* h_skin) {
+    if (!pl || !sk) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!h_local || !h_global || !h_skin) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != sk->device || dev != pl->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    const int64_t per_char = (int64_t)sk->plan.n * 48;
+    const int64_t batch = pl->batch_bytes / per_char;
+    if (batch < 1) return fail(HS_ERR_INVALID_ARG, "pipeline batch smaller than one character");
+    int64_t b = 0;
+    for (int64_t c0 = 0; c0 < n_chars; c0 += batch, ++b) {
+        const int i = (int)(b % 3);
+        const int64_t nb = std::min(batch, n_chars - c0);
+        const size_t bytes = (size_t)(nb * per_char);
+        const int64_t foff = c0 * sk->plan.n * 12;
+        cudaError_t e = cudaMemcpyAsync(pl->d_in[i], h_local + foff, bytes, cudaMemcpyHostToDevice, pl->st[i]);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+        hs_status s = scan_impl(sk, pl->d_in[i], nb, pl->d_g[i], pl->d_s[i], pl->st[i], HS_ALGO_AUTO, -1, 0);
+        if (s != HS_OK) return s;
+        if ((e = cudaMemcpyAsync(h_global + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(h_skin + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                cudaSuccess)
+            return cuda_fail(e, "D2H");
+    }
+    for (int i = 0; i < 3; ++i) {
+        cudaError_t e = cudaStreamSynchronize(pl->st[i]);
+        if (e != cudaSuccess) return cuda_fail(e, "pipeline sync");
+    }
+    return HS_OK;
+}
+
+hs_status hs_pipeline_destroy(hs_pipeline* pl) {
+    if (!pl) return HS_OK;
+    for (int i = 0; i < 3; ++i) {
+        if (pl->st[i]) cudaStreamSynchronize(pl->st[i]);
+        cudaFree(pl->d_in[i]);
+        cudaFree(pl->d_g[i]);
+        cudaFree(pl->d_s[i]);
+        if (pl->st[i]) cudaStreamDestroy(pl->st[i]);
+    }
+    delete pl;
+    return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,628 @@
+// kernels.cu — hand-written sm_100a kernels for the Hierarchy-Scan + fused
+// Bind MeshPose (§1 steps 2-3, Eq. 1, Algs. 1-4).  DESIGN.md §5.
+//
+// Every pose is a 3x4 fp32 affine [R|t] (48 B).  compose(a, b) = a (x) b with
+// the parent on the LEFT (Alg. 1's "M[jointID] = M[curParentID] * M[jointID]",
+// PAPER.md:81).  No tensor cores: a chain of tiny 3x4 products is not a dense
+// contraction (BASELINE.json north_star); the path is HBM-bound.
+#include "kernels.cuh"
+
+#include <cstdint>
+
+namespace hs {
+namespace {
+
+enum : int { kSrcRoot = -1, kSrcPrev = -2, kSrcNone = -3 };
+
+// ------------------------------------------------------------------ 3x4 algebra
+struct M34 {
+    float v[12];
+};
+
+__device__ __forceinline__ void compose(const float* __restrict__ a, const float* __restrict__ b,
+                                        float* __restrict__ c) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float x = a[4 * r + 0] * b[k];
+            x = fmaf(a[4 * r + 1], b[4 + k], x);
+            c[4 * r + k] = fmaf(a[4 * r + 2], b[8 + k], x);
+        }
+        float t = fmaf(a[4 * r + 0], b[3], a[4 * r + 3]);
+        t = fmaf(a[4 * r + 1], b[7], t);
+        c[4 * r + 3] = fmaf(a[4 * r + 2], b[11], t);
+    }
+}
+
+__device__ __forceinline__ void ld3(const float* p, float* v) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float4 a = q[0], b = q[1], c = q[2];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
+}
+
+__device__ __forceinline__ void st3(float* p, const float* v) {
+    float4* q = reinterpret_cast<float4*>(p);
+    q[0] = make_float4(v[0], v[1], v[2], v[3]);
+    q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    q[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
+__device__ __forceinline__ void ldg3(const float* p, float* v) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) {
+    }
+}
+// 1D bulk copy global -> shared, completion signalled on an mbarrier (TMA, UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// 1D bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_consumers(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// ================================================================== chunked kernel
+// Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
+// producer.  Per tile of C characters (F = C*J joints, user order in smem):
+//   phase 1  each compute thread folds its chunk of K consecutive internal
+//            positions left-to-right (in-chunk parent = previous position) and
+//            publishes the running product at anchor joints into P;
+//   phase 2  pointer jumping (Alg. 2) over the anchor forest, ping-pong P;
+//   phase 3  each thread re-folds its chunk starting from the final P of each
+//            segment head's parent, writes G in place over L, and S = G (x) IB
+//            (IB held in registers) into the S buffer;
+// then the producer bulk-stores G and S and refills the stage.
+template <int K>
+__global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int NS = a.stages, NSS = a.sbufs;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* done = full + 4;
+    uint64_t* sfree = done + 4;
+    float* LG = reinterpret_cast<float*>(smem + 128);
+    const int64_t tile_f = (int64_t)a.F * 12;
+    float* SB = LG + NS * tile_f;
+    float* P = SB + NSS * tile_f;
+
+    const int nwc = (int)(blockDim.x >> 5) - 1;
+    const int NC = nwc * 32;
+    const int warp = threadIdx.x >> 5;
+    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
+    const int64_t my_tiles =
+        blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const bool do_skin = a.sout != nullptr;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == nwc) {
+        // ------------------------------------------------------------ producer
+        if ((threadIdx.x & 31) != 0) return;
+        auto issue_load = [&](int64_t it) {
+            const int stage = (int)(it % NS);
+            const int64_t tile = blockIdx.x + it * gridDim.x;
+            const int64_t c0 = tile * a.C;
+            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+            mbar_expect_tx(&full[stage], bytes);
+            bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
+        };
+        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
+        for (int64_t it = 0; it < my_tiles; ++it) {
+            const int stage = (int)(it % NS);
+            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
+            const int64_t tile = blockIdx.x + it * gridDim.x;
+            const int64_t c0 = tile * a.C;
+            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
+            if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+            bulk_commit();
+            bulk_wait_read_all();                 // smem of this tile has been read out
+            if (do_skin) mbar_arrive(&sfree[it % NSS]);
+            if (it + NS < my_tiles) issue_load(it + NS);
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int t = threadIdx.x;
+    const bool active = t < a.T;
+    uint64_t m[K];
+    float ibr[K][12];
+    int p1 = 0;
+    if (active) {
+        p1 = a.p1len[t];
+#pragma unroll
+        for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
+    } else {
+#pragma unroll
+        for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
+    }
+    if (do_skin) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int src = (int)(int16_t)(m[s] >> 32);
+            const int ibu = (int)((m[s] >> 16) & 0xffff);
+            if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
+        }
+    }
+
+    for (int64_t it = 0; it < my_tiles; ++it) {
+        const int stage = (int)(it % NS);
+        float* L = LG + stage * tile_f;
+        mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
+
+        // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
+        if (p1 > 0) {
+            float acc[12];
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                if (s < p1) {
+                    const int off = (int)(m[s] & 0xffff);
+                    const int src = (int)(int16_t)(m[s] >> 32);
+                    const int own = (int)(int16_t)(m[s] >> 48);
+                    float l[12];
+                    ld3(L + off * 12, l);
+                    if (src == kSrcPrev) {
+                        float tmp[12];
+                        compose(acc, l, tmp);
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                    }
+                    if (own >= 0) st3(P + own * 12, acc);
+                }
+            }
+        }
+        bar_consumers(NC);
+
+        // phase 2: pointer jumping over anchors (snapshot semantics via ping-pong)
+        for (int r = 0; r < a.R2; ++r) {
+            const int e1 = __ldg(a.round_off + r + 1);
+            for (int e = __ldg(a.round_off + r) + t; e < e1; e += NC) {
+                const uint64_t w = __ldg(a.rounds + e);
+                const int dst = (int)(w & 0xffff), self = (int)((w >> 16) & 0xffff),
+                          link = (int)((w >> 32) & 0xffff);
+                float x[12], y[12], z[12];
+                ld3(P + link * 12, x);
+                ld3(P + self * 12, y);
+                compose(x, y, z);
+                st3(P + dst * 12, z);
+            }
+            bar_consumers(NC);
+        }
+
+        // phase 3: final fold, G in place, S into the S buffer
+        float* S = SB + (it % NSS) * tile_f;
+        if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
+        {
+            float acc[12];
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int src = (int)(int16_t)(m[s] >> 32);
+                if (src == kSrcNone) continue;
+                const int off = (int)(m[s] & 0xffff);
+                float l[12];
+                ld3(L + off * 12, l);
+                if (src == kSrcPrev) {
+                    float tmp[12];
+                    compose(acc, l, tmp);
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                } else if (src == kSrcRoot) {
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                } else {
+                    float pa[12];
+                    ld3(P + src * 12, pa);
+                    compose(pa, l, acc);
+                }
+                st3(L + off * 12, acc);
+                if (do_skin) {
+                    float sk[12];
+                    compose(acc, ibr[s], sk);
+                    st3(S + off * 12, sk);
+                }
+            }
+        }
+        fence_proxy_async();
+        bar_consumers(NC);
+        if (t == 0) mbar_arrive(&done[stage]);
+    }
+}
+
+// ================================================================== doubling (Alg. 2)
+// One CTA per group of C characters, one thread per (character, joint) in USER
+// order (pointer jumping is order-agnostic).  Round r: V[j] <- V[anc_r(j)] (x) V[j]
+// on the previous round's snapshot (ping-pong smem), PAPER.md:113-124 with the
+// "pow(2,n) layer parent" hop of PAPER.md:139 (reading R6).
+__global__ void __launch_bounds__(1024) doubling_kernel(const float* __restrict__ local,
+                                                        float* __restrict__ gout,
+                                                        float* __restrict__ sout,
+                                                        const float* __restrict__ ib,
+                                                        const int32_t* __restrict__ lift, int J,
+                                                        int C, int rounds, int64_t n_chars) {
+    extern __shared__ __align__(16) float sm[];
+    const int F = C * J;
+    float* buf0 = sm;
+    float* buf1 = sm + F * 12;
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int nc = (int)min((int64_t)C, n_chars - c0);
+    const int f = threadIdx.x;
+    const int cl = f / J, u = f - cl * J;
+    const bool valid = f < F && cl < nc;
+    float v[12];
+    if (valid) ldg3(local + (c0 * J + f) * 12, v);
+    if (f < F) st3(buf0 + f * 12, v);
+    __syncthreads();
+    float* cur = buf0;
+    float* nxt = buf1;
+    for (int r = 0; r < rounds; ++r) {
+        if (f < F) {
+            const int anc = __ldg(lift + (int64_t)r * J + u);
+            if (anc >= 0) {
+                float x[12], y[12];
+                ld3(cur + (cl * J + anc) * 12, x);
+                compose(x, v, y);
+#pragma unroll
+                for (int e = 0; e < 12; ++e) v[e] = y[e];
+            }
+            st3(nxt + f * 12, v);
+        }
+        __syncthreads();
+        float* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    if (valid) {
+        st3(gout + (c0 * J + f) * 12, v);
+        if (sout) {
+            float b[12], s[12];
+            ldg3(ib + (int64_t)u * 12, b);
+            compose(v, b, s);
+            st3(sout + (c0 * J + f) * 12, s);
+        }
+    }
+}
+
+// ================================================================== Gateau (Alg. 1)
+__global__ void gateau_kernel(const float* __restrict__ local, float* __restrict__ gout,
+                              float* __restrict__ sout, const float* __restrict__ ib,
+                              const int32_t* __restrict__ parents, int J, int64_t n_chars) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_chars * J) return;
+    const int64_t c = idx / J;
+    const int u = (int)(idx - c * J);
+    const float* lc = local + c * J * 12;
+    float acc[12];
+    ldg3(lc + (int64_t)u * 12, acc);
+    for (int p = __ldg(parents + u); p >= 0; p = __ldg(parents + p)) {  // reading R5
+        float x[12], y[12];
+        ldg3(lc + (int64_t)p * 12, x);
+        compose(x, acc, y);
+#pragma unroll
+        for (int e = 0; e < 12; ++e) acc[e] = y[e];
+    }
+    st3(gout + idx * 12, acc);
+    if (sout) {
+        float b[12], s[12];
+        ldg3(ib + (int64_t)u * 12, b);
+        compose(acc, b, s);
+        st3(sout + idx * 12, s);
+    }
+}
+
+// ================================================================== KIYA leaf walk
+__global__ void leaf_kernel(const float* __restrict__ local, float* __restrict__ gout,
+                            float* __restrict__ sout, const float* __restrict__ ib,
+                            const int32_t* __restrict__ path_off, const int32_t* __restrict__ path,
+                            int n_leaves, int J, int64_t n_chars) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_chars * n_leaves) return;
+    const int64_t c = idx / n_leaves;
+    const int leaf = (int)(idx - c * n_leaves);
+    const float* lc = local + c * J * 12;
+    float acc[12];
+    const int e0 = __ldg(path_off + leaf), e1 = __ldg(path_off + leaf + 1);
+    for (int e = e0; e < e1; ++e) {   // root ... leaf
+        const int u = __ldg(path + e);
+        float l[12];
+        ldg3(lc + (int64_t)u * 12, l);
+        if (e == e0) {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) acc[k] = l[k];
+        } else {
+            float y[12];
+            compose(acc, l, y);
+#pragma unroll
+            for (int k = 0; k < 12; ++k) acc[k] = y[k];
+        }
+        st3(gout + (c * J + u) * 12, acc);
+        if (sout) {
+            float b[12], s[12];
+            ldg3(ib + (int64_t)u * 12, b);
+            compose(acc, b, s);
+            st3(sout + (c * J + u) * 12, s);
+        }
+    }
+}
+
+// ================================================================== split (multi-CTA)
+// Thread per (character, chunk).  Global-memory fallback for skeletons that do
+// not fit one CTA; the anchor scan between p1 and p3 is a recursive hs_scan on
+// the anchor skeleton.
+template <int K>
+__global__ void split_p1_kernel(const float* __restrict__ local, float* __restrict__ pg,
+                                const int4* __restrict__ meta, int nchunks, int J, int nslots,
+                                int64_t n_chars) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_chars * nchunks) return;
+    const int64_t c = idx / nchunks;
+    const int ch = (int)(idx - c * nchunks);
+    const float* lc = local + c * J * 12;
+    float* pc = pg + c * nslots * 12;
+    float acc[12];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const int4 mm = __ldg(meta + (int64_t)ch * K + s);
+        if (mm.y == kSrcNone) break;
+        float l[12];
+        ldg3(lc + (int64_t)mm.x * 12, l);
+        if (mm.y == kSrcPrev) {
+            float y[12];
+            compose(acc, l, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) acc[e] = y[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < 12; ++e) acc[e] = l[e];
+        }
+        if (mm.z >= 0) st3(pc + (int64_t)mm.z * 12, acc);
+    }
+}
+
+template <int K>
+__global__ void split_p3_kernel(const float* __restrict__ local, float* __restrict__ gout,
+                                float* __restrict__ sout, const float* __restrict__ ib,
+                                const float* __restrict__ pf, const int4* __restrict__ meta,
+                                int nchunks, int J, int nslots, int64_t n_chars) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_chars * nchunks) return;
+    const int64_t c = idx / nchunks;
+    const int ch = (int)(idx - c * nchunks);
+    const float* lc = local + c * J * 12;
+    const float* pc = pf + c * nslots * 12;
+    float acc[12];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const int4 mm = __ldg(meta + (int64_t)ch * K + s);
+        if (mm.y == kSrcNone) break;
+        float l[12];
+        ldg3(lc + (int64_t)mm.x * 12, l);
+        if (mm.y == kSrcPrev) {
+            float y[12];
+            compose(acc, l, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) acc[e] = y[e];
+        } else if (mm.y == kSrcRoot) {
+#pragma unroll
+            for (int e = 0; e < 12; ++e) acc[e] = l[e];
+        } else {
+            float pa[12];
+            ldg3(pc + (int64_t)mm.y * 12, pa);
+            compose(pa, l, acc);
+        }
+        st3(gout + (c * J + mm.x) * 12, acc);
+        if (sout) {
+            float b[12], sk[12];
+            ldg3(ib + (int64_t)mm.x * 12, b);
+            compose(acc, b, sk);
+            st3(sout + (c * J + mm.x) * 12, sk);
+        }
+    }
+}
+
+template <int K>
+void* chunked_ptr() { return reinterpret_cast<void*>(&chunked_kernel<K>); }
+
+void* chunked_fn(int K) {
+    switch (K) {
+        case 3: return chunked_ptr<3>();
+        case 5: return chunked_ptr<5>();
+        case 7: return chunked_ptr<7>();
+        case 9: return chunked_ptr<9>();
+        case 11: return chunked_ptr<11>();
+        case 13: return chunked_ptr<13>();
+        case 15: return chunked_ptr<15>();
+        default: return nullptr;
+    }
+}
+
+int g_sms = 0;
+int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
+}  // namespace
+
+cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
+    // The attribute is per function, shared by every skeleton handle: raise it to the
+    // device's opt-in maximum once so handles with different smem needs coexist.
+    void* fn = chunked_fn(K);
+    if (!fn) return cudaErrorInvalidValue;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    if (smem_bytes > optin) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes) {
+    void* fn = chunked_fn(K);
+    int nb = 0;
+    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
+                   cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
+    void* fn = chunked_fn(K);
+    if (!fn) return cudaErrorInvalidValue;
+    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
+    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : max_chunked_blocks_per_sm(K, a.threads, a.smem_bytes);
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > ntiles) grid = ntiles;
+    if (grid < 1) grid = 1;
+    ChunkedArgs args = a;
+    void* params[] = {&args};
+    return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(a.threads), params, (size_t)a.smem_bytes, st);
+}
+
+cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,
+                            const int32_t* lift, int32_t J, int32_t R, int32_t rounds,
+                            int64_t n_chars, cudaStream_t st) {
+    if (J > 1024) return cudaErrorInvalidValue;
+    int C = 1024 / J;
+    if (C < 1) C = 1;
+    if (rounds < 0 || rounds > R) rounds = R;
+    const size_t smem = (size_t)2 * C * J * 48;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 1024 * 48);
+        attr = true;
+    }
+    const int64_t blocks = (n_chars + C - 1) / C;
+    doubling_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lift, J, C, rounds,
+                                                           n_chars);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gateau(const float* local, float* gout, float* sout, const float* ib,
+                          const int32_t* parents, int32_t J, int64_t n_chars, cudaStream_t st) {
+    const int64_t n = n_chars * J;
+    gateau_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(local, gout, sout, ib, parents, J, n_chars);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_leaf(const float* local, float* gout, float* sout, const float* ib,
+                        const int32_t* path_off, const int32_t* path, int32_t n_leaves, int32_t J,
+                        int64_t n_chars, cudaStream_t st) {
+    const int64_t n = n_chars * n_leaves;
+    leaf_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(local, gout, sout, ib, path_off, path,
+                                                             n_leaves, J, n_chars);
+    return cudaGetLastError();
+}
+
+#define HS_SPLIT_CASE(KK)                                                                        \
+    case KK:                                                                                     \
+        split_p1_kernel<KK><<<blocks, 128, 0, st>>>(local, pg, reinterpret_cast<const int4*>(meta), \
+                                                    nchunks, J, nslots, n_chars);                 \
+        break;
+
+cudaError_t launch_split_p1(int K, const float* local, float* pg, const int32_t* meta,
+                            int32_t nchunks, int32_t J, int32_t nslots, int64_t n_chars,
+                            cudaStream_t st) {
+    const int64_t n = n_chars * nchunks;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    switch (K) {
+        HS_SPLIT_CASE(3) HS_SPLIT_CASE(5) HS_SPLIT_CASE(7) HS_SPLIT_CASE(9) HS_SPLIT_CASE(11)
+        HS_SPLIT_CASE(13) HS_SPLIT_CASE(15)
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+#undef HS_SPLIT_CASE
+
+#define HS_SPLIT_CASE(KK)                                                                         \
+    case KK:                                                                                      \
+        split_p3_kernel<KK><<<blocks, 128, 0, st>>>(local, gout, sout, ib, pf,                    \
+                                                    reinterpret_cast<const int4*>(meta), nchunks, J, \
+                                                    nslots, n_chars);                              \
+        break;
+
+cudaError_t launch_split_p3(int K, const float* local, float* gout, float* sout, const float* ib,
+                            const float* pf, const int32_t* meta, int32_t nchunks, int32_t J,
+                            int32_t nslots, int64_t n_chars, cudaStream_t st) {
+    const int64_t n = n_chars * nchunks;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    switch (K) {
+        HS_SPLIT_CASE(3) HS_SPLIT_CASE(5) HS_SPLIT_CASE(7) HS_SPLIT_CASE(9) HS_SPLIT_CASE(11)
+        HS_SPLIT_CASE(13) HS_SPLIT_CASE(15)
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+#undef HS_SPLIT_CASE
+
+}  // namespace hs

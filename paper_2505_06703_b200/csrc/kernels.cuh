@@ -1,0 +1,53 @@
+// kernels.cuh — launch interface of the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hs {
+
+// Persistent TMA tile kernel (HS_ALGO_CHUNKED), DESIGN.md §5.1.
+struct ChunkedArgs {
+    const float* local;        // [n_chars][J][12]
+    float* gout;               // [n_chars][J][12]
+    float* sout;               // [n_chars][J][12] or nullptr (no bind epilogue)
+    const float* ib;           // [J][12] user order (used when sout != nullptr)
+    int64_t n_chars;
+    int32_t J, C, F, T;        // joints, chars per tile, joints per tile, compute threads
+    int32_t nslots, R2;
+    const uint64_t* meta;      // [T][K]
+    const int32_t* p1len;      // [T]
+    const int32_t* round_off;  // [R2+1]
+    const uint64_t* rounds;
+    int32_t stages, sbufs;
+    int64_t smem_bytes;
+    int32_t threads;           // consumer warps * 32 + 32 (producer warp)
+    int32_t ctas_per_sm;       // 0 = occupancy maximum
+};
+cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
+cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes);
+
+// Alg. 2: radix-2 pointer jumping, one thread per joint.
+cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,
+                            const int32_t* lift, int32_t J, int32_t R, int32_t rounds,
+                            int64_t n_chars, cudaStream_t st);
+
+// Alg. 1: thread per joint walks all ancestors.
+cudaError_t launch_gateau(const float* local, float* gout, float* sout, const float* ib,
+                          const int32_t* parents, int32_t J, int64_t n_chars, cudaStream_t st);
+
+// KIYA leaf walk: thread per leaf fills its root path top-down.
+cudaError_t launch_leaf(const float* local, float* gout, float* sout, const float* ib,
+                        const int32_t* path_off, const int32_t* path, int32_t n_leaves, int32_t J,
+                        int64_t n_chars, cudaStream_t st);
+
+// Multi-CTA (split) path: phase 1 and phase 3 over chunks.
+cudaError_t launch_split_p1(int K, const float* local, float* pg, const int32_t* meta,
+                            int32_t nchunks, int32_t J, int32_t nslots, int64_t n_chars,
+                            cudaStream_t st);
+cudaError_t launch_split_p3(int K, const float* local, float* gout, float* sout, const float* ib,
+                            const float* pf, const int32_t* meta, int32_t nchunks, int32_t J,
+                            int32_t nslots, int64_t n_chars, cudaStream_t st);
+
+}  // namespace hs

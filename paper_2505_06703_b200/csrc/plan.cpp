@@ -1,0 +1,200 @@
+// plan.cpp — host topology preprocessor (see plan.hpp and DESIGN.md §5).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace hs {
+
+namespace {
+constexpr int kOk = 0, kInvalid = 1, kEmpty = 2, kOutOfRange = 3, kCycle = 4, kUnsupported = 8;
+constexpr int32_t kMaxJoints = 1 << 20;
+}  // namespace
+
+int build_plan(const int32_t* parents, int32_t n, Plan& P, std::string& err) {
+    if (n < 0 || (n > 0 && !parents)) { err = "parents is null or n_joints < 0"; return kInvalid; }
+    if (n == 0) { err = "n_joints == 0"; return kEmpty; }
+    if (n > kMaxJoints) { err = "n_joints above HS_MAX_JOINTS"; return kUnsupported; }
+    P = Plan();
+    P.n = n;
+    P.parents.assign(parents, parents + n);
+    for (int32_t j = 0; j < n; ++j)
+        if (parents[j] < -1 || parents[j] >= n) {
+            err = "parent of joint " + std::to_string(j) + " out of range: " + std::to_string(parents[j]);
+            return kOutOfRange;
+        }
+    // children in ascending label order (CSR)
+    std::vector<int32_t> first(n + 1, 0), kids(n);
+    for (int32_t j = 0; j < n; ++j) if (parents[j] >= 0) first[parents[j] + 1]++;
+    for (int32_t j = 0; j < n; ++j) first[j + 1] += first[j];
+    {
+        std::vector<int32_t> fill(first.begin(), first.end() - 1);
+        for (int32_t j = 0; j < n; ++j) if (parents[j] >= 0) kids[fill[parents[j]]++] = j;
+    }
+    // DFS preorder from the roots (ascending), children ascending; nodes not
+    // reached lie on (or under) a cycle.
+    std::vector<int32_t> dfs;
+    dfs.reserve(n);
+    std::vector<int32_t> stack;
+    // roots pushed in descending order so the smallest label is popped first
+    for (int32_t r = n - 1; r >= 0; --r) if (parents[r] == -1) stack.push_back(r);
+    while (!stack.empty()) {
+        int32_t v = stack.back();
+        stack.pop_back();
+        dfs.push_back(v);
+        for (int32_t e = first[v + 1] - 1; e >= first[v]; --e) stack.push_back(kids[e]);
+    }
+    if ((int32_t)dfs.size() != n) { err = "parent chain contains a cycle"; return kCycle; }
+
+    P.level.assign(n, 0);
+    for (int32_t v : dfs) P.level[v] = parents[v] < 0 ? 1 : P.level[parents[v]] + 1;
+    P.L = *std::max_element(P.level.begin(), P.level.end());
+    P.R = 0;
+    while ((1LL << P.R) < P.L) ++P.R;
+
+    P.identity = true;
+    for (int32_t j = 0; j < n; ++j) if (parents[j] >= j) { P.identity = false; break; }
+    P.order.resize(n);
+    if (P.identity) for (int32_t i = 0; i < n; ++i) P.order[i] = i;
+    else P.order = dfs;
+    P.rank.resize(n);
+    for (int32_t i = 0; i < n; ++i) P.rank[P.order[i]] = i;
+    P.ipar.resize(n);
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t q = parents[P.order[i]];
+        P.ipar[i] = q < 0 ? -1 : P.rank[q];
+    }
+    // Eq. 2 lift table, user labels: anc[0] = Parent, anc[r+1][u] = anc[r][anc[r][u]].
+    P.lift.assign((size_t)P.R * n, -1);
+    for (int r = 0; r < P.R; ++r)
+        for (int32_t u = 0; u < n; ++u) {
+            int32_t a = r == 0 ? parents[u] : P.lift[(size_t)(r - 1) * n + u];
+            if (r > 0 && a >= 0) a = P.lift[(size_t)(r - 1) * n + a];
+            P.lift[(size_t)r * n + u] = a;
+        }
+    for (int32_t u = 0; u < n; ++u) if (first[u + 1] == first[u]) P.leaves.push_back(u);
+    return kOk;
+}
+
+ChunkDecomp decompose(const std::vector<int32_t>& par, int K) {
+    const int32_t F = (int32_t)par.size();
+    ChunkDecomp d;
+    d.K = K;
+    d.src.assign(F, SRC_ROOT);
+    d.slot_of.assign(F, -1);
+    for (int32_t f = 0; f < F; ++f) {
+        int32_t q = par[f];
+        if (q < 0) d.src[f] = SRC_ROOT;
+        else if (q == f - 1 && q / K == f / K) d.src[f] = SRC_PREV;
+        else d.src[f] = q;
+    }
+    std::vector<char> is_anchor(F, 0);
+    for (int32_t f = 0; f < F; ++f)
+        if (d.src[f] >= 0) is_anchor[d.src[f]] = 1;
+    for (int32_t f = 0; f < F; ++f)
+        if (is_anchor[f]) { d.slot_of[f] = (int32_t)d.slots.size(); d.slots.push_back(f); }
+    std::vector<int32_t> head(F);
+    for (int32_t f = 0; f < F; ++f) head[f] = d.src[f] == SRC_PREV ? head[f - 1] : f;
+    d.link0.resize(d.slots.size());
+    for (size_t s = 0; s < d.slots.size(); ++s) {
+        int32_t h = head[d.slots[s]];
+        d.link0[s] = d.src[h] >= 0 ? d.slot_of[d.src[h]] : -1;
+    }
+    return d;
+}
+
+TileProgram build_tile_program(const Plan& p, int K, int C) {
+    TileProgram tp;
+    const int32_t n = p.n;
+    tp.K = K;
+    tp.C = C;
+    tp.F = C * n;
+    tp.T = (tp.F + K - 1) / K;
+    std::vector<int32_t> par(tp.F);
+    for (int c = 0; c < C; ++c)
+        for (int32_t i = 0; i < n; ++i) par[c * n + i] = p.ipar[i] < 0 ? -1 : c * n + p.ipar[i];
+    ChunkDecomp d = decompose(par, K);
+    const int32_t S = (int32_t)d.slots.size();
+    tp.nslots = S;
+    // pointer-jumping rounds over the anchor forest, ping-pong P buffers
+    std::vector<int32_t> lk = d.link0, latest(S, 0);
+    tp.round_off.push_back(0);
+    for (int r = 0;; ++r) {
+        bool any = false;
+        for (int32_t s = 0; s < S; ++s) if (lk[s] >= 0) { any = true; break; }
+        if (!any) break;
+        for (int32_t s = 0; s < S; ++s) {
+            if (lk[s] < 0) continue;
+            uint64_t dst = (uint64_t)(((r + 1) & 1) * S + s);
+            uint64_t self = (uint64_t)(latest[s] * S + s);
+            uint64_t link = (uint64_t)(latest[lk[s]] * S + lk[s]);
+            tp.rounds.push_back(dst | (self << 16) | (link << 32));
+        }
+        std::vector<int32_t> nl(S, -1);
+        for (int32_t s = 0; s < S; ++s) {
+            if (lk[s] < 0) continue;
+            latest[s] = (r + 1) & 1;
+            nl[s] = lk[lk[s]];
+        }
+        lk.swap(nl);
+        tp.round_off.push_back((int32_t)tp.rounds.size());
+        tp.R2 = r + 1;
+    }
+    tp.meta.assign((size_t)tp.T * K, 0);
+    tp.p1len.assign(tp.T, 0);
+    for (int32_t t = 0; t < tp.T; ++t)
+        for (int s = 0; s < K; ++s) {
+            int32_t f = t * K + s;
+            int32_t src = SRC_NONE, own = -1;
+            uint64_t off = 0, ibu = 0;
+            if (f < tp.F) {
+                int32_t c = f / n, i = f % n;
+                off = (uint64_t)(c * n + p.order[i]);
+                ibu = (uint64_t)p.order[i];
+                src = d.src[f] >= 0 ? latest[d.slot_of[d.src[f]]] * S + d.slot_of[d.src[f]] : d.src[f];
+                own = d.slot_of[f];
+                if (own >= 0) tp.p1len[t] = s + 1;
+            }
+            tp.meta[(size_t)t * K + s] = off | (ibu << 16) | ((uint64_t)(uint16_t)(int16_t)src << 32) |
+                                         ((uint64_t)(uint16_t)(int16_t)own << 48);
+        }
+    return tp;
+}
+
+SplitProgram build_split_program(const Plan& p, int K) {
+    SplitProgram sp;
+    sp.K = K;
+    const int32_t n = p.n;
+    ChunkDecomp d = decompose(p.ipar, K);
+    sp.nslots = (int32_t)d.slots.size();
+    sp.nchunks = (n + K - 1) / K;
+    sp.meta.assign((size_t)sp.nchunks * K * 4, 0);
+    for (int32_t f = 0; f < sp.nchunks * K; ++f) {
+        int32_t* m = &sp.meta[(size_t)f * 4];
+        if (f >= n) { m[0] = 0; m[1] = SRC_NONE; m[2] = -1; m[3] = 0; continue; }
+        m[0] = p.order[f];
+        m[1] = d.src[f] >= 0 ? d.slot_of[d.src[f]] : d.src[f];
+        m[2] = d.slot_of[f];
+        m[3] = 0;
+    }
+    sp.anchor_parents = d.link0;
+    return sp;
+}
+
+void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob) {
+    block_of.resize(p.n);
+    mpob.assign(p.n, -1);
+    for (int32_t i = 0; i < p.n; ++i) block_of[i] = i / B;
+    for (int32_t i = 0; i < p.n; ++i) {
+        int32_t a = p.ipar[i];
+        while (a >= 0 && a / B == i / B) a = p.ipar[a];
+        mpob[i] = a;
+    }
+}
+
+int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs) {
+    int64_t tileb = (int64_t)tp.F * 48;
+    return (int64_t)stages * tileb + (int64_t)sbufs * tileb + 2LL * tp.nslots * 48 + 128;
+}
+
+}  // namespace hs

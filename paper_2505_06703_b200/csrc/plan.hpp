@@ -1,0 +1,84 @@
+// plan.hpp — host topology preprocessor for the Hierarchy-Scan (runs once per
+// skeleton, never per frame; no CUDA).  See DESIGN.md §5.
+//
+// What it builds, and the passages it implements:
+//   * validation: range / cycle / empty (SPEC.md:63-72 errors; a forward parent
+//     is accepted and reordered — DESIGN.md reading R17);
+//   * levels, L and R = ceil(log2 L) (Table 1 "hierarchy layer");
+//   * internal topological order: the user order when it is already topological
+//     (parent < child), else DFS preorder with roots/children ascending
+//     ("traversing the skeleton tree in order ... the parent node of any tree node
+//     must have a smaller sequence number");
+//   * Eq. 2 MultiParent lift table anc[r][j] = 2^r-th ancestor,
+//     used by the Alg. 2 doubling kernel;
+//   * the paper's block layout / MaxParentOutBlock — exported
+//     for tests; the B200 kernels use the chunk/anchor program below instead;
+//   * the CHUNK/ANCHOR program (this build's generalisation of Alg. 3,
+//     PAPER.md:145-175, with per-thread chunks of K consecutive internal positions
+//     as the "blocks", serial in-chunk composition instead of in-block doubling,
+//     and pointer jumping (Alg. 2) over the chunks' anchor joints instead of the
+//     serial MaxParentOutBlock walk).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace hs {
+
+enum : int32_t { SRC_ROOT = -1, SRC_PREV = -2, SRC_NONE = -3 };
+
+// Chunk decomposition of a flat forest given in topological order (par[f] < f).
+struct ChunkDecomp {
+    int K = 0;
+    std::vector<int32_t> src;      // per node: SRC_ROOT, SRC_PREV, or anchor node index (>= 0)
+    std::vector<int32_t> slot_of;  // per node: anchor slot or -1
+    std::vector<int32_t> slots;    // slot -> node (ascending node index => topological)
+    std::vector<int32_t> link0;    // slot -> slot of anchor(seghead(node)), or -1
+};
+ChunkDecomp decompose(const std::vector<int32_t>& par, int K);
+
+// Persistent-tile program for the single-CTA chunked kernel.
+struct TileProgram {
+    int K = 0, C = 0, F = 0, T = 0;     // chunk, chars per tile, joints per tile, compute threads
+    int nslots = 0, R2 = 0;             // anchor slots per tile, pointer-jumping rounds
+    std::vector<uint64_t> meta;         // [T][K]: off | ibu<<16 | (u16)src<<32 | (u16)own<<48
+    std::vector<int32_t> p1len;         // [T]: phase-1 length (last own anchor + 1)
+    std::vector<int32_t> round_off;     // [R2 + 1] offsets into rounds
+    std::vector<uint64_t> rounds;       // dst | self<<16 | link<<32  (P locations)
+};
+
+// Multi-CTA (split) program: the same decomposition over ONE character with
+// unbounded size; slots index a global workspace [n_chars][nslots][12].
+struct SplitProgram {
+    int K = 0, nchunks = 0, nslots = 0;
+    std::vector<int32_t> meta;          // [nchunks][K][4]: off(user j), src, own, pad
+    std::vector<int32_t> anchor_parents;// [nslots]: link0 (the anchor skeleton, topological)
+};
+
+struct Plan {
+    int32_t n = 0;
+    std::vector<int32_t> parents;       // user labels
+    std::vector<int32_t> level;         // user labels, root = 1
+    int32_t L = 0, R = 0;
+    bool identity = true;
+    std::vector<int32_t> order;         // internal -> user
+    std::vector<int32_t> rank;          // user -> internal
+    std::vector<int32_t> ipar;          // internal parents
+    std::vector<int32_t> lift;          // [R][n] user labels (Eq. 2 powers of two)
+    std::vector<int32_t> leaves;        // user labels of leaves (KIYA kernel)
+};
+
+// Returns 0 (HS_OK) or an hs_status code; err gets a message.
+int build_plan(const int32_t* parents, int32_t n, Plan& out, std::string& err);
+
+TileProgram build_tile_program(const Plan& p, int K, int C);
+SplitProgram build_split_program(const Plan& p, int K);
+
+// The paper's block layout for block size B over INTERNAL positions (exports).
+void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);
+
+// Shared-memory bytes of the chunked kernel for a tile program and stage counts.
+int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs);
+
+}  // namespace hs

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bar (BASELINE.json north_star): max |element| error <= 1e-4 for G and S on
+rigid inputs with |t| <= 1, depth <= 1024; bitwise on the exact-arithmetic
+family (every product exact in fp32) and on the cases with no multiply.
+All inputs come from hsgen (host generator); expected values from oracle/.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import hsgen
+import oracle
+from tests import brute
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2505_06703_b200 as hs  # noqa: E402
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    hs.build()
+    torch.cuda.init()
+
+
+def gpu_scan(parents, local, ib=None, algo="auto", max_rounds=-1, skin=True, **create):
+    sk = hs.Skeleton(parents, ib, **create)
+    x = torch.from_numpy(np.ascontiguousarray(local)).cuda()
+    g, s = sk.scan(x, algo=algo, max_rounds=max_rounds, skin=skin)
+    torch.cuda.synchronize()
+    out = g.cpu().numpy(), (s.cpu().numpy() if s is not None else None)
+    sk.close()
+    return out
+
+
+def max_err(a, b):
+    return float(np.abs(a.astype(np.float64) - b).max()) if a.size else 0.0
+
+
+# ------------------------------------------------------------------ configs 1-4, full size
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_config_parity_full(cfg):
+    (name, n_chars, seed, type_, ib_seed), = hsgen.CONFIGS[cfg]
+    par = hsgen.skeleton(name)
+    J = len(par)
+    local = hsgen.local_poses(seed, J, n_chars, type_=type_)
+    ib = hsgen.inv_bind(ib_seed, J)
+    g, s = gpu_scan(par, local, ib)
+    G, S = oracle.scan(par, local, ib)
+    eg, es = max_err(g, G), max_err(s, S)
+    print(f"config {cfg} {name} x {n_chars}: max err global {eg:.3e} skin {es:.3e}")
+    assert eg <= TOL and es <= TOL
+    # the root's global equals its local bitwise (no multiply on a root)
+    roots = np.where(par < 0)[0]
+    assert np.array_equal(g[:, roots], local[:, roots])
+
+
+# ------------------------------------------------------------------ exact family, every path
+EXACT_CASES = [
+    ("hum32", {}), ("hum64", {}), ("chain256", {}), ("tree1024", {}),
+    ("hum64", {"chunk": 3}), ("chain256", {"chunk": 11}), ("tree1024", {"chunk": 5}),
+    ("hum64", {"tile_joints": 200}), ("tree1024", {"stages": 2, "sbufs": 1}),
+    ("tree1024", {"force_split": True}), ("chain256", {"force_split": True, "chunk": 3}),
+]
+
+
+@pytest.mark.parametrize("name,create", EXACT_CASES)
+def test_exact_family_bitwise(name, create):
+    par = hsgen.skeleton(name)
+    J = len(par)
+    n_chars = 37  # ragged against every tile size
+    local = hsgen.exact_poses(31, J, n_chars)
+    ib = hsgen.exact_inv_bind(31, J)
+    G, S = oracle.scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib, **create)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
+
+
+@pytest.mark.parametrize("algo", ["doubling", "gateau", "leaf"])
+@pytest.mark.parametrize("name", ["hum64", "chain256", "tree1024"])
+def test_exact_family_comparison_algorithms(algo, name):
+    par = hsgen.skeleton(name)
+    J = len(par)
+    local = hsgen.exact_poses(32, J, 9)
+    ib = hsgen.exact_inv_bind(32, J)
+    G, S = oracle.scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib, algo=algo)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
+
+
+def test_permuted_labels():
+    """Non-topological user order (forward parents): reordered internally."""
+    base = hsgen.skeleton("tree1024")
+    perm = hsgen.permutation(7, 1024)
+    par, _ = hsgen.relabel(base, perm)
+    assert hs.Plan(par).query("identity_order") == 0
+    local = hsgen.exact_poses(33, 1024, 5)
+    ib = hsgen.exact_inv_bind(33, 1024)
+    G, S = oracle.scan(par, local, ib)
+    for create in ({}, {"force_split": True}):
+        g, s = gpu_scan(par, local, ib, **create)
+        assert np.array_equal(g, G) and np.array_equal(s, S)
+    # rigid inputs, tolerance, and equality with the unpermuted problem
+    local = hsgen.local_poses(34, 1024, 50)
+    g, _ = gpu_scan(par, local)
+    G, _ = oracle.scan(par, local)
+    assert max_err(g, G) <= TOL
+
+
+def test_large_skeleton_multi_cta_path():
+    """16,384-joint tree, L = 1024: beyond one CTA -> the split (multi-CTA) path."""
+    par = hsgen.random_tree(77, 16384, 1024)
+    sk = hs.Skeleton(par)
+    assert sk.query("path") == hs.ALGO["split"]
+    assert sk.query("split_levels") >= 1
+    sk.close()
+    local = hsgen.exact_poses(35, 16384, 3)
+    ib = hsgen.exact_inv_bind(35, 16384)
+    G, S = oracle.scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
+    local = hsgen.local_poses(36, 16384, 4)
+    g, s = gpu_scan(par, local)
+    G, S = oracle.scan(par, local)
+    e = max_err(g, G)
+    print(f"16384-joint L=1024 tree: max err {e:.3e}")
+    assert e <= 2 * TOL  # L = 1024 stress: margin measured, see DESIGN.md §3
+
+
+def test_chain1024_stress():
+    par = hsgen.chain(1024)
+    local = hsgen.local_poses(37, 1024, 200)
+    ib = hsgen.inv_bind(37, 1024)
+    g, s = gpu_scan(par, local, ib)
+    G, S = oracle.scan(par, local, ib)
+    eg, es = max_err(g, G), max_err(s, S)
+    print(f"chain1024 (|t|<=1 locals and IB): global {eg:.3e} skin {es:.3e}")
+    assert eg <= TOL and es <= TOL
+
+
+# ------------------------------------------------------------------ closed forms / degenerate
+def test_identity_locals_bitwise():
+    par = hsgen.skeleton("tree1024")
+    I = np.zeros((3, 1024, 3, 4), np.float32)
+    I[..., 0, 0] = I[..., 1, 1] = I[..., 2, 2] = 1
+    ib = hsgen.inv_bind(4, 1024)
+    g, s = gpu_scan(par, I, ib)
+    assert np.array_equal(g, I) and np.array_equal(s, np.broadcast_to(ib, s.shape))
+
+
+def test_dyadic_translation_chain_bitwise():
+    J = 256
+    rng = np.random.default_rng(3)
+    t = rng.integers(-8, 9, size=(2, J, 3)) / 8.0
+    local = np.zeros((2, J, 3, 4), np.float32)
+    local[..., 0, 0] = local[..., 1, 1] = local[..., 2, 2] = 1
+    local[..., 3] = t
+    g, _ = gpu_scan(hsgen.chain(J), local)
+    assert np.array_equal(g[..., 3], np.cumsum(t, axis=1))
+
+
+@pytest.mark.parametrize("algo", ["auto", "doubling", "gateau", "leaf"])
+def test_single_joint_and_all_roots(algo):
+    for par in ([-1], [-1] * 10):
+        local = hsgen.local_poses(40, len(par), 33)
+        g, s = gpu_scan(par, local, algo=algo)
+        assert np.array_equal(g, local) and np.array_equal(s, local)
+
+
+def test_zero_characters_is_noop():
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    x = torch.zeros((0, 32, 3, 4), device="cuda")
+    g, s = sk.scan(x)
+    assert g.shape == (0, 32, 3, 4)
+
+
+def test_global_only_mode():
+    par = hsgen.skeleton("hum64")
+    local = hsgen.exact_poses(41, 64, 20)
+    g, s = gpu_scan(par, local, skin=False)
+    assert s is None
+    assert np.array_equal(g, oracle.scan(par, local)[0])
+
+
+def test_bind_pose_gives_identity_skin():
+    """SPEC.md:218 / Acceptance 6: model == bind pose -> skin == I (fp32 bound)."""
+    for name in ("hum64", "tree1024"):
+        par = hsgen.skeleton(name)
+        J = len(par)
+        bind_local = hsgen.local_poses(42, J, 1)
+        Gb, _ = oracle.scan(par, bind_local)
+        ib = np.stack([np.linalg.inv(brute.homog(m))[:3] for m in Gb[0]]).astype(np.float32)
+        _, s = gpu_scan(par, bind_local, ib)
+        I = np.zeros((3, 4)); I[0, 0] = I[1, 1] = I[2, 2] = 1
+        e = max_err(s[0], np.broadcast_to(I, s[0].shape))
+        print(f"{name} bind-pose skin vs I: {e:.3e}")
+        assert e <= TOL
+
+
+# ------------------------------------------------------------------ round induction (P6)
+def test_doubling_round_induction():
+    """after d rounds of Alg. 2 on a 64-chain, each joint equals the
+    product of its 2^d nearest chain nodes (computed by the oracle on the sub-chain)."""
+    J = 64
+    local = hsgen.exact_poses(43, J, 1)
+    assert hs.Plan(hsgen.chain(J)).query("rounds") == 6
+    for d in range(0, 7):
+        g, _ = gpu_scan(hsgen.chain(J), local, algo="doubling", max_rounds=d)
+        for i in range(J):
+            lo = max(0, i - (1 << d) + 1)
+            sub, _ = oracle.scan(hsgen.chain(i - lo + 1), local[0, lo:i + 1])
+            assert np.array_equal(g[0, i], sub[-1]), (d, i)
+
+
+# ------------------------------------------------------------------ determinism / independence
+def test_determinism_and_character_independence():
+    par = hsgen.skeleton("tree1024")
+    local = hsgen.local_poses(44, 1024, 64)
+    g1, s1 = gpu_scan(par, local)
+    g2, s2 = gpu_scan(par, local)
+    assert np.array_equal(g1, g2) and np.array_equal(s1, s2)
+    g3, s3 = gpu_scan(par, local[17:18])
+    assert np.array_equal(g3[0], g1[17]) and np.array_equal(s3[0], s1[17])
+    par = hsgen.skeleton("hum64")
+    local = hsgen.local_poses(45, 64, 100)
+    ga, _ = gpu_scan(par, local)
+    gb, _ = gpu_scan(par, local[50:])
+    assert np.array_equal(ga[50:], gb)
+
+
+def test_host_pipeline_matches_device_path():
+    par = hsgen.skeleton("chain256")
+    ib = hsgen.inv_bind(3, 256)
+    local = hsgen.local_poses(46, 256, 3000)
+    g_dev, s_dev = gpu_scan(par, local, ib)
+    sk = hs.Skeleton(par, ib)
+    pl = hs.Pipeline(batch_bytes=256 * 48 * 700)  # several batches + a ragged one
+    hl = torch.from_numpy(local).pin_memory()
+    hg = torch.empty_like(hl).pin_memory()
+    hsk = torch.empty_like(hl).pin_memory()
+    pl.scan_host(sk, hl, hg, hsk)
+    assert np.array_equal(hg.numpy(), g_dev) and np.array_equal(hsk.numpy(), s_dev)
+
+
+# ------------------------------------------------------------------ ABI error behaviour
+def test_abi_errors():
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    x = torch.zeros((4, 32, 3, 4), device="cuda")
+    y = torch.zeros_like(x)
+    with pytest.raises(hs.HSError) as e:
+        sk.scan_into(x, x, y)
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    with pytest.raises(hs.HSError) as e:
+        sk.scan_into(x.data_ptr() + 4, y, None, n_chars=2)
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    with pytest.raises(hs.HSError) as e:
+        sk.scan_into(x, y, None, algo="split")
+    assert e.value.status == hs.HS_ERR_UNSUPPORTED
+    with pytest.raises(hs.HSError) as e:
+        sk.scan_into(x, y, None, algo="chunked", max_rounds=2)
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    for bad, code in (([], hs.HS_ERR_EMPTY), ([0], hs.HS_ERR_CYCLE), ([-1, 9], hs.HS_ERR_OUT_OF_RANGE)):
+        with pytest.raises(hs.HSError) as e:
+            hs.Skeleton(bad)
+        assert e.value.status == code
