@@ -125,9 +125,9 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
     const int max_threads = 224;  // compute threads per CTA (launch bounds 256 incl. producer)
-    while (C > 1 && ((int64_t)C * n + sk->K - 1) / sk->K > max_threads) --C;
-    if (!(o.force_split && depth == 0) && ((int64_t)C * n + sk->K - 1) / sk->K <= max_threads &&
-        (int64_t)C * n <= 65535) {
+    const int64_t TC = (n + sk->K - 1) / sk->K;  // compute threads per character
+    while (C > 1 && C * TC > max_threads) --C;
+    if (!(o.force_split && depth == 0) && C * TC <= max_threads && (int64_t)C * n <= 65535) {
         sk->tp = hs::build_tile_program(P, sk->K, C);
         const int want_stages = o.stages, want_sbufs = o.sbufs;
         const int cand[][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};

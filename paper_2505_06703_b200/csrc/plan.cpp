@@ -104,20 +104,24 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K) {
 }
 
 TileProgram build_tile_program(const Plan& p, int K, int C) {
+    // Chunks never straddle characters: every character of a tile runs the same
+    // program (same association order), so a character's bits do not depend on
+    // its position in the batch, the tile size or the GPU count.
     TileProgram tp;
     const int32_t n = p.n;
+    const ChunkDecomp d = decompose(p.ipar, K);
+    const int32_t TC = (n + K - 1) / K;        // chunks (threads) per character
+    const int32_t Sc = (int32_t)d.slots.size();
     tp.K = K;
     tp.C = C;
     tp.F = C * n;
-    tp.T = (tp.F + K - 1) / K;
-    std::vector<int32_t> par(tp.F);
-    for (int c = 0; c < C; ++c)
-        for (int32_t i = 0; i < n; ++i) par[c * n + i] = p.ipar[i] < 0 ? -1 : c * n + p.ipar[i];
-    ChunkDecomp d = decompose(par, K);
-    const int32_t S = (int32_t)d.slots.size();
+    tp.T = C * TC;
+    const int32_t S = C * Sc;
     tp.nslots = S;
-    // pointer-jumping rounds over the anchor forest, ping-pong P buffers
-    std::vector<int32_t> lk = d.link0, latest(S, 0);
+    // pointer-jumping rounds over the tile's anchor forest (C disjoint copies), ping-pong P
+    std::vector<int32_t> lk(S), latest(S, 0);
+    for (int c = 0; c < C; ++c)
+        for (int32_t s = 0; s < Sc; ++s) lk[c * Sc + s] = d.link0[s] < 0 ? -1 : c * Sc + d.link0[s];
     tp.round_off.push_back(0);
     for (int r = 0;; ++r) {
         bool any = false;
@@ -142,21 +146,28 @@ TileProgram build_tile_program(const Plan& p, int K, int C) {
     }
     tp.meta.assign((size_t)tp.T * K, 0);
     tp.p1len.assign(tp.T, 0);
-    for (int32_t t = 0; t < tp.T; ++t)
-        for (int s = 0; s < K; ++s) {
-            int32_t f = t * K + s;
-            int32_t src = SRC_NONE, own = -1;
-            uint64_t off = 0, ibu = 0;
-            if (f < tp.F) {
-                int32_t c = f / n, i = f % n;
-                off = (uint64_t)(c * n + p.order[i]);
-                ibu = (uint64_t)p.order[i];
-                src = d.src[f] >= 0 ? latest[d.slot_of[d.src[f]]] * S + d.slot_of[d.src[f]] : d.src[f];
-                own = d.slot_of[f];
-                if (own >= 0) tp.p1len[t] = s + 1;
+    for (int c = 0; c < C; ++c)
+        for (int32_t tc = 0; tc < TC; ++tc) {
+            const int32_t t = c * TC + tc;
+            for (int s = 0; s < K; ++s) {
+                const int32_t i = tc * K + s;     // internal position within the character
+                int32_t src = SRC_NONE, own = -1;
+                uint64_t off = 0, ibu = 0;
+                if (i < n) {
+                    off = (uint64_t)(c * n + p.order[i]);
+                    ibu = (uint64_t)p.order[i];
+                    if (d.src[i] >= 0) {
+                        const int32_t slot = c * Sc + d.slot_of[d.src[i]];
+                        src = latest[slot] * S + slot;
+                    } else {
+                        src = d.src[i];
+                    }
+                    own = d.slot_of[i] >= 0 ? c * Sc + d.slot_of[i] : -1;
+                    if (own >= 0) tp.p1len[t] = s + 1;
+                }
+                tp.meta[(size_t)t * K + s] = off | (ibu << 16) | ((uint64_t)(uint16_t)(int16_t)src << 32) |
+                                             ((uint64_t)(uint16_t)(int16_t)own << 48);
             }
-            tp.meta[(size_t)t * K + s] = off | (ibu << 16) | ((uint64_t)(uint16_t)(int16_t)src << 32) |
-                                         ((uint64_t)(uint16_t)(int16_t)own << 48);
         }
     return tp;
 }
