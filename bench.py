@@ -59,6 +59,8 @@ def parse_args(argv=None):
     ap.add_argument("--tile-ctas", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--tile-joints", type=int, default=0)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--output", type=int, default=0, help="1 = TMA bulk store, 2 = copy-out")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no checks, no e2e, no cpu baseline")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
@@ -236,7 +238,8 @@ def run_ours(args):
         J = len(par)
         ib = hsgen.inv_bind(ib_seed, J)
         c0, n = shard(n_total, rank, world, args.scaling)
-        sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints)
+        sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints,
+                         stages=args.stages, output=args.output)
         local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
         if n:
             rc = hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, c0, n, local.data_ptr(),
@@ -326,7 +329,9 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (no flush)", "algo": args.algo,
                    "per_launch_ms": {w["name"]: per_type_ms[t] for t, w in enumerate(work)},
                    "chunk": work[dom]["sk"].query("chunk"),
-                   "tile_chars": work[dom]["sk"].query("tile_chars")},
+                   "tile_chars": work[dom]["sk"].query("tile_chars"),
+                   "stages": {w["name"]: w["sk"].query("stages") for w in work},
+                   "output": work[dom]["sk"].query("output")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"chunked_kernel ({work[dom]['name']} launch)",

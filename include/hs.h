@@ -73,8 +73,11 @@ typedef struct {
                              0 = auto (1024)                                                  */
     int32_t force_split;  /* 1 = use the multi-CTA program even when one CTA would fit          */
     int32_t stages;       /* TMA load stages of the chunked kernel (2 or 3); 0 = auto           */
-    int32_t sbufs;        /* skin staging buffers (1 or 2); 0 = auto                            */
-    int32_t reserved[3];  /* must be zero                                                      */
+    int32_t sbufs;        /* skin staging buffers (1 or 2, TMA-store output only); 0 = auto     */
+    int32_t output;       /* chunked kernel output path: 0 = auto, 1 = TMA bulk stores issued by
+                             the producer warp, 2 = coalesced 512-byte-per-warp stores by the
+                             compute warps (frees the stage without waiting for the drain)    */
+    int32_t reserved[2];  /* must be zero                                                      */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -142,7 +145,8 @@ typedef enum {
     HS_Q_THREADS = 10,       /* threads per CTA of the chunked kernel (incl. producer warp)    */
     HS_Q_STAGES = 11,        /* TMA load stages                                                */
     HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
-    HS_Q_SPLIT_LEVELS = 13   /* recursion depth of the multi-CTA path (0 if single-CTA)         */
+    HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
+    HS_Q_OUTPUT = 14         /* chunked output path in use (1 = TMA bulk store, 2 = copy-out)   */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

@@ -54,7 +54,7 @@ struct hs_skeleton {
     int K = 7;
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
-    int stages = 0, sbufs = 0, threads = 0;
+    int stages = 0, sbufs = 0, threads = 0, output = 2;
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -105,7 +105,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.reserved[0] || o.reserved[1] || o.reserved[2])
+        o.output < 0 || o.output > 2 || o.reserved[0] || o.reserved[1])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -130,11 +130,17 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!(o.force_split && depth == 0) && C * TC <= max_threads && (int64_t)C * n <= 65535) {
         sk->tp = hs::build_tile_program(P, sk->K, C);
         const int want_stages = o.stages, want_sbufs = o.sbufs;
-        const int cand[][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
-        for (auto& c : cand) {
+        sk->output = o.output ? o.output : 2;
+        const int cand_tma[][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
+        const int cand_copy[][2] = {{4, 1}, {3, 1}, {2, 1}};
+        std::vector<std::pair<int, int>> cand;
+        if (sk->output == 1) for (auto& c : cand_tma) cand.emplace_back(c[0], c[1]);
+        else for (auto& c : cand_copy) cand.emplace_back(c[0], c[1]);
+        for (auto& cc : cand) {
+            const int c[2] = {cc.first, cc.second};
             if (want_stages && c[0] != want_stages) continue;
             if (want_sbufs && c[1] != want_sbufs) continue;
-            int64_t b = hs::tile_smem_bytes(sk->tp, c[0], c[1]);
+            int64_t b = hs::tile_smem_bytes(sk->tp, c[0], c[1], sk->output == 2);
             if (b <= smem_optin && 2 * sk->tp.nslots < 32768) {
                 sk->stages = c[0];
                 sk->sbufs = c[1];
@@ -228,6 +234,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
+            a.store_mode = sk->output == 1 ? 0 : 1;
             e = hs::launch_chunked(sk->K, a, st);
             break;
         }
@@ -362,6 +369,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_STAGES: *v = sk->stages; break;
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
+        case HS_Q_OUTPUT: *v = sk->output; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
     return HS_OK;

@@ -118,6 +118,16 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ void copy_out(float4* __restrict__ dst, const float4* __restrict__ src,
+                                         int nv, int t, int NC) {
+    int v = t;
+    for (; v + 3 * NC < nv; v += 4 * NC) {
+        const float4 x0 = src[v], x1 = src[v + NC], x2 = src[v + 2 * NC], x3 = src[v + 3 * NC];
+        dst[v] = x0; dst[v + NC] = x1; dst[v + 2 * NC] = x2; dst[v + 3 * NC] = x3;
+    }
+    for (; v < nv; v += NC) dst[v] = src[v];
+}
+
 // ================================================================== chunked kernel
 // Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
 // producer.  Per tile of C characters (F = C*J joints, user order in smem):
@@ -139,7 +149,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     float* LG = reinterpret_cast<float*>(smem + 128);
     const int64_t tile_f = (int64_t)a.F * 12;
     float* SB = LG + NS * tile_f;
-    float* P = SB + NSS * tile_f;
+    // TMA-store output: P has its own region.  Copy-out output: P lives in the S buffer
+    // (P is dead once phase 3a has read it; S is written only afterwards).
+    float* P = a.store_mode == 0 ? SB + NSS * tile_f : SB;
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
@@ -150,7 +162,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     const bool do_skin = a.sout != nullptr;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], a.store_mode == 0 ? 1 : (blockDim.x >> 5) - 1);
+        }
         for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
         fence_mbar_init();
     }
@@ -168,22 +183,33 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             mbar_expect_tx(&full[stage], bytes);
             bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
         };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
-        for (int64_t it = 0; it < my_tiles; ++it) {
-            const int stage = (int)(it % NS);
-            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
-            const int64_t tile = blockIdx.x + it * gridDim.x;
-            const int64_t c0 = tile * a.C;
-            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
-            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
-            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-            if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-            bulk_commit();
-            bulk_wait_read_all();                 // smem of this tile has been read out
-            if (do_skin) mbar_arrive(&sfree[it % NSS]);
-            if (it + NS < my_tiles) issue_load(it + NS);
+        if (a.store_mode == 0) {
+            // outputs leave through TMA bulk stores issued here
+            for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
+            for (int64_t it = 0; it < my_tiles; ++it) {
+                const int stage = (int)(it % NS);
+                mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
+                const int64_t tile = blockIdx.x + it * gridDim.x;
+                const int64_t c0 = tile * a.C;
+                const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
+                const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+                bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
+                if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+                bulk_commit();
+                bulk_wait_read_all();                 // smem of this tile has been read out
+                if (do_skin) mbar_arrive(&sfree[it % NSS]);
+                if (it + NS < my_tiles) issue_load(it + NS);
+            }
+            bulk_wait_all();
+        } else {
+            // outputs leave through the consumers' coalesced stores; refill as soon as a
+            // stage's copy-out is done (done[stage] counts one arrival per consumer warp)
+            for (int64_t it = 0; it < my_tiles; ++it) {
+                const int stage = (int)(it % NS);
+                if (it >= NS) mbar_wait(&done[stage], (uint32_t)(((it / NS) - 1) & 1));
+                issue_load(it);
+            }
         }
-        bulk_wait_all();
         return;
     }
 
@@ -214,6 +240,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         const int stage = (int)(it % NS);
         float* L = LG + stage * tile_f;
         mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
+        if (a.store_mode != 0 && it > 0) bar_consumers(NC);  // last tile's S copy-out done
 
         // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
         if (p1 > 0) {
@@ -257,9 +284,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             bar_consumers(NC);
         }
 
-        // phase 3: final fold, G in place, S into the S buffer
+        // phase 3: final fold, G in place (and, with TMA-store output, S into the S buffer)
         float* S = SB + (it % NSS) * tile_f;
-        if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
+        const bool fused_skin = do_skin && a.store_mode == 0;
+        if (fused_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
         {
             float acc[12];
 #pragma unroll
@@ -283,16 +311,47 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                     compose(pa, l, acc);
                 }
                 st3(L + off * 12, acc);
-                if (do_skin) {
+                if (fused_skin) {
                     float sk[12];
                     compose(acc, ibr[s], sk);
                     st3(S + off * 12, sk);
                 }
             }
         }
+        if (a.store_mode == 0) {
+            fence_proxy_async();
+            bar_consumers(NC);
+            if (t == 0) mbar_arrive(&done[stage]);
+            continue;
+        }
+        bar_consumers(NC);  // every P read done: the S buffer may now be overwritten
+        const int64_t tile = blockIdx.x + it * gridDim.x;
+        const int64_t c0 = tile * a.C;
+        const int nv = (int)(min((int64_t)a.C, a.n_chars - c0) * a.J * 3);
+        if (do_skin) {
+            // phase 3b: S = G (x) IB from this thread's own G (conflict-free re-read)
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int src = (int)(int16_t)(m[s] >> 32);
+                if (src == kSrcNone) continue;
+                const int off = (int)(m[s] & 0xffff);
+                float g[12], sk[12];
+                ld3(L + off * 12, g);
+                compose(g, ibr[s], sk);
+                st3(S + off * 12, sk);
+            }
+        }
+        // coalesced copy-out: 512 contiguous bytes per warp instruction
+        copy_out(reinterpret_cast<float4*>(a.gout + c0 * a.J * 12), reinterpret_cast<const float4*>(L),
+                 nv, t, NC);
+        if (do_skin) {
+            bar_consumers(NC);
+            copy_out(reinterpret_cast<float4*>(a.sout + c0 * a.J * 12),
+                     reinterpret_cast<const float4*>(S), nv, t, NC);
+        }
         fence_proxy_async();
-        bar_consumers(NC);
-        if (t == 0) mbar_arrive(&done[stage]);
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&done[stage]);
     }
 }
 
