@@ -77,7 +77,9 @@ typedef struct {
     int32_t output;       /* chunked kernel output path: 0 = auto, 1 = TMA bulk stores issued by
                              the producer warp, 2 = coalesced 512-byte-per-warp stores by the
                              compute warps (frees the stage without waiting for the drain)    */
-    int32_t reserved[2];  /* must be zero                                                      */
+    int32_t pbuf;         /* anchor buffer P: 2 = ping-pong (one barrier per round), 1 = single
+                             buffer (two barriers per round, half the shared memory); 0 = auto */
+    int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -146,7 +148,9 @@ typedef enum {
     HS_Q_STAGES = 11,        /* TMA load stages                                                */
     HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
-    HS_Q_OUTPUT = 14         /* chunked output path in use (1 = TMA bulk store, 2 = copy-out)   */
+    HS_Q_OUTPUT = 14,        /* chunked output path in use (1 = TMA bulk store, 2 = copy-out)   */
+    HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
+    HS_Q_SBUFS = 16          /* skin staging buffers of the chunked kernel                      */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

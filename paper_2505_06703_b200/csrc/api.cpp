@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -105,7 +106,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.output < 0 || o.output > 2 || o.reserved[0] || o.reserved[1])
+        o.output < 0 || o.output > 2 || o.pbuf < 0 || o.pbuf > 2 || o.reserved[0])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -128,20 +129,27 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     const int64_t TC = (n + sk->K - 1) / sk->K;  // compute threads per character
     while (C > 1 && C * TC > max_threads) --C;
     if (!(o.force_split && depth == 0) && C * TC <= max_threads && (int64_t)C * n <= 65535) {
-        sk->tp = hs::build_tile_program(P, sk->K, C);
         const int want_stages = o.stages, want_sbufs = o.sbufs;
-        sk->output = o.output ? o.output : 2;
-        const int cand_tma[][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
-        const int cand_copy[][2] = {{4, 1}, {3, 1}, {2, 1}};
-        std::vector<std::pair<int, int>> cand;
-        if (sk->output == 1) for (auto& c : cand_tma) cand.emplace_back(c[0], c[1]);
-        else for (auto& c : cand_copy) cand.emplace_back(c[0], c[1]);
-        for (auto& cc : cand) {
-            const int c[2] = {cc.first, cc.second};
+        sk->output = o.output ? o.output : 1;
+        // candidates in preference order: (stages, sbufs, ping-pong P)
+        std::vector<std::array<int, 3>> cand;
+        if (sk->output == 1)
+            cand = {{3, 2, 1}, {3, 2, 0}, {3, 1, 1}, {3, 1, 0}, {2, 2, 1}, {2, 2, 0}, {2, 1, 1}, {2, 1, 0}};
+        else
+            cand = {{4, 1, 1}, {3, 1, 1}, {2, 1, 1}};
+        const int nc_threads = (int)(((C * TC) + 31) / 32 * 32);
+        hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
+        hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
+        const bool single_ok = tp_sb.max_round_entries <= 4 * nc_threads;
+        for (auto& c : cand) {
             if (want_stages && c[0] != want_stages) continue;
             if (want_sbufs && c[1] != want_sbufs) continue;
-            int64_t b = hs::tile_smem_bytes(sk->tp, c[0], c[1], sk->output == 2);
-            if (b <= smem_optin && 2 * sk->tp.nslots < 32768) {
+            if (!c[2] && !single_ok) continue;
+            if (o.pbuf && (c[2] ? 2 : 1) != o.pbuf) continue;
+            const hs::TileProgram& tp = c[2] ? tp_pp : tp_sb;
+            int64_t b = hs::tile_smem_bytes(tp, c[0], c[1], sk->output == 2);
+            if (b <= smem_optin && 2 * tp.nslots < 32768) {
+                sk->tp = tp;
                 sk->stages = c[0];
                 sk->sbufs = c[1];
                 sk->smem = b;
@@ -235,6 +243,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
             a.store_mode = sk->output == 1 ? 0 : 1;
+            a.p_single = sk->tp.pingpong ? 0 : 1;
             e = hs::launch_chunked(sk->K, a, st);
             break;
         }
@@ -370,6 +379,8 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
         case HS_Q_OUTPUT: *v = sk->output; break;
+        case HS_Q_SBUFS: *v = sk->sbufs; break;
+        case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
     return HS_OK;
@@ -422,7 +433,7 @@ hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
         case HS_Q_ANCHORS: *v = (int64_t)p->decomp.slots.size(); break;
         case HS_Q_IDENTITY_ORDER: *v = p->plan.identity ? 1 : 0; break;
         case HS_Q_ANCHOR_ROUNDS: {
-            hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1);
+            hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1, true);
             *v = tp.R2;
             break;
         }

@@ -104,8 +104,9 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t 
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() {
@@ -194,11 +195,19 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
                 const uint32_t bytes = (uint32_t)(nc * a.J * 48);
                 bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-                if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-                bulk_commit();
-                bulk_wait_read_all();                 // smem of this tile has been read out
-                if (do_skin) mbar_arrive(&sfree[it % NSS]);
+                bulk_commit();                        // group: G of this tile
+                if (do_skin) {
+                    bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+                    bulk_commit();                    // group: S of this tile
+                    bulk_wait_read<1>();              // G read out (S may still drain)
+                } else {
+                    bulk_wait_read<0>();
+                }
                 if (it + NS < my_tiles) issue_load(it + NS);
+                if (do_skin) {
+                    bulk_wait_read<0>();
+                    mbar_arrive(&sfree[it % NSS]);
+                }
             }
             bulk_wait_all();
         } else {
@@ -268,20 +277,56 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         }
         bar_consumers(NC);
 
-        // phase 2: pointer jumping over anchors (snapshot semantics via ping-pong)
+        // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
+        // snapshot semantics: ping-pong P, or a single P with every read of a round
+        // before any of its writes (entries held in registers, <= 4 per thread)
         for (int r = 0; r < a.R2; ++r) {
-            const int e1 = __ldg(a.round_off + r + 1);
-            for (int e = __ldg(a.round_off + r) + t; e < e1; e += NC) {
-                const uint64_t w = __ldg(a.rounds + e);
-                const int dst = (int)(w & 0xffff), self = (int)((w >> 16) & 0xffff),
-                          link = (int)((w >> 32) & 0xffff);
-                float x[12], y[12], z[12];
-                ld3(P + link * 12, x);
-                ld3(P + self * 12, y);
-                compose(x, y, z);
-                st3(P + dst * 12, z);
+            const int eb = __ldg(a.round_off + r), e1 = __ldg(a.round_off + r + 1);
+            if (!a.p_single) {
+                int e = eb + t;
+                for (; e + NC < e1; e += 2 * NC) {   // two independent entries in flight
+                    const uint64_t w0 = __ldg(a.rounds + e), w1 = __ldg(a.rounds + e + NC);
+                    float x0[12], y0[12], z0[12], x1[12], y1[12], z1[12];
+                    ld3(P + ((w0 >> 32) & 0xffff) * 12, x0);
+                    ld3(P + ((w0 >> 16) & 0xffff) * 12, y0);
+                    ld3(P + ((w1 >> 32) & 0xffff) * 12, x1);
+                    ld3(P + ((w1 >> 16) & 0xffff) * 12, y1);
+                    compose(x0, y0, z0);
+                    compose(x1, y1, z1);
+                    st3(P + (w0 & 0xffff) * 12, z0);
+                    st3(P + (w1 & 0xffff) * 12, z1);
+                }
+                if (e < e1) {
+                    const uint64_t w = __ldg(a.rounds + e);
+                    float x[12], y[12], z[12];
+                    ld3(P + ((w >> 32) & 0xffff) * 12, x);
+                    ld3(P + ((w >> 16) & 0xffff) * 12, y);
+                    compose(x, y, z);
+                    st3(P + (w & 0xffff) * 12, z);
+                }
+                bar_consumers(NC);
+            } else {
+                float z[4][12];
+                int dst[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = eb + t + q * NC;
+                    dst[q] = -1;
+                    if (e < e1) {
+                        const uint64_t w = __ldg(a.rounds + e);
+                        float x[12], y[12];
+                        ld3(P + ((w >> 32) & 0xffff) * 12, x);
+                        ld3(P + ((w >> 16) & 0xffff) * 12, y);
+                        compose(x, y, z[q]);
+                        dst[q] = (int)(w & 0xffff);
+                    }
+                }
+                bar_consumers(NC);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (dst[q] >= 0) st3(P + dst[q] * 12, z[q]);
+                bar_consumers(NC);
             }
-            bar_consumers(NC);
         }
 
         // phase 3: final fold, G in place (and, with TMA-store output, S into the S buffer)

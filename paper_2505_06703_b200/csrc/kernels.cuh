@@ -24,6 +24,7 @@ struct ChunkedArgs {
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
     int32_t store_mode;        // 0 = TMA bulk stores by the producer, 1 = coalesced STG copy-out
+    int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute

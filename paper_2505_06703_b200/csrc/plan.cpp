@@ -103,7 +103,7 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K) {
     return d;
 }
 
-TileProgram build_tile_program(const Plan& p, int K, int C) {
+TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
     // Chunks never straddle characters: every character of a tile runs the same
     // program (same association order), so a character's bits do not depend on
     // its position in the batch, the tile size or the GPU count.
@@ -116,6 +116,7 @@ TileProgram build_tile_program(const Plan& p, int K, int C) {
     tp.C = C;
     tp.F = C * n;
     tp.T = C * TC;
+    tp.pingpong = pingpong;
     const int32_t S = C * Sc;
     tp.nslots = S;
     // pointer-jumping rounds over the tile's anchor forest (C disjoint copies), ping-pong P
@@ -127,17 +128,23 @@ TileProgram build_tile_program(const Plan& p, int K, int C) {
         bool any = false;
         for (int32_t s = 0; s < S; ++s) if (lk[s] >= 0) { any = true; break; }
         if (!any) break;
+        int32_t n_r = 0;
         for (int32_t s = 0; s < S; ++s) {
             if (lk[s] < 0) continue;
-            uint64_t dst = (uint64_t)(((r + 1) & 1) * S + s);
+            // ping-pong: read buffer `latest`, write the other; single buffer: all reads of
+            // a round precede its writes (two barriers), so every location is the slot.
+            const int32_t wbuf = pingpong ? ((r + 1) & 1) : 0;
+            uint64_t dst = (uint64_t)(wbuf * S + s);
             uint64_t self = (uint64_t)(latest[s] * S + s);
             uint64_t link = (uint64_t)(latest[lk[s]] * S + lk[s]);
             tp.rounds.push_back(dst | (self << 16) | (link << 32));
+            ++n_r;
         }
+        tp.max_round_entries = std::max(tp.max_round_entries, n_r);
         std::vector<int32_t> nl(S, -1);
         for (int32_t s = 0; s < S; ++s) {
             if (lk[s] < 0) continue;
-            latest[s] = (r + 1) & 1;
+            latest[s] = pingpong ? ((r + 1) & 1) : 0;
             nl[s] = lk[lk[s]];
         }
         lk.swap(nl);
@@ -204,7 +211,7 @@ void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vec
 }
 
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs, bool p_in_sbuf) {
-    const int64_t tileb = (int64_t)tp.F * 48, pb = 2LL * tp.nslots * 48;
+    const int64_t tileb = (int64_t)tp.F * 48, pb = (tp.pingpong ? 2LL : 1LL) * tp.nslots * 48;
     if (p_in_sbuf) return 128 + (int64_t)stages * tileb + std::max(tileb, pb);
     return 128 + (int64_t)stages * tileb + (int64_t)sbufs * tileb + pb;
 }

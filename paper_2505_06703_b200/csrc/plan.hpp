@@ -42,6 +42,8 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K);
 struct TileProgram {
     int K = 0, C = 0, F = 0, T = 0;     // chunk, chars per tile, joints per tile, compute threads
     int nslots = 0, R2 = 0;             // anchor slots per tile, pointer-jumping rounds
+    bool pingpong = true;               // P double-buffered (else: 2 barriers per round)
+    int max_round_entries = 0;          // largest round (single buffer needs <= 4 per thread)
     std::vector<uint64_t> meta;         // [T][K]: off | ibu<<16 | (u16)src<<32 | (u16)own<<48
     std::vector<int32_t> p1len;         // [T]: phase-1 length (last own anchor + 1)
     std::vector<int32_t> round_off;     // [R2 + 1] offsets into rounds
@@ -72,7 +74,7 @@ struct Plan {
 // Returns 0 (HS_OK) or an hs_status code; err gets a message.
 int build_plan(const int32_t* parents, int32_t n, Plan& out, std::string& err);
 
-TileProgram build_tile_program(const Plan& p, int K, int C);
+TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong);
 SplitProgram build_split_program(const Plan& p, int K);
 
 // The paper's block layout for block size B over INTERNAL positions (exports).
