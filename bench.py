@@ -60,7 +60,7 @@ def parse_args(argv=None):
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--tile-joints", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
-    ap.add_argument("--output", type=int, default=0, help="1 = TMA bulk store, 2 = copy-out")
+    ap.add_argument("--ib", type=int, default=0, help="inverse bind: 1 = smem, 2 = L1/L2")
     ap.add_argument("--sbufs", type=int, default=0)
     ap.add_argument("--pbuf", type=int, default=0)
     ap.add_argument("--profile", action="store_true",
@@ -241,7 +241,7 @@ def run_ours(args):
         ib = hsgen.inv_bind(ib_seed, J)
         c0, n = shard(n_total, rank, world, args.scaling)
         sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints,
-                         stages=args.stages, output=args.output, sbufs=args.sbufs,
+                         stages=args.stages, ib_placement=args.ib, sbufs=args.sbufs,
                          pbuf=args.pbuf)
         local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
         if n:
@@ -336,7 +336,7 @@ def run_ours(args):
                    "stages": {w["name"]: w["sk"].query("stages") for w in work},
                    "sbufs": {w["name"]: w["sk"].query("sbufs") for w in work},
                    "pbufs": {w["name"]: w["sk"].query("pbufs") for w in work},
-                   "output": work[dom]["sk"].query("output")},
+                   "ib_placement": {w["name"]: w["sk"].query("ib_placement") for w in work}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"chunked_kernel ({work[dom]['name']} launch)",

@@ -73,10 +73,9 @@ typedef struct {
                              0 = auto (1024)                                                  */
     int32_t force_split;  /* 1 = use the multi-CTA program even when one CTA would fit          */
     int32_t stages;       /* TMA load stages of the chunked kernel (2 or 3); 0 = auto           */
-    int32_t sbufs;        /* skin staging buffers (1 or 2, TMA-store output only); 0 = auto     */
-    int32_t output;       /* chunked kernel output path: 0 = auto, 1 = TMA bulk stores issued by
-                             the producer warp, 2 = coalesced 512-byte-per-warp stores by the
-                             compute warps (frees the stage without waiting for the drain)    */
+    int32_t sbufs;        /* skin staging buffers (1 or 2); 0 = auto                            */
+    int32_t ib_placement; /* inverse bind for the epilogue: 1 = staged in shared memory, 2 = read
+                             through L1/L2; 0 = auto (shared memory when it fits)             */
     int32_t pbuf;         /* anchor buffer P: 2 = ping-pong (one barrier per round), 1 = single
                              buffer (two barriers per round, half the shared memory); 0 = auto */
     int32_t reserved[1];  /* must be zero                                                      */
@@ -148,7 +147,7 @@ typedef enum {
     HS_Q_STAGES = 11,        /* TMA load stages                                                */
     HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
-    HS_Q_OUTPUT = 14,        /* chunked output path in use (1 = TMA bulk store, 2 = copy-out)   */
+    HS_Q_IB_PLACEMENT = 14,  /* chunked kernel: 1 = inverse bind in smem, 2 = via L1/L2          */
     HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
     HS_Q_SBUFS = 16          /* skin staging buffers of the chunked kernel                      */
 } hs_query;

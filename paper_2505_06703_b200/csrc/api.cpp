@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
@@ -55,7 +56,7 @@ struct hs_skeleton {
     int K = 7;
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
-    int stages = 0, sbufs = 0, threads = 0, output = 2;
+    int stages = 0, sbufs = 0, threads = 0, ib_smem = 0;
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -106,7 +107,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.output < 0 || o.output > 2 || o.pbuf < 0 || o.pbuf > 2 || o.reserved[0])
+        o.ib_placement < 0 || o.ib_placement > 2 || o.pbuf < 0 || o.pbuf > 2 || o.reserved[0])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -129,29 +130,28 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     const int64_t TC = (n + sk->K - 1) / sk->K;  // compute threads per character
     while (C > 1 && C * TC > max_threads) --C;
     if (!(o.force_split && depth == 0) && C * TC <= max_threads && (int64_t)C * n <= 65535) {
-        const int want_stages = o.stages, want_sbufs = o.sbufs;
-        sk->output = o.output ? o.output : 1;
-        // candidates in preference order: (stages, sbufs, ping-pong P)
-        std::vector<std::array<int, 3>> cand;
-        if (sk->output == 1)
-            cand = {{3, 2, 1}, {3, 2, 0}, {3, 1, 1}, {3, 1, 0}, {2, 2, 1}, {2, 2, 0}, {2, 1, 1}, {2, 1, 0}};
-        else
-            cand = {{4, 1, 1}, {3, 1, 1}, {2, 1, 1}};
+        // candidates in preference order: (stages, sbufs, ping-pong P, IB in smem)
+        std::vector<std::array<int, 4>> cand;
+        for (int ibs : {1, 0})
+            for (auto ss : {std::array<int, 2>{3, 2}, {3, 1}, {2, 2}, {2, 1}})
+                for (int pp : {1, 0}) cand.push_back({ss[0], ss[1], pp, ibs});
         const int nc_threads = (int)(((C * TC) + 31) / 32 * 32);
         hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
         hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
         const bool single_ok = tp_sb.max_round_entries <= 4 * nc_threads;
         for (auto& c : cand) {
-            if (want_stages && c[0] != want_stages) continue;
-            if (want_sbufs && c[1] != want_sbufs) continue;
-            if (!c[2] && !single_ok) continue;
+            if (o.stages && c[0] != o.stages) continue;
+            if (o.sbufs && c[1] != o.sbufs) continue;
             if (o.pbuf && (c[2] ? 2 : 1) != o.pbuf) continue;
+            if (o.ib_placement && (c[3] ? 1 : 2) != o.ib_placement) continue;
+            if (!c[2] && !single_ok) continue;
             const hs::TileProgram& tp = c[2] ? tp_pp : tp_sb;
-            int64_t b = hs::tile_smem_bytes(tp, c[0], c[1], sk->output == 2);
+            const int64_t b = hs::tile_smem_bytes(tp, c[0], c[1]) + (c[3] ? (int64_t)n * 48 : 0);
             if (b <= smem_optin && 2 * tp.nslots < 32768) {
                 sk->tp = tp;
                 sk->stages = c[0];
                 sk->sbufs = c[1];
+                sk->ib_smem = c[3];
                 sk->smem = b;
                 sk->chunked = true;
                 break;
@@ -242,9 +242,25 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
-            a.store_mode = sk->output == 1 ? 0 : 1;
+            a.ib_smem = sk->ib_smem;
             a.p_single = sk->tp.pingpong ? 0 : 1;
+            a.prof = nullptr;
+            if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
+                cudaMalloc(reinterpret_cast<void**>(&a.prof), 6 * sizeof(unsigned long long));
+                cudaMemsetAsync(a.prof, 0, 6 * sizeof(unsigned long long), st);
+            }
             e = hs::launch_chunked(sk->K, a, st);
+            if (a.prof) {
+                unsigned long long h[6];
+                cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                const double n = h[5] ? (double)h[5] : 1.0;
+                std::fprintf(stderr,
+                             "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f phase1 %.0f phase2 %.0f "
+                             "wait_sbuf %.0f phase3 %.0f\n",
+                             J, h[5], h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n);
+                cudaFree(a.prof);
+            }
             break;
         }
         case HS_ALGO_DOUBLING:
@@ -378,7 +394,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_STAGES: *v = sk->stages; break;
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
-        case HS_Q_OUTPUT: *v = sk->output; break;
+        case HS_Q_IB_PLACEMENT: *v = sk->chunked ? (sk->ib_smem ? 1 : 2) : 0; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");

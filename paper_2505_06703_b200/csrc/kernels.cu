@@ -119,27 +119,19 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-__device__ __forceinline__ void copy_out(float4* __restrict__ dst, const float4* __restrict__ src,
-                                         int nv, int t, int NC) {
-    int v = t;
-    for (; v + 3 * NC < nv; v += 4 * NC) {
-        const float4 x0 = src[v], x1 = src[v + NC], x2 = src[v + 2 * NC], x3 = src[v + 3 * NC];
-        dst[v] = x0; dst[v + NC] = x1; dst[v + 2 * NC] = x2; dst[v + 3 * NC] = x3;
-    }
-    for (; v < nv; v += NC) dst[v] = src[v];
-}
-
 // ================================================================== chunked kernel
 // Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
-// producer.  Per tile of C characters (F = C*J joints, user order in smem):
+// producer (bulk loads of the tile's local poses, bulk stores of G and S).
+// Per tile of C characters (F = C*J joints, user order in smem):
 //   phase 1  each compute thread folds its chunk of K consecutive internal
 //            positions left-to-right (in-chunk parent = previous position) and
 //            publishes the running product at anchor joints into P;
-//   phase 2  pointer jumping (Alg. 2) over the anchor forest, ping-pong P;
+//   phase 2  pointer jumping (Alg. 2) over the anchor forest;
 //   phase 3  each thread re-folds its chunk starting from the final P of each
-//            segment head's parent, writes G in place over L, and S = G (x) IB
-//            (IB held in registers) into the S buffer;
-// then the producer bulk-stores G and S and refills the stage.
+//            segment head's parent, writes G in place over L and S = G (x) IB
+//            into the S buffer.
+// Both folds load the whole chunk up front and select instead of branching, so
+// the K dependent composes run back to back (no smem round trip between them).
 template <int K>
 __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -150,23 +142,18 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     float* LG = reinterpret_cast<float*>(smem + 128);
     const int64_t tile_f = (int64_t)a.F * 12;
     float* SB = LG + NS * tile_f;
-    // TMA-store output: P has its own region.  Copy-out output: P lives in the S buffer
-    // (P is dead once phase 3a has read it; S is written only afterwards).
-    float* P = a.store_mode == 0 ? SB + NSS * tile_f : SB;
+    float* P = SB + NSS * tile_f;
+    float* IBs = P + (a.p_single ? 1 : 2) * a.nslots * 12;   // used when a.ib_smem
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
     const int warp = threadIdx.x >> 5;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    const int64_t my_tiles =
-        blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const bool do_skin = a.sout != nullptr;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&done[s], a.store_mode == 0 ? 1 : (blockDim.x >> 5) - 1);
-        }
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
         for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
         fence_mbar_init();
     }
@@ -177,58 +164,41 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         if ((threadIdx.x & 31) != 0) return;
         auto issue_load = [&](int64_t it) {
             const int stage = (int)(it % NS);
-            const int64_t tile = blockIdx.x + it * gridDim.x;
-            const int64_t c0 = tile * a.C;
-            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
-            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
             mbar_expect_tx(&full[stage], bytes);
             bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
         };
-        if (a.store_mode == 0) {
-            // outputs leave through TMA bulk stores issued here
-            for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
-            for (int64_t it = 0; it < my_tiles; ++it) {
-                const int stage = (int)(it % NS);
-                mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
-                const int64_t tile = blockIdx.x + it * gridDim.x;
-                const int64_t c0 = tile * a.C;
-                const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
-                const uint32_t bytes = (uint32_t)(nc * a.J * 48);
-                bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-                bulk_commit();                        // group: G of this tile
-                if (do_skin) {
-                    bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-                    bulk_commit();                    // group: S of this tile
-                    bulk_wait_read<1>();              // G read out (S may still drain)
-                } else {
-                    bulk_wait_read<0>();
-                }
-                if (it + NS < my_tiles) issue_load(it + NS);
-                if (do_skin) {
-                    bulk_wait_read<0>();
-                    mbar_arrive(&sfree[it % NSS]);
-                }
+        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
+        for (int64_t it = 0; it < my_tiles; ++it) {
+            const int stage = (int)(it % NS);
+            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
+            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
+            bulk_commit();                            // group: G of this tile
+            if (do_skin) {
+                bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+                bulk_commit();                        // group: S of this tile
+                bulk_wait_read<1>();                  // G read out (S may still drain)
+            } else {
+                bulk_wait_read<0>();
             }
-            bulk_wait_all();
-        } else {
-            // outputs leave through the consumers' coalesced stores; refill as soon as a
-            // stage's copy-out is done (done[stage] counts one arrival per consumer warp)
-            for (int64_t it = 0; it < my_tiles; ++it) {
-                const int stage = (int)(it % NS);
-                if (it >= NS) mbar_wait(&done[stage], (uint32_t)(((it / NS) - 1) & 1));
-                issue_load(it);
+            if (it + NS < my_tiles) issue_load(it + NS);
+            if (do_skin) {
+                bulk_wait_read<0>();
+                mbar_arrive(&sfree[it % NSS]);
             }
         }
+        bulk_wait_all();
         return;
     }
 
     // ---------------------------------------------------------------- consumers
     const int t = threadIdx.x;
-    const bool active = t < a.T;
     uint64_t m[K];
-    float ibr[K][12];
     int p1 = 0;
-    if (active) {
+    if (t < a.T) {
         p1 = a.p1len[t];
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
@@ -236,46 +206,57 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
     }
-    if (do_skin) {
-#pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const int src = (int)(int16_t)(m[s] >> 32);
-            const int ibu = (int)((m[s] >> 16) & 0xffff);
-            if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
-        }
+    if (do_skin && a.ib_smem) {   // the skeleton's inverse bind, shared by every tile
+        const float4* src = reinterpret_cast<const float4*>(a.ib);
+        float4* dst = reinterpret_cast<float4*>(IBs);
+        for (int v = t; v < a.J * 3; v += NC) dst[v] = __ldg(src + v);
     }
+    bar_consumers(NC);
 
+    // debug phase profile (HS_DEBUG_PROF): consumer thread 0 accumulates clock64 deltas
+    long long prof_last = 0;
+    auto prof_mark = [&](int slot) {
+        if (a.prof && t == 0) {
+            const long long now = clock64();
+            if (slot >= 0) atomicAdd(a.prof + slot, (unsigned long long)(now - prof_last));
+            prof_last = now;
+        }
+    };
     for (int64_t it = 0; it < my_tiles; ++it) {
         const int stage = (int)(it % NS);
         float* L = LG + stage * tile_f;
+        prof_mark(-1);
         mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
-        if (a.store_mode != 0 && it > 0) bar_consumers(NC);  // last tile's S copy-out done
+        prof_mark(0);
 
-        // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
+        // phase 1: in-chunk fold, publish anchors (location = slot)
         if (p1 > 0) {
+            float l[K][12];
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                if (s < p1) ld3(L + (int)(m[s] & 0xffff) * 12, l[s]);
             float acc[12];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 if (s < p1) {
-                    const int off = (int)(m[s] & 0xffff);
                     const int src = (int)(int16_t)(m[s] >> 32);
                     const int own = (int)(int16_t)(m[s] >> 48);
-                    float l[12];
-                    ld3(L + off * 12, l);
-                    if (src == kSrcPrev) {
-                        float tmp[12];
-                        compose(acc, l, tmp);
+                    if (s == 0) {
 #pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                        for (int e = 0; e < 12; ++e) acc[e] = l[0][e];
                     } else {
+                        float c[12];
+                        compose(acc, l[s], c);
+                        const bool prev = src == kSrcPrev;
 #pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                        for (int e = 0; e < 12; ++e) acc[e] = prev ? c[e] : l[s][e];
                     }
                     if (own >= 0) st3(P + own * 12, acc);
                 }
             }
         }
         bar_consumers(NC);
+        prof_mark(1);
 
         // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
         // snapshot semantics: ping-pong P, or a single P with every read of a round
@@ -329,74 +310,52 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             }
         }
 
-        // phase 3: final fold, G in place (and, with TMA-store output, S into the S buffer)
+        // phase 3: final fold; G in place over L, S = G (x) IB into the S buffer
+        prof_mark(2);
         float* S = SB + (it % NSS) * tile_f;
-        const bool fused_skin = do_skin && a.store_mode == 0;
-        if (fused_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
+        if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
+        prof_mark(3);
         {
-            float acc[12];
+            // one-joint-ahead prefetch: the next L is loaded before this joint's stores
+            float lnext[12], acc[12];
+            if ((int)(int16_t)(m[0] >> 32) != kSrcNone) ld3(L + (int)(m[0] & 0xffff) * 12, lnext);
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;
+                if (src == kSrcNone) continue;   // only trailing positions of a thread
                 const int off = (int)(m[s] & 0xffff);
                 float l[12];
-                ld3(L + off * 12, l);
-                if (src == kSrcPrev) {
-                    float tmp[12];
-                    compose(acc, l, tmp);
 #pragma unroll
-                    for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
-                } else if (src == kSrcRoot) {
-#pragma unroll
-                    for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                } else {
-                    float pa[12];
-                    ld3(P + src * 12, pa);
-                    compose(pa, l, acc);
+                for (int e = 0; e < 12; ++e) l[e] = lnext[e];
+                if (s + 1 < K && (int)(int16_t)(m[s + 1] >> 32) != kSrcNone)
+                    ld3(L + (int)(m[s + 1] & 0xffff) * 12, lnext);
+                float base[12], c[12];
+                if (src >= 0) ld3(P + src * 12, base);   // segment head: parent's final
+                const int ibu = (int)((m[s] >> 16) & 0xffff);
+                float ib[12];
+                if (do_skin) {
+                    if (a.ib_smem) ld3(IBs + ibu * 12, ib);
+                    else ldg3(a.ib + (int64_t)ibu * 12, ib);
                 }
+                const bool prev = src == kSrcPrev, root = src == kSrcRoot;
+#pragma unroll
+                for (int e = 0; e < 12; ++e) base[e] = prev ? acc[e] : base[e];
+                compose(base, l, c);
+#pragma unroll
+                for (int e = 0; e < 12; ++e) acc[e] = root ? l[e] : c[e];
                 st3(L + off * 12, acc);
-                if (fused_skin) {
+                if (do_skin) {
                     float sk[12];
-                    compose(acc, ibr[s], sk);
+                    compose(acc, ib, sk);
                     st3(S + off * 12, sk);
                 }
             }
         }
-        if (a.store_mode == 0) {
-            fence_proxy_async();
-            bar_consumers(NC);
-            if (t == 0) mbar_arrive(&done[stage]);
-            continue;
-        }
-        bar_consumers(NC);  // every P read done: the S buffer may now be overwritten
-        const int64_t tile = blockIdx.x + it * gridDim.x;
-        const int64_t c0 = tile * a.C;
-        const int nv = (int)(min((int64_t)a.C, a.n_chars - c0) * a.J * 3);
-        if (do_skin) {
-            // phase 3b: S = G (x) IB from this thread's own G (conflict-free re-read)
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;
-                const int off = (int)(m[s] & 0xffff);
-                float g[12], sk[12];
-                ld3(L + off * 12, g);
-                compose(g, ibr[s], sk);
-                st3(S + off * 12, sk);
-            }
-        }
-        // coalesced copy-out: 512 contiguous bytes per warp instruction
-        copy_out(reinterpret_cast<float4*>(a.gout + c0 * a.J * 12), reinterpret_cast<const float4*>(L),
-                 nv, t, NC);
-        if (do_skin) {
-            bar_consumers(NC);
-            copy_out(reinterpret_cast<float4*>(a.sout + c0 * a.J * 12),
-                     reinterpret_cast<const float4*>(S), nv, t, NC);
-        }
         fence_proxy_async();
-        __syncwarp();
-        if ((t & 31) == 0) mbar_arrive(&done[stage]);
+        bar_consumers(NC);
+        if (t == 0) mbar_arrive(&done[stage]);
+        prof_mark(4);
+        if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
     }
 }
 

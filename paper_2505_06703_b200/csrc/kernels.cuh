@@ -23,8 +23,9 @@ struct ChunkedArgs {
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
-    int32_t store_mode;        // 0 = TMA bulk stores by the producer, 1 = coalesced STG copy-out
+    int32_t ib_smem;           // 1 = inverse bind staged in shared memory, 0 = read through L1/L2
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
+    unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute

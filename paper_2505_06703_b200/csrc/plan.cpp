@@ -210,9 +210,8 @@ void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vec
     }
 }
 
-int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs, bool p_in_sbuf) {
+int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs) {
     const int64_t tileb = (int64_t)tp.F * 48, pb = (tp.pingpong ? 2LL : 1LL) * tp.nslots * 48;
-    if (p_in_sbuf) return 128 + (int64_t)stages * tileb + std::max(tileb, pb);
     return 128 + (int64_t)stages * tileb + (int64_t)sbufs * tileb + pb;
 }
 

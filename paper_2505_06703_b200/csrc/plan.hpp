@@ -80,8 +80,8 @@ SplitProgram build_split_program(const Plan& p, int K);
 // The paper's block layout for block size B over INTERNAL positions (exports).
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);
 
-// Shared-memory bytes of the chunked kernel for a tile program and stage counts;
-// p_in_sbuf: the copy-out output path keeps P inside the (single) S buffer.
-int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs, bool p_in_sbuf);
+// Shared-memory bytes of the chunked kernel for a tile program and stage counts
+// (without the optional inverse-bind copy, J * 48 bytes).
+int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs);
 
 }  // namespace hs
