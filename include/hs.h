@@ -78,7 +78,8 @@ typedef struct {
                              through L1/L2; 0 = auto (shared memory when it fits)             */
     int32_t pbuf;         /* anchor buffer P: 2 = ping-pong (one barrier per round), 1 = single
                              buffer (two barriers per round, half the shared memory); 0 = auto */
-    int32_t reserved[1];  /* must be zero                                                      */
+    int32_t kernel;       /* chunked kernel variant: 1 = row-parallel (three lanes per chunk, lane q
+                             owns row q), 2 = one thread per chunk; 0 = auto (1)              */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -149,7 +150,8 @@ typedef enum {
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
     HS_Q_IB_PLACEMENT = 14,  /* chunked kernel: 1 = inverse bind in smem, 2 = via L1/L2          */
     HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
-    HS_Q_SBUFS = 16          /* skin staging buffers of the chunked kernel                      */
+    HS_Q_SBUFS = 16,         /* skin staging buffers of the chunked kernel                      */
+    HS_Q_KERNEL = 17         /* chunked kernel variant (1 row-parallel, 2 thread per chunk)     */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

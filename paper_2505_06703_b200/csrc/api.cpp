@@ -57,6 +57,7 @@ struct hs_skeleton {
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
     int stages = 0, sbufs = 0, threads = 0, ib_smem = 0;
+    bool rows = true;              // row-parallel kernel (3 lanes per chunk)
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -107,7 +108,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.ib_placement < 0 || o.ib_placement > 2 || o.pbuf < 0 || o.pbuf > 2 || o.reserved[0])
+        o.ib_placement < 0 || o.ib_placement > 2 || o.pbuf < 0 || o.pbuf > 2 || o.kernel < 0 || o.kernel > 2)
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -135,10 +136,11 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         for (int ibs : {1, 0})
             for (auto ss : {std::array<int, 2>{3, 2}, {3, 1}, {2, 2}, {2, 1}})
                 for (int pp : {1, 0}) cand.push_back({ss[0], ss[1], pp, ibs});
-        const int nc_threads = (int)(((C * TC) + 31) / 32 * 32);
+        // phase-2 workers: rows kernel = 3-lane groups (10 per warp), else threads
+        const int workers = sk->rows ? (int)((C * TC + 9) / 10 * 10) : (int)(((C * TC) + 31) / 32 * 32);
         hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
         hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
-        const bool single_ok = tp_sb.max_round_entries <= 4 * nc_threads;
+        const bool single_ok = tp_sb.max_round_entries <= 4 * workers;
         for (auto& c : cand) {
             if (o.stages && c[0] != o.stages) continue;
             if (o.sbufs && c[1] != o.sbufs) continue;
@@ -194,7 +196,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     }
     if (sk->chunked) {
         const hs::TileProgram& tp = sk->tp;
-        sk->threads = ((tp.T + 31) / 32) * 32 + 32;
+        sk->threads = sk->rows ? ((tp.T + 9) / 10) * 32 + 32 : ((tp.T + 31) / 32) * 32 + 32;
         if ((e = upload(&sk->d_meta, tp.meta.data(), tp.meta.size())) != cudaSuccess ||
             (e = upload(&sk->d_p1len, tp.p1len.data(), tp.p1len.size())) != cudaSuccess ||
             (e = upload(&sk->d_round_off, tp.round_off.data(), tp.round_off.size())) != cudaSuccess ||
@@ -243,6 +245,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
             a.ib_smem = sk->ib_smem;
+            a.rows = sk->rows ? 1 : 0;
             a.p_single = sk->tp.pingpong ? 0 : 1;
             a.prof = nullptr;
             if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
@@ -396,6 +399,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
         case HS_Q_IB_PLACEMENT: *v = sk->chunked ? (sk->ib_smem ? 1 : 2) : 0; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
+        case HS_Q_KERNEL: *v = sk->chunked ? (sk->rows ? 1 : 2) : 0; break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
