@@ -145,9 +145,9 @@ class Plan:
         return out.reshape(-1, self.n) if what == "lift" else out
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().hs_plan_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hs_plan_destroy(self._h)
+        self._h = None
 
     __del__ = close
 
@@ -221,9 +221,9 @@ class Skeleton:
         return g, s
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().hs_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hs_destroy(self._h)
+        self._h = None
 
     __del__ = close
 
@@ -247,9 +247,9 @@ class Pipeline:
                                   ptr(h_skin)), "hs_scan_host")
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().hs_pipeline_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hs_pipeline_destroy(self._h)
+        self._h = None
 
     __del__ = close
 

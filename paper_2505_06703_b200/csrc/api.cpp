@@ -127,10 +127,13 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     // --- chunked (single-CTA) program: C characters per tile, ~tile_target joints
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
-    const int max_threads = 224;  // compute threads per CTA (launch bounds 256 incl. producer)
-    const int64_t TC = (n + sk->K - 1) / sk->K;  // compute threads per character
-    while (C > 1 && C * TC > max_threads) --C;
-    if (!(o.force_split && depth == 0) && C * TC <= max_threads && (int64_t)C * n <= 65535) {
+    const int64_t TC = (n + sk->K - 1) / sk->K;  // chunks per character
+    sk->rows = o.kernel != 2;
+    // chunks per CTA: rows kernel 10 per warp and <= 15 compute warps (launch bounds 512 with
+    // the producer warp); thread-per-chunk kernel <= 224 threads (launch bounds 256)
+    const int max_chunks = sk->rows ? 150 : 224;
+    while (C > 1 && C * TC > max_chunks) --C;
+    if (!(o.force_split && depth == 0) && C * TC <= max_chunks && (int64_t)C * n <= 65535) {
         // candidates in preference order: (stages, sbufs, ping-pong P, IB in smem)
         std::vector<std::array<int, 4>> cand;
         for (int ibs : {1, 0})
@@ -253,6 +256,12 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 cudaMemsetAsync(a.prof, 0, 6 * sizeof(unsigned long long), st);
             }
             e = hs::launch_chunked(sk->K, a, st);
+            if (e != cudaSuccess) {
+                char buf[256];
+                std::snprintf(buf, sizeof(buf), "chunked launch (K=%d rows=%d threads=%d smem=%lld stages=%d sbufs=%d)",
+                              sk->K, a.rows, a.threads, (long long)a.smem_bytes, a.stages, a.sbufs);
+                return cuda_fail(e, buf);
+            }
             if (a.prof) {
                 unsigned long long h[6];
                 cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);

@@ -567,15 +567,16 @@ __global__ void __launch_bounds__(512, 1) rows_kernel(const ChunkedArgs a) {
             float acc[4];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
+                // every lane runs every step (the __syncwarp below needs the full warp)
                 const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;
+                const bool valid = src != kSrcNone;
                 const int off = (int)(m[s] & 0xffff);
                 float l[12], base[4], c[4];
-                ld3(L + off * 12, l);
+                if (valid) ld3(L + off * 12, l);
                 if (src >= 0) ld4(P + src * 12 + 4 * q, base);
                 float ib[12];
                 const int ibu = (int)((m[s] >> 16) & 0xffff);
-                if (do_skin) {
+                if (do_skin && valid) {
                     if (a.ib_smem) ld3(IBs + ibu * 12, ib);
                     else ldg3(a.ib + (int64_t)ibu * 12, ib);
                 }
@@ -587,11 +588,13 @@ __global__ void __launch_bounds__(512, 1) rows_kernel(const ChunkedArgs a) {
                 for (int e = 0; e < 4; ++e)
                     acc[e] = root ? (q == 0 ? l[e] : (q == 1 ? l[4 + e] : l[8 + e])) : c[e];
                 __syncwarp();   // the chunk's three lanes have read L[off] before it is overwritten
-                st4(L + off * 12 + 4 * q, acc);
-                if (do_skin) {
-                    float sk[4];
-                    rowmul(acc, ib, sk);
-                    st4(S + off * 12 + 4 * q, sk);
+                if (valid) {
+                    st4(L + off * 12 + 4 * q, acc);
+                    if (do_skin) {
+                        float sk[4];
+                        rowmul(acc, ib, sk);
+                        st4(S + off * 12 + 4 * q, sk);
+                    }
                 }
             }
         }
