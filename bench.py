@@ -60,10 +60,8 @@ def parse_args(argv=None):
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--tile-joints", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
-    ap.add_argument("--ib", type=int, default=0, help="inverse bind: 1 = smem, 2 = L1/L2")
     ap.add_argument("--sbufs", type=int, default=0)
     ap.add_argument("--pbuf", type=int, default=0)
-    ap.add_argument("--kernel", type=int, default=0, help="1 = row-parallel, 2 = thread per chunk")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no checks, no e2e, no cpu baseline")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
@@ -242,8 +240,7 @@ def run_ours(args):
         ib = hsgen.inv_bind(ib_seed, J)
         c0, n = shard(n_total, rank, world, args.scaling)
         sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints,
-                         stages=args.stages, ib_placement=args.ib, sbufs=args.sbufs,
-                         pbuf=args.pbuf, kernel=args.kernel)
+                         stages=args.stages, sbufs=args.sbufs, pbuf=args.pbuf)
         local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
         if n:
             rc = hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, c0, n, local.data_ptr(),
@@ -336,9 +333,7 @@ def run_ours(args):
                    "tile_chars": work[dom]["sk"].query("tile_chars"),
                    "stages": {w["name"]: w["sk"].query("stages") for w in work},
                    "sbufs": {w["name"]: w["sk"].query("sbufs") for w in work},
-                   "pbufs": {w["name"]: w["sk"].query("pbufs") for w in work},
-                   "kernel": work[dom]["sk"].query("kernel"),
-                   "ib_placement": {w["name"]: w["sk"].query("ib_placement") for w in work}},
+                   "pbufs": {w["name"]: w["sk"].query("pbufs") for w in work}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"chunked_kernel ({work[dom]['name']} launch)",

@@ -68,18 +68,15 @@ hs_status hs_skeleton_create(const int32_t* parents, int32_t n_joints, const flo
 
 /* Creation options (hs_skeleton_create uses all-zero = automatic). */
 typedef struct {
-    int32_t chunk;        /* K, joints per thread chunk: odd in 3..15; 0 = auto (7)            */
+    int32_t chunk;        /* K, joints per thread chunk: odd in 3..11; 0 = auto (7)            */
     int32_t tile_joints;  /* target joints per CTA tile (chars per tile = max(1, this / n));
                              0 = auto (1024)                                                  */
     int32_t force_split;  /* 1 = use the multi-CTA program even when one CTA would fit          */
     int32_t stages;       /* TMA load stages of the chunked kernel (2 or 3); 0 = auto           */
     int32_t sbufs;        /* skin staging buffers (1 or 2); 0 = auto                            */
-    int32_t ib_placement; /* inverse bind for the epilogue: 1 = staged in shared memory, 2 = read
-                             through L1/L2; 0 = auto (shared memory when it fits)             */
     int32_t pbuf;         /* anchor buffer P: 2 = ping-pong (one barrier per round), 1 = single
                              buffer (two barriers per round, half the shared memory); 0 = auto */
-    int32_t kernel;       /* chunked kernel variant: 1 = row-parallel (three lanes per chunk, lane q
-                             owns row q), 2 = one thread per chunk; 0 = auto (1)              */
+    int32_t reserved[2];  /* must be zero                                                      */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -148,10 +145,8 @@ typedef enum {
     HS_Q_STAGES = 11,        /* TMA load stages                                                */
     HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
-    HS_Q_IB_PLACEMENT = 14,  /* chunked kernel: 1 = inverse bind in smem, 2 = via L1/L2          */
     HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
-    HS_Q_SBUFS = 16,         /* skin staging buffers of the chunked kernel                      */
-    HS_Q_KERNEL = 17         /* chunked kernel variant (1 row-parallel, 2 thread per chunk)     */
+    HS_Q_SBUFS = 16          /* skin staging buffers of the chunked kernel                      */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

@@ -39,7 +39,7 @@ cudaError_t upload(T** dptr, const T* host, size_t count) {
     return cudaMemcpy(*dptr, host, count * sizeof(T), cudaMemcpyHostToDevice);
 }
 
-bool is_valid_k(int k) { return k >= 3 && k <= 15 && (k & 1); }
+bool is_valid_k(int k) { return k >= 3 && k <= 11 && (k & 1); }
 
 }  // namespace
 
@@ -56,8 +56,7 @@ struct hs_skeleton {
     int K = 7;
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
-    int stages = 0, sbufs = 0, threads = 0, ib_smem = 0;
-    bool rows = true;              // row-parallel kernel (3 lanes per chunk)
+    int stages = 0, sbufs = 0, threads = 0;
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -108,7 +107,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.ib_placement < 0 || o.ib_placement > 2 || o.pbuf < 0 || o.pbuf > 2 || o.kernel < 0 || o.kernel > 2)
+        o.pbuf < 0 || o.pbuf > 2 || o.reserved[0] || o.reserved[1])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -128,19 +127,13 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
     const int64_t TC = (n + sk->K - 1) / sk->K;  // chunks per character
-    sk->rows = o.kernel != 2;
-    // chunks per CTA: rows kernel 10 per warp and <= 15 compute warps (launch bounds 512 with
-    // the producer warp); thread-per-chunk kernel <= 224 threads (launch bounds 256)
-    const int max_chunks = sk->rows ? 150 : 224;
+    const int max_chunks = 224;  // compute threads per CTA (launch bounds 256 with the producer warp)
     while (C > 1 && C * TC > max_chunks) --C;
     if (!(o.force_split && depth == 0) && C * TC <= max_chunks && (int64_t)C * n <= 65535) {
-        // candidates in preference order: (stages, sbufs, ping-pong P, IB in smem)
-        std::vector<std::array<int, 4>> cand;
-        for (int ibs : {1, 0})
-            for (auto ss : {std::array<int, 2>{3, 2}, {3, 1}, {2, 2}, {2, 1}})
-                for (int pp : {1, 0}) cand.push_back({ss[0], ss[1], pp, ibs});
-        // phase-2 workers: rows kernel = 3-lane groups (10 per warp), else threads
-        const int workers = sk->rows ? (int)((C * TC + 9) / 10 * 10) : (int)(((C * TC) + 31) / 32 * 32);
+        // candidates in preference order: (stages, sbufs, ping-pong P)
+        const int cand[][3] = {{3, 2, 1}, {3, 2, 0}, {3, 1, 1}, {3, 1, 0},
+                               {2, 2, 1}, {2, 2, 0}, {2, 1, 1}, {2, 1, 0}};
+        const int workers = (int)(((C * TC) + 31) / 32 * 32);
         hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
         hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
         const bool single_ok = tp_sb.max_round_entries <= 4 * workers;
@@ -148,15 +141,13 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
             if (o.stages && c[0] != o.stages) continue;
             if (o.sbufs && c[1] != o.sbufs) continue;
             if (o.pbuf && (c[2] ? 2 : 1) != o.pbuf) continue;
-            if (o.ib_placement && (c[3] ? 1 : 2) != o.ib_placement) continue;
             if (!c[2] && !single_ok) continue;
             const hs::TileProgram& tp = c[2] ? tp_pp : tp_sb;
-            const int64_t b = hs::tile_smem_bytes(tp, c[0], c[1]) + (c[3] ? (int64_t)n * 48 : 0);
+            const int64_t b = hs::tile_smem_bytes(tp, c[0], c[1]);
             if (b <= smem_optin && 2 * tp.nslots < 32768) {
                 sk->tp = tp;
                 sk->stages = c[0];
                 sk->sbufs = c[1];
-                sk->ib_smem = c[3];
                 sk->smem = b;
                 sk->chunked = true;
                 break;
@@ -199,7 +190,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     }
     if (sk->chunked) {
         const hs::TileProgram& tp = sk->tp;
-        sk->threads = sk->rows ? ((tp.T + 9) / 10) * 32 + 32 : ((tp.T + 31) / 32) * 32 + 32;
+        sk->threads = ((tp.T + 31) / 32) * 32 + 32;
         if ((e = upload(&sk->d_meta, tp.meta.data(), tp.meta.size())) != cudaSuccess ||
             (e = upload(&sk->d_p1len, tp.p1len.data(), tp.p1len.size())) != cudaSuccess ||
             (e = upload(&sk->d_round_off, tp.round_off.data(), tp.round_off.size())) != cudaSuccess ||
@@ -247,8 +238,6 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
-            a.ib_smem = sk->ib_smem;
-            a.rows = sk->rows ? 1 : 0;
             a.p_single = sk->tp.pingpong ? 0 : 1;
             a.prof = nullptr;
             if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
@@ -258,8 +247,8 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             e = hs::launch_chunked(sk->K, a, st);
             if (e != cudaSuccess) {
                 char buf[256];
-                std::snprintf(buf, sizeof(buf), "chunked launch (K=%d rows=%d threads=%d smem=%lld stages=%d sbufs=%d)",
-                              sk->K, a.rows, a.threads, (long long)a.smem_bytes, a.stages, a.sbufs);
+                std::snprintf(buf, sizeof(buf), "chunked launch (K=%d threads=%d smem=%lld stages=%d sbufs=%d)",
+                              sk->K, a.threads, (long long)a.smem_bytes, a.stages, a.sbufs);
                 return cuda_fail(e, buf);
             }
             if (a.prof) {
@@ -406,9 +395,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_STAGES: *v = sk->stages; break;
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
-        case HS_Q_IB_PLACEMENT: *v = sk->chunked ? (sk->ib_smem ? 1 : 2) : 0; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
-        case HS_Q_KERNEL: *v = sk->chunked ? (sk->rows ? 1 : 2) : 0; break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }

@@ -121,17 +121,15 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
 
 // ================================================================== chunked kernel
 // Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
-// producer (bulk loads of the tile's local poses, bulk stores of G and S).
-// Per tile of C characters (F = C*J joints, user order in smem):
+// producer.  Per tile of C characters (F = C*J joints, user order in smem):
 //   phase 1  each compute thread folds its chunk of K consecutive internal
 //            positions left-to-right (in-chunk parent = previous position) and
 //            publishes the running product at anchor joints into P;
-//   phase 2  pointer jumping (Alg. 2) over the anchor forest;
+//   phase 2  pointer jumping (Alg. 2) over the anchor forest, ping-pong P;
 //   phase 3  each thread re-folds its chunk starting from the final P of each
-//            segment head's parent, writes G in place over L and S = G (x) IB
-//            into the S buffer.
-// Both folds load the whole chunk up front and select instead of branching, so
-// the K dependent composes run back to back (no smem round trip between them).
+//            segment head's parent, writes G in place over L, and S = G (x) IB
+//            (IB held in registers) into the S buffer;
+// then the producer bulk-stores G and S and refills the stage.
 template <int K>
 __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -143,13 +141,13 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     const int64_t tile_f = (int64_t)a.F * 12;
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
-    float* IBs = P + (a.p_single ? 1 : 2) * a.nslots * 12;   // used when a.ib_smem
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
     const int warp = threadIdx.x >> 5;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t my_tiles =
+        blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const bool do_skin = a.sout != nullptr;
 
     if (threadIdx.x == 0) {
@@ -164,8 +162,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         if ((threadIdx.x & 31) != 0) return;
         auto issue_load = [&](int64_t it) {
             const int stage = (int)(it % NS);
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
+            const int64_t tile = blockIdx.x + it * gridDim.x;
+            const int64_t c0 = tile * a.C;
+            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
             mbar_expect_tx(&full[stage], bytes);
             bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
         };
@@ -173,22 +173,16 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         for (int64_t it = 0; it < my_tiles; ++it) {
             const int stage = (int)(it % NS);
             mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
+            const int64_t tile = blockIdx.x + it * gridDim.x;
+            const int64_t c0 = tile * a.C;
+            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
             bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-            bulk_commit();                            // group: G of this tile
-            if (do_skin) {
-                bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-                bulk_commit();                        // group: S of this tile
-                bulk_wait_read<1>();                  // G read out (S may still drain)
-            } else {
-                bulk_wait_read<0>();
-            }
+            if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+            bulk_commit();
+            bulk_wait_read<0>();                  // smem of this tile has been read out
+            if (do_skin) mbar_arrive(&sfree[it % NSS]);
             if (it + NS < my_tiles) issue_load(it + NS);
-            if (do_skin) {
-                bulk_wait_read<0>();
-                mbar_arrive(&sfree[it % NSS]);
-            }
         }
         bulk_wait_all();
         return;
@@ -196,9 +190,11 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
 
     // ---------------------------------------------------------------- consumers
     const int t = threadIdx.x;
+    const bool active = t < a.T;
     uint64_t m[K];
+    float ibr[K][12];
     int p1 = 0;
-    if (t < a.T) {
+    if (active) {
         p1 = a.p1len[t];
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
@@ -206,12 +202,14 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
     }
-    if (do_skin && a.ib_smem) {   // the skeleton's inverse bind, shared by every tile
-        const float4* src = reinterpret_cast<const float4*>(a.ib);
-        float4* dst = reinterpret_cast<float4*>(IBs);
-        for (int v = t; v < a.J * 3; v += NC) dst[v] = __ldg(src + v);
+    if (do_skin) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const int src = (int)(int16_t)(m[s] >> 32);
+            const int ibu = (int)((m[s] >> 16) & 0xffff);
+            if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
+        }
     }
-    bar_consumers(NC);
 
     // debug phase profile (HS_DEBUG_PROF): consumer thread 0 accumulates clock64 deltas
     long long prof_last = 0;
@@ -229,61 +227,48 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
         prof_mark(0);
 
-        // phase 1: in-chunk fold, publish anchors (location = slot)
+        // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
         if (p1 > 0) {
-            float l[K][12];
-#pragma unroll
-            for (int s = 0; s < K; ++s)
-                if (s < p1) ld3(L + (int)(m[s] & 0xffff) * 12, l[s]);
             float acc[12];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 if (s < p1) {
+                    const int off = (int)(m[s] & 0xffff);
                     const int src = (int)(int16_t)(m[s] >> 32);
                     const int own = (int)(int16_t)(m[s] >> 48);
-                    if (s == 0) {
+                    float l[12];
+                    ld3(L + off * 12, l);
+                    if (src == kSrcPrev) {
+                        float tmp[12];
+                        compose(acc, l, tmp);
 #pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = l[0][e];
+                        for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
                     } else {
-                        float c[12];
-                        compose(acc, l[s], c);
-                        const bool prev = src == kSrcPrev;
 #pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = prev ? c[e] : l[s][e];
+                        for (int e = 0; e < 12; ++e) acc[e] = l[e];
                     }
                     if (own >= 0) st3(P + own * 12, acc);
                 }
             }
         }
         bar_consumers(NC);
-        prof_mark(1);
 
+        prof_mark(1);
         // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
         // snapshot semantics: ping-pong P, or a single P with every read of a round
         // before any of its writes (entries held in registers, <= 4 per thread)
         for (int r = 0; r < a.R2; ++r) {
             const int eb = __ldg(a.round_off + r), e1 = __ldg(a.round_off + r + 1);
             if (!a.p_single) {
-                int e = eb + t;
-                for (; e + NC < e1; e += 2 * NC) {   // two independent entries in flight
-                    const uint64_t w0 = __ldg(a.rounds + e), w1 = __ldg(a.rounds + e + NC);
-                    float x0[12], y0[12], z0[12], x1[12], y1[12], z1[12];
-                    ld3(P + ((w0 >> 32) & 0xffff) * 12, x0);
-                    ld3(P + ((w0 >> 16) & 0xffff) * 12, y0);
-                    ld3(P + ((w1 >> 32) & 0xffff) * 12, x1);
-                    ld3(P + ((w1 >> 16) & 0xffff) * 12, y1);
-                    compose(x0, y0, z0);
-                    compose(x1, y1, z1);
-                    st3(P + (w0 & 0xffff) * 12, z0);
-                    st3(P + (w1 & 0xffff) * 12, z1);
-                }
-                if (e < e1) {
+                for (int e = eb + t; e < e1; e += NC) {
                     const uint64_t w = __ldg(a.rounds + e);
+                    const int dst = (int)(w & 0xffff), self = (int)((w >> 16) & 0xffff),
+                              link = (int)((w >> 32) & 0xffff);
                     float x[12], y[12], z[12];
-                    ld3(P + ((w >> 32) & 0xffff) * 12, x);
-                    ld3(P + ((w >> 16) & 0xffff) * 12, y);
+                    ld3(P + link * 12, x);
+                    ld3(P + self * 12, y);
                     compose(x, y, z);
-                    st3(P + (w & 0xffff) * 12, z);
+                    st3(P + dst * 12, z);
                 }
                 bar_consumers(NC);
             } else {
@@ -309,292 +294,39 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 bar_consumers(NC);
             }
         }
-
-        // phase 3: final fold; G in place over L, S = G (x) IB into the S buffer
         prof_mark(2);
+
+        // phase 3: final fold, G in place, S into the S buffer
         float* S = SB + (it % NSS) * tile_f;
         if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
         prof_mark(3);
         {
-            // one-joint-ahead prefetch: the next L is loaded before this joint's stores
-            float lnext[12], acc[12];
-            if ((int)(int16_t)(m[0] >> 32) != kSrcNone) ld3(L + (int)(m[0] & 0xffff) * 12, lnext);
+            float acc[12];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;   // only trailing positions of a thread
+                if (src == kSrcNone) continue;
                 const int off = (int)(m[s] & 0xffff);
                 float l[12];
+                ld3(L + off * 12, l);
+                if (src == kSrcPrev) {
+                    float tmp[12];
+                    compose(acc, l, tmp);
 #pragma unroll
-                for (int e = 0; e < 12; ++e) l[e] = lnext[e];
-                if (s + 1 < K && (int)(int16_t)(m[s + 1] >> 32) != kSrcNone)
-                    ld3(L + (int)(m[s + 1] & 0xffff) * 12, lnext);
-                float base[12], c[12];
-                if (src >= 0) ld3(P + src * 12, base);   // segment head: parent's final
-                const int ibu = (int)((m[s] >> 16) & 0xffff);
-                float ib[12];
-                if (do_skin) {
-                    if (a.ib_smem) ld3(IBs + ibu * 12, ib);
-                    else ldg3(a.ib + (int64_t)ibu * 12, ib);
+                    for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                } else if (src == kSrcRoot) {
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                } else {
+                    float pa[12];
+                    ld3(P + src * 12, pa);
+                    compose(pa, l, acc);
                 }
-                const bool prev = src == kSrcPrev, root = src == kSrcRoot;
-#pragma unroll
-                for (int e = 0; e < 12; ++e) base[e] = prev ? acc[e] : base[e];
-                compose(base, l, c);
-#pragma unroll
-                for (int e = 0; e < 12; ++e) acc[e] = root ? l[e] : c[e];
                 st3(L + off * 12, acc);
                 if (do_skin) {
                     float sk[12];
-                    compose(acc, ib, sk);
+                    compose(acc, ibr[s], sk);
                     st3(S + off * 12, sk);
-                }
-            }
-        }
-        fence_proxy_async();
-        bar_consumers(NC);
-        if (t == 0) mbar_arrive(&done[stage]);
-        prof_mark(4);
-        if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
-    }
-}
-
-
-// ================================================================== rows kernel
-// Row-parallel variant of the chunked kernel (the default): three lanes per chunk,
-// lane q owning ROW q of every left operand.  Row q of A (x) B needs only row q of
-// A and all of B, so each lane folds its row independently: 12 FMA per joint per
-// lane instead of 36 per thread, three times the warps to hide smem/FMA latency,
-// and a quarter of the registers.  Ten chunks per warp (lanes 30, 31 idle) keep a
-// chunk's three lanes in one warp, so G can be written in place over L after a
-// __syncwarp.  Same host program (meta / p1len / rounds) as chunked_kernel.
-__device__ __forceinline__ void rowmul(const float* __restrict__ a4, const float* __restrict__ b,
-                                       float* __restrict__ c4) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        float x = a4[0] * b[k];
-        x = fmaf(a4[1], b[4 + k], x);
-        c4[k] = fmaf(a4[2], b[8 + k], x);
-    }
-    float t = fmaf(a4[0], b[3], a4[3]);
-    t = fmaf(a4[1], b[7], t);
-    c4[3] = fmaf(a4[2], b[11], t);
-}
-__device__ __forceinline__ void ld4(const float* p, float* v) {
-    const float4 x = *reinterpret_cast<const float4*>(p);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-}
-__device__ __forceinline__ void st4(float* p, const float* v) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-}
-
-template <int K>
-__global__ void __launch_bounds__(512, 1) rows_kernel(const ChunkedArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int NS = a.stages, NSS = a.sbufs;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* done = full + 4;
-    uint64_t* sfree = done + 4;
-    float* LG = reinterpret_cast<float*>(smem + 128);
-    const int64_t tile_f = (int64_t)a.F * 12;
-    float* SB = LG + NS * tile_f;
-    float* P = SB + NSS * tile_f;
-    float* IBs = P + (a.p_single ? 1 : 2) * a.nslots * 12;
-
-    const int nwc = (int)(blockDim.x >> 5) - 1;
-    const int NC = nwc * 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const bool do_skin = a.sout != nullptr;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
-        for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == nwc) {
-        // ------------------------------------------------------------ producer
-        if (lane != 0) return;
-        auto issue_load = [&](int64_t it) {
-            const int stage = (int)(it % NS);
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
-            mbar_expect_tx(&full[stage], bytes);
-            bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
-        };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
-        for (int64_t it = 0; it < my_tiles; ++it) {
-            const int stage = (int)(it % NS);
-            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
-            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-            bulk_commit();
-            if (do_skin) {
-                bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-                bulk_commit();
-                bulk_wait_read<1>();
-            } else {
-                bulk_wait_read<0>();
-            }
-            if (it + NS < my_tiles) issue_load(it + NS);
-            if (do_skin) {
-                bulk_wait_read<0>();
-                mbar_arrive(&sfree[it % NSS]);
-            }
-        }
-        bulk_wait_all();
-        return;
-    }
-
-    // ---------------------------------------------------------------- consumers
-    const int t = threadIdx.x;
-    const int q = lane % 3;                       // row owned by this lane
-    const int chunk = warp * 10 + lane / 3;       // lanes 30, 31: chunk beyond T (idle)
-    const bool active = lane < 30 && chunk < a.T;
-    uint64_t m[K];
-    int p1 = 0;
-    if (active) {
-        p1 = a.p1len[chunk];
-#pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)chunk * K + s];
-    } else {
-#pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
-    }
-    if (do_skin && a.ib_smem) {
-        const float4* src = reinterpret_cast<const float4*>(a.ib);
-        float4* dst = reinterpret_cast<float4*>(IBs);
-        for (int v = t; v < a.J * 3; v += NC) dst[v] = __ldg(src + v);
-    }
-    // phase-2 work split: groups of 3 lanes, 10 groups per warp
-    const int group = warp * 10 + lane / 3;
-    const int ngroups = nwc * 10;
-    bar_consumers(NC);
-
-    long long prof_last = 0;
-    auto prof_mark = [&](int slot) {
-        if (a.prof && t == 0) {
-            const long long now = clock64();
-            if (slot >= 0) atomicAdd(a.prof + slot, (unsigned long long)(now - prof_last));
-            prof_last = now;
-        }
-    };
-    for (int64_t it = 0; it < my_tiles; ++it) {
-        const int stage = (int)(it % NS);
-        float* L = LG + stage * tile_f;
-        prof_mark(-1);
-        mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
-        prof_mark(0);
-
-        // phase 1: row q of the in-chunk fold; publish row q at anchors
-        if (p1 > 0) {
-            float acc[4];
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                if (s < p1) {
-                    const int src = (int)(int16_t)(m[s] >> 32);
-                    const int own = (int)(int16_t)(m[s] >> 48);
-                    float l[12];
-                    ld3(L + (int)(m[s] & 0xffff) * 12, l);
-                    float lr[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) lr[e] = q == 0 ? l[e] : (q == 1 ? l[4 + e] : l[8 + e]);
-                    if (s == 0) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[e] = lr[e];
-                    } else {
-                        float c[4];
-                        rowmul(acc, l, c);
-                        const bool prev = src == kSrcPrev;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[e] = prev ? c[e] : lr[e];
-                    }
-                    if (own >= 0) st4(P + own * 12 + 4 * q, acc);
-                }
-            }
-        }
-        bar_consumers(NC);
-        prof_mark(1);
-
-        // phase 2: pointer jumping over the anchor forest, row-parallel
-        for (int r = 0; r < a.R2; ++r) {
-            const int eb = __ldg(a.round_off + r), e1 = __ldg(a.round_off + r + 1);
-            if (!a.p_single) {
-                for (int e = eb + group; e < e1; e += ngroups) {
-                    if (lane >= 30) break;
-                    const uint64_t w = __ldg(a.rounds + e);
-                    float x[4], y[12], z[4];
-                    ld4(P + ((w >> 32) & 0xffff) * 12 + 4 * q, x);
-                    ld3(P + ((w >> 16) & 0xffff) * 12, y);
-                    rowmul(x, y, z);
-                    st4(P + (w & 0xffff) * 12 + 4 * q, z);
-                }
-                bar_consumers(NC);
-            } else {
-                float z[4][4];
-                int dst[4];
-#pragma unroll
-                for (int k2 = 0; k2 < 4; ++k2) {
-                    const int e = eb + group + k2 * ngroups;
-                    dst[k2] = -1;
-                    if (lane < 30 && e < e1) {
-                        const uint64_t w = __ldg(a.rounds + e);
-                        float x[4], y[12];
-                        ld4(P + ((w >> 32) & 0xffff) * 12 + 4 * q, x);
-                        ld3(P + ((w >> 16) & 0xffff) * 12, y);
-                        rowmul(x, y, z[k2]);
-                        dst[k2] = (int)(w & 0xffff);
-                    }
-                }
-                bar_consumers(NC);
-#pragma unroll
-                for (int k2 = 0; k2 < 4; ++k2)
-                    if (dst[k2] >= 0) st4(P + dst[k2] * 12 + 4 * q, z[k2]);
-                bar_consumers(NC);
-            }
-        }
-
-        // phase 3: row q of the final fold; G row in place, S row into the S buffer
-        prof_mark(2);
-        float* S = SB + (it % NSS) * tile_f;
-        if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
-        prof_mark(3);
-        {
-            float acc[4];
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                // every lane runs every step (the __syncwarp below needs the full warp)
-                const int src = (int)(int16_t)(m[s] >> 32);
-                const bool valid = src != kSrcNone;
-                const int off = (int)(m[s] & 0xffff);
-                float l[12], base[4], c[4];
-                if (valid) ld3(L + off * 12, l);
-                if (src >= 0) ld4(P + src * 12 + 4 * q, base);
-                float ib[12];
-                const int ibu = (int)((m[s] >> 16) & 0xffff);
-                if (do_skin && valid) {
-                    if (a.ib_smem) ld3(IBs + ibu * 12, ib);
-                    else ldg3(a.ib + (int64_t)ibu * 12, ib);
-                }
-                const bool prev = src == kSrcPrev, root = src == kSrcRoot;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) base[e] = prev ? acc[e] : base[e];
-                rowmul(base, l, c);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    acc[e] = root ? (q == 0 ? l[e] : (q == 1 ? l[4 + e] : l[8 + e])) : c[e];
-                __syncwarp();   // the chunk's three lanes have read L[off] before it is overwritten
-                if (valid) {
-                    st4(L + off * 12 + 4 * q, acc);
-                    if (do_skin) {
-                        float sk[4];
-                        rowmul(acc, ib, sk);
-                        st4(S + off * 12 + 4 * q, sk);
-                    }
                 }
             }
         }
@@ -796,19 +528,15 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
 }
 
 template <int K>
-void* chunked_ptr(bool rows) {
-    return rows ? reinterpret_cast<void*>(&rows_kernel<K>) : reinterpret_cast<void*>(&chunked_kernel<K>);
-}
+void* chunked_ptr() { return reinterpret_cast<void*>(&chunked_kernel<K>); }
 
-void* chunked_fn(int K, bool rows) {
+void* chunked_fn(int K) {
     switch (K) {
-        case 3: return chunked_ptr<3>(rows);
-        case 5: return chunked_ptr<5>(rows);
-        case 7: return chunked_ptr<7>(rows);
-        case 9: return chunked_ptr<9>(rows);
-        case 11: return chunked_ptr<11>(rows);
-        case 13: return chunked_ptr<13>(rows);
-        case 15: return chunked_ptr<15>(rows);
+        case 3: return chunked_ptr<3>();
+        case 5: return chunked_ptr<5>();
+        case 7: return chunked_ptr<7>();
+        case 9: return chunked_ptr<9>();
+        case 11: return chunked_ptr<11>();
         default: return nullptr;
     }
 }
@@ -834,17 +562,13 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
-    for (bool rows : {false, true}) {
-        void* fn = chunked_fn(K, rows);
-        if (!fn) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    void* fn = chunked_fn(K);
+    if (!fn) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
-int max_chunked_blocks_per_sm(int K, bool rows, int threads, int64_t smem_bytes) {
-    void* fn = chunked_fn(K, rows);
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes) {
+    void* fn = chunked_fn(K);
     int nb = 0;
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
                    cudaSuccess)
@@ -853,11 +577,10 @@ int max_chunked_blocks_per_sm(int K, bool rows, int threads, int64_t smem_bytes)
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    void* fn = chunked_fn(K, a.rows != 0);
+    void* fn = chunked_fn(K);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm
-                                   : max_chunked_blocks_per_sm(K, a.rows != 0, a.threads, a.smem_bytes);
+    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : max_chunked_blocks_per_sm(K, a.threads, a.smem_bytes);
     int64_t grid = (int64_t)sm_count() * per_sm;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
@@ -914,7 +637,6 @@ cudaError_t launch_split_p1(int K, const float* local, float* pg, const int32_t*
     const unsigned blocks = (unsigned)((n + 127) / 128);
     switch (K) {
         HS_SPLIT_CASE(3) HS_SPLIT_CASE(5) HS_SPLIT_CASE(7) HS_SPLIT_CASE(9) HS_SPLIT_CASE(11)
-        HS_SPLIT_CASE(13) HS_SPLIT_CASE(15)
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -935,7 +657,6 @@ cudaError_t launch_split_p3(int K, const float* local, float* gout, float* sout,
     const unsigned blocks = (unsigned)((n + 127) / 128);
     switch (K) {
         HS_SPLIT_CASE(3) HS_SPLIT_CASE(5) HS_SPLIT_CASE(7) HS_SPLIT_CASE(9) HS_SPLIT_CASE(11)
-        HS_SPLIT_CASE(13) HS_SPLIT_CASE(15)
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

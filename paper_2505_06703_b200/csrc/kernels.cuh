@@ -23,14 +23,12 @@ struct ChunkedArgs {
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
-    int32_t ib_smem;           // 1 = inverse bind staged in shared memory, 0 = read through L1/L2
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
-    int32_t rows;              // 1 = row-parallel kernel (3 lanes per chunk), 0 = thread per chunk
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute
-int max_chunked_blocks_per_sm(int K, bool rows, int threads, int64_t smem_bytes);
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes);
 
 // Alg. 2: radix-2 pointer jumping, one thread per joint.
 cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,

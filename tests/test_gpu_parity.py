@@ -68,10 +68,8 @@ EXACT_CASES = [
     ("hum32", {}), ("hum64", {}), ("chain256", {}), ("tree1024", {}),
     ("hum64", {"chunk": 3}), ("chain256", {"chunk": 11}), ("tree1024", {"chunk": 5}),
     ("hum64", {"tile_joints": 200}), ("tree1024", {"stages": 2, "sbufs": 1}),
-    ("tree1024", {"pbuf": 2, "ib_placement": 2}), ("chain256", {"pbuf": 1, "ib_placement": 1}),
-    ("hum32", {"pbuf": 1, "ib_placement": 2, "stages": 3, "sbufs": 2}),
-    ("hum64", {"kernel": 2}), ("tree1024", {"kernel": 2, "pbuf": 1}), ("chain256", {"kernel": 2}),
-    ("tree1024", {"kernel": 1, "pbuf": 1, "chunk": 9}),
+    ("tree1024", {"pbuf": 2}), ("chain256", {"pbuf": 1}), ("tree1024", {"pbuf": 1, "chunk": 9}),
+    ("hum32", {"pbuf": 1, "stages": 3, "sbufs": 2}),
     ("tree1024", {"force_split": True}), ("chain256", {"force_split": True, "chunk": 3}),
 ]
 
