@@ -68,7 +68,7 @@ hs_status hs_skeleton_create(const int32_t* parents, int32_t n_joints, const flo
 
 /* Creation options (hs_skeleton_create uses all-zero = automatic). */
 typedef struct {
-    int32_t chunk;        /* K, joints per thread chunk: odd in 3..11; 0 = auto (7)            */
+    int32_t chunk;        /* K, joints per thread chunk: odd in 3..11; 0 = auto (5)            */
     int32_t tile_joints;  /* target joints per CTA tile (chars per tile = max(1, this / n));
                              0 = auto (1024)                                                  */
     int32_t force_split;  /* 1 = use the multi-CTA program even when one CTA would fit          */

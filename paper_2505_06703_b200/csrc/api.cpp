@@ -122,7 +122,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (e != cudaSuccess) { delete sk; return cuda_fail(e, "cudaDeviceGetAttribute"); }
 
     const hs::Plan& P = sk->plan;
-    sk->K = o.chunk ? o.chunk : 7;
+    sk->K = o.chunk ? o.chunk : 5;
     // --- chunked (single-CTA) program: C characters per tile, ~tile_target joints
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
@@ -131,8 +131,9 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     while (C > 1 && C * TC > max_chunks) --C;
     if (!(o.force_split && depth == 0) && C * TC <= max_chunks && (int64_t)C * n <= 65535) {
         // candidates in preference order: (stages, sbufs, ping-pong P)
-        const int cand[][3] = {{3, 2, 1}, {3, 2, 0}, {3, 1, 1}, {3, 1, 0},
-                               {2, 2, 1}, {2, 2, 0}, {2, 1, 1}, {2, 1, 0}};
+        // (ping-pong P measured faster than the single buffer: one barrier per round)
+        const int cand[][3] = {{3, 2, 1}, {3, 1, 1}, {2, 2, 1}, {2, 1, 1},
+                               {3, 2, 0}, {3, 1, 0}, {2, 2, 0}, {2, 1, 0}};
         const int workers = (int)(((C * TC) + 31) / 32 * 32);
         hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
         hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
@@ -428,7 +429,7 @@ hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk
         std::string err;
         int st = hs::build_plan(parents, n_joints, p->plan, err);
         if (st != 0) { delete p; return fail((hs_status)st, err); }
-        p->K = chunk == 0 ? 7 : chunk;
+        p->K = chunk == 0 ? 5 : chunk;
         if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..15"); }
         p->block_size = block_size <= 0 ? 64 : block_size;
         p->decomp = hs::decompose(p->plan.ipar, p->K);
