@@ -83,6 +83,20 @@ def shard(n_total: int, rank: int, world: int, scaling: str):
     return lo, hi - lo
 
 
+def reduce_over_ranks(ms_rank: float, joints_rank: int, world: int, device):
+    """(max over ranks of the timed-region ms, sum over ranks of joints processed).
+    Outside the timed region; NCCL on the GPU path, gloo in the CPU tests."""
+    if world <= 1:
+        return ms_rank, joints_rank
+    import torch
+    import torch.distributed as dist
+    mx = torch.tensor([ms_rank], dtype=torch.float64, device=device)
+    sm = torch.tensor([float(joints_rank)], dtype=torch.float64, device=device)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return float(mx.item()), int(sm.item())
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -291,14 +305,7 @@ def run_ours(args):
     ms_rank = start.elapsed_time(stop)
     per_type_ms = [statistics.mean(events[t][0][k].elapsed_time(events[t][1][k]) for k in range(K))
                    for t in range(len(work))]
-    ms = ms_rank
-    joints_total = joints_rank
-    if world > 1:
-        tt = torch.tensor([ms_rank, float(joints_rank)], dtype=torch.float64, device=dev)
-        mx = tt.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        ms, joints_total = float(mx[0]), int(tt[1])
+    ms, joints_total = reduce_over_ranks(ms_rank, joints_rank, world, dev)
     value = joints_total * K / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (largest byte share: tree1024's launch)
