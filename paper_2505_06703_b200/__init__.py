@@ -19,6 +19,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libhs.so")
+# A/B experiments may point the binding at another in-tree build of the same sources.
+_LOAD_PATH = os.environ.get("HS_LIB", LIB_PATH)
 _SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu")]
 _DEPS = _SOURCES + [os.path.join(_HERE, "csrc", f) for f in ("plan.hpp", "kernels.cuh")] + [
     os.path.join(_ROOT, "include", "hs.h")]
@@ -80,9 +82,9 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    if not os.path.exists(_LOAD_PATH):
+        raise ImportError(f"{_LOAD_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(_LOAD_PATH)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     L.hs_skeleton_create.argtypes = [vp, i32, vp, ctypes.POINTER(vp)]
     L.hs_skeleton_create_ex.argtypes = [vp, i32, vp, ctypes.POINTER(_CreateOpts), ctypes.POINTER(vp)]

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <array>
 #include <stdexcept>
 
 namespace hs {
@@ -103,6 +104,95 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K) {
     return d;
 }
 
+namespace {
+
+// Bank-conflict-aware numbering of the tile's anchor slots.  A 128-bit shared
+// access of a quarter warp (8 lanes) is conflict-free when the 8 addresses fall in
+// distinct 16-byte bank groups; a P entry is 48 B = 3 groups, so slot s touches
+// groups (3s + k) mod 8 and 8 slots are conflict-free iff their residues mod 8
+// differ.  The sets that must differ are: the anchors one quarter warp reads in
+// the same phase-3 step, and the anchors it writes in the same phase-1 step.
+// Greedy colouring with 8 colours (residues), balanced class sizes; slot =
+// colour + 8 * rank within the colour.  Returns the new index of every raw slot
+// and the padded slot count (a multiple of 8, so ping-pong buffers keep residues).
+std::vector<int32_t> colour_slots(int32_t S, const std::vector<std::vector<int32_t>>& sets,
+                                  int32_t* S_out) {
+    std::vector<std::vector<int32_t>> member(S);
+    for (int32_t k = 0; k < (int32_t)sets.size(); ++k)
+        for (int32_t s : sets[k]) member[s].push_back(k);
+    std::vector<int32_t> order(S);
+    for (int32_t s = 0; s < S; ++s) order[s] = s;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return member[a].size() > member[b].size(); });
+    std::vector<int32_t> colour(S, -1), count(8, 0);
+    const int32_t cap = (S + 7) / 8 + 1;
+    for (int32_t s : order) {
+        int conflicts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int32_t k : member[s])
+            for (int32_t o : sets[k])
+                if (o != s && colour[o] >= 0) conflicts[colour[o]]++;
+        int best = -1;
+        for (int c = 0; c < 8; ++c) {
+            if (count[c] >= cap) continue;
+            if (best < 0 || conflicts[c] < conflicts[best] ||
+                (conflicts[c] == conflicts[best] && count[c] < count[best]))
+                best = c;
+        }
+        colour[s] = best;
+        count[best]++;
+    }
+    int32_t maxc = 0;
+    for (int c = 0; c < 8; ++c) maxc = std::max(maxc, count[c]);
+    std::vector<int32_t> next(8, 0), idx(S);
+    for (int32_t s = 0; s < S; ++s) idx[s] = colour[s] + 8 * next[colour[s]]++;
+    *S_out = 8 * maxc;
+    return idx;
+}
+
+// Order one round's entries so every aligned run of 8 (one quarter warp) has
+// distinct self residues and distinct link residues where possible.
+void order_round(std::vector<std::array<int32_t, 3>>& ent) {   // {dst, self, link} locations
+    std::vector<std::vector<std::array<int32_t, 3>>> bucket(8);
+    for (auto& e : ent) bucket[e[1] & 7].push_back(e);
+    std::vector<std::array<int32_t, 3>> out;
+    out.reserve(ent.size());
+    size_t left = ent.size();
+    while (left) {
+        bool used_s[8] = {}, used_l[8] = {};
+        for (int pos = 0; pos < 8 && left; ++pos) {
+            int bs = -1;
+            size_t bi = 0;
+            // 1) an unused self residue with an entry whose link residue is unused
+            for (int c = 0; c < 8 && bs < 0; ++c) {
+                if (used_s[c]) continue;
+                for (size_t i = 0; i < bucket[c].size(); ++i)
+                    if (!used_l[bucket[c][i][2] & 7]) { bs = c; bi = i; break; }
+            }
+            // 2) else any entry with an unused self residue (largest bucket first)
+            if (bs < 0) {
+                for (int c = 0; c < 8; ++c)
+                    if (!used_s[c] && !bucket[c].empty() && (bs < 0 || bucket[c].size() > bucket[bs].size())) bs = c;
+                bi = 0;
+            }
+            // 3) else anything
+            if (bs < 0) {
+                for (int c = 0; c < 8; ++c)
+                    if (!bucket[c].empty() && (bs < 0 || bucket[c].size() > bucket[bs].size())) bs = c;
+                bi = 0;
+            }
+            auto e = bucket[bs][bi];
+            bucket[bs].erase(bucket[bs].begin() + (long)bi);
+            used_s[e[1] & 7] = true;
+            used_l[e[2] & 7] = true;
+            out.push_back(e);
+            --left;
+        }
+    }
+    ent.swap(out);
+}
+
+}  // namespace
+
 TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
     // Chunks never straddle characters: every character of a tile runs the same
     // program (same association order), so a character's bits do not depend on
@@ -117,32 +207,51 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
     tp.F = C * n;
     tp.T = C * TC;
     tp.pingpong = pingpong;
-    const int32_t S = C * Sc;
+    const int32_t Sraw = C * Sc;
+    // conflict sets (quarter warp x step) for phase-3 reads and phase-1 writes
+    std::vector<std::vector<int32_t>> sets;
+    {
+        std::vector<std::vector<int32_t>> rd((size_t)((tp.T + 7) / 8) * K), wr(rd.size());
+        for (int c = 0; c < C; ++c)
+            for (int32_t tc = 0; tc < TC; ++tc) {
+                const int32_t t = c * TC + tc;
+                for (int s = 0; s < K; ++s) {
+                    const int32_t i = tc * K + s;
+                    if (i >= n) continue;
+                    const size_t k = (size_t)(t / 8) * K + s;
+                    if (d.src[i] >= 0) rd[k].push_back(c * Sc + d.slot_of[d.src[i]]);
+                    if (d.slot_of[i] >= 0) wr[k].push_back(c * Sc + d.slot_of[i]);
+                }
+            }
+        for (auto& v : rd) if (v.size() > 1) sets.push_back(v);
+        for (auto& v : wr) if (v.size() > 1) sets.push_back(v);
+    }
+    int32_t S = 0;
+    const std::vector<int32_t> idx = Sraw ? colour_slots(Sraw, sets, &S) : std::vector<int32_t>();
     tp.nslots = S;
-    // pointer-jumping rounds over the tile's anchor forest (C disjoint copies), ping-pong P
-    std::vector<int32_t> lk(S), latest(S, 0);
+    // pointer-jumping rounds over the tile's anchor forest (C disjoint copies)
+    std::vector<int32_t> lk(Sraw), latest(Sraw, 0);
     for (int c = 0; c < C; ++c)
         for (int32_t s = 0; s < Sc; ++s) lk[c * Sc + s] = d.link0[s] < 0 ? -1 : c * Sc + d.link0[s];
     tp.round_off.push_back(0);
     for (int r = 0;; ++r) {
         bool any = false;
-        for (int32_t s = 0; s < S; ++s) if (lk[s] >= 0) { any = true; break; }
+        for (int32_t s = 0; s < Sraw; ++s) if (lk[s] >= 0) { any = true; break; }
         if (!any) break;
-        int32_t n_r = 0;
-        for (int32_t s = 0; s < S; ++s) {
+        std::vector<std::array<int32_t, 3>> ent;
+        for (int32_t s = 0; s < Sraw; ++s) {
             if (lk[s] < 0) continue;
             // ping-pong: read buffer `latest`, write the other; single buffer: all reads of
             // a round precede its writes (two barriers), so every location is the slot.
             const int32_t wbuf = pingpong ? ((r + 1) & 1) : 0;
-            uint64_t dst = (uint64_t)(wbuf * S + s);
-            uint64_t self = (uint64_t)(latest[s] * S + s);
-            uint64_t link = (uint64_t)(latest[lk[s]] * S + lk[s]);
-            tp.rounds.push_back(dst | (self << 16) | (link << 32));
-            ++n_r;
+            ent.push_back({wbuf * S + idx[s], latest[s] * S + idx[s], latest[lk[s]] * S + idx[lk[s]]});
         }
-        tp.max_round_entries = std::max(tp.max_round_entries, n_r);
-        std::vector<int32_t> nl(S, -1);
-        for (int32_t s = 0; s < S; ++s) {
+        order_round(ent);
+        for (auto& e : ent)
+            tp.rounds.push_back((uint64_t)e[0] | ((uint64_t)e[1] << 16) | ((uint64_t)e[2] << 32));
+        tp.max_round_entries = std::max(tp.max_round_entries, (int32_t)ent.size());
+        std::vector<int32_t> nl(Sraw, -1);
+        for (int32_t s = 0; s < Sraw; ++s) {
             if (lk[s] < 0) continue;
             latest[s] = pingpong ? ((r + 1) & 1) : 0;
             nl[s] = lk[lk[s]];
@@ -164,12 +273,12 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
                     off = (uint64_t)(c * n + p.order[i]);
                     ibu = (uint64_t)p.order[i];
                     if (d.src[i] >= 0) {
-                        const int32_t slot = c * Sc + d.slot_of[d.src[i]];
-                        src = latest[slot] * S + slot;
+                        const int32_t raw = c * Sc + d.slot_of[d.src[i]];
+                        src = latest[raw] * S + idx[raw];
                     } else {
                         src = d.src[i];
                     }
-                    own = d.slot_of[i] >= 0 ? c * Sc + d.slot_of[i] : -1;
+                    own = d.slot_of[i] >= 0 ? idx[c * Sc + d.slot_of[i]] : -1;
                     if (own >= 0) tp.p1len[t] = s + 1;
                 }
                 tp.meta[(size_t)t * K + s] = off | (ibu << 16) | ((uint64_t)(uint16_t)(int16_t)src << 32) |
