@@ -68,7 +68,7 @@ struct hs_skeleton {
     uint64_t* d_meta = nullptr;
     int32_t* d_p1len = nullptr;
     int32_t* d_round_off = nullptr;
-    uint64_t* d_rounds = nullptr;
+    uint32_t* d_rounds = nullptr;
     int32_t* d_split_meta = nullptr;
     int32_t* d_path_off = nullptr;
     int32_t* d_path = nullptr;
@@ -237,6 +237,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.nslots = sk->tp.nslots; a.R2 = sk->tp.R2;
             a.meta = sk->d_meta; a.p1len = sk->d_p1len; a.round_off = sk->d_round_off;
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
+            a.n_rounds_entries = (int32_t)sk->tp.rounds.size();
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
             a.p_single = sk->tp.pingpong ? 0 : 1;

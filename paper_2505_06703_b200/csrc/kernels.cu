@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     const int64_t tile_f = (int64_t)a.F * 12;
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
+    int32_t* s_round_off = reinterpret_cast<int32_t*>(P + (a.p_single ? 1 : 2) * a.nslots * 12);
+    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + a.R2 + 1);
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
@@ -210,6 +212,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
         }
     }
+    // phase-2 tables: identical for every tile, staged once per CTA
+    for (int i = t; i <= a.R2; i += NC) s_round_off[i] = __ldg(a.round_off + i);
+    for (int i = t; i < a.n_rounds_entries; i += NC) s_rounds[i] = __ldg(a.rounds + i);
+    bar_consumers(NC);
 
     // debug phase profile (HS_DEBUG_PROF): consumer thread 0 accumulates clock64 deltas
     long long prof_last = 0;
@@ -256,14 +262,17 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         prof_mark(1);
         // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
         // snapshot semantics: ping-pong P, or a single P with every read of a round
-        // before any of its writes (entries held in registers, <= 4 per thread)
+        // before any of its writes (entries held in registers, <= 4 per thread).
+        // Descriptors (slot | dst buf | self buf | link location) come from smem.
+        const int S2 = a.nslots;
         for (int r = 0; r < a.R2; ++r) {
-            const int eb = __ldg(a.round_off + r), e1 = __ldg(a.round_off + r + 1);
+            const int eb = s_round_off[r], e1 = s_round_off[r + 1];
             if (!a.p_single) {
                 for (int e = eb + t; e < e1; e += NC) {
-                    const uint64_t w = __ldg(a.rounds + e);
-                    const int dst = (int)(w & 0xffff), self = (int)((w >> 16) & 0xffff),
-                              link = (int)((w >> 32) & 0xffff);
+                    const uint32_t w = s_rounds[e];
+                    const int slot = (int)(w & 0x3fff);
+                    const int dst = slot + ((w >> 14) & 1) * S2, self = slot + ((w >> 15) & 1) * S2,
+                              link = (int)(w >> 16);
                     float x[12], y[12], z[12];
                     ld3(P + link * 12, x);
                     ld3(P + self * 12, y);
@@ -279,12 +288,12 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                     const int e = eb + t + q * NC;
                     dst[q] = -1;
                     if (e < e1) {
-                        const uint64_t w = __ldg(a.rounds + e);
+                        const uint32_t w = s_rounds[e];
                         float x[12], y[12];
-                        ld3(P + ((w >> 32) & 0xffff) * 12, x);
-                        ld3(P + ((w >> 16) & 0xffff) * 12, y);
+                        ld3(P + (int)(w >> 16) * 12, x);
+                        ld3(P + (int)(w & 0x3fff) * 12, y);
                         compose(x, y, z[q]);
-                        dst[q] = (int)(w & 0xffff);
+                        dst[q] = (int)(w & 0x3fff);
                     }
                 }
                 bar_consumers(NC);

@@ -18,7 +18,8 @@ struct ChunkedArgs {
     const uint64_t* meta;      // [T][K]
     const int32_t* p1len;      // [T]
     const int32_t* round_off;  // [R2+1]
-    const uint64_t* rounds;
+    const uint32_t* rounds;    // phase-2 descriptors (copied to smem by each CTA)
+    int32_t n_rounds_entries;
     int32_t stages, sbufs;
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)

@@ -247,8 +247,11 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
             ent.push_back({wbuf * S + idx[s], latest[s] * S + idx[s], latest[lk[s]] * S + idx[lk[s]]});
         }
         order_round(ent);
-        for (auto& e : ent)
-            tp.rounds.push_back((uint64_t)e[0] | ((uint64_t)e[1] << 16) | ((uint64_t)e[2] << 32));
+        // 32-bit descriptor: slot | dst buffer << 14 | self buffer << 15 | link location << 16
+        for (auto& e : ent) {
+            const uint32_t slot = (uint32_t)(e[1] % S), sbuf = (uint32_t)(e[1] / S), wbuf = (uint32_t)(e[0] / S);
+            tp.rounds.push_back(slot | (wbuf << 14) | (sbuf << 15) | ((uint32_t)e[2] << 16));
+        }
         tp.max_round_entries = std::max(tp.max_round_entries, (int32_t)ent.size());
         std::vector<int32_t> nl(Sraw, -1);
         for (int32_t s = 0; s < Sraw; ++s) {
@@ -321,7 +324,8 @@ void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vec
 
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs) {
     const int64_t tileb = (int64_t)tp.F * 48, pb = (tp.pingpong ? 2LL : 1LL) * tp.nslots * 48;
-    return 128 + (int64_t)stages * tileb + (int64_t)sbufs * tileb + pb;
+    const int64_t tables = ((int64_t)(tp.R2 + 1) * 4 + (int64_t)tp.rounds.size() * 4 + 15) / 16 * 16;
+    return 128 + (int64_t)stages * tileb + (int64_t)sbufs * tileb + pb + tables;
 }
 
 }  // namespace hs

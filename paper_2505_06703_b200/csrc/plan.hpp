@@ -47,7 +47,7 @@ struct TileProgram {
     std::vector<uint64_t> meta;         // [T][K]: off | ibu<<16 | (u16)src<<32 | (u16)own<<48
     std::vector<int32_t> p1len;         // [T]: phase-1 length (last own anchor + 1)
     std::vector<int32_t> round_off;     // [R2 + 1] offsets into rounds
-    std::vector<uint64_t> rounds;       // dst | self<<16 | link<<32  (P locations)
+    std::vector<uint32_t> rounds;       // slot | dst buf<<14 | self buf<<15 | link location<<16
 };
 
 // Multi-CTA (split) program: the same decomposition over ONE character with
@@ -81,7 +81,7 @@ SplitProgram build_split_program(const Plan& p, int K);
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);
 
 // Shared-memory bytes of the chunked kernel for a tile program and stage counts
-// (without the optional inverse-bind copy, J * 48 bytes).
+// (tiles, skin buffers, anchor buffers, and the phase-2 tables staged in smem).
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs);
 
 }  // namespace hs
