@@ -76,7 +76,10 @@ typedef struct {
     int32_t sbufs;        /* skin staging buffers (1 or 2); 0 = auto                            */
     int32_t pbuf;         /* anchor buffer P: 2 = ping-pong (one barrier per round), 1 = single
                              buffer (two barriers per round, half the shared memory); 0 = auto */
-    int32_t reserved[2];  /* must be zero                                                      */
+    int32_t chunking;     /* thread chunks: 1 = runs of K consecutive internal positions (the
+                             paper's index blocks), 2 = heavy-path pieces packed per thread
+                             (fewer anchors); 0 = auto (2)                                    */
+    int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -146,7 +149,8 @@ typedef enum {
     HS_Q_DEVICE = 12,        /* CUDA device ordinal the handle lives on                        */
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
     HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
-    HS_Q_SBUFS = 16          /* skin staging buffers of the chunked kernel                      */
+    HS_Q_SBUFS = 16,         /* skin staging buffers of the chunked kernel                      */
+    HS_Q_CHUNKING = 17       /* chunk construction in use (1 consecutive, 2 heavy-path pieces)  */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);
@@ -174,9 +178,11 @@ typedef enum {
     HS_X_MPOB = 4,         /* int32 [n]   MaxParentOutBlock of each INTERNAL position, internal
                                           position of the nearest ancestor in another block, -1   */
     HS_X_CHUNK_SRC = 5,    /* int32 [n]   per INTERNAL position: -1 root, -2 previous joint of the
-                                          same chunk, >= 0 anchor = internal position of parent   */
-    HS_X_ANCHOR_LINK = 6   /* int32 [A]   per anchor slot (ascending internal position): link to
+                                          same chunk list, >= 0 anchor = internal position of parent */
+    HS_X_ANCHOR_LINK = 6,  /* int32 [A]   per anchor slot (ascending internal position): link to
                                           the anchor slot of its segment head's parent, or -1     */
+    HS_X_CHUNK_LISTS = 7   /* int32 [T][K] internal positions of each thread's chunk, -1 padded
+                                          (T = HS_Q_THREADS of the plan)                           */
 } hs_plan_export_what;
 
 /* Copy an export into buf (buf_bytes must be >= the export's size). */

@@ -37,10 +37,10 @@ ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf":
 QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "tile_chars": 5,
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
          "stages": 11, "device": 12, "split_levels": 13,
-         "pbufs": 15, "sbufs": 16}
+         "pbufs": 15, "sbufs": 16, "chunking": 17}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
-          "anchor_link": 6}
+          "anchor_link": 6, "chunk_lists": 7}
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -66,7 +66,7 @@ class _CreateOpts(ctypes.Structure):
     _fields_ = [("chunk", ctypes.c_int32), ("tile_joints", ctypes.c_int32),
                 ("force_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("sbufs", ctypes.c_int32), ("pbuf", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("chunking", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _ScanOpts(ctypes.Structure):
@@ -138,13 +138,19 @@ class Plan:
             size = self.query("rounds") * self.n
         elif what == "anchor_link":
             size = self.query("anchors")
+        elif what == "chunk_lists":
+            size = self.query("threads") * self.query("chunk")
         else:
             size = self.n
         out = np.empty(max(size, 1), np.int32)
         _check(lib().hs_plan_export(self._h, EXPORT[what], out.ctypes.data, out.nbytes),
                "hs_plan_export")
         out = out[:size]
-        return out.reshape(-1, self.n) if what == "lift" else out
+        if what == "lift":
+            return out.reshape(-1, self.n)
+        if what == "chunk_lists":
+            return out.reshape(-1, self.query("chunk"))
+        return out
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -158,7 +164,8 @@ class Skeleton:
     """A skeleton handle on the current CUDA device (hs_skeleton_create_ex)."""
 
     def __init__(self, parents, inv_bind=None, *, chunk: int = 0, tile_joints: int = 0,
-                 force_split: bool = False, stages: int = 0, sbufs: int = 0, pbuf: int = 0):
+                 force_split: bool = False, stages: int = 0, sbufs: int = 0, pbuf: int = 0,
+                 chunking: int = 0):
         L = lib()
         p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
         self.n_joints = len(p)
@@ -167,7 +174,7 @@ class Skeleton:
             ib = np.ascontiguousarray(np.asarray(inv_bind, dtype=np.float32))
             if ib.shape != (self.n_joints, 3, 4):
                 raise ValueError(f"inv_bind must be [{self.n_joints}, 3, 4]")
-        o = _CreateOpts(chunk, tile_joints, int(force_split), stages, sbufs, pbuf)
+        o = _CreateOpts(chunk, tile_joints, int(force_split), stages, sbufs, pbuf, chunking)
         h = ctypes.c_void_p()
         _check(L.hs_skeleton_create_ex(p.ctypes.data if self.n_joints else None, self.n_joints,
                                        None if ib is None else ib.ctypes.data, ctypes.byref(o),

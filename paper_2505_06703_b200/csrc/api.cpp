@@ -56,7 +56,7 @@ struct hs_skeleton {
     int K = 7;
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
-    int stages = 0, sbufs = 0, threads = 0;
+    int stages = 0, sbufs = 0, threads = 0, chunking = 1;
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -107,7 +107,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.pbuf < 0 || o.pbuf > 2 || o.reserved[0] || o.reserved[1])
+        o.pbuf < 0 || o.pbuf > 2 || o.chunking < 0 || o.chunking > 2 || o.reserved[0])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -126,7 +126,9 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     // --- chunked (single-CTA) program: C characters per tile, ~tile_target joints
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
-    const int64_t TC = (n + sk->K - 1) / sk->K;  // chunks per character
+    const int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE : hs::CHUNK_HEAVY;
+    sk->chunking = mode;
+    const int64_t TC = hs::build_tile_program(P, sk->K, 1, true, mode).T;  // chunks per character
     const int max_chunks = 224;  // compute threads per CTA (launch bounds 256 with the producer warp)
     while (C > 1 && C * TC > max_chunks) --C;
     if (!(o.force_split && depth == 0) && C * TC <= max_chunks && (int64_t)C * n <= 65535) {
@@ -135,8 +137,8 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         const int cand[][3] = {{3, 2, 1}, {3, 1, 1}, {2, 2, 1}, {2, 1, 1},
                                {3, 2, 0}, {3, 1, 0}, {2, 2, 0}, {2, 1, 0}};
         const int workers = (int)(((C * TC) + 31) / 32 * 32);
-        hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true);
-        hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false);
+        hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true, mode);
+        hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false, mode);
         const bool single_ok = tp_sb.max_round_entries <= 4 * workers;
         for (auto& c : cand) {
             if (o.stages && c[0] != o.stages) continue;
@@ -398,6 +400,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
+        case HS_Q_CHUNKING: *v = sk->chunking == hs::CHUNK_CONSECUTIVE ? 1 : 2; break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
@@ -433,7 +436,8 @@ hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk
         p->K = chunk == 0 ? 5 : chunk;
         if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..15"); }
         p->block_size = block_size <= 0 ? 64 : block_size;
-        p->decomp = hs::decompose(p->plan.ipar, p->K);
+        std::vector<int32_t> pos(p->plan.order);
+        p->decomp = hs::decompose(p->plan.ipar, p->K, hs::CHUNK_HEAVY, &pos);
         *out = p;
         return HS_OK;
     } catch (const std::bad_alloc&) {
@@ -449,9 +453,10 @@ hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
         case HS_Q_ROUNDS: *v = p->plan.R; break;
         case HS_Q_CHUNK: *v = p->K; break;
         case HS_Q_ANCHORS: *v = (int64_t)p->decomp.slots.size(); break;
+        case HS_Q_THREADS: *v = (int64_t)p->decomp.lists.size(); break;
         case HS_Q_IDENTITY_ORDER: *v = p->plan.identity ? 1 : 0; break;
         case HS_Q_ANCHOR_ROUNDS: {
-            hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1, true);
+            hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1, true, hs::CHUNK_HEAVY);
             *v = tp.R2;
             break;
         }
@@ -477,6 +482,11 @@ hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_
         }
         case HS_X_CHUNK_SRC: tmp = p->decomp.src; break;
         case HS_X_ANCHOR_LINK: tmp = p->decomp.link0; break;
+        case HS_X_CHUNK_LISTS:
+            tmp.assign(p->decomp.lists.size() * (size_t)p->K, -1);
+            for (size_t t = 0; t < p->decomp.lists.size(); ++t)
+                for (size_t s = 0; s < p->decomp.lists[t].size(); ++s) tmp[t * p->K + s] = p->decomp.lists[t][s];
+            break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown export");
     }
     if ((int64_t)(tmp.size() * sizeof(int32_t)) > buf_bytes) return fail(HS_ERR_INVALID_ARG, "buffer too small");

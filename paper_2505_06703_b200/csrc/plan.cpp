@@ -77,25 +77,121 @@ int build_plan(const int32_t* parents, int32_t n, Plan& P, std::string& err) {
     return kOk;
 }
 
-ChunkDecomp decompose(const std::vector<int32_t>& par, int K) {
+namespace {
+
+// Heavy-path pieces: walk every root's heavy path (child of largest subtree height,
+// smallest index on ties), recursing into the light children; cut each path into
+// pieces of at most K joints.  A piece is a parent-to-child chain.
+std::vector<std::vector<int32_t>> heavy_pieces(const std::vector<int32_t>& par, int K) {
+    const int32_t F = (int32_t)par.size();
+    std::vector<int32_t> first(F + 1, 0), kids(F), height(F, 1);
+    for (int32_t f = 0; f < F; ++f) if (par[f] >= 0) first[par[f] + 1]++;
+    for (int32_t f = 0; f < F; ++f) first[f + 1] += first[f];
+    {
+        std::vector<int32_t> fill(first.begin(), first.end() - 1);
+        for (int32_t f = 0; f < F; ++f) if (par[f] >= 0) kids[fill[par[f]]++] = f;
+    }
+    for (int32_t f = F - 1; f >= 0; --f)          // par[f] < f: reverse order is bottom-up
+        if (par[f] >= 0) height[par[f]] = std::max(height[par[f]], height[f] + 1);
+    std::vector<std::vector<int32_t>> pieces;
+    std::vector<int32_t> stack;                   // path starts
+    for (int32_t f = F - 1; f >= 0; --f) if (par[f] < 0) stack.push_back(f);
+    std::vector<int32_t> path;
+    while (!stack.empty()) {
+        int32_t v = stack.back();
+        stack.pop_back();
+        path.clear();
+        for (;;) {
+            path.push_back(v);
+            int32_t h = -1;
+            for (int32_t e = first[v]; e < first[v + 1]; ++e)
+                if (h < 0 || height[kids[e]] > height[h]) h = kids[e];
+            if (h < 0) break;
+            for (int32_t e = first[v + 1] - 1; e >= first[v]; --e)
+                if (kids[e] != h) stack.push_back(kids[e]);
+            v = h;
+        }
+        for (size_t i = 0; i < path.size(); i += (size_t)K)
+            pieces.emplace_back(path.begin() + (long)i, path.begin() + (long)std::min(path.size(), i + (size_t)K));
+    }
+    return pieces;
+}
+
+// First-fit-decreasing packing of pieces into lists of at most K joints.
+std::vector<std::vector<int32_t>> pack_pieces(std::vector<std::vector<int32_t>> pieces, int K) {
+    std::stable_sort(pieces.begin(), pieces.end(),
+                     [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) { return a.size() > b.size(); });
+    std::vector<std::vector<int32_t>> lists;
+    std::vector<int> room;
+    for (auto& pc : pieces) {
+        size_t i = 0;
+        while (i < lists.size() && room[i] < (int)pc.size()) ++i;
+        if (i == lists.size()) { lists.emplace_back(); room.push_back(K); }
+        lists[i].insert(lists[i].end(), pc.begin(), pc.end());
+        room[i] -= (int)pc.size();
+    }
+    return lists;
+}
+
+// Order lists so that each quarter warp (8 consecutive lists = threads) reads, at
+// every step, joints whose smem residues (3*pos mod 8, i.e. pos mod 8) differ.
+void order_lists(std::vector<std::vector<int32_t>>& lists, const std::vector<int32_t>& pos, int K) {
+    std::vector<std::vector<int32_t>> out;
+    out.reserve(lists.size());
+    std::vector<char> taken(lists.size(), 0);
+    size_t left = lists.size();
+    while (left) {
+        std::vector<std::array<char, 8>> used((size_t)K);
+        for (auto& u : used) u.fill(0);
+        for (int slot = 0; slot < 8 && left; ++slot) {
+            size_t best = 0;
+            int best_cost = 1 << 30;
+            for (size_t i = 0; i < lists.size(); ++i) {
+                if (taken[i]) continue;
+                int cost = 0;
+                for (size_t s = 0; s < lists[i].size(); ++s) cost += used[s][pos[lists[i][s]] & 7];
+                cost = cost * 64 - (int)lists[i].size();     // prefer full lists on ties
+                if (cost < best_cost) { best_cost = cost; best = i; }
+            }
+            taken[best] = 1;
+            --left;
+            for (size_t s = 0; s < lists[best].size(); ++s) used[s][pos[lists[best][s]] & 7] = 1;
+            out.push_back(lists[best]);
+        }
+    }
+    lists.swap(out);
+}
+
+}  // namespace
+
+ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const std::vector<int32_t>* pos) {
     const int32_t F = (int32_t)par.size();
     ChunkDecomp d;
     d.K = K;
+    if (mode == CHUNK_CONSECUTIVE) {
+        for (int32_t f = 0; f < F; f += K) {
+            d.lists.emplace_back();
+            for (int32_t g = f; g < std::min(F, f + K); ++g) d.lists.back().push_back(g);
+        }
+    } else {
+        d.lists = pack_pieces(heavy_pieces(par, K), K);
+        if (pos) order_lists(d.lists, *pos, K);
+    }
     d.src.assign(F, SRC_ROOT);
     d.slot_of.assign(F, -1);
-    for (int32_t f = 0; f < F; ++f) {
-        int32_t q = par[f];
-        if (q < 0) d.src[f] = SRC_ROOT;
-        else if (q == f - 1 && q / K == f / K) d.src[f] = SRC_PREV;
-        else d.src[f] = q;
-    }
+    std::vector<int32_t> head(F);
+    for (auto& L : d.lists)
+        for (size_t i = 0; i < L.size(); ++i) {
+            const int32_t f = L[i], q = par[f];
+            if (q < 0) { d.src[f] = SRC_ROOT; head[f] = f; }
+            else if (i > 0 && q == L[i - 1]) { d.src[f] = SRC_PREV; head[f] = head[q]; }
+            else { d.src[f] = q; head[f] = f; }
+        }
     std::vector<char> is_anchor(F, 0);
     for (int32_t f = 0; f < F; ++f)
         if (d.src[f] >= 0) is_anchor[d.src[f]] = 1;
     for (int32_t f = 0; f < F; ++f)
         if (is_anchor[f]) { d.slot_of[f] = (int32_t)d.slots.size(); d.slots.push_back(f); }
-    std::vector<int32_t> head(F);
-    for (int32_t f = 0; f < F; ++f) head[f] = d.src[f] == SRC_PREV ? head[f - 1] : f;
     d.link0.resize(d.slots.size());
     for (size_t s = 0; s < d.slots.size(); ++s) {
         int32_t h = head[d.slots[s]];
@@ -193,14 +289,16 @@ void order_round(std::vector<std::array<int32_t, 3>>& ent) {   // {dst, self, li
 
 }  // namespace
 
-TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
+TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int mode) {
     // Chunks never straddle characters: every character of a tile runs the same
     // program (same association order), so a character's bits do not depend on
     // its position in the batch, the tile size or the GPU count.
     TileProgram tp;
     const int32_t n = p.n;
-    const ChunkDecomp d = decompose(p.ipar, K);
-    const int32_t TC = (n + K - 1) / K;        // chunks (threads) per character
+    std::vector<int32_t> pos(n);               // smem position (joint index) of internal i
+    for (int32_t i = 0; i < n; ++i) pos[i] = p.order[i];
+    const ChunkDecomp d = decompose(p.ipar, K, mode, &pos);
+    const int32_t TC = (int32_t)d.lists.size();   // chunks (threads) per character
     const int32_t Sc = (int32_t)d.slots.size();
     tp.K = K;
     tp.C = C;
@@ -215,9 +313,8 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
         for (int c = 0; c < C; ++c)
             for (int32_t tc = 0; tc < TC; ++tc) {
                 const int32_t t = c * TC + tc;
-                for (int s = 0; s < K; ++s) {
-                    const int32_t i = tc * K + s;
-                    if (i >= n) continue;
+                for (int s = 0; s < (int)d.lists[tc].size(); ++s) {
+                    const int32_t i = d.lists[tc][s];
                     const size_t k = (size_t)(t / 8) * K + s;
                     if (d.src[i] >= 0) rd[k].push_back(c * Sc + d.slot_of[d.src[i]]);
                     if (d.slot_of[i] >= 0) wr[k].push_back(c * Sc + d.slot_of[i]);
@@ -269,10 +366,11 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong) {
         for (int32_t tc = 0; tc < TC; ++tc) {
             const int32_t t = c * TC + tc;
             for (int s = 0; s < K; ++s) {
-                const int32_t i = tc * K + s;     // internal position within the character
+                const bool has = s < (int)d.lists[tc].size();
+                const int32_t i = has ? d.lists[tc][s] : -1;   // internal position within the character
                 int32_t src = SRC_NONE, own = -1;
                 uint64_t off = 0, ibu = 0;
-                if (i < n) {
+                if (has) {
                     off = (uint64_t)(c * n + p.order[i]);
                     ibu = (uint64_t)p.order[i];
                     if (d.src[i] >= 0) {
@@ -295,18 +393,20 @@ SplitProgram build_split_program(const Plan& p, int K) {
     SplitProgram sp;
     sp.K = K;
     const int32_t n = p.n;
-    ChunkDecomp d = decompose(p.ipar, K);
+    ChunkDecomp d = decompose(p.ipar, K, CHUNK_HEAVY, nullptr);
     sp.nslots = (int32_t)d.slots.size();
-    sp.nchunks = (n + K - 1) / K;
+    sp.nchunks = (int32_t)d.lists.size();
     sp.meta.assign((size_t)sp.nchunks * K * 4, 0);
-    for (int32_t f = 0; f < sp.nchunks * K; ++f) {
-        int32_t* m = &sp.meta[(size_t)f * 4];
-        if (f >= n) { m[0] = 0; m[1] = SRC_NONE; m[2] = -1; m[3] = 0; continue; }
-        m[0] = p.order[f];
-        m[1] = d.src[f] >= 0 ? d.slot_of[d.src[f]] : d.src[f];
-        m[2] = d.slot_of[f];
-        m[3] = 0;
-    }
+    for (int32_t c = 0; c < sp.nchunks; ++c)
+        for (int s = 0; s < K; ++s) {
+            int32_t* m = &sp.meta[((size_t)c * K + s) * 4];
+            if (s >= (int)d.lists[c].size()) { m[0] = 0; m[1] = SRC_NONE; m[2] = -1; m[3] = 0; continue; }
+            const int32_t f = d.lists[c][s];
+            m[0] = p.order[f];
+            m[1] = d.src[f] >= 0 ? d.slot_of[d.src[f]] : d.src[f];
+            m[2] = d.slot_of[f];
+            m[3] = 0;
+        }
     sp.anchor_parents = d.link0;
     return sp;
 }

@@ -27,16 +27,25 @@
 namespace hs {
 
 enum : int32_t { SRC_ROOT = -1, SRC_PREV = -2, SRC_NONE = -3 };
+enum : int { CHUNK_CONSECUTIVE = 0, CHUNK_HEAVY = 1 };
 
-// Chunk decomposition of a flat forest given in topological order (par[f] < f).
+// Chunk decomposition of a flat forest given in topological order (par[f] < f):
+// per-thread lists of at most K nodes; a node's parent is either the previous node
+// of its list (PREV), absent (ROOT), or an ANCHOR elsewhere.
+//   CHUNK_CONSECUTIVE  lists = runs of K consecutive positions (the paper's index
+//                      blocks, at thread granularity)
+//   CHUNK_HEAVY        lists = heavy-path pieces (<= K joints) packed first-fit
+//                      decreasing, then ordered for conflict-free smem access
 struct ChunkDecomp {
     int K = 0;
+    std::vector<std::vector<int32_t>> lists;
     std::vector<int32_t> src;      // per node: SRC_ROOT, SRC_PREV, or anchor node index (>= 0)
     std::vector<int32_t> slot_of;  // per node: anchor slot or -1
     std::vector<int32_t> slots;    // slot -> node (ascending node index => topological)
     std::vector<int32_t> link0;    // slot -> slot of anchor(seghead(node)), or -1
 };
-ChunkDecomp decompose(const std::vector<int32_t>& par, int K);
+ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode,
+                      const std::vector<int32_t>* smem_pos);
 
 // Persistent-tile program for the single-CTA chunked kernel.
 struct TileProgram {
@@ -74,7 +83,7 @@ struct Plan {
 // Returns 0 (HS_OK) or an hs_status code; err gets a message.
 int build_plan(const int32_t* parents, int32_t n, Plan& out, std::string& err);
 
-TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong);
+TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int mode);
 SplitProgram build_split_program(const Plan& p, int K);
 
 // The paper's block layout for block size B over INTERNAL positions (exports).

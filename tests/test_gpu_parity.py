@@ -70,6 +70,7 @@ EXACT_CASES = [
     ("hum64", {"tile_joints": 200}), ("tree1024", {"stages": 2, "sbufs": 1}),
     ("tree1024", {"pbuf": 2}), ("chain256", {"pbuf": 1}), ("tree1024", {"pbuf": 1, "chunk": 9}),
     ("hum32", {"pbuf": 1, "stages": 3, "sbufs": 2}),
+    ("tree1024", {"chunking": 1}), ("hum64", {"chunking": 1, "chunk": 7}),
     ("tree1024", {"force_split": True}), ("chain256", {"force_split": True, "chunk": 3}),
 ]
 

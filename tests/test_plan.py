@@ -170,6 +170,7 @@ def _chunk_emulation(par, local, K):
     order = pl.export("order")
     src = pl.export("chunk_src")
     link = pl.export("anchor_link")
+    lists = [[int(f) for f in row if f >= 0] for row in pl.export("chunk_lists")]
     n = len(par)
     H = np.zeros((n, 4, 4)); H[:, :3] = local[order]; H[:, 3, 3] = 1
     anchors = sorted(set(int(s) for s in src if s >= 0))
@@ -177,9 +178,9 @@ def _chunk_emulation(par, local, K):
     assert len(anchors) == len(link)
     # phase 1: per-chunk left fold; publish at anchors
     P = np.zeros((len(anchors), 4, 4))
-    for c0 in range(0, n, K):
+    for chunk in lists:
         acc = None
-        for f in range(c0, min(c0 + K, n)):
+        for f in chunk:
             acc = acc @ H[f] if src[f] == -2 else H[f]
             if f in slot:
                 P[slot[f]] = acc
@@ -194,9 +195,9 @@ def _chunk_emulation(par, local, K):
         lk = np.array([lk[lk[s]] if lk[s] >= 0 else -1 for s in range(len(anchors))], np.int32)
     # phase 3: re-fold from the final anchor values
     G = np.zeros((n, 4, 4))
-    for c0 in range(0, n, K):
+    for chunk in lists:
         acc = None
-        for f in range(c0, min(c0 + K, n)):
+        for f in chunk:
             if src[f] == -2:
                 acc = acc @ H[f]
             elif src[f] == -1:
@@ -232,13 +233,22 @@ def test_decomposition_invariants():
         rank = np.empty(n, int); rank[order] = np.arange(n)
         ipar = np.array([-1 if par[u] < 0 else rank[par[u]] for u in order])
         src = pl.export("chunk_src")
+        lists = pl.export("chunk_lists")
+        flat = lists[lists >= 0]
+        assert sorted(flat) == list(range(n))          # every joint in exactly one list
+        assert lists.shape[1] == K
+        prev_of = {}
+        for row in lists:
+            row = [int(f) for f in row if f >= 0]
+            for a, b in zip(row, row[1:]):
+                prev_of[b] = a
         for f in range(n):
             if src[f] == -1:
                 assert ipar[f] == -1
             elif src[f] == -2:
-                assert ipar[f] == f - 1 and (f - 1) // K == f // K
+                assert prev_of.get(f) == ipar[f]
             else:
-                assert src[f] == ipar[f] and not (ipar[f] == f - 1 and (f - 1) // K == f // K)
+                assert src[f] == ipar[f] and prev_of.get(f) != ipar[f]
         assert pl.query("anchors") == len(set(int(s) for s in src if s >= 0))
 
 
