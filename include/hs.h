@@ -78,7 +78,8 @@ typedef struct {
                              buffer (two barriers per round, half the shared memory); 0 = auto */
     int32_t chunking;     /* thread chunks: 1 = runs of K consecutive internal positions (the
                              paper's index blocks), 2 = heavy-path pieces packed per thread
-                             (fewer anchors); 0 = auto (2)                                    */
+                             (fewer anchors); 0 = auto (2 when it cuts phase-2 work without
+                             adding threads per character, else 1)                           */
     int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 

@@ -126,7 +126,15 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     // --- chunked (single-CTA) program: C characters per tile, ~tile_target joints
     const int tile_target = o.tile_joints ? o.tile_joints : 1024;
     int C = std::max(1, tile_target / std::max(1, n));
-    const int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE : hs::CHUNK_HEAVY;
+    // chunk construction: heavy-path pieces cut anchors on branchy skeletons, but may need
+    // more threads per character (smaller tiles); auto keeps them only when they do not
+    int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE : hs::CHUNK_HEAVY;
+    if (o.chunking == 0) {
+        const hs::TileProgram a1 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_CONSECUTIVE);
+        const hs::TileProgram a2 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_HEAVY);
+        const bool fewer = a2.rounds.size() < a1.rounds.size();
+        mode = (fewer && a2.T <= a1.T) ? hs::CHUNK_HEAVY : hs::CHUNK_CONSECUTIVE;
+    }
     sk->chunking = mode;
     const int64_t TC = hs::build_tile_program(P, sk->K, 1, true, mode).T;  // chunks per character
     const int max_chunks = 224;  // compute threads per CTA (launch bounds 256 with the producer warp)
