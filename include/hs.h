@@ -151,7 +151,10 @@ typedef enum {
     HS_Q_SPLIT_LEVELS = 13,  /* recursion depth of the multi-CTA path (0 if single-CTA)         */
     HS_Q_PBUFS = 15,         /* anchor buffers of the chunked kernel (2 ping-pong, 1 single)    */
     HS_Q_SBUFS = 16,         /* skin staging buffers of the chunked kernel                      */
-    HS_Q_CHUNKING = 17       /* chunk construction in use (1 consecutive, 2 heavy-path pieces)  */
+    HS_Q_CHUNKING = 17,      /* chunk construction in use (1 consecutive, 2 heavy-path pieces)  */
+    HS_Q_TILE_SLOTS = 18,    /* plan only: P slots of the one-character tile program            */
+    HS_Q_TILE_ROUNDS_ENTRIES = 19, /* plan only: phase-2 descriptors of that program           */
+    HS_Q_TILE_R2 = 20        /* plan only: its pointer-jumping rounds                           */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);
@@ -182,8 +185,14 @@ typedef enum {
                                           same chunk list, >= 0 anchor = internal position of parent */
     HS_X_ANCHOR_LINK = 6,  /* int32 [A]   per anchor slot (ascending internal position): link to
                                           the anchor slot of its segment head's parent, or -1     */
-    HS_X_CHUNK_LISTS = 7   /* int32 [T][K] internal positions of each thread's chunk, -1 padded
+    HS_X_CHUNK_LISTS = 7,  /* int32 [T][K] internal positions of each thread's chunk, -1 padded
                                           (T = HS_Q_THREADS of the plan)                           */
+    /* The chunked kernel's tile program for ONE character (ping-pong P), as uploaded: */
+    HS_X_TILE_META = 8,    /* uint64 [T][K]: user joint | ibu<<16 | int16 src<<32 | int16 own<<48;
+                              src: -1 root, -2 previous, -3 none, >= 0 P location of the parent */
+    HS_X_TILE_P1LEN = 9,   /* int32 [T]: phase-1 length of each thread                          */
+    HS_X_TILE_ROUND_OFF = 10, /* int32 [R2+1]: start of each pointer-jumping round              */
+    HS_X_TILE_ROUNDS = 11  /* uint32 [E]: slot | dst buffer<<14 | self buffer<<15 | link loc<<16 */
 } hs_plan_export_what;
 
 /* Copy an export into buf (buf_bytes must be >= the export's size). */

@@ -37,10 +37,12 @@ ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf":
 QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "tile_chars": 5,
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
          "stages": 11, "device": 12, "split_levels": 13,
-         "pbufs": 15, "sbufs": 16, "chunking": 17}
+         "pbufs": 15, "sbufs": 16, "chunking": 17, "tile_slots": 18, "tile_rounds_entries": 19,
+         "tile_r2": 20}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
-          "anchor_link": 6, "chunk_lists": 7}
+          "anchor_link": 6, "chunk_lists": 7, "tile_meta": 8, "tile_p1len": 9,
+          "tile_round_off": 10, "tile_rounds": 11}
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -134,6 +136,16 @@ class Plan:
         return v.value
 
     def export(self, what: str) -> np.ndarray:
+        if what.startswith("tile_"):
+            T, K = self.query("threads"), self.query("chunk")
+            dtype, size = {"tile_meta": (np.uint64, T * K), "tile_p1len": (np.int32, T),
+                           "tile_round_off": (np.int32, self.query("tile_r2") + 1),
+                           "tile_rounds": (np.uint32, self.query("tile_rounds_entries"))}[what]
+            out = np.empty(max(size, 1), dtype)
+            _check(lib().hs_plan_export(self._h, EXPORT[what], out.ctypes.data, out.nbytes),
+                   "hs_plan_export")
+            out = out[:size]
+            return out.reshape(T, K) if what == "tile_meta" else out
         if what == "lift":
             size = self.query("rounds") * self.n
         elif what == "anchor_link":

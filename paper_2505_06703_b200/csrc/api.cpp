@@ -48,6 +48,7 @@ struct hs_plan {
     int K = 7;
     int block_size = 64;
     hs::ChunkDecomp decomp;
+    hs::TileProgram tile;   // the chunked kernel's program for one character (ping-pong P)
 };
 
 struct hs_skeleton {
@@ -445,7 +446,8 @@ hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk
         if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..15"); }
         p->block_size = block_size <= 0 ? 64 : block_size;
         std::vector<int32_t> pos(p->plan.order);
-        p->decomp = hs::decompose(p->plan.ipar, p->K, hs::CHUNK_HEAVY, &pos);
+        p->decomp = hs::decompose(p->plan.ipar, p->K, hs::CHUNK_HEAVY, &pos, true);
+        p->tile = hs::build_tile_program(p->plan, p->K, 1, true, hs::CHUNK_HEAVY);
         *out = p;
         return HS_OK;
     } catch (const std::bad_alloc&) {
@@ -462,6 +464,9 @@ hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
         case HS_Q_CHUNK: *v = p->K; break;
         case HS_Q_ANCHORS: *v = (int64_t)p->decomp.slots.size(); break;
         case HS_Q_THREADS: *v = (int64_t)p->decomp.lists.size(); break;
+        case HS_Q_TILE_SLOTS: *v = p->tile.nslots; break;
+        case HS_Q_TILE_ROUNDS_ENTRIES: *v = (int64_t)p->tile.rounds.size(); break;
+        case HS_Q_TILE_R2: *v = p->tile.R2; break;
         case HS_Q_IDENTITY_ORDER: *v = p->plan.identity ? 1 : 0; break;
         case HS_Q_ANCHOR_ROUNDS: {
             hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1, true, hs::CHUNK_HEAVY);
@@ -477,7 +482,17 @@ hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_
     if (!p || !buf) return fail(HS_ERR_INVALID_ARG, "null argument");
     std::vector<int32_t> tmp;
     const hs::Plan& P = p->plan;
+    const hs::TileProgram& tp = p->tile;
+    auto raw = [&](const void* src, size_t bytes) -> hs_status {
+        if ((int64_t)bytes > buf_bytes) return fail(HS_ERR_INVALID_ARG, "buffer too small");
+        if (bytes) std::memcpy(buf, src, bytes);
+        return HS_OK;
+    };
     switch (what) {
+        case HS_X_TILE_META: return raw(tp.meta.data(), tp.meta.size() * sizeof(uint64_t));
+        case HS_X_TILE_P1LEN: return raw(tp.p1len.data(), tp.p1len.size() * sizeof(int32_t));
+        case HS_X_TILE_ROUND_OFF: return raw(tp.round_off.data(), tp.round_off.size() * sizeof(int32_t));
+        case HS_X_TILE_ROUNDS: return raw(tp.rounds.data(), tp.rounds.size() * sizeof(uint32_t));
         case HS_X_LEVELS: tmp = P.level; break;
         case HS_X_ORDER: tmp = P.order; break;
         case HS_X_LIFT: tmp = P.lift; break;

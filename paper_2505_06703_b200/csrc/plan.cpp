@@ -133,6 +133,51 @@ std::vector<std::vector<int32_t>> pack_pieces(std::vector<std::vector<int32_t>> 
     return lists;
 }
 
+// Pairwise-swap local search over a sequence cut into quarter-warp groups of 8:
+// item i contributes residue keys keys[i][d] (d = 0..D-1, -1 = no access); the cost
+// of a group is sum_d max_r count(d, r) — the wavefronts its D 128-bit accesses
+// take.  Swaps items between groups while the total cost drops.
+void swap_search(std::vector<std::vector<int>>& keys, std::vector<int32_t>& perm, int D) {
+    const int n = (int)perm.size();
+    const int G = (n + 7) / 8;
+    if (G < 2) return;
+    std::vector<int> cnt((size_t)G * D * 8, 0);
+    auto at = [&](int g, int d, int r) -> int& { return cnt[((size_t)g * D + d) * 8 + r]; };
+    auto gmax = [&](int g, int d) { int m = 0; for (int r = 0; r < 8; ++r) m = std::max(m, at(g, d, r)); return m; };
+    for (int i = 0; i < n; ++i)
+        for (int d = 0; d < D; ++d)
+            if (keys[perm[i]][d] >= 0) at(i / 8, d, keys[perm[i]][d])++;
+    for (int pass = 0; pass < 8; ++pass) {
+        bool improved = false;
+        for (int i = 0; i < n; ++i)
+            for (int j = (i / 8 + 1) * 8; j < n; ++j) {
+                const int gi = i / 8, gj = j / 8;
+                int before = 0, after = 0;
+                for (int d = 0; d < D; ++d) {
+                    const int ki = keys[perm[i]][d], kj = keys[perm[j]][d];
+                    if (ki == kj) continue;
+                    before += gmax(gi, d) + gmax(gj, d);
+                    if (ki >= 0) { at(gi, d, ki)--; at(gj, d, ki)++; }
+                    if (kj >= 0) { at(gj, d, kj)--; at(gi, d, kj)++; }
+                    after += gmax(gi, d) + gmax(gj, d);
+                    if (ki >= 0) { at(gi, d, ki)++; at(gj, d, ki)--; }
+                    if (kj >= 0) { at(gj, d, kj)++; at(gi, d, kj)--; }
+                }
+                if (after < before) {
+                    for (int d = 0; d < D; ++d) {
+                        const int ki = keys[perm[i]][d], kj = keys[perm[j]][d];
+                        if (ki == kj) continue;
+                        if (ki >= 0) { at(gi, d, ki)--; at(gj, d, ki)++; }
+                        if (kj >= 0) { at(gj, d, kj)--; at(gi, d, kj)++; }
+                    }
+                    std::swap(perm[i], perm[j]);
+                    improved = true;
+                }
+            }
+        if (!improved) break;
+    }
+}
+
 // Order lists so that each quarter warp (8 consecutive lists = threads) reads, at
 // every step, joints whose smem residues (3*pos mod 8, i.e. pos mod 8) differ.
 void order_lists(std::vector<std::vector<int32_t>>& lists, const std::vector<int32_t>& pos, int K) {
@@ -159,12 +204,20 @@ void order_lists(std::vector<std::vector<int32_t>>& lists, const std::vector<int
             out.push_back(lists[best]);
         }
     }
-    lists.swap(out);
+    std::vector<std::vector<int>> keys(out.size(), std::vector<int>((size_t)K, -1));
+    for (size_t i = 0; i < out.size(); ++i)
+        for (size_t s = 0; s < out[i].size(); ++s) keys[i][s] = pos[out[i][s]] & 7;
+    std::vector<int32_t> perm(out.size());
+    for (size_t i = 0; i < out.size(); ++i) perm[i] = (int32_t)i;
+    swap_search(keys, perm, K);
+    lists.clear();
+    for (int32_t i : perm) lists.push_back(out[i]);
 }
 
 }  // namespace
 
-ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const std::vector<int32_t>* pos) {
+ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const std::vector<int32_t>* pos,
+                      bool pad_to_warp) {
     const int32_t F = (int32_t)par.size();
     ChunkDecomp d;
     d.K = K;
@@ -175,7 +228,11 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const st
         }
     } else {
         d.lists = pack_pieces(heavy_pieces(par, K), K);
+        // idle lanes of the last warp are free: empty lists give the ordering room
+        if (pad_to_warp) d.lists.resize((d.lists.size() + 31) / 32 * 32);
         if (pos) order_lists(d.lists, *pos, K);
+        if (pad_to_warp)   // keep empty lists only where the ordering placed them before a real one
+            while (!d.lists.empty() && d.lists.back().empty()) d.lists.pop_back();
     }
     d.src.assign(F, SRC_ROOT);
     d.slot_of.assign(F, -1);
@@ -284,7 +341,13 @@ void order_round(std::vector<std::array<int32_t, 3>>& ent) {   // {dst, self, li
             --left;
         }
     }
-    ent.swap(out);
+    std::vector<std::vector<int>> keys(out.size(), std::vector<int>(2));
+    for (size_t i = 0; i < out.size(); ++i) { keys[i][0] = out[i][1] & 7; keys[i][1] = out[i][2] & 7; }
+    std::vector<int32_t> perm(out.size());
+    for (size_t i = 0; i < out.size(); ++i) perm[i] = (int32_t)i;
+    swap_search(keys, perm, 2);
+    ent.clear();
+    for (int32_t i : perm) ent.push_back(out[i]);
 }
 
 }  // namespace
@@ -297,7 +360,7 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int m
     const int32_t n = p.n;
     std::vector<int32_t> pos(n);               // smem position (joint index) of internal i
     for (int32_t i = 0; i < n; ++i) pos[i] = p.order[i];
-    const ChunkDecomp d = decompose(p.ipar, K, mode, &pos);
+    const ChunkDecomp d = decompose(p.ipar, K, mode, &pos, C == 1);
     const int32_t TC = (int32_t)d.lists.size();   // chunks (threads) per character
     const int32_t Sc = (int32_t)d.slots.size();
     tp.K = K;
@@ -393,7 +456,7 @@ SplitProgram build_split_program(const Plan& p, int K) {
     SplitProgram sp;
     sp.K = K;
     const int32_t n = p.n;
-    ChunkDecomp d = decompose(p.ipar, K, CHUNK_HEAVY, nullptr);
+    ChunkDecomp d = decompose(p.ipar, K, CHUNK_HEAVY, nullptr, false);
     sp.nslots = (int32_t)d.slots.size();
     sp.nchunks = (int32_t)d.lists.size();
     sp.meta.assign((size_t)sp.nchunks * K * 4, 0);

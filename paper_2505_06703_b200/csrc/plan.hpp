@@ -45,7 +45,7 @@ struct ChunkDecomp {
     std::vector<int32_t> link0;    // slot -> slot of anchor(seghead(node)), or -1
 };
 ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode,
-                      const std::vector<int32_t>* smem_pos);
+                      const std::vector<int32_t>* smem_pos, bool pad_to_warp);
 
 // Persistent-tile program for the single-CTA chunked kernel.
 struct TileProgram {

@@ -262,3 +262,20 @@ def test_errors_from_plan():
     with pytest.raises(hs.HSError) as e:
         hs.Plan([-1, 0], chunk=4)
     assert e.value.status == hs.HS_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("name", ["hum32", "hum64", "chain256", "tree1024", "perm_tree"])
+def test_tile_program_emulation_bitwise(name):
+    """Replay the exact uploaded tile program (ping-pong locations, colouring, round
+    order) on the host: bitwise equal to the oracle on the exact family."""
+    from tests import tile_emulator
+    if name == "perm_tree":
+        par, _ = hsgen.relabel(hsgen.skeleton("tree1024"), hsgen.permutation(3, 1024))
+    else:
+        par = hsgen.skeleton(name)
+    J = len(par)
+    local = hsgen.exact_poses(22, J, 1)[0]
+    ib = hsgen.exact_inv_bind(22, J)
+    G, S = oracle.scan(par, local, ib)
+    g, s, _ = tile_emulator.run(hs.Plan(par), local, ib)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
