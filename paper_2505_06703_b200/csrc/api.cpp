@@ -134,7 +134,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         const hs::TileProgram a1 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_CONSECUTIVE);
         const hs::TileProgram a2 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_HEAVY);
         const bool fewer = a2.rounds.size() < a1.rounds.size();
-        mode = (fewer && a2.T <= a1.T) ? hs::CHUNK_HEAVY : hs::CHUNK_CONSECUTIVE;
+        mode = (fewer && a2.lists_nonempty <= a1.lists_nonempty) ? hs::CHUNK_HEAVY : hs::CHUNK_CONSECUTIVE;
     }
     sk->chunking = mode;
     const int64_t TC = hs::build_tile_program(P, sk->K, 1, true, mode).T;  // chunks per character

@@ -147,7 +147,8 @@ void swap_search(std::vector<std::vector<int>>& keys, std::vector<int32_t>& perm
     for (int i = 0; i < n; ++i)
         for (int d = 0; d < D; ++d)
             if (keys[perm[i]][d] >= 0) at(i / 8, d, keys[perm[i]][d])++;
-    for (int pass = 0; pass < 8; ++pass) {
+    const int passes = n > 4096 ? 1 : (n > 1024 ? 3 : 8);   // O(n^2) per pass
+    for (int pass = 0; pass < passes; ++pass) {
         bool improved = false;
         for (int i = 0; i < n; ++i)
             for (int j = (i / 8 + 1) * 8; j < n; ++j) {
@@ -362,6 +363,8 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int m
     for (int32_t i = 0; i < n; ++i) pos[i] = p.order[i];
     const ChunkDecomp d = decompose(p.ipar, K, mode, &pos, C == 1);
     const int32_t TC = (int32_t)d.lists.size();   // chunks (threads) per character
+    tp.lists_nonempty = 0;
+    for (auto& l : d.lists) tp.lists_nonempty += l.empty() ? 0 : 1;
     const int32_t Sc = (int32_t)d.slots.size();
     tp.K = K;
     tp.C = C;

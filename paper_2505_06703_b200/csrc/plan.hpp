@@ -53,6 +53,7 @@ struct TileProgram {
     int nslots = 0, R2 = 0;             // anchor slots per tile, pointer-jumping rounds
     bool pingpong = true;               // P double-buffered (else: 2 barriers per round)
     int max_round_entries = 0;          // largest round (single buffer needs <= 4 per thread)
+    int lists_nonempty = 0;             // chunks with work per character (T may include padding)
     std::vector<uint64_t> meta;         // [T][K]: off | ibu<<16 | (u16)src<<32 | (u16)own<<48
     std::vector<int32_t> p1len;         // [T]: phase-1 length (last own anchor + 1)
     std::vector<int32_t> round_off;     // [R2 + 1] offsets into rounds
