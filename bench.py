@@ -63,7 +63,6 @@ def parse_args(argv=None):
     ap.add_argument("--sbufs", type=int, default=0)
     ap.add_argument("--pbuf", type=int, default=0)
     ap.add_argument("--chunking", type=int, default=0, help="1 = consecutive, 2 = heavy-path pieces")
-    ap.add_argument("--pipeline", type=int, default=0, help="1 = chunked, 2 = software-pipelined")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no checks, no e2e, no cpu baseline")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
@@ -257,7 +256,7 @@ def run_ours(args):
         c0, n = shard(n_total, rank, world, args.scaling)
         sk = hs.Skeleton(par, ib, chunk=args.chunk, tile_joints=args.tile_joints,
                          stages=args.stages, sbufs=args.sbufs, pbuf=args.pbuf,
-                         chunking=args.chunking, pipeline=args.pipeline)
+                         chunking=args.chunking)
         local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
         if n:
             rc = hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, c0, n, local.data_ptr(),
@@ -344,8 +343,7 @@ def run_ours(args):
                    "stages": {w["name"]: w["sk"].query("stages") for w in work},
                    "sbufs": {w["name"]: w["sk"].query("sbufs") for w in work},
                    "pbufs": {w["name"]: w["sk"].query("pbufs") for w in work},
-                   "chunking": work[dom]["sk"].query("chunking"),
-                   "pipelined": {w["name"]: w["sk"].query("pipelined") for w in work}},
+                   "chunking": work[dom]["sk"].query("chunking")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"chunked_kernel ({work[dom]['name']} launch)",

@@ -80,10 +80,7 @@ typedef struct {
                              paper's index blocks), 2 = heavy-path pieces packed per thread
                              (fewer anchors); 0 = auto (2 when it cuts phase-2 work without
                              adding threads per character, else 1)                           */
-    int32_t pipeline;     /* 1 = chunked kernel (phases 1, 2, 3 of one tile in sequence); 2 = the
-                             software-pipelined kernel (phase 3 of tile i-1 runs inside tile
-                             i's pointer-jumping rounds; needs the single-buffer P program);
-                             0 = auto (pipelined when it fits)                                */
+    int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 
 /* hs_skeleton_create with explicit options (opts == NULL: automatic).
@@ -157,8 +154,7 @@ typedef enum {
     HS_Q_CHUNKING = 17,      /* chunk construction in use (1 consecutive, 2 heavy-path pieces)  */
     HS_Q_TILE_SLOTS = 18,    /* plan only: P slots of the one-character tile program            */
     HS_Q_TILE_ROUNDS_ENTRIES = 19, /* plan only: phase-2 descriptors of that program           */
-    HS_Q_TILE_R2 = 20,       /* plan only: its pointer-jumping rounds                           */
-    HS_Q_PIPELINED = 21      /* 1 if hs_scan runs the software-pipelined chunked kernel         */
+    HS_Q_TILE_R2 = 20        /* plan only: its pointer-jumping rounds                           */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

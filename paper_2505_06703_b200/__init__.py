@@ -38,7 +38,7 @@ QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "til
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
          "stages": 11, "device": 12, "split_levels": 13,
          "pbufs": 15, "sbufs": 16, "chunking": 17, "tile_slots": 18, "tile_rounds_entries": 19,
-         "tile_r2": 20, "pipelined": 21}
+         "tile_r2": 20}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
           "anchor_link": 6, "chunk_lists": 7, "tile_meta": 8, "tile_p1len": 9,
@@ -68,7 +68,7 @@ class _CreateOpts(ctypes.Structure):
     _fields_ = [("chunk", ctypes.c_int32), ("tile_joints", ctypes.c_int32),
                 ("force_split", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("sbufs", ctypes.c_int32), ("pbuf", ctypes.c_int32),
-                ("chunking", ctypes.c_int32), ("pipeline", ctypes.c_int32)]
+                ("chunking", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _ScanOpts(ctypes.Structure):
@@ -177,7 +177,7 @@ class Skeleton:
 
     def __init__(self, parents, inv_bind=None, *, chunk: int = 0, tile_joints: int = 0,
                  force_split: bool = False, stages: int = 0, sbufs: int = 0, pbuf: int = 0,
-                 chunking: int = 0, pipeline: int = 0):
+                 chunking: int = 0):
         L = lib()
         p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
         self.n_joints = len(p)
@@ -186,8 +186,7 @@ class Skeleton:
             ib = np.ascontiguousarray(np.asarray(inv_bind, dtype=np.float32))
             if ib.shape != (self.n_joints, 3, 4):
                 raise ValueError(f"inv_bind must be [{self.n_joints}, 3, 4]")
-        o = _CreateOpts(chunk, tile_joints, int(force_split), stages, sbufs, pbuf, chunking,
-                        pipeline)
+        o = _CreateOpts(chunk, tile_joints, int(force_split), stages, sbufs, pbuf, chunking)
         h = ctypes.c_void_p()
         _check(L.hs_skeleton_create_ex(p.ctypes.data if self.n_joints else None, self.n_joints,
                                        None if ib is None else ib.ctypes.data, ctypes.byref(o),

@@ -58,7 +58,6 @@ struct hs_skeleton {
     bool chunked = false;          // single-CTA chunked path fits
     hs::TileProgram tp;
     int stages = 0, sbufs = 0, threads = 0, chunking = 1;
-    bool pipelined = false;        // pipelined_kernel (phase 3 of tile i-1 folded into tile i's rounds)
     int64_t smem = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
@@ -109,7 +108,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.pbuf < 0 || o.pbuf > 2 || o.chunking < 0 || o.chunking > 2 || o.pipeline < 0 || o.pipeline > 2)
+        o.pbuf < 0 || o.pbuf > 2 || o.chunking < 0 || o.chunking > 2 || o.reserved[0])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -150,26 +149,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         hs::TileProgram tp_pp = hs::build_tile_program(P, sk->K, C, true, mode);
         hs::TileProgram tp_sb = hs::build_tile_program(P, sk->K, C, false, mode);
         const bool single_ok = tp_sb.max_round_entries <= 4 * workers;
-        // software-pipelined kernel first (two single-buffer P areas), unless disabled
-        if (o.pipeline != 1 && single_ok && !(o.pbuf == 2)) {
-            const int pcand[][2] = {{3, 1}, {2, 2}, {2, 1}};
-            for (auto& c : pcand) {
-                if (o.stages && c[0] != o.stages) continue;
-                if (o.sbufs && c[1] != o.sbufs) continue;
-                const int64_t b = hs::tile_smem_bytes(tp_sb, c[0], c[1]) + (int64_t)tp_sb.nslots * 48;
-                if (b <= smem_optin && 2 * tp_sb.nslots < 32768) {
-                    sk->tp = tp_sb;
-                    sk->stages = c[0];
-                    sk->sbufs = c[1];
-                    sk->smem = b;
-                    sk->chunked = true;
-                    sk->pipelined = true;
-                    break;
-                }
-            }
-        }
         for (auto& c : cand) {
-            if (sk->chunked || o.pipeline == 2) break;
             if (o.stages && c[0] != o.stages) continue;
             if (o.sbufs && c[1] != o.sbufs) continue;
             if (o.pbuf && (c[2] ? 2 : 1) != o.pbuf) continue;
@@ -269,7 +249,6 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.meta = sk->d_meta; a.p1len = sk->d_p1len; a.round_off = sk->d_round_off;
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
             a.n_rounds_entries = (int32_t)sk->tp.rounds.size();
-            a.pipelined = sk->pipelined ? 1 : 0;
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
             a.p_single = sk->tp.pingpong ? 0 : 1;
@@ -431,7 +410,6 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
         case HS_Q_CHUNKING: *v = sk->chunking == hs::CHUNK_CONSECUTIVE ? 1 : 2; break;
-        case HS_Q_PIPELINED: *v = sk->pipelined ? 1 : 0; break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }

@@ -347,223 +347,6 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     }
 }
 
-
-// ================================================================== pipelined kernel
-// Software-pipelined variant of chunked_kernel (the default): iteration `it` runs
-// phase 1 of tile it, then the pointer-jumping rounds of tile it with, folded into
-// the same barrier intervals, the phase-3 steps (and bind) of tile it-1.  Phase 3's
-// latency hides in the rounds' barrier shadow.  Two P areas (tile parity), each a
-// single buffer (all reads of a round, barrier, writes, barrier); the tile program
-// must be built without ping-pong.  Same producer and smem ring as chunked_kernel.
-template <int K>
-__global__ void __launch_bounds__(256, 1) pipelined_kernel(const ChunkedArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int NS = a.stages, NSS = a.sbufs;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* done = full + 4;
-    uint64_t* sfree = done + 4;
-    float* LG = reinterpret_cast<float*>(smem + 128);
-    const int64_t tile_f = (int64_t)a.F * 12;
-    float* SB = LG + NS * tile_f;
-    float* P0 = SB + NSS * tile_f;                       // two P areas, by tile parity
-    const int parea = a.nslots * 12;
-    int32_t* s_round_off = reinterpret_cast<int32_t*>(P0 + 2 * parea);
-    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + a.R2 + 1);
-
-    const int nwc = (int)(blockDim.x >> 5) - 1;
-    const int NC = nwc * 32;
-    const int warp = threadIdx.x >> 5;
-    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const bool do_skin = a.sout != nullptr;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
-        for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == nwc) {
-        // ------------------------------------------------------------ producer
-        if ((threadIdx.x & 31) != 0) return;
-        auto issue_load = [&](int64_t it) {
-            const int stage = (int)(it % NS);
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
-            mbar_expect_tx(&full[stage], bytes);
-            bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
-        };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
-        for (int64_t it = 0; it < my_tiles; ++it) {
-            const int stage = (int)(it % NS);
-            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const uint32_t bytes = (uint32_t)(min((int64_t)a.C, a.n_chars - c0) * a.J * 48);
-            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-            if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
-            bulk_commit();
-            bulk_wait_read<0>();
-            if (do_skin) mbar_arrive(&sfree[it % NSS]);
-            if (it + NS < my_tiles) issue_load(it + NS);
-        }
-        bulk_wait_all();
-        return;
-    }
-
-    // ---------------------------------------------------------------- consumers
-    const int t = threadIdx.x;
-    uint64_t m[K];
-    float ibr[K][12];
-    int p1 = 0;
-    if (t < a.T) {
-        p1 = a.p1len[t];
-#pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
-    } else {
-#pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
-    }
-    if (do_skin) {
-#pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const int src = (int)(int16_t)(m[s] >> 32);
-            const int ibu = (int)((m[s] >> 16) & 0xffff);
-            if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
-        }
-    }
-    for (int i = t; i <= a.R2; i += NC) s_round_off[i] = __ldg(a.round_off + i);
-    for (int i = t; i < a.n_rounds_entries; i += NC) s_rounds[i] = __ldg(a.rounds + i);
-    bar_consumers(NC);
-
-    long long prof_last = 0;
-    auto prof_mark = [&](int slot) {
-        if (a.prof && t == 0) {
-            const long long now = clock64();
-            if (slot >= 0) atomicAdd(a.prof + slot, (unsigned long long)(now - prof_last));
-            prof_last = now;
-        }
-    };
-
-    for (int64_t it = 0; it <= my_tiles; ++it) {
-        const bool has_cur = it < my_tiles, has_prv = it > 0;
-        const int st_cur = (int)(it % NS), st_prv = (int)((it + NS - 1) % NS);
-        float* Lc = LG + st_cur * tile_f;
-        float* Lp = LG + st_prv * tile_f;
-        float* Pc = P0 + (it & 1) * parea;
-        const float* Pp = P0 + ((it + 1) & 1) * parea;
-        float* S = SB + ((it + NSS - 1) % NSS) * tile_f;
-        prof_mark(-1);
-        if (has_cur) mbar_wait(&full[st_cur], (uint32_t)((it / NS) & 1));
-        if (has_prv && do_skin && it - 1 >= NSS)
-            mbar_wait(&sfree[(it - 1) % NSS], (uint32_t)((((it - 1) / NSS) - 1) & 1));
-        prof_mark(0);
-
-        // phase 1 of tile it
-        if (has_cur && p1 > 0) {
-            float acc[12];
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                if (s < p1) {
-                    const int off = (int)(m[s] & 0xffff);
-                    const int src = (int)(int16_t)(m[s] >> 32);
-                    const int own = (int)(int16_t)(m[s] >> 48);
-                    float l[12];
-                    ld3(Lc + off * 12, l);
-                    if (src == kSrcPrev) {
-                        float tmp[12];
-                        compose(acc, l, tmp);
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                    }
-                    if (own >= 0) st3(Pc + own * 12, acc);
-                }
-            }
-        }
-        bar_consumers(NC);
-        prof_mark(1);
-
-        const int R2c = has_cur ? a.R2 : 0;
-        float acc3[12];                         // phase-3 running pose of tile it-1
-        // one pointer-jumping round of tile it: all reads, barrier, writes, barrier
-        auto round_read = [&](int r, float (&z)[4][12], int (&dst)[4]) {
-            const int eb = s_round_off[r], e1 = s_round_off[r + 1];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int e = eb + t + q * NC;
-                dst[q] = -1;
-                if (e < e1) {
-                    const uint32_t w = s_rounds[e];
-                    float x[12], y[12];
-                    ld3(Pc + (int)(w >> 16) * 12, x);
-                    ld3(Pc + (int)(w & 0x3fff) * 12, y);
-                    compose(x, y, z[q]);
-                    dst[q] = (int)(w & 0x3fff);
-                }
-            }
-        };
-#pragma unroll
-        for (int r = 0; r < K; ++r) {
-            float z[4][12];
-            int dst[4] = {-1, -1, -1, -1};
-            if (r < R2c) round_read(r, z, dst);
-            // phase-3 step r of tile it-1 (its P finals are complete since last iteration)
-            if (has_prv) {
-                const int src = (int)(int16_t)(m[r] >> 32);
-                if (src != kSrcNone) {
-                    const int off = (int)(m[r] & 0xffff);
-                    float l[12];
-                    ld3(Lp + off * 12, l);
-                    if (src == kSrcPrev) {
-                        float tmp[12];
-                        compose(acc3, l, tmp);
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) acc3[e] = tmp[e];
-                    } else if (src == kSrcRoot) {
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) acc3[e] = l[e];
-                    } else {
-                        float pa[12];
-                        ld3(Pp + src * 12, pa);
-                        compose(pa, l, acc3);
-                    }
-                    st3(Lp + off * 12, acc3);
-                    if (do_skin) {
-                        float sk[12];
-                        compose(acc3, ibr[r], sk);
-                        st3(S + off * 12, sk);
-                    }
-                }
-                if (r == K - 1) fence_proxy_async();   // G/S writes -> the producer's TMA store
-            }
-            if (r < R2c) {
-                bar_consumers(NC);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (dst[q] >= 0) st3(Pc + dst[q] * 12, z[q]);
-                bar_consumers(NC);
-            }
-        }
-        for (int r = K; r < R2c; ++r) {
-            float z[4][12];
-            int dst[4];
-            round_read(r, z, dst);
-            bar_consumers(NC);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (dst[q] >= 0) st3(Pc + dst[q] * 12, z[q]);
-            bar_consumers(NC);
-        }
-        bar_consumers(NC);                      // every phase-3 store of tile it-1 is done
-        if (has_prv && t == 0) mbar_arrive(&done[st_prv]);
-        prof_mark(2);
-        if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
-    }
-}
-
 // ================================================================== doubling (Alg. 2)
 // One CTA per group of C characters, one thread per (character, joint) in USER
 // order (pointer jumping is order-agnostic).  Round r: V[j] <- V[anc_r(j)] (x) V[j]
@@ -754,17 +537,15 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
 }
 
 template <int K>
-void* chunked_ptr(bool pipe) {
-    return pipe ? reinterpret_cast<void*>(&pipelined_kernel<K>) : reinterpret_cast<void*>(&chunked_kernel<K>);
-}
+void* chunked_ptr() { return reinterpret_cast<void*>(&chunked_kernel<K>); }
 
-void* chunked_fn(int K, bool pipe) {
+void* chunked_fn(int K) {
     switch (K) {
-        case 3: return chunked_ptr<3>(pipe);
-        case 5: return chunked_ptr<5>(pipe);
-        case 7: return chunked_ptr<7>(pipe);
-        case 9: return chunked_ptr<9>(pipe);
-        case 11: return chunked_ptr<11>(pipe);
+        case 3: return chunked_ptr<3>();
+        case 5: return chunked_ptr<5>();
+        case 7: return chunked_ptr<7>();
+        case 9: return chunked_ptr<9>();
+        case 11: return chunked_ptr<11>();
         default: return nullptr;
     }
 }
@@ -790,17 +571,13 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
-    for (bool pipe : {false, true}) {
-        void* fn = chunked_fn(K, pipe);
-        if (!fn) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    void* fn = chunked_fn(K);
+    if (!fn) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
-int max_chunked_blocks_per_sm(int K, bool pipe, int threads, int64_t smem_bytes) {
-    void* fn = chunked_fn(K, pipe);
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes) {
+    void* fn = chunked_fn(K);
     int nb = 0;
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
                    cudaSuccess)
@@ -809,11 +586,10 @@ int max_chunked_blocks_per_sm(int K, bool pipe, int threads, int64_t smem_bytes)
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    void* fn = chunked_fn(K, a.pipelined != 0);
+    void* fn = chunked_fn(K);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm
-                                   : max_chunked_blocks_per_sm(K, a.pipelined != 0, a.threads, a.smem_bytes);
+    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : max_chunked_blocks_per_sm(K, a.threads, a.smem_bytes);
     int64_t grid = (int64_t)sm_count() * per_sm;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;

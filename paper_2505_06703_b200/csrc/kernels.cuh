@@ -24,13 +24,12 @@ struct ChunkedArgs {
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
-    int32_t pipelined;         // 1 = pipelined_kernel (phase 3 of tile i-1 inside tile i's rounds)
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute
-int max_chunked_blocks_per_sm(int K, bool pipe, int threads, int64_t smem_bytes);
+int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes);
 
 // Alg. 2: radix-2 pointer jumping, one thread per joint.
 cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,

@@ -71,8 +71,6 @@ EXACT_CASES = [
     ("tree1024", {"pbuf": 2}), ("chain256", {"pbuf": 1}), ("tree1024", {"pbuf": 1, "chunk": 9}),
     ("hum32", {"pbuf": 1, "stages": 3, "sbufs": 2}),
     ("tree1024", {"chunking": 1}), ("hum64", {"chunking": 1, "chunk": 7}),
-    ("tree1024", {"pipeline": 1}), ("hum64", {"pipeline": 1}), ("chain256", {"pipeline": 2, "chunk": 7}),
-    ("hum32", {"pipeline": 2, "stages": 2, "sbufs": 2}),
     ("tree1024", {"force_split": True}), ("chain256", {"force_split": True, "chunk": 3}),
 ]
 
