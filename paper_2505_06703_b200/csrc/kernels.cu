@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     if (warp == nwc) {
         // ------------------------------------------------------------ producer
         if ((threadIdx.x & 31) != 0) return;
+        const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
         auto issue_load = [&](int64_t it) {
             const int stage = (int)(it % NS);
             const int64_t tile = blockIdx.x + it * gridDim.x;
@@ -169,7 +170,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
             const uint32_t bytes = (uint32_t)(nc * a.J * 48);
             mbar_expect_tx(&full[stage], bytes);
-            bulk_g2s(LG + stage * tile_f, a.local + c0 * a.J * 12, bytes, &full[stage]);
+            const char* src = reinterpret_cast<const char*>(a.local + c0 * a.J * 12);
+            char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
+            for (uint32_t o = 0; o < bytes; o += piece)
+                bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
         };
         for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
         for (int64_t it = 0; it < my_tiles; ++it) {
@@ -179,8 +183,17 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             const int64_t c0 = tile * a.C;
             const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
             const uint32_t bytes = (uint32_t)(nc * a.J * 48);
-            bulk_s2g(a.gout + c0 * a.J * 12, LG + stage * tile_f, bytes);
-            if (do_skin) bulk_s2g(a.sout + c0 * a.J * 12, SB + (it % NSS) * tile_f, bytes);
+            {
+                char* g = reinterpret_cast<char*>(a.gout + c0 * a.J * 12);
+                const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
+                char* s = do_skin ? reinterpret_cast<char*>(a.sout + c0 * a.J * 12) : nullptr;
+                const char* ss = reinterpret_cast<const char*>(SB + (it % NSS) * tile_f);
+                for (uint32_t o = 0; o < bytes; o += piece) {
+                    const uint32_t nb = min(piece, bytes - o);
+                    bulk_s2g(g + o, sg + o, nb);
+                    if (do_skin) bulk_s2g(s + o, ss + o, nb);
+                }
+            }
             bulk_commit();
             bulk_wait_read<0>();                  // smem of this tile has been read out
             if (do_skin) mbar_arrive(&sfree[it % NSS]);

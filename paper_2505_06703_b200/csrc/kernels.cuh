@@ -24,6 +24,7 @@ struct ChunkedArgs {
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
+    int32_t bulk_piece;        // bytes per TMA bulk copy (0 = one copy per tile and buffer)
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
