@@ -78,8 +78,9 @@ typedef struct {
                              buffer (two barriers per round, half the shared memory); 0 = auto */
     int32_t chunking;     /* thread chunks: 1 = runs of K consecutive internal positions (the
                              paper's index blocks), 2 = heavy-path pieces packed per thread
-                             (fewer anchors); 0 = auto (2 when it cuts phase-2 work without
-                             adding threads per character, else 1)                           */
+                             (fewer anchors), 3 = heavy paths longer than K on consecutive
+                             lanes joined by a warp-shuffle scan (fewest anchors, shallow
+                             anchor forest); 0 = auto (see hs_skeleton_create_ex)          */
     int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 
@@ -168,10 +169,14 @@ const char* hs_last_error(void);
  * ------------------------------------------------------------------------- */
 typedef struct hs_plan hs_plan;
 
-/* parents as in hs_skeleton_create; chunk = K (odd, 3..15; 0 = auto);
- * block_size = the paper's block size for the MaxParentOutBlock export (0 = 64). */
+/* parents as in hs_skeleton_create; chunk = K (odd, 3..11; 0 = auto); the plan's
+ * chunk program uses chunking 3 (runs); block_size = the paper's block size for the
+ * MaxParentOutBlock export (0 = 64). */
 hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk,
                          int32_t block_size, hs_plan** out);
+/* The same with the creation options that shape the program (chunk K, chunking). */
+hs_status hs_plan_create_ex(const int32_t* parents, int32_t n_joints, const hs_create_opts* opts,
+                            int32_t block_size, hs_plan** out);
 hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* value);
 
 typedef enum {

@@ -99,6 +99,7 @@ def lib():
     L.hs_last_error.argtypes = []
     L.hs_last_error.restype = ctypes.c_char_p
     L.hs_plan_create.argtypes = [vp, i32, i32, i32, ctypes.POINTER(vp)]
+    L.hs_plan_create_ex.argtypes = [vp, i32, ctypes.POINTER(_CreateOpts), i32, ctypes.POINTER(vp)]
     L.hs_plan_query.argtypes = [vp, i32, ctypes.POINTER(i64)]
     L.hs_plan_export.argtypes = [vp, i32, vp, i64]
     L.hs_plan_destroy.argtypes = [vp]
@@ -106,7 +107,7 @@ def lib():
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
     for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
-              "hs_skeleton_query", "hs_plan_create", "hs_plan_query", "hs_plan_export",
+              "hs_skeleton_query", "hs_plan_create", "hs_plan_create_ex", "hs_plan_query", "hs_plan_export",
               "hs_plan_destroy", "hs_pipeline_create", "hs_scan_host", "hs_pipeline_destroy"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -121,13 +122,14 @@ def _check(status: int, where: str):
 class Plan:
     """Host-only view of the topology preprocessor (no CUDA)."""
 
-    def __init__(self, parents, chunk: int = 0, block_size: int = 0):
+    def __init__(self, parents, chunk: int = 0, block_size: int = 0, chunking: int = 0):
         L = lib()
         p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
         self.n = len(p)
         h = ctypes.c_void_p()
-        _check(L.hs_plan_create(p.ctypes.data if self.n else None, self.n, chunk, block_size,
-                                ctypes.byref(h)), "hs_plan_create")
+        o = _CreateOpts(chunk, 0, 0, 0, 0, 0, chunking)
+        _check(L.hs_plan_create_ex(p.ctypes.data if self.n else None, self.n, ctypes.byref(o),
+                                   block_size, ctypes.byref(h)), "hs_plan_create")
         self._h = h
 
     def query(self, what: str) -> int:

@@ -108,7 +108,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
     if ((o.chunk && !is_valid_k(o.chunk)) || o.tile_joints < 0 || (o.stages && (o.stages < 2 || o.stages > 3)) ||
         (o.sbufs && (o.sbufs < 1 || o.sbufs > 2)) || o.force_split < 0 || o.force_split > 1 ||
-        o.pbuf < 0 || o.pbuf > 2 || o.chunking < 0 || o.chunking > 2 || o.reserved[0])
+        o.pbuf < 0 || o.pbuf > 2 || o.chunking < 0 || o.chunking > 3 || o.reserved[0])
         return fail(HS_ERR_INVALID_ARG, "invalid hs_create_opts");
     if (depth > 32) return fail(HS_ERR_UNSUPPORTED, "split recursion too deep");
     hs_skeleton* sk = new (std::nothrow) hs_skeleton();
@@ -129,7 +129,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     int C = std::max(1, tile_target / std::max(1, n));
     // chunk construction: heavy-path pieces cut anchors on branchy skeletons, but may need
     // more threads per character (smaller tiles); auto keeps them only when they do not
-    int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE : hs::CHUNK_HEAVY;
+    int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE : (o.chunking == 3 ? hs::CHUNK_RUNS : hs::CHUNK_HEAVY);
     if (o.chunking == 0) {
         const hs::TileProgram a1 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_CONSECUTIVE);
         const hs::TileProgram a2 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_HEAVY);
@@ -249,6 +249,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.meta = sk->d_meta; a.p1len = sk->d_p1len; a.round_off = sk->d_round_off;
             a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
             a.n_rounds_entries = (int32_t)sk->tp.rounds.size();
+            a.has_runs = sk->tp.has_runs ? 1 : 0;
             a.bulk_piece = 8192;   // 8 KB TMA bulk copies (measured +2% over one copy per tile)
             if (const char* bp = std::getenv("HS_BULK_PIECE")) a.bulk_piece = std::atoi(bp) & ~15;  // tuning aid
             a.smem_bytes = sk->smem; a.threads = sk->threads;
@@ -411,7 +412,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_DEVICE: *v = sk->device; break;
         case HS_Q_SPLIT_LEVELS: *v = sk->split_levels; break;
         case HS_Q_SBUFS: *v = sk->sbufs; break;
-        case HS_Q_CHUNKING: *v = sk->chunking == hs::CHUNK_CONSECUTIVE ? 1 : 2; break;
+        case HS_Q_CHUNKING: *v = sk->chunking == hs::CHUNK_CONSECUTIVE ? 1 : (sk->chunking == hs::CHUNK_RUNS ? 3 : 2); break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
@@ -436,25 +437,39 @@ const char* hs_status_string(hs_status s) {
 const char* hs_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ host-only plan
-hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk, int32_t block_size,
-                         hs_plan** out) {
+hs_status hs_plan_create_ex(const int32_t* parents, int32_t n_joints, const hs_create_opts* opts,
+                            int32_t block_size, hs_plan** out) {
     if (!out) return fail(HS_ERR_INVALID_ARG, "out is null");
+    hs_create_opts o;
+    std::memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
     try {
         hs_plan* p = new hs_plan();
         std::string err;
         int st = hs::build_plan(parents, n_joints, p->plan, err);
         if (st != 0) { delete p; return fail((hs_status)st, err); }
-        p->K = chunk == 0 ? 5 : chunk;
-        if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..15"); }
+        p->K = o.chunk == 0 ? 5 : o.chunk;
+        if (!is_valid_k(p->K)) { delete p; return fail(HS_ERR_INVALID_ARG, "chunk must be odd in 3..11"); }
+        if (o.chunking < 0 || o.chunking > 3) { delete p; return fail(HS_ERR_INVALID_ARG, "bad chunking"); }
+        const int mode = o.chunking == 1 ? hs::CHUNK_CONSECUTIVE
+                                         : (o.chunking == 2 ? hs::CHUNK_HEAVY : hs::CHUNK_RUNS);
         p->block_size = block_size <= 0 ? 64 : block_size;
         std::vector<int32_t> pos(p->plan.order);
-        p->decomp = hs::decompose(p->plan.ipar, p->K, hs::CHUNK_HEAVY, &pos, true);
-        p->tile = hs::build_tile_program(p->plan, p->K, 1, true, hs::CHUNK_HEAVY);
+        p->decomp = hs::decompose(p->plan.ipar, p->K, mode, &pos, true);
+        p->tile = hs::build_tile_program(p->plan, p->K, 1, true, mode);
         *out = p;
         return HS_OK;
     } catch (const std::bad_alloc&) {
         return fail(HS_ERR_OOM, "host allocation failed");
     }
+}
+
+hs_status hs_plan_create(const int32_t* parents, int32_t n_joints, int32_t chunk, int32_t block_size,
+                         hs_plan** out) {
+    hs_create_opts o;
+    std::memset(&o, 0, sizeof(o));
+    o.chunk = chunk;
+    return hs_plan_create_ex(parents, n_joints, &o, block_size, out);
 }
 
 hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {

@@ -12,7 +12,7 @@
 namespace hs {
 namespace {
 
-enum : int { kSrcRoot = -1, kSrcPrev = -2, kSrcNone = -3 };
+enum : int { kSrcRoot = -1, kSrcPrev = -2, kSrcNone = -3, kSrcRun = -4 };
 
 // ------------------------------------------------------------------ 3x4 algebra
 struct M34 {
@@ -208,9 +208,12 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     const bool active = t < a.T;
     uint64_t m[K];
     float ibr[K][12];
-    int p1 = 0;
+    int p1 = 0, run_back = 0, run_anchor = -1;
     if (active) {
-        p1 = a.p1len[t];
+        const int info = a.p1len[t];
+        p1 = info & 0xff;
+        run_back = (info >> 8) & 0xff;
+        run_anchor = (int)((uint32_t)info >> 16) - 1;
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
     } else {
@@ -247,8 +250,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         prof_mark(0);
 
         // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
+        float acc[12];
         if (p1 > 0) {
-            float acc[12];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 if (s < p1) {
@@ -267,6 +270,39 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                         for (int e = 0; e < 12; ++e) acc[e] = l[e];
                     }
                     if (own >= 0) st3(P + own * 12, acc);
+                }
+            }
+        }
+        // phase 2a: heavy paths longer than K sit on consecutive lanes (runs); a
+        // segmented warp-shuffle scan joins their pieces (Hillis-Steele over lanes,
+        // parent on the left), then each run lane lifts its anchors by its exclusive
+        // prefix.  No CTA barrier: runs never cross a warp.
+        float excl[12];
+        if (a.has_runs) {
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                float u[12];
+#pragma unroll
+                for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
+                if (run_back >= d) {
+                    float w[12];
+                    compose(u, acc, w);
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc[e] = w[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 12; ++e) excl[e] = __shfl_up_sync(0xffffffffu, acc[e], 1);
+            if (run_back > 0) {
+#pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    const int own = (int)(int16_t)(m[s] >> 48);
+                    if (own >= 0) {
+                        float x[12], y[12];
+                        ld3(P + own * 12, x);
+                        compose(excl, x, y);
+                        st3(P + own * 12, y);
+                    }
                 }
             }
         }
@@ -339,6 +375,19 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 } else if (src == kSrcRoot) {
 #pragma unroll
                     for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                } else if (src == kSrcRun) {
+                    // first joint of a run lane: parent = previous lane's tail, whose
+                    // global pose is P[run anchor] (x) (exclusive scan of the run)
+                    float base[12];
+                    if (run_anchor >= 0) {
+                        float pa[12];
+                        ld3(P + run_anchor * 12, pa);
+                        compose(pa, excl, base);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) base[e] = excl[e];
+                    }
+                    compose(base, l, acc);
                 } else {
                     float pa[12];
                     ld3(P + src * 12, pa);

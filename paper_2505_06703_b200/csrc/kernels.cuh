@@ -16,7 +16,7 @@ struct ChunkedArgs {
     int32_t J, C, F, T;        // joints, chars per tile, joints per tile, compute threads
     int32_t nslots, R2;
     const uint64_t* meta;      // [T][K]
-    const int32_t* p1len;      // [T]
+    const int32_t* p1len;      // [T]: phase-1 length | run_back << 8 | (run anchor + 1) << 16
     const int32_t* round_off;  // [R2+1]
     const uint32_t* rounds;    // phase-2 descriptors (copied to smem by each CTA)
     int32_t n_rounds_entries;
@@ -24,6 +24,7 @@ struct ChunkedArgs {
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
+    int32_t has_runs;          // lanes joined by the warp-shuffle scan (CHUNK_RUNS programs)
     int32_t bulk_piece;        // bytes per TMA bulk copy (0 = one copy per tile and buffer)
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)

@@ -79,10 +79,10 @@ int build_plan(const int32_t* parents, int32_t n, Plan& P, std::string& err) {
 
 namespace {
 
-// Heavy-path pieces: walk every root's heavy path (child of largest subtree height,
-// smallest index on ties), recursing into the light children; cut each path into
-// pieces of at most K joints.  A piece is a parent-to-child chain.
-std::vector<std::vector<int32_t>> heavy_pieces(const std::vector<int32_t>& par, int K) {
+// Heavy paths: walk every root's heavy path (child of largest subtree height,
+// smallest index on ties), recursing into the light children.  Each path is a
+// parent-to-child chain; together they partition the forest.
+std::vector<std::vector<int32_t>> heavy_paths(const std::vector<int32_t>& par) {
     const int32_t F = (int32_t)par.size();
     std::vector<int32_t> first(F + 1, 0), kids(F), height(F, 1);
     for (int32_t f = 0; f < F; ++f) if (par[f] >= 0) first[par[f] + 1]++;
@@ -93,16 +93,15 @@ std::vector<std::vector<int32_t>> heavy_pieces(const std::vector<int32_t>& par, 
     }
     for (int32_t f = F - 1; f >= 0; --f)          // par[f] < f: reverse order is bottom-up
         if (par[f] >= 0) height[par[f]] = std::max(height[par[f]], height[f] + 1);
-    std::vector<std::vector<int32_t>> pieces;
+    std::vector<std::vector<int32_t>> paths;
     std::vector<int32_t> stack;                   // path starts
     for (int32_t f = F - 1; f >= 0; --f) if (par[f] < 0) stack.push_back(f);
-    std::vector<int32_t> path;
     while (!stack.empty()) {
         int32_t v = stack.back();
         stack.pop_back();
-        path.clear();
+        paths.emplace_back();
         for (;;) {
-            path.push_back(v);
+            paths.back().push_back(v);
             int32_t h = -1;
             for (int32_t e = first[v]; e < first[v + 1]; ++e)
                 if (h < 0 || height[kids[e]] > height[h]) h = kids[e];
@@ -111,9 +110,16 @@ std::vector<std::vector<int32_t>> heavy_pieces(const std::vector<int32_t>& par, 
                 if (kids[e] != h) stack.push_back(kids[e]);
             v = h;
         }
+    }
+    return paths;
+}
+
+// Heavy-path pieces of at most K joints (a piece is a parent-to-child chain).
+std::vector<std::vector<int32_t>> heavy_pieces(const std::vector<int32_t>& par, int K) {
+    std::vector<std::vector<int32_t>> pieces;
+    for (auto& path : heavy_paths(par))
         for (size_t i = 0; i < path.size(); i += (size_t)K)
             pieces.emplace_back(path.begin() + (long)i, path.begin() + (long)std::min(path.size(), i + (size_t)K));
-    }
     return pieces;
 }
 
@@ -137,7 +143,8 @@ std::vector<std::vector<int32_t>> pack_pieces(std::vector<std::vector<int32_t>> 
 // item i contributes residue keys keys[i][d] (d = 0..D-1, -1 = no access); the cost
 // of a group is sum_d max_r count(d, r) — the wavefronts its D 128-bit accesses
 // take.  Swaps items between groups while the total cost drops.
-void swap_search(std::vector<std::vector<int>>& keys, std::vector<int32_t>& perm, int D) {
+void swap_search(std::vector<std::vector<int>>& keys, std::vector<int32_t>& perm, int D,
+                 const std::vector<char>* movable = nullptr) {
     const int n = (int)perm.size();
     const int G = (n + 7) / 8;
     if (G < 2) return;
@@ -152,6 +159,7 @@ void swap_search(std::vector<std::vector<int>>& keys, std::vector<int32_t>& perm
         bool improved = false;
         for (int i = 0; i < n; ++i)
             for (int j = (i / 8 + 1) * 8; j < n; ++j) {
+                if (movable && (!(*movable)[i] || !(*movable)[j])) continue;
                 const int gi = i / 8, gj = j / 8;
                 int before = 0, after = 0;
                 for (int d = 0; d < D; ++d) {
@@ -227,6 +235,42 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const st
             d.lists.emplace_back();
             for (int32_t g = f; g < std::min(F, f + K); ++g) d.lists.back().push_back(g);
         }
+    } else if (mode == CHUNK_RUNS) {
+        // Paths longer than K become RUNS: their pieces on consecutive lanes, so one
+        // warp-shuffle segmented scan joins them (a run restarts at a warp boundary).
+        // Shorter paths are packed per lane.  Lanes are per character from lane 0.
+        auto paths = heavy_paths(par);
+        std::stable_sort(paths.begin(), paths.end(),
+                         [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) { return a.size() > b.size(); });
+        std::vector<std::vector<int32_t>> shortp;
+        for (auto& path : paths) {
+            if ((int)path.size() <= K) { shortp.push_back(path); continue; }
+            for (size_t i = 0; i < path.size(); i += (size_t)K) {
+                const int b = (i > 0 && d.lists.size() % 32 != 0) ? d.run_back.back() + 1 : 0;
+                d.lists.emplace_back(path.begin() + (long)i, path.begin() + (long)std::min(path.size(), i + (size_t)K));
+                d.run_back.push_back(b);
+            }
+        }
+        const size_t nrun = d.lists.size();
+        for (auto& l : pack_pieces(shortp, K)) { d.lists.push_back(l); d.run_back.push_back(0); }
+        if (pad_to_warp) {
+            d.lists.resize((d.lists.size() + 31) / 32 * 32);
+            d.run_back.resize(d.lists.size(), 0);
+        }
+        if (pos && d.lists.size() > nrun) {   // conflict-aware order of the packed (movable) lanes
+            std::vector<std::vector<int>> keys(d.lists.size(), std::vector<int>((size_t)K, -1));
+            std::vector<char> movable(d.lists.size(), 0);
+            for (size_t i = 0; i < d.lists.size(); ++i) {
+                movable[i] = i >= nrun;
+                for (size_t s = 0; s < d.lists[i].size(); ++s) keys[i][s] = (*pos)[d.lists[i][s]] & 7;
+            }
+            std::vector<int32_t> perm(d.lists.size());
+            for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
+            swap_search(keys, perm, K, &movable);
+            std::vector<std::vector<int32_t>> out;
+            for (int32_t i : perm) out.push_back(d.lists[i]);
+            d.lists.swap(out);
+        }
     } else {
         d.lists = pack_pieces(heavy_pieces(par, K), K);
         // idle lanes of the last warp are free: empty lists give the ordering room
@@ -237,14 +281,20 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const st
     }
     d.src.assign(F, SRC_ROOT);
     d.slot_of.assign(F, -1);
+    if (d.run_back.size() != d.lists.size()) d.run_back.assign(d.lists.size(), 0);
     std::vector<int32_t> head(F);
-    for (auto& L : d.lists)
+    for (size_t li = 0; li < d.lists.size(); ++li) {
+        const auto& L = d.lists[li];
         for (size_t i = 0; i < L.size(); ++i) {
             const int32_t f = L[i], q = par[f];
             if (q < 0) { d.src[f] = SRC_ROOT; head[f] = f; }
             else if (i > 0 && q == L[i - 1]) { d.src[f] = SRC_PREV; head[f] = head[q]; }
-            else { d.src[f] = q; head[f] = f; }
+            else if (i == 0 && d.run_back[li] > 0) {   // joined by the warp scan: q = previous lane's tail
+                d.src[f] = SRC_RUN;
+                head[f] = head[q];
+            } else { d.src[f] = q; head[f] = f; }
         }
+    }
     std::vector<char> is_anchor(F, 0);
     for (int32_t f = 0; f < F; ++f)
         if (d.src[f] >= 0) is_anchor[d.src[f]] = 1;
@@ -255,6 +305,7 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const st
         int32_t h = head[d.slots[s]];
         d.link0[s] = d.src[h] >= 0 ? d.slot_of[d.src[h]] : -1;
     }
+    d.head = head;
     return d;
 }
 
@@ -361,7 +412,7 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int m
     const int32_t n = p.n;
     std::vector<int32_t> pos(n);               // smem position (joint index) of internal i
     for (int32_t i = 0; i < n; ++i) pos[i] = p.order[i];
-    const ChunkDecomp d = decompose(p.ipar, K, mode, &pos, C == 1);
+    const ChunkDecomp d = decompose(p.ipar, K, mode, &pos, C == 1 || mode == CHUNK_RUNS);
     const int32_t TC = (int32_t)d.lists.size();   // chunks (threads) per character
     tp.lists_nonempty = 0;
     for (auto& l : d.lists) tp.lists_nonempty += l.empty() ? 0 : 1;
@@ -428,9 +479,24 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int m
     }
     tp.meta.assign((size_t)tp.T * K, 0);
     tp.p1len.assign(tp.T, 0);
+    for (int32_t tc = 0; tc < TC; ++tc)
+        if (d.run_back[tc] > 0 || (tc + 1 < TC && d.run_back[tc + 1] > 0)) tp.has_runs = true;
     for (int c = 0; c < C; ++c)
         for (int32_t tc = 0; tc < TC; ++tc) {
             const int32_t t = c * TC + tc;
+            // lane info: run_back (bits 8..15) and the run head's anchor P location + 1
+            // (bits 16..31, 0 = none) for lanes joined by the warp scan
+            const bool in_run = d.run_back[tc] > 0 || (tc + 1 < TC && d.run_back[tc + 1] > 0);
+            int32_t info = 0;
+            if (d.run_back[tc] > 0 && !d.lists[tc].empty()) {
+                const int32_t h = d.head[d.lists[tc][0]];
+                int32_t loc = -1;
+                if (d.src[h] >= 0) {
+                    const int32_t raw = c * Sc + d.slot_of[d.src[h]];
+                    loc = latest[raw] * S + idx[raw];
+                }
+                info = (d.run_back[tc] << 8) | ((loc + 1) << 16);
+            }
             for (int s = 0; s < K; ++s) {
                 const bool has = s < (int)d.lists[tc].size();
                 const int32_t i = has ? d.lists[tc][s] : -1;   // internal position within the character
@@ -446,11 +512,12 @@ TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int m
                         src = d.src[i];
                     }
                     own = d.slot_of[i] >= 0 ? idx[c * Sc + d.slot_of[i]] : -1;
-                    if (own >= 0) tp.p1len[t] = s + 1;
+                    if (own >= 0 || in_run) tp.p1len[t] = s + 1;   // runs need the whole piece product
                 }
                 tp.meta[(size_t)t * K + s] = off | (ibu << 16) | ((uint64_t)(uint16_t)(int16_t)src << 32) |
                                              ((uint64_t)(uint16_t)(int16_t)own << 48);
             }
+            tp.p1len[t] |= info;
         }
     return tp;
 }

@@ -26,8 +26,8 @@
 
 namespace hs {
 
-enum : int32_t { SRC_ROOT = -1, SRC_PREV = -2, SRC_NONE = -3 };
-enum : int { CHUNK_CONSECUTIVE = 0, CHUNK_HEAVY = 1 };
+enum : int32_t { SRC_ROOT = -1, SRC_PREV = -2, SRC_NONE = -3, SRC_RUN = -4 };
+enum : int { CHUNK_CONSECUTIVE = 0, CHUNK_HEAVY = 1, CHUNK_RUNS = 2 };
 
 // Chunk decomposition of a flat forest given in topological order (par[f] < f):
 // per-thread lists of at most K nodes; a node's parent is either the previous node
@@ -36,13 +36,18 @@ enum : int { CHUNK_CONSECUTIVE = 0, CHUNK_HEAVY = 1 };
 //                      blocks, at thread granularity)
 //   CHUNK_HEAVY        lists = heavy-path pieces (<= K joints) packed first-fit
 //                      decreasing, then ordered for conflict-free smem access
+//   CHUNK_RUNS         heavy paths longer than K on consecutive lanes (RUNS, joined
+//                      by a warp-shuffle segmented scan: src SRC_RUN on a lane's first
+//                      joint), the other paths packed as in CHUNK_HEAVY
 struct ChunkDecomp {
     int K = 0;
     std::vector<std::vector<int32_t>> lists;
-    std::vector<int32_t> src;      // per node: SRC_ROOT, SRC_PREV, or anchor node index (>= 0)
+    std::vector<int32_t> run_back; // per list (lane): preceding lanes of its run in the warp
+    std::vector<int32_t> src;      // per node: SRC_ROOT, SRC_PREV, SRC_RUN, or anchor node (>= 0)
     std::vector<int32_t> slot_of;  // per node: anchor slot or -1
     std::vector<int32_t> slots;    // slot -> node (ascending node index => topological)
     std::vector<int32_t> link0;    // slot -> slot of anchor(seghead(node)), or -1
+    std::vector<int32_t> head;     // per node: first joint of its segment (through PREV / RUN)
 };
 ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode,
                       const std::vector<int32_t>* smem_pos, bool pad_to_warp);
@@ -55,7 +60,9 @@ struct TileProgram {
     int max_round_entries = 0;          // largest round (single buffer needs <= 4 per thread)
     int lists_nonempty = 0;             // chunks with work per character (T may include padding)
     std::vector<uint64_t> meta;         // [T][K]: off | ibu<<16 | (u16)src<<32 | (u16)own<<48
-    std::vector<int32_t> p1len;         // [T]: phase-1 length (last own anchor + 1)
+    std::vector<int32_t> p1len;         // [T]: phase-1 length (bits 0..7) | run_back << 8 |
+                                        //      (run anchor P location + 1) << 16
+    bool has_runs = false;              // some lanes are joined by the warp-shuffle scan
     std::vector<int32_t> round_off;     // [R2 + 1] offsets into rounds
     std::vector<uint32_t> rounds;       // slot | dst buf<<14 | self buf<<15 | link location<<16
 };

@@ -162,11 +162,11 @@ def test_order_is_topological_and_block_layout_brute_force(seed):
         assert mpob[i] == a
 
 
-def _chunk_emulation(par, local, K):
+def _chunk_emulation(par, local, K, chunking=3):
     """Emulate this build's chunk/anchor algorithm on the host from
     the exported decomposition, in fp64.  On the exact-arithmetic family every
     association order gives the same bits, so this pins the decomposition."""
-    pl = hs.Plan(par, chunk=K)
+    pl = hs.Plan(par, chunk=K, chunking=chunking)
     order = pl.export("order")
     src = pl.export("chunk_src")
     link = pl.export("anchor_link")
@@ -176,14 +176,25 @@ def _chunk_emulation(par, local, K):
     anchors = sorted(set(int(s) for s in src if s >= 0))
     slot = {a: k for k, a in enumerate(anchors)}
     assert len(anchors) == len(link)
-    # phase 1: per-chunk left fold; publish at anchors
+    # phase 1: per-chunk left fold (a RUN joint restarts like a head); publish anchors
     P = np.zeros((len(anchors), 4, 4))
+    full = []
     for chunk in lists:
         acc = None
         for f in chunk:
             acc = acc @ H[f] if src[f] == -2 else H[f]
             if f in slot:
                 P[slot[f]] = acc
+        full.append(acc)
+    # phase 2a: a lane whose first joint is RUN (-4) continues the previous lane's run;
+    # lift its anchors by the product of the run's earlier lanes (exclusive prefix)
+    excl = [None] * len(lists)
+    for li, chunk in enumerate(lists):
+        if chunk and src[chunk[0]] == -4:
+            excl[li] = full[li - 1] if excl[li - 1] is None else excl[li - 1] @ full[li - 1]
+            for f in chunk:
+                if f in slot:
+                    P[slot[f]] = excl[li] @ P[slot[f]]
     # phase 2: pointer jumping over the anchor forest (snapshot semantics)
     lk = link.copy()
     while np.any(lk >= 0):
@@ -193,15 +204,17 @@ def _chunk_emulation(par, local, K):
                 Pn[s] = P[lk[s]] @ P[s]
         P = Pn
         lk = np.array([lk[lk[s]] if lk[s] >= 0 else -1 for s in range(len(anchors))], np.int32)
-    # phase 3: re-fold from the final anchor values
+    # phase 3: re-fold from the final anchor values (RUN: parent = previous lane's tail)
     G = np.zeros((n, 4, 4))
-    for chunk in lists:
+    for li, chunk in enumerate(lists):
         acc = None
         for f in chunk:
             if src[f] == -2:
                 acc = acc @ H[f]
             elif src[f] == -1:
                 acc = H[f]
+            elif src[f] == -4:
+                acc = G[lists[li - 1][-1]] @ H[f]
             else:
                 acc = P[slot[src[f]]] @ H[f]
             G[f] = acc
@@ -209,16 +222,17 @@ def _chunk_emulation(par, local, K):
     return out
 
 
+@pytest.mark.parametrize("chunking", [1, 2, 3])
 @pytest.mark.parametrize("K", [3, 7, 11])
 @pytest.mark.parametrize("name", ["hum64", "chain256", "tree1024", "perm_tree"])
-def test_chunk_anchor_decomposition_reproduces_oracle_bitwise(name, K):
+def test_chunk_anchor_decomposition_reproduces_oracle_bitwise(name, K, chunking):
     if name == "perm_tree":
         par, _ = hsgen.relabel(hsgen.skeleton("tree1024"), hsgen.permutation(3, 1024))
     else:
         par = hsgen.skeleton(name)
     local = hsgen.exact_poses(21, len(par), 1)[0]
     g_ref, _ = oracle.scan(par, local)
-    g = _chunk_emulation(par, local.astype(np.float64), K)
+    g = _chunk_emulation(par, local.astype(np.float64), K, chunking)
     assert np.array_equal(g, g_ref)
 
 
@@ -227,7 +241,7 @@ def test_decomposition_invariants():
     for trial in range(20):
         par = _random_forest(rng, int(rng.integers(1, 400)), permute=bool(trial % 2))
         K = [3, 5, 7, 9][trial % 4]
-        pl = hs.Plan(par, chunk=K)
+        pl = hs.Plan(par, chunk=K, chunking=[1, 2, 3][trial % 3])
         order = pl.export("order")
         n = len(par)
         rank = np.empty(n, int); rank[order] = np.arange(n)
@@ -247,6 +261,10 @@ def test_decomposition_invariants():
                 assert ipar[f] == -1
             elif src[f] == -2:
                 assert prev_of.get(f) == ipar[f]
+            elif src[f] == -4:   # RUN: parent is the previous lane's last joint
+                lane = [i for i, row in enumerate(lists) if f in row][0]
+                prev = [int(x) for x in lists[lane - 1] if x >= 0]
+                assert list(lists[lane]).index(f) == 0 and prev[-1] == ipar[f]
             else:
                 assert src[f] == ipar[f] and prev_of.get(f) != ipar[f]
         assert pl.query("anchors") == len(set(int(s) for s in src if s >= 0))
@@ -264,18 +282,22 @@ def test_errors_from_plan():
     assert e.value.status == hs.HS_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("name", ["hum32", "hum64", "chain256", "tree1024", "perm_tree"])
-def test_tile_program_emulation_bitwise(name):
+@pytest.mark.parametrize("chunking", [1, 2, 3])
+@pytest.mark.parametrize("name", ["hum32", "hum64", "chain256", "tree1024", "perm_tree", "forest"])
+def test_tile_program_emulation_bitwise(name, chunking):
     """Replay the exact uploaded tile program (ping-pong locations, colouring, round
     order) on the host: bitwise equal to the oracle on the exact family."""
     from tests import tile_emulator
     if name == "perm_tree":
         par, _ = hsgen.relabel(hsgen.skeleton("tree1024"), hsgen.permutation(3, 1024))
+    elif name == "forest":   # several long chains + a tree: runs split at warp boundaries
+        a, b = hsgen.chain(200), hsgen.skeleton("tree1024")
+        par = np.concatenate([a, np.where(a >= 0, a + 200, -1), np.where(b >= 0, b + 400, -1)]).astype(np.int32)
     else:
         par = hsgen.skeleton(name)
     J = len(par)
     local = hsgen.exact_poses(22, J, 1)[0]
     ib = hsgen.exact_inv_bind(22, J)
     G, S = oracle.scan(par, local, ib)
-    g, s, _ = tile_emulator.run(hs.Plan(par), local, ib)
+    g, s, _ = tile_emulator.run(hs.Plan(par, chunking=chunking), local, ib)
     assert np.array_equal(g, G) and np.array_equal(s, S)

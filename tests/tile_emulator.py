@@ -18,7 +18,7 @@ import collections
 
 import numpy as np
 
-SRC_ROOT, SRC_PREV, SRC_NONE = -1, -2, -3
+SRC_ROOT, SRC_PREV, SRC_NONE, SRC_RUN = -1, -2, -3, -4
 
 
 def _h(m):
@@ -78,6 +78,10 @@ def run(plan, local, inv_bind=None, count=False):
     SK = [None] * J
     wc = WavefrontCounter() if count else None
     dec = [[decode_meta(meta[t, s]) for s in range(K)] for t in range(T)]
+    info = [int(x) for x in p1len]
+    p1len = [x & 0xFF for x in info]
+    run_back = [(x >> 8) & 0xFF for x in info]
+    run_anchor = [((x & 0xFFFFFFFF) >> 16) - 1 for x in info]
     P_BASE = 0          # the P region's base residue is common to all its accesses
     NC = (T + 31) // 32 * 32
 
@@ -99,6 +103,26 @@ def run(plan, local, inv_bind=None, count=False):
                 wc.matrix("p1 L load", w)
             for w in sts.values():
                 wc.matrix("p1 P store", w)
+    # phase 2a: segmented warp scan over runs (Hillis-Steele over lanes, as the kernel)
+    excl = [None] * T
+    for w0 in range(0, T, 32):
+        lanes = list(range(w0, min(T, w0 + 32)))
+        v = {t: accs[t] for t in lanes}
+        d = 1
+        while d < 32:
+            nv = dict(v)
+            for t in lanes:
+                if run_back[t] >= d:
+                    nv[t] = v[t - d] @ v[t]
+            v = nv
+            d <<= 1
+        for t in lanes:
+            if run_back[t] > 0:
+                excl[t] = v[t - 1]
+                for s in range(K):
+                    own = dec[t][s][3]
+                    if own >= 0:
+                        P[own] = excl[t] @ P[own]
     # phase 2
     for r in range(len(round_off) - 1):
         e0, e1 = int(round_off[r]), int(round_off[r + 1])
@@ -133,6 +157,9 @@ def run(plan, local, inv_bind=None, count=False):
                 accs[t] = accs[t] @ L[off]
             elif src == SRC_ROOT:
                 accs[t] = L[off].copy()
+            elif src == SRC_RUN:
+                base = P[run_anchor[t]] @ excl[t] if run_anchor[t] >= 0 else excl[t]
+                accs[t] = base @ L[off]
             else:
                 accs[t] = P[src] @ L[off]
                 pl[t // 32].append((t % 32, P_BASE + src * 48))
