@@ -80,7 +80,9 @@ typedef struct {
                              paper's index blocks), 2 = heavy-path pieces packed per thread
                              (fewer anchors), 3 = heavy paths longer than K on consecutive
                              lanes joined by a warp-shuffle scan (fewest anchors, shallow
-                             anchor forest); 0 = auto (see hs_skeleton_create_ex)          */
+                             anchor forest); 0 = auto: 3 for one-character tiles when it at
+                             least halves the pointer-jumping work, else 2 when it cuts that
+                             work without adding threads per character, else 1              */
     int32_t reserved[1];  /* must be zero                                                      */
 } hs_create_opts;
 

@@ -135,6 +135,15 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         const hs::TileProgram a2 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_HEAVY);
         const bool fewer = a2.rounds.size() < a1.rounds.size();
         mode = (fewer && a2.lists_nonempty <= a1.lists_nonempty) ? hs::CHUNK_HEAVY : hs::CHUNK_CONSECUTIVE;
+        // runs pad every character to whole warps; worth it for one-character tiles
+        // whose pointer jumping they cut by half or more (measured: tree1024 -8%, and a
+        // loss on 64/256-joint skeletons packed several per tile)
+        const int tile_target = o.tile_joints ? o.tile_joints : 1024;
+        if (tile_target / std::max(1, n) <= 1) {
+            const hs::TileProgram a3 = hs::build_tile_program(P, sk->K, 1, true, hs::CHUNK_RUNS);
+            const size_t best = std::min(a1.rounds.size(), a2.rounds.size());
+            if (a3.rounds.size() * 2 <= best && a3.T <= 224) mode = hs::CHUNK_RUNS;
+        }
     }
     sk->chunking = mode;
     const int64_t TC = hs::build_tile_program(P, sk->K, 1, true, mode).T;  // chunks per character

@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
         }
     }
+    // longest run prefix in this warp: the scan needs ceil(log2(max + 1)) steps
+    const int warp_maxrb = a.has_runs ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
     // phase-2 tables: identical for every tile, staged once per CTA
     for (int i = t; i <= a.R2; i += NC) s_round_off[i] = __ldg(a.round_off + i);
     for (int i = t; i < a.n_rounds_entries; i += NC) s_rounds[i] = __ldg(a.rounds + i);
@@ -278,9 +280,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         // parent on the left), then each run lane lifts its anchors by its exclusive
         // prefix.  No CTA barrier: runs never cross a warp.
         float excl[12];
-        if (a.has_runs) {
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+        if (warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
+            for (int d = 1; d <= warp_maxrb; d <<= 1) {
                 float u[12];
 #pragma unroll
                 for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
