@@ -130,7 +130,7 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
 //            segment head's parent, writes G in place over L, and S = G (x) IB
 //            (IB held in registers) into the S buffer;
 // then the producer bulk-stores G and S and refills the stage.
-template <int K>
+template <int K, bool RUNS>
 __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int NS = a.stages, NSS = a.sbufs;
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         }
     }
     // longest run prefix in this warp: the scan needs ceil(log2(max + 1)) steps
-    const int warp_maxrb = a.has_runs ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
+    const int warp_maxrb = RUNS ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
     // phase-2 tables: identical for every tile, staged once per CTA
     for (int i = t; i <= a.R2; i += NC) s_round_off[i] = __ldg(a.round_off + i);
     for (int i = t; i < a.n_rounds_entries; i += NC) s_rounds[i] = __ldg(a.rounds + i);
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         // parent on the left), then each run lane lifts its anchors by its exclusive
         // prefix.  No CTA barrier: runs never cross a warp.
         float excl[12];
-        if (warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
+        if (RUNS && warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
             for (int d = 1; d <= warp_maxrb; d <<= 1) {
                 float u[12];
 #pragma unroll
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 } else if (src == kSrcRoot) {
 #pragma unroll
                     for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                } else if (src == kSrcRun) {
+                } else if (RUNS && src == kSrcRun) {
                     // first joint of a run lane: parent = previous lane's tail, whose
                     // global pose is P[run anchor] (x) (exclusive scan of the run)
                     float base[12];
@@ -600,15 +600,18 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
 }
 
 template <int K>
-void* chunked_ptr() { return reinterpret_cast<void*>(&chunked_kernel<K>); }
+void* chunked_ptr(bool runs) {
+    return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true>)
+                : reinterpret_cast<void*>(&chunked_kernel<K, false>);
+}
 
-void* chunked_fn(int K) {
+void* chunked_fn(int K, bool runs) {
     switch (K) {
-        case 3: return chunked_ptr<3>();
-        case 5: return chunked_ptr<5>();
-        case 7: return chunked_ptr<7>();
-        case 9: return chunked_ptr<9>();
-        case 11: return chunked_ptr<11>();
+        case 3: return chunked_ptr<3>(runs);
+        case 5: return chunked_ptr<5>(runs);
+        case 7: return chunked_ptr<7>(runs);
+        case 9: return chunked_ptr<9>(runs);
+        case 11: return chunked_ptr<11>(runs);
         default: return nullptr;
     }
 }
@@ -634,13 +637,17 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
-    void* fn = chunked_fn(K);
-    if (!fn) return cudaErrorInvalidValue;
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    for (bool runs : {false, true}) {
+        void* fn = chunked_fn(K, runs);
+        if (!fn) return cudaErrorInvalidValue;
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
-int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes) {
-    void* fn = chunked_fn(K);
+int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes) {
+    void* fn = chunked_fn(K, runs);
     int nb = 0;
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
                    cudaSuccess)
@@ -649,10 +656,11 @@ int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes) {
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    void* fn = chunked_fn(K);
+    void* fn = chunked_fn(K, a.has_runs != 0);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
-    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : max_chunked_blocks_per_sm(K, a.threads, a.smem_bytes);
+    int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm
+                                   : max_chunked_blocks_per_sm(K, a.has_runs != 0, a.threads, a.smem_bytes);
     int64_t grid = (int64_t)sm_count() * per_sm;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;

@@ -31,7 +31,7 @@ struct ChunkedArgs {
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute
-int max_chunked_blocks_per_sm(int K, int threads, int64_t smem_bytes);
+int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes);
 
 // Alg. 2: radix-2 pointer jumping, one thread per joint.
 cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,
