@@ -266,8 +266,8 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.p_single = sk->tp.pingpong ? 0 : 1;
             a.prof = nullptr;
             if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
-                cudaMalloc(reinterpret_cast<void**>(&a.prof), 6 * sizeof(unsigned long long));
-                cudaMemsetAsync(a.prof, 0, 6 * sizeof(unsigned long long), st);
+                cudaMalloc(reinterpret_cast<void**>(&a.prof), 8 * sizeof(unsigned long long));
+                cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st);
             }
             e = hs::launch_chunked(sk->K, a, st);
             if (e != cudaSuccess) {
@@ -277,14 +277,15 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 return cuda_fail(e, buf);
             }
             if (a.prof) {
-                unsigned long long h[6];
+                unsigned long long h[8];
                 cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);
                 const double n = h[5] ? (double)h[5] : 1.0;
                 std::fprintf(stderr,
                              "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f phase1 %.0f phase2 %.0f "
-                             "wait_sbuf %.0f phase3 %.0f\n",
-                             J, h[5], h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n);
+                             "wait_sbuf %.0f phase3 %.0f (thread 0: fold %.0f scan+lift %.0f)\n",
+                             J, h[5], h[0] / n, (h[1] + h[6] + h[7]) / n, h[2] / n, h[3] / n, h[4] / n,
+                             h[6] / n, h[7] / n);
                 cudaFree(a.prof);
             }
             break;

@@ -163,8 +163,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         // ------------------------------------------------------------ producer
         if ((threadIdx.x & 31) != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
-        auto issue_load = [&](int64_t it) {
-            const int stage = (int)(it % NS);
+        // stage / S-buffer indices and mbarrier parities advance incrementally: no
+        // 64-bit division in the loop
+        auto issue_load = [&](int64_t it, int stage) {
             const int64_t tile = blockIdx.x + it * gridDim.x;
             const int64_t c0 = tile * a.C;
             const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
@@ -175,10 +176,11 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             for (uint32_t o = 0; o < bytes; o += piece)
                 bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
         };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it);
+        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it, (int)it);
+        int stage = 0, sb = 0;
+        uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
-            const int stage = (int)(it % NS);
-            mbar_wait(&done[stage], (uint32_t)((it / NS) & 1));
+            mbar_wait(&done[stage], phase);
             const int64_t tile = blockIdx.x + it * gridDim.x;
             const int64_t c0 = tile * a.C;
             const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 char* g = reinterpret_cast<char*>(a.gout + c0 * a.J * 12);
                 const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
                 char* s = do_skin ? reinterpret_cast<char*>(a.sout + c0 * a.J * 12) : nullptr;
-                const char* ss = reinterpret_cast<const char*>(SB + (it % NSS) * tile_f);
+                const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
                 for (uint32_t o = 0; o < bytes; o += piece) {
                     const uint32_t nb = min(piece, bytes - o);
                     bulk_s2g(g + o, sg + o, nb);
@@ -196,8 +198,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             }
             bulk_commit();
             bulk_wait_read<0>();                  // smem of this tile has been read out
-            if (do_skin) mbar_arrive(&sfree[it % NSS]);
-            if (it + NS < my_tiles) issue_load(it + NS);
+            if (do_skin) mbar_arrive(&sfree[sb]);
+            if (it + NS < my_tiles) issue_load(it + NS, stage);
+            if (++stage == NS) { stage = 0; phase ^= 1u; }
+            if (++sb == NSS) sb = 0;
         }
         bulk_wait_all();
         return;
@@ -244,11 +248,12 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             prof_last = now;
         }
     };
+    int stage = 0, sb = 0;
+    uint32_t phase = 0, sphase = 0;   // full[] parity; sfree[] parity of the S buffer's last use
     for (int64_t it = 0; it < my_tiles; ++it) {
-        const int stage = (int)(it % NS);
         float* L = LG + stage * tile_f;
         prof_mark(-1);
-        mbar_wait(&full[stage], (uint32_t)((it / NS) & 1));
+        mbar_wait(&full[stage], phase);
         prof_mark(0);
 
         // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
@@ -275,6 +280,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 }
             }
         }
+        prof_mark(6);   // phase-1 fold of thread 0 (before any barrier)
         // phase 2a: heavy paths longer than K sit on consecutive lanes (runs); a
         // segmented warp-shuffle scan joins their pieces (Hillis-Steele over lanes,
         // parent on the left), then each run lane lifts its anchors by its exclusive
@@ -307,6 +313,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 }
             }
         }
+        prof_mark(7);   // phase-2a scan + lift of thread 0's warp
         bar_consumers(NC);
 
         prof_mark(1);
@@ -356,8 +363,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         prof_mark(2);
 
         // phase 3: final fold, G in place, S into the S buffer
-        float* S = SB + (it % NSS) * tile_f;
-        if (do_skin && it >= NSS) mbar_wait(&sfree[it % NSS], (uint32_t)(((it / NSS) - 1) & 1));
+        float* S = SB + sb * tile_f;
+        if (do_skin && it >= NSS) mbar_wait(&sfree[sb], sphase);
         prof_mark(3);
         {
             float acc[12];
@@ -407,6 +414,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         if (t == 0) mbar_arrive(&done[stage]);
         prof_mark(4);
         if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
+        if (++stage == NS) { stage = 0; phase ^= 1u; }
+        if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }   // parity of use q-1
     }
 }
 
