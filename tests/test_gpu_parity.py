@@ -274,3 +274,37 @@ def test_abi_errors():
         with pytest.raises(hs.HSError) as e:
             hs.Skeleton(bad)
         assert e.value.status == code
+
+
+# ------------------------------------------------------------------ Fig. 7 shape (NEXT-2)
+def test_fig7_shape_depth_sweep():
+    """beyond ~30 levels the paper's method is 'significantly better' than
+    Gateau (Alg. 1) and KIYA; both walk ancestors, so their time grows with depth while
+    ours stays flat.  Small crowd, same seeded inputs, parity checked per cell."""
+    import statistics
+    res = {}
+    for depth in (15, 60, 120):
+        par = hsgen.random_tree(100 + depth, 300, depth)
+        local = hsgen.local_poses(7, 300, 2000)
+        x = torch.from_numpy(local).cuda()
+        g, s = torch.empty_like(x), torch.empty_like(x)
+        sk = hs.Skeleton(par)
+        G, _ = oracle.scan(par, local[:8])
+        for algo in ("auto", "gateau", "leaf"):
+            sk.scan_into(x, g, s, algo=algo)
+            torch.cuda.synchronize()
+            assert max_err(g[:8].cpu().numpy(), G) <= TOL
+            ts = []
+            for _ in range(7):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(); sk.scan_into(x, g, s, algo=algo); e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            res[(depth, algo)] = statistics.median(ts)
+        sk.close()
+    print(res)
+    for depth in (60, 120):
+        assert res[(depth, "auto")] < res[(depth, "gateau")]
+        assert res[(depth, "auto")] < res[(depth, "leaf")]
+    assert res[(120, "gateau")] > 2.5 * res[(15, "gateau")]       # ancestor walks grow with depth
+    assert res[(120, "auto")] < 2.0 * res[(15, "auto")]            # ours does not
