@@ -284,6 +284,11 @@ def run_ours(args):
     check = None
     if not (args.no_check or args.profile):
         check = sampled_parity(work, rank)
+        if world > 1:   # every rank checks its own shard; the job passes only if all do
+            worst = torch.tensor([check["worst"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(worst, op=dist.ReduceOp.MAX)
+            check["worst_all_ranks"] = float(worst.item())
+            check["pass"] = check["worst_all_ranks"] <= check["tolerance"]
 
     # ---- warm-up, then exactly K timed steps between barrier + synchronize
     for _ in range(args.warmup):
@@ -384,6 +389,7 @@ def sampled_parity(work, rank, per_type=24):
         out[w["name"]] = {"chars": len(idx), "max_err_global": eg, "max_err_skin": es,
                           "gen_elements_differing": gen_mismatch}
     out["tolerance"] = 1e-4
+    out["worst"] = worst
     out["pass"] = worst <= 1e-4
     if not out["pass"]:
         print(f"PARITY FAILURE: {out}", file=sys.stderr)
