@@ -70,6 +70,11 @@ def lib():
         L.hsg_permutation.restype = None
         L.hsg_signed_perm.argtypes = [ctypes.c_int, ctypes.c_void_p]
         L.hsg_signed_perm.restype = None
+        L.hsg_clips.argtypes = [u64, u64, u64, u64, u64, ctypes.c_float, ctypes.c_float,
+                                ctypes.c_void_p]
+        L.hsg_clips.restype = None
+        L.hsg_layers.argtypes = [u64, u64, u64, u64, u64, u64, ctypes.c_float, ctypes.c_void_p]
+        L.hsg_layers.restype = None
         _lib = L
     return _lib
 
@@ -190,3 +195,24 @@ CONFIGS = {
     5: [("hum64", 333_334, 5, 0, 2), ("chain256", 333_333, 5, 1, 3),
         ("tree1024", 333_333, 5, 2, 4)],
 }
+
+
+# --- Stage-1 inputs (NEXT-1) -----------------------------------------------------
+LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])
+
+
+def clips(seed: int, J: int, n_clips: int, n_keys: int, type_: int = 0,
+          scale=(1.0, 1.0)) -> np.ndarray:
+    """Keyframes [n_clips, n_keys, J, 10] fp32: t(3), q(w,x,y,z), s(3)."""
+    out = np.empty((n_clips, n_keys, J, 10), np.float32)
+    lib().hsg_clips(seed, type_, n_clips, n_keys, J, scale[0], scale[1], out.ctypes.data)
+    return out
+
+
+def layers(seed: int, n_chars: int, n_layers: int, n_clips: int, time_span: float,
+           char0: int = 0, type_: int = 0) -> np.ndarray:
+    """Per-character animation layers [n_chars, n_layers] (clip, time, weight)."""
+    out = np.zeros((n_chars, n_layers), LAYER_DTYPE)
+    if n_chars:
+        lib().hsg_layers(seed, type_, char0, n_chars, n_layers, n_clips, time_span, out.ctypes.data)
+    return out

@@ -235,3 +235,53 @@ void hsg_permutation(uint64_t seed, uint64_t type, int32_t n, int32_t* perm) {
         int32_t tmp = perm[i]; perm[i] = perm[j]; perm[j] = tmp;
     }
 }
+
+/* ---- Stage-1 inputs (NEXT-1): animation clips and per-character layer states ----
+ * Clip keys: fp32 [n_clips][n_keys][J][10] = t(3), q = (w,x,y,z), s(3); stream
+ * 8*type + 7, counter character = clip*n_keys + key; rotation draws k = 0..2
+ * (Shoemake), translation k = 3..5 (unit ball), scale k = 6: s = lo + (hi-lo)*u
+ * for all three axes (lo = hi = 1 gives rigid keys). */
+void hsg_clips(uint64_t seed, uint64_t type, uint64_t n_clips, uint64_t n_keys, uint64_t J,
+               float scale_lo, float scale_hi, float* keys) {
+    const uint64_t s = 8 * type + 7;
+    for (uint64_t c = 0; c < n_clips; ++c)
+        for (uint64_t k = 0; k < n_keys; ++k)
+            for (uint64_t j = 0; j < J; ++j) {
+                const uint64_t ch = c * n_keys + k;
+                double R[9], t[3];
+                (void)R;
+                double u0 = hsg_u(seed, s, ch, J, j, 0), u1 = hsg_u(seed, s, ch, J, j, 1),
+                       u2 = hsg_u(seed, s, ch, J, j, 2);
+                double s1 = sqrt(1.0 - u0), s2 = sqrt(u0);
+                double a1 = 2.0 * HSG_PI * u1, a2 = 2.0 * HSG_PI * u2;
+                double x = s1 * sin(a1), y = s1 * cos(a1), z = s2 * sin(a2), w = s2 * cos(a2);
+                ball_from_u(hsg_u(seed, s, ch, J, j, 3), hsg_u(seed, s, ch, J, j, 4),
+                            hsg_u(seed, s, ch, J, j, 5), t);
+                const double sc = (double)scale_lo + ((double)scale_hi - (double)scale_lo) *
+                                                         hsg_u(seed, s, ch, J, j, 6);
+                float* o = keys + ((c * n_keys + k) * J + j) * 10;
+                o[0] = (float)t[0]; o[1] = (float)t[1]; o[2] = (float)t[2];
+                o[3] = (float)w; o[4] = (float)x; o[5] = (float)y; o[6] = (float)z;
+                o[7] = o[8] = o[9] = (float)sc;
+            }
+}
+
+/* Layer states of characters [char0, char0 + n_chars): int32 clip, f32 time, f32 weight,
+ * int32 pad per layer; stream 8*(type + 32) + 7, counter (character, layer): clip =
+ * floor(u0 * n_clips), time = u1 * time_span, weight = 0.05 + 0.95 * u2. */
+void hsg_layers(uint64_t seed, uint64_t type, uint64_t char0, uint64_t n_chars, uint64_t n_layers,
+                uint64_t n_clips, float time_span, void* out) {
+    const uint64_t s = 8 * (type + 32) + 7;
+    unsigned char* base = (unsigned char*)out;
+    for (uint64_t c = 0; c < n_chars; ++c)
+        for (uint64_t l = 0; l < n_layers; ++l) {
+            const uint64_t ch = char0 + c;
+            int32_t clip = (int32_t)floor(hsg_u(seed, s, ch, n_layers, l, 0) * (double)n_clips);
+            if (clip >= (int32_t)n_clips) clip = (int32_t)n_clips - 1;
+            const float tm = (float)(hsg_u(seed, s, ch, n_layers, l, 1) * (double)time_span);
+            const float wt = (float)(0.05 + 0.95 * hsg_u(seed, s, ch, n_layers, l, 2));
+            unsigned char* p = base + (c * n_layers + l) * 16;
+            const int32_t pad = 0;
+            memcpy(p, &clip, 4); memcpy(p + 4, &tm, 4); memcpy(p + 8, &wt, 4); memcpy(p + 12, &pad, 4);
+        }
+}

@@ -19,15 +19,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "stage1.c")]
 
 STATUS = {0: "ok", 2: "empty", 3: "out_of_range", 4: "cycle", 6: "nomem"}
 
 
 def build(force: bool = False) -> str:
     """Compile oracle.c with -O2 -ffp-contract=off (no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(s)
+                                                for s in _SRCS):
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-shared",
-               "-fPIC", "-pthread", "-o", _SO, _SRC]
+               "-fPIC", "-pthread", "-o", _SO, *_SRCS, "-lm"]
         subprocess.run(cmd, check=True)
     return _SO
 
@@ -51,6 +53,21 @@ def lib():
                                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                ctypes.POINTER(ctypes.c_double)]
         L.orc_scan.restype = ctypes.c_int
+        vp = ctypes.c_void_p
+        L.orc_key_index.argtypes = [ctypes.c_float, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float)]
+        L.orc_key_index.restype = None
+        L.orc_sample.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_float, ctypes.c_int32,
+                                 ctypes.c_float, ctypes.c_int32, vp]
+        L.orc_sample.restype = None
+        L.orc_blend.argtypes = [ctypes.c_int32, vp, vp, vp]
+        L.orc_blend.restype = None
+        L.orc_trs_to_matrix.argtypes = [vp, vp]
+        L.orc_trs_to_matrix.restype = None
+        L.orc_animate.argtypes = [i32p, ctypes.c_int32, vp, ctypes.c_int32, ctypes.c_float,
+                                  ctypes.c_int32, vp, ctypes.c_int32, vp, ctypes.c_int64, vp, vp, vp,
+                                  ctypes.c_int]
+        L.orc_animate.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -134,3 +151,60 @@ def scan_discard(parents, local, inv_bind=None, nthreads: int | None = None) -> 
     if st:
         raise OracleError(st)
     return cs.value
+
+
+# ---------------------------------------------------------------- Stage 1 (NEXT-1)
+LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])
+
+
+def key_index(t: float, n_keys: int, fps: float, wrap: int):
+    k = ctypes.c_int32()
+    a = ctypes.c_float()
+    lib().orc_key_index(t, n_keys, fps, wrap, ctypes.byref(k), ctypes.byref(a))
+    return k.value, a.value
+
+
+def sample(clip_keys, fps: float, wrap: int, t: float, joint: int) -> np.ndarray:
+    """clip_keys: [n_keys, J, 10] fp32 (one clip) -> fp64 Trs (t3, q wxyz, s3)."""
+    ck = np.ascontiguousarray(clip_keys, np.float32)
+    out = np.empty(10, np.float64)
+    lib().orc_sample(ck.ctypes.data, ck.shape[0], ck.shape[1], fps, wrap, t, joint, out.ctypes.data)
+    return out
+
+
+def blend(poses, weights) -> np.ndarray:
+    p = np.ascontiguousarray(poses, np.float64).reshape(-1, 10)
+    w = np.ascontiguousarray(weights, np.float64)
+    out = np.empty(10, np.float64)
+    lib().orc_blend(len(p), p.ctypes.data, w.ctypes.data, out.ctypes.data)
+    return out
+
+
+def trs_to_matrix(trs) -> np.ndarray:
+    t = np.ascontiguousarray(trs, np.float64)
+    out = np.empty(12, np.float64)
+    lib().orc_trs_to_matrix(t.ctypes.data, out.ctypes.data)
+    return out.reshape(3, 4)
+
+
+def animate(parents, keys, fps: float, wrap: int, layers, inv_bind=None, nthreads=None,
+            return_local=False):
+    """Stage 1 + scan + bind in fp64.  keys: [n_clips, n_keys, J, 10] fp32; layers:
+    structured [n_chars, n_layers] of LAYER_DTYPE.  Returns (G, S[, L])."""
+    p, pp = _i32(parents)
+    J = len(p)
+    k = np.ascontiguousarray(keys, np.float32)
+    assert k.shape[2] == J and k.shape[3] == 10
+    lay = np.ascontiguousarray(layers, LAYER_DTYPE)
+    n_chars, n_layers = lay.shape
+    ib = None if inv_bind is None else np.ascontiguousarray(inv_bind, np.float32)
+    g = np.empty((n_chars, J, 3, 4), np.float64)
+    s = np.empty_like(g)
+    loc = np.empty_like(g) if return_local else None
+    st = lib().orc_animate(pp, J, k.ctypes.data, k.shape[1], fps, wrap, lay.ctypes.data, n_layers,
+                           None if ib is None else ib.ctypes.data, n_chars, g.ctypes.data,
+                           s.ctypes.data, None if loc is None else loc.ctypes.data,
+                           nthreads or os.cpu_count() or 1)
+    if st:
+        raise OracleError(st)
+    return (g, s, loc) if return_local else (g, s)
