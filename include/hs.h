@@ -132,6 +132,38 @@ typedef struct {
 hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,
                      float* skin_out, void* cuda_stream, const hs_scan_opts* opts);
 
+/* ---------------------------------------------------------------------------
+ * Stage 1 fused ahead of the scan ("Sample
+ * animation data and generate local pose in local space").
+ * Per character and joint: sample each animation layer's clip at its time (keys
+ * uniformly spaced at `fps`; linear t/s, normalised-lerp rotation with the
+ * shortest-arc sign fix; an exact key time returns the key), blend the layers
+ * (weights normalised; quaternions sign-aligned to layer 0; one layer = its
+ * sample), build L = [R(q) diag(s) | t], then Hierarchy-Scan + Bind as hs_scan.
+ * The local poses never touch HBM (96 instead of 144 bytes per joint).
+ * ------------------------------------------------------------------------- */
+typedef struct hs_clipset hs_clipset;
+
+/* keys: host fp32 [n_clips][n_keys][n_joints][10] = t(3), q(w,x,y,z), s(3), for the
+ * skeleton `sk` (same n_joints); key k of a clip is at time k / fps; wrap: 0 = clamp,
+ * 1 = loop (duration = (n_keys - 1) / fps).  Copied to the handle's device. */
+hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_clips, int32_t n_keys,
+                            float fps, int32_t wrap, hs_clipset** out);
+hs_status hs_clipset_destroy(hs_clipset* cs);
+
+/* One animation layer of one character (16 bytes). */
+typedef struct {
+    int32_t clip;      /* clip index in the clip set                                  */
+    float time;        /* seconds                                                     */
+    float weight;      /* blend weight (> 0 for at least one layer)                   */
+    int32_t reserved;  /* ignored                                                     */
+} hs_layer;
+
+/* layers: device [n_chars][n_layers] hs_layer (n_layers 1..8), 16-byte aligned; outputs
+ * as hs_scan.  Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise). */
+hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                     int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream);
+
 /* Destroy a handle (NULL-safe).  The caller guarantees no hs_scan using it is
  * still in flight.  Frees its device tables with cudaFree (device-synchronising). */
 hs_status hs_destroy(hs_skeleton* sk);

@@ -103,12 +103,16 @@ def lib():
     L.hs_plan_query.argtypes = [vp, i32, ctypes.POINTER(i64)]
     L.hs_plan_export.argtypes = [vp, i32, vp, i64]
     L.hs_plan_destroy.argtypes = [vp]
+    L.hs_clipset_create.argtypes = [vp, vp, i32, i32, ctypes.c_float, i32, ctypes.POINTER(vp)]
+    L.hs_clipset_destroy.argtypes = [vp]
+    L.hs_animate.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
     for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
               "hs_skeleton_query", "hs_plan_create", "hs_plan_create_ex", "hs_plan_query", "hs_plan_export",
-              "hs_plan_destroy", "hs_pipeline_create", "hs_scan_host", "hs_pipeline_destroy"):
+              "hs_plan_destroy", "hs_pipeline_create", "hs_scan_host", "hs_pipeline_destroy",
+              "hs_clipset_create", "hs_clipset_destroy", "hs_animate"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -247,6 +251,54 @@ class Skeleton:
         self._h = None
 
     __del__ = close
+
+
+LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])
+
+
+class ClipSet:
+    """Animation clips for one skeleton (hs_clipset_create): keys [n_clips, n_keys, J, 10]
+    fp32 = t(3), q(w,x,y,z), s(3), uniformly spaced at fps; wrap 0 clamp / 1 loop."""
+
+    def __init__(self, sk: "Skeleton", keys, fps: float, wrap: int = 1):
+        k = np.ascontiguousarray(np.asarray(keys, dtype=np.float32))
+        if k.ndim != 4 or k.shape[2] != sk.n_joints or k.shape[3] != 10:
+            raise ValueError(f"keys must be [n_clips, n_keys, {sk.n_joints}, 10]")
+        h = ctypes.c_void_p()
+        _check(lib().hs_clipset_create(sk.handle, k.ctypes.data, k.shape[0], k.shape[1], fps, wrap,
+                                       ctypes.byref(h)), "hs_clipset_create")
+        self._h, self.n_clips, self.n_keys = h, k.shape[0], k.shape[1]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hs_clipset_destroy(self._h)
+        self._h = None
+
+    __del__ = close
+
+
+def animate(sk: "Skeleton", clips: ClipSet, layers, global_out=None, skin_out=None, stream=None,
+            skin: bool = True):
+    """Stage 1 + Hierarchy-Scan + Bind (hs_animate).  layers: CUDA tensor [N, n_layers, 4]
+    int32 / float32 bit pattern of hs_layer, or a numpy LAYER_DTYPE array (copied)."""
+    import torch
+    if isinstance(layers, np.ndarray):
+        layers = torch.from_numpy(np.ascontiguousarray(layers).view(np.int32).reshape(
+            layers.shape[0], layers.shape[1], 4)).cuda()
+    n, nl = layers.shape[0], layers.shape[1]
+    if global_out is None:
+        global_out = torch.empty((n, sk.n_joints, 3, 4), dtype=torch.float32, device=layers.device)
+    if skin_out is None and skin:
+        skin_out = torch.empty_like(global_out)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_animate(sk.handle, clips.handle, layers.data_ptr(), nl, n, global_out.data_ptr(),
+                            None if skin_out is None else skin_out.data_ptr(), st), "hs_animate")
+    return global_out, skin_out
 
 
 class Pipeline:

@@ -76,6 +76,13 @@ struct hs_skeleton {
     int32_t n_leaves = 0;
 };
 
+struct hs_clipset {
+    int device = 0;
+    int32_t n_clips = 0, n_keys = 0, n_joints = 0, wrap = 0;
+    float fps = 0.f, duration = 0.f;
+    float* d_keys = nullptr;   // [n_clips][n_keys][n_joints][12] packed {t,qw} {qxyz,sx} {sy,sz,0,0}
+};
+
 struct hs_pipeline {
     int device = 0;
     int64_t batch_bytes = 0;
@@ -244,7 +251,8 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, float* gout,
-                    float* sout, cudaStream_t st, int algo, int max_rounds, int tile_ctas) {
+                    float* sout, cudaStream_t st, int algo, int max_rounds, int tile_ctas,
+                    const hs_clipset* cs = nullptr, const void* layers = nullptr, int n_layers = 0) {
     const int32_t J = sk->plan.n;
     cudaError_t e = cudaSuccess;
     if (algo == HS_ALGO_AUTO) algo = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT;
@@ -264,6 +272,13 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.smem_bytes = sk->smem; a.threads = sk->threads;
             a.ctas_per_sm = tile_ctas;
             a.p_single = sk->tp.pingpong ? 0 : 1;
+            a.layers = layers;
+            a.keys = cs ? cs->d_keys : nullptr;
+            a.n_layers = n_layers;
+            a.n_keys = cs ? cs->n_keys : 0;
+            a.wrap = cs ? cs->wrap : 0;
+            a.fps = cs ? cs->fps : 0.f;
+            a.duration = cs ? cs->duration : 0.f;
             a.prof = nullptr;
             if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
                 cudaMalloc(reinterpret_cast<void**>(&a.prof), 8 * sizeof(unsigned long long));
@@ -392,6 +407,57 @@ hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars,
     if (dev != sk->device) return fail(HS_ERR_WRONG_DEVICE, "handle belongs to another device");
     return scan_impl(sk, local, n_chars, global_out, skin_out, static_cast<cudaStream_t>(cuda_stream),
                      algo, max_rounds, tile_ctas);
+}
+
+hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_clips, int32_t n_keys,
+                            float fps, int32_t wrap, hs_clipset** out) {
+    if (!sk || !keys || !out) return fail(HS_ERR_INVALID_ARG, "null argument");
+    if (n_clips <= 0 || n_keys <= 0 || !(fps > 0.f) || wrap < 0 || wrap > 1)
+        return fail(HS_ERR_INVALID_ARG, "n_clips, n_keys, fps must be positive; wrap 0 or 1");
+    const int32_t J = sk->plan.n;
+    if ((int64_t)n_clips * n_keys * J > ((int64_t)1 << 31))
+        return fail(HS_ERR_INVALID_ARG, "clip set too large");
+    hs_clipset* cs = new (std::nothrow) hs_clipset();
+    if (!cs) return fail(HS_ERR_OOM, "host allocation failed");
+    cudaGetDevice(&cs->device);
+    cs->n_clips = n_clips; cs->n_keys = n_keys; cs->n_joints = J; cs->wrap = wrap; cs->fps = fps;
+    cs->duration = (float)(n_keys - 1) / fps;   // same fp32 operation as the oracle (R20)
+    std::vector<float> packed((size_t)n_clips * n_keys * J * 12, 0.f);
+    for (size_t r = 0; r < (size_t)n_clips * n_keys * J; ++r) {
+        const float* s = keys + r * 10;
+        float* d = packed.data() + r * 12;
+        for (int e = 0; e < 10; ++e) d[e] = s[e];   // t0 t1 t2 qw | qx qy qz sx | sy sz 0 0
+    }
+    cudaError_t e = upload(&cs->d_keys, packed.data(), packed.size());
+    if (e != cudaSuccess) { delete cs; return cuda_fail(e, "clip upload"); }
+    *out = cs;
+    return HS_OK;
+}
+
+hs_status hs_clipset_destroy(hs_clipset* cs) {
+    if (!cs) return HS_OK;
+    cudaFree(cs->d_keys);
+    delete cs;
+    return HS_OK;
+}
+
+hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                     int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream) {
+    if (!sk || !cs) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!layers || !global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (n_layers < 1 || n_layers > 8) return fail(HS_ERR_INVALID_ARG, "n_layers must be in 1..8");
+    if (cs->n_joints != sk->plan.n) return fail(HS_ERR_INVALID_ARG, "clip set built for another skeleton");
+    if (!aligned16(layers) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)))
+        return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+    if (skin_out == global_out) return fail(HS_ERR_INVALID_ARG, "outputs alias");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != sk->device || dev != cs->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "hs_animate needs a single-CTA skeleton");
+    return scan_impl(sk, nullptr, n_chars, global_out, skin_out, static_cast<cudaStream_t>(cuda_stream),
+                     HS_ALGO_CHUNKED, -1, 0, cs, layers, n_layers);
 }
 
 hs_status hs_scan(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,

@@ -119,6 +119,112 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// ================================================================== Stage 1 (NEXT-1)
+// Keyframe sampling, layer blending and TRS -> 3x4 (
+// DESIGN.md readings R19-R23), fused ahead of the scan: the local pose is computed
+// in shared memory instead of being read from HBM.  Keys on the device are packed
+// per (clip, key, joint) as three float4: {tx,ty,tz,qw} {qx,qy,qz,sx} {sy,sz,-,-}.
+// The time -> key decision uses the oracle's exact fp32 operation sequence.
+__device__ __forceinline__ void key_index(float t, int n_keys, float fps, float duration, int wrap,
+                                          int& k0, float& a) {
+    if (n_keys <= 1) { k0 = 0; a = 0.0f; return; }
+    float tt;
+    if (wrap == 1) {
+        const float q = floorf(__fdiv_rn(t, duration));
+        tt = __fsub_rn(t, __fmul_rn(q, duration));
+        if (tt < 0.0f) tt = 0.0f;
+    } else {
+        tt = t < 0.0f ? 0.0f : (t > duration ? duration : t);
+    }
+    const float u = __fmul_rn(tt, fps);
+    const float kf = floorf(u);
+    float frac = __fsub_rn(u, kf);
+    int ki = (int)kf;
+    if (ki >= n_keys - 1) { ki = n_keys - 1; frac = 0.0f; }
+    if (ki < 0) { ki = 0; frac = 0.0f; }
+    k0 = ki;
+    a = frac;
+}
+
+// Sample joint j of clip `clip`: trs = t(3), q(w,x,y,z)(4), s(3).
+__device__ __forceinline__ void sample_trs(const float4* __restrict__ keys, int n_keys, int J, int clip,
+                                           int j, int k0, float a, float* trs) {
+    const float4* p0 = keys + ((int64_t)(clip * n_keys + k0) * J + j) * 3;
+    const float4 x0 = __ldg(p0), y0 = __ldg(p0 + 1), z0 = __ldg(p0 + 2);
+    if (a == 0.0f) {
+        trs[0] = x0.x; trs[1] = x0.y; trs[2] = x0.z; trs[3] = x0.w;
+        trs[4] = y0.x; trs[5] = y0.y; trs[6] = y0.z;
+        trs[7] = y0.w; trs[8] = z0.x; trs[9] = z0.y;
+        return;
+    }
+    const float4* p1 = p0 + (int64_t)J * 3;
+    const float4 x1 = __ldg(p1), y1 = __ldg(p1 + 1), z1 = __ldg(p1 + 2);
+    const float b = 1.0f - a;
+    trs[0] = b * x0.x + a * x1.x; trs[1] = b * x0.y + a * x1.y; trs[2] = b * x0.z + a * x1.z;
+    trs[7] = b * y0.w + a * y1.w; trs[8] = b * z0.x + a * z1.x; trs[9] = b * z0.y + a * z1.y;
+    const float d = x0.w * x1.w + y0.x * y1.x + y0.y * y1.y + y0.z * y1.z;
+    const float as = d < 0.0f ? -a : a;
+    float qw = b * x0.w + as * x1.w, qx = b * y0.x + as * y1.x, qy = b * y0.y + as * y1.y,
+          qz = b * y0.z + as * y1.z;
+    const float inv = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    trs[3] = qw * inv; trs[4] = qx * inv; trs[5] = qy * inv; trs[6] = qz * inv;
+}
+
+__device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
+    const float w = trs[3], x = trs[4], y = trs[5], z = trs[6];
+    const float sx = trs[7], sy = trs[8], sz = trs[9];
+    m[0] = (1.0f - 2.0f * (y * y + z * z)) * sx; m[1] = 2.0f * (x * y - w * z) * sy;
+    m[2] = 2.0f * (x * z + w * y) * sz;          m[3] = trs[0];
+    m[4] = 2.0f * (x * y + w * z) * sx;          m[5] = (1.0f - 2.0f * (x * x + z * z)) * sy;
+    m[6] = 2.0f * (y * z - w * x) * sz;          m[7] = trs[1];
+    m[8] = 2.0f * (x * z - w * y) * sx;          m[9] = 2.0f * (y * z + w * x) * sy;
+    m[10] = (1.0f - 2.0f * (x * x + y * y)) * sz; m[11] = trs[2];
+}
+
+// Local pose of joint j for one character's layers (n_layers <= 8): blend of samples.
+__device__ __forceinline__ void stage1_local(const ChunkedArgs& a, const int4* __restrict__ lay, int j,
+                                             float* m) {
+    float acc[10], first[10];
+    float wsum = 0.0f;
+    const int nl = a.n_layers;
+    for (int l = 0; l < nl; ++l) {
+        const int4 L = __ldg(lay + l);
+        const float t = __int_as_float(L.y), w = __int_as_float(L.z);
+        int k0;
+        float fr;
+        key_index(t, a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
+        float s[10];
+        sample_trs(reinterpret_cast<const float4*>(a.keys), a.n_keys, a.J, L.x, j, k0, fr, s);
+        if (l == 0) {
+#pragma unroll
+            for (int e = 0; e < 10; ++e) { first[e] = s[e]; acc[e] = w * s[e]; }
+        } else {
+            const float d = s[3] * first[3] + s[4] * first[4] + s[5] * first[5] + s[6] * first[6];
+            const float ws = d < 0.0f ? -w : w;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) acc[e] += w * s[e];
+#pragma unroll
+            for (int e = 3; e < 7; ++e) acc[e] += ws * s[e];
+#pragma unroll
+            for (int e = 7; e < 10; ++e) acc[e] += w * s[e];
+        }
+        wsum += w;
+    }
+    if (nl == 1) {
+        trs_to_m34(first, m);   // one layer: the sample itself (R22)
+        return;
+    }
+    const float iw = 1.0f / wsum;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) acc[e] *= iw;
+#pragma unroll
+    for (int e = 7; e < 10; ++e) acc[e] *= iw;
+    const float inv = rsqrtf(acc[3] * acc[3] + acc[4] * acc[4] + acc[5] * acc[5] + acc[6] * acc[6]);
+#pragma unroll
+    for (int e = 3; e < 7; ++e) acc[e] *= inv;
+    trs_to_m34(acc, m);
+}
+
 // ================================================================== chunked kernel
 // Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
 // producer.  Per tile of C characters (F = C*J joints, user order in smem):
@@ -130,7 +236,7 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
 //            segment head's parent, writes G in place over L, and S = G (x) IB
 //            (IB held in registers) into the S buffer;
 // then the producer bulk-stores G and S and refills the stage.
-template <int K, bool RUNS>
+template <int K, bool RUNS, bool PRO>
 __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int NS = a.stages, NSS = a.sbufs;
@@ -176,7 +282,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             for (uint32_t o = 0; o < bytes; o += piece)
                 bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
         };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it, (int)it);
+        if (!PRO)
+            for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it, (int)it);
         int stage = 0, sb = 0;
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
@@ -199,7 +306,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             bulk_commit();
             bulk_wait_read<0>();                  // smem of this tile has been read out
             if (do_skin) mbar_arrive(&sfree[sb]);
-            if (it + NS < my_tiles) issue_load(it + NS, stage);
+            if (PRO) mbar_arrive(&full[stage]);   // Stage 1 computes tiles in place: stage free
+            else if (it + NS < my_tiles) issue_load(it + NS, stage);
             if (++stage == NS) { stage = 0; phase ^= 1u; }
             if (++sb == NSS) sb = 0;
         }
@@ -253,7 +361,27 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     for (int64_t it = 0; it < my_tiles; ++it) {
         float* L = LG + stage * tile_f;
         prof_mark(-1);
-        mbar_wait(&full[stage], phase);
+        if (!PRO) {
+            mbar_wait(&full[stage], phase);
+        } else {
+            // phase 0 (Stage 1): this thread's joints' local poses, computed in place in
+            // the stage buffer once the producer has stored that stage's last tile
+            if (it >= NS) mbar_wait(&full[stage], phase ^ 1u);
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int src = (int)(int16_t)(m[s] >> 32);
+                if (src == kSrcNone) continue;
+                const int off = (int)(m[s] & 0xffff);
+                const int u = (int)((m[s] >> 16) & 0xffff);
+                const int64_t ch = c0 + off / a.J;
+                if (ch >= a.n_chars) continue;
+                const int4* lay = reinterpret_cast<const int4*>(a.layers) + ch * a.n_layers;
+                float lm[12];
+                stage1_local(a, lay, u, lm);
+                st3(L + off * 12, lm);
+            }
+        }
         prof_mark(0);
 
         // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
@@ -609,18 +737,21 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
 }
 
 template <int K>
-void* chunked_ptr(bool runs) {
-    return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true>)
-                : reinterpret_cast<void*>(&chunked_kernel<K, false>);
+void* chunked_ptr(bool runs, bool pro) {
+    if (pro)
+        return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true, true>)
+                    : reinterpret_cast<void*>(&chunked_kernel<K, false, true>);
+    return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true, false>)
+                : reinterpret_cast<void*>(&chunked_kernel<K, false, false>);
 }
 
-void* chunked_fn(int K, bool runs) {
+void* chunked_fn(int K, bool runs, bool pro) {
     switch (K) {
-        case 3: return chunked_ptr<3>(runs);
-        case 5: return chunked_ptr<5>(runs);
-        case 7: return chunked_ptr<7>(runs);
-        case 9: return chunked_ptr<9>(runs);
-        case 11: return chunked_ptr<11>(runs);
+        case 3: return chunked_ptr<3>(runs, pro);
+        case 5: return chunked_ptr<5>(runs, pro);
+        case 7: return chunked_ptr<7>(runs, pro);
+        case 9: return chunked_ptr<9>(runs, pro);
+        case 11: return chunked_ptr<11>(runs, pro);
         default: return nullptr;
     }
 }
@@ -646,17 +777,18 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
-    for (bool runs : {false, true}) {
-        void* fn = chunked_fn(K, runs);
-        if (!fn) return cudaErrorInvalidValue;
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        if (e != cudaSuccess) return e;
-    }
+    for (bool runs : {false, true})
+        for (bool pro : {false, true}) {
+            void* fn = chunked_fn(K, runs, pro);
+            if (!fn) return cudaErrorInvalidValue;
+            e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+            if (e != cudaSuccess) return e;
+        }
     return cudaSuccess;
 }
 
 int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes) {
-    void* fn = chunked_fn(K, runs);
+    void* fn = chunked_fn(K, runs, false);
     int nb = 0;
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
                    cudaSuccess)
@@ -665,7 +797,7 @@ int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes)
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    void* fn = chunked_fn(K, a.has_runs != 0);
+    void* fn = chunked_fn(K, a.has_runs != 0, a.layers != nullptr);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
     int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm

@@ -27,6 +27,11 @@ struct ChunkedArgs {
     int32_t has_runs;          // lanes joined by the warp-shuffle scan (CHUNK_RUNS programs)
     int32_t bulk_piece;        // bytes per TMA bulk copy (0 = one copy per tile and buffer)
     int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
+    // Stage-1 prologue (hs_animate): layers != nullptr replaces the local-pose input
+    const void* layers;        // device [n_chars][n_layers] hs_layer (16 B)
+    const float* keys;         // device [n_clips][n_keys][J][12] packed keys
+    int32_t n_layers, n_keys, wrap;
+    float fps, duration;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);

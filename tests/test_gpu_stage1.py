@@ -1,0 +1,94 @@
+"""GPU parity of the fused Stage-1 prologue (hs_animate) against
+the fp64 oracle (oracle.animate): sampling, blending, TRS, then scan + bind."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import hsgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2505_06703_b200 as hs  # noqa: E402
+
+TOL = 1e-4
+
+
+def run(par, keys, fps, wrap, lay, ib=None, **create):
+    sk = hs.Skeleton(par, ib, **create)
+    cs = hs.ClipSet(sk, keys, fps, wrap)
+    g, s = hs.animate(sk, cs, lay)
+    torch.cuda.synchronize()
+    return g.cpu().numpy(), s.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,n_layers,wrap", [("hum64", 2, 1), ("chain256", 3, 0),
+                                                ("tree1024", 2, 1), ("hum32", 1, 1),
+                                                ("tree1024", 1, 0)])
+def test_animate_parity(name, n_layers, wrap):
+    par = hsgen.skeleton(name)
+    J = len(par)
+    keys = hsgen.clips(11, J, 4, 31)
+    lay = hsgen.layers(11, 97, n_layers, 4, 1.6)     # times beyond the 1 s duration: wrap
+    ib = hsgen.inv_bind(11, J)
+    g, s = run(par, keys, 30.0, wrap, lay, ib)
+    G, S = oracle.animate(par, keys, 30.0, wrap, lay, ib)
+    eg, es = float(np.abs(g - G).max()), float(np.abs(s - S).max())
+    print(f"{name} layers={n_layers} wrap={wrap}: global {eg:.2e} skin {es:.2e}")
+    assert eg <= TOL and es <= TOL
+
+
+def test_animate_key_times_bitwise_on_exact_keys():
+    """One layer at exact key times on exact-family keys: Stage 1 returns the key's TRS
+    matrix and every product is exact -> bitwise equal to the oracle."""
+    par = hsgen.skeleton("tree1024")
+    J = len(par)
+    keys = np.zeros((2, 5, J, 10), np.float32)
+    keys[..., 7:] = 1.0
+    rng = np.random.default_rng(5)
+    quats = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]], np.float32)
+    keys[..., 3:7] = quats[rng.integers(0, 4, size=keys.shape[:3])]
+    keys[..., :3] = rng.integers(-1, 2, size=keys.shape[:3] + (3,))
+    lay = np.zeros((40, 1), hs.LAYER_DTYPE)
+    lay["clip"][:, 0] = rng.integers(0, 2, 40)
+    lay["time"][:, 0] = rng.integers(0, 5, 40) / 4.0
+    lay["weight"][:, 0] = 1.0
+    g, s = run(par, keys, 4.0, 0, lay)
+    G, S = oracle.animate(par, keys, 4.0, 0, lay)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
+
+
+def test_animate_scaled_shallow_skeleton():
+    par = hsgen.skeleton("hum32")
+    keys = hsgen.clips(12, 32, 3, 9, scale=(0.8, 1.25))
+    lay = hsgen.layers(12, 50, 3, 3, 0.7)
+    g, s = run(par, keys, 10.0, 1, lay)
+    G, S = oracle.animate(par, keys, 10.0, 1, lay)
+    assert float(np.abs(g - G).max()) <= TOL
+
+
+def test_animate_equals_scan_of_oracle_locals_chunk_variants():
+    """Same bits whatever chunking / K the skeleton uses (Stage 1 is per joint)."""
+    par = hsgen.skeleton("hum64")
+    keys = hsgen.clips(13, 64, 2, 7)
+    lay = hsgen.layers(13, 33, 2, 2, 0.5)
+    outs = [run(par, keys, 12.0, 1, lay, chunk=k, chunking=c)[0] for k, c in ((5, 1), (7, 2), (3, 3))]
+    G, _ = oracle.animate(par, keys, 12.0, 1, lay)
+    for g in outs:
+        assert float(np.abs(g - G).max()) <= TOL
+
+
+def test_animate_errors():
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    cs = hs.ClipSet(sk, hsgen.clips(1, 32, 1, 3), 10.0, 1)
+    lay = torch.zeros((4, 9, 4), dtype=torch.int32, device="cuda")
+    with pytest.raises(hs.HSError) as e:
+        hs.animate(sk, cs, lay)            # 9 layers > 8
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    other = hs.Skeleton(hsgen.skeleton("hum64"))
+    with pytest.raises(hs.HSError):
+        hs.animate(other, cs, torch.zeros((4, 1, 4), dtype=torch.int32, device="cuda"))
