@@ -59,6 +59,7 @@ struct hs_skeleton {
     hs::TileProgram tp;
     int stages = 0, sbufs = 0, threads = 0, chunking = 1;
     int64_t smem = 0;
+    int smem_optin = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
     int split_levels = 0;
@@ -80,7 +81,7 @@ struct hs_clipset {
     int device = 0;
     int32_t n_clips = 0, n_keys = 0, n_joints = 0, wrap = 0;
     float fps = 0.f, duration = 0.f;
-    float* d_keys = nullptr;   // [n_clips][n_keys][n_joints][12] packed {t,qw} {qxyz,sx} {sy,sz,0,0}
+    float* d_keys = nullptr;   // [n_clips][n_keys][3][n_joints] float4: {t,qw} {qxyz,sx} {sy,sz,0,0}
 };
 
 struct hs_pipeline {
@@ -128,6 +129,7 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     int smem_optin = 0;
     e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, sk->device);
     if (e != cudaSuccess) { delete sk; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+    sk->smem_optin = smem_optin;
 
     const hs::Plan& P = sk->plan;
     sk->K = o.chunk ? o.chunk : 5;
@@ -279,10 +281,27 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.wrap = cs ? cs->wrap : 0;
             a.fps = cs ? cs->fps : 0.f;
             a.duration = cs ? cs->duration : 0.f;
+            a.desc_off = 0;
+            if (layers) {
+                // Stage 1: a [stages][C * n_layers] int4 descriptor ring after the tables;
+                // a third stage is dropped if the ring does not fit beside it
+                for (;;) {
+                    const int64_t base = hs::tile_smem_bytes(sk->tp, a.stages, a.sbufs);
+                    const int64_t need = base + (int64_t)a.stages * a.C * n_layers * 16;
+                    if (need <= sk->smem_optin) {
+                        a.desc_off = (int32_t)base;
+                        a.smem_bytes = need;
+                        break;
+                    }
+                    if (a.stages <= 2)
+                        return fail(HS_ERR_UNSUPPORTED, "no shared memory left for the Stage-1 descriptors");
+                    --a.stages;
+                }
+            }
             a.prof = nullptr;
             if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
-                cudaMalloc(reinterpret_cast<void**>(&a.prof), 8 * sizeof(unsigned long long));
-                cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st);
+                cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
+                cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
             }
             e = hs::launch_chunked(sk->K, a, st);
             if (e != cudaSuccess) {
@@ -292,14 +311,14 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 return cuda_fail(e, buf);
             }
             if (a.prof) {
-                unsigned long long h[8];
+                unsigned long long h[10];
                 cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);
                 const double n = h[5] ? (double)h[5] : 1.0;
                 std::fprintf(stderr,
-                             "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f phase1 %.0f phase2 %.0f "
+                             "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f stage1 %.0f phase1 %.0f phase2 %.0f "
                              "wait_sbuf %.0f phase3 %.0f (thread 0: fold %.0f scan+lift %.0f)\n",
-                             J, h[5], h[0] / n, (h[1] + h[6] + h[7]) / n, h[2] / n, h[3] / n, h[4] / n,
+                             J, h[5], h[0] / n, h[8] / n, (h[1] + h[6] + h[7]) / n, h[2] / n, h[3] / n, h[4] / n,
                              h[6] / n, h[7] / n);
                 cudaFree(a.prof);
             }
@@ -415,19 +434,23 @@ hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_
     if (n_clips <= 0 || n_keys <= 0 || !(fps > 0.f) || wrap < 0 || wrap > 1)
         return fail(HS_ERR_INVALID_ARG, "n_clips, n_keys, fps must be positive; wrap 0 or 1");
     const int32_t J = sk->plan.n;
-    if ((int64_t)n_clips * n_keys * J > ((int64_t)1 << 31))
+    if ((int64_t)n_clips * n_keys * J * 3 >= ((int64_t)1 << 31))   // int32 float4 indices
         return fail(HS_ERR_INVALID_ARG, "clip set too large");
     hs_clipset* cs = new (std::nothrow) hs_clipset();
     if (!cs) return fail(HS_ERR_OOM, "host allocation failed");
     cudaGetDevice(&cs->device);
     cs->n_clips = n_clips; cs->n_keys = n_keys; cs->n_joints = J; cs->wrap = wrap; cs->fps = fps;
     cs->duration = (float)(n_keys - 1) / fps;   // same fp32 operation as the oracle (R20)
+    // planar float4 layout: per (clip, key) row, plane p in {0,1,2} holds joint j's
+    // float4 p at [row][p][j] — consecutive joints on consecutive lanes read 512
+    // contiguous bytes per warp load
     std::vector<float> packed((size_t)n_clips * n_keys * J * 12, 0.f);
-    for (size_t r = 0; r < (size_t)n_clips * n_keys * J; ++r) {
-        const float* s = keys + r * 10;
-        float* d = packed.data() + r * 12;
-        for (int e = 0; e < 10; ++e) d[e] = s[e];   // t0 t1 t2 qw | qx qy qz sx | sy sz 0 0
-    }
+    for (size_t row = 0; row < (size_t)n_clips * n_keys; ++row)
+        for (int32_t j = 0; j < J; ++j) {
+            const float* s = keys + (row * J + j) * 10;
+            for (int e = 0; e < 10; ++e)   // t0 t1 t2 qw | qx qy qz sx | sy sz 0 0
+                packed[((row * 3 + e / 4) * J + j) * 4 + e % 4] = s[e];
+        }
     cudaError_t e = upload(&cs->d_keys, packed.data(), packed.size());
     if (e != cudaSuccess) { delete cs; return cuda_fail(e, "clip upload"); }
     *out = cs;

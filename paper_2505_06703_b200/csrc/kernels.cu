@@ -9,6 +9,13 @@
 
 #include <cstdint>
 
+#ifndef HS_S1_E
+#define HS_S1_E 1      // Stage-1 elements per thread per pass
+#endif
+#ifndef HS_S1_PIPE
+#define HS_S1_PIPE 0   // issue layer l + 1's key loads before layer l's arithmetic
+#endif
+
 namespace hs {
 namespace {
 
@@ -123,7 +130,7 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
 // Keyframe sampling, layer blending and TRS -> 3x4 (
 // DESIGN.md readings R19-R23), fused ahead of the scan: the local pose is computed
 // in shared memory instead of being read from HBM.  Keys on the device are packed
-// per (clip, key, joint) as three float4: {tx,ty,tz,qw} {qx,qy,qz,sx} {sy,sz,-,-}.
+// per (clip, key) row as three planar float4 arrays over joints: {tx,ty,tz,qw} {qx,qy,qz,sx} {sy,sz,-,-}.
 // The time -> key decision uses the oracle's exact fp32 operation sequence.
 __device__ __forceinline__ void key_index(float t, int n_keys, float fps, float duration, int wrap,
                                           int& k0, float& a) {
@@ -146,19 +153,41 @@ __device__ __forceinline__ void key_index(float t, int n_keys, float fps, float 
     a = frac;
 }
 
-// Sample joint j of clip `clip`: trs = t(3), q(w,x,y,z)(4), s(3).
-__device__ __forceinline__ void sample_trs(const float4* __restrict__ keys, int n_keys, int J, int clip,
-                                           int j, int k0, float a, float* trs) {
-    const float4* p0 = keys + ((int64_t)(clip * n_keys + k0) * J + j) * 3;
-    const float4 x0 = __ldg(p0), y0 = __ldg(p0 + 1), z0 = __ldg(p0 + 2);
-    if (a == 0.0f) {
+// MUFU approximations (rel. error ~2^-22): a unit quaternion's norm and the weight
+// sum are far from denormal, so the IEEE fix-up paths of rsqrtf / '/' buy nothing.
+__device__ __forceinline__ float rsqrt_fast(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Layer descriptor of one (character, layer) of a tile, written by the producer
+// warp ahead of the consumers (smem ring, one slot per stage):
+//   x = float4 index of key k0 of the layer's clip at joint 0,
+//   y = float4 offset from key k0 to key k0 + 1 (0 when frac == 0: one key),
+//   z = frac (fp32 bits), w = weight (fp32 bits).
+__device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
+    int k0;
+    float fr;
+    key_index(__int_as_float(L.y), a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
+    const int row = (L.x * a.n_keys + k0) * a.J * 3;
+    return make_int4(row, fr != 0.0f ? a.J * 3 : 0, __float_as_int(fr), L.z);
+}
+
+// Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
+__device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float4 z0, float4 x1, float4 y1,
+                                           float4 z1, float a, float* trs) {
+    if (a == 0.0f) {   // on a key: that key exactly (R21)
         trs[0] = x0.x; trs[1] = x0.y; trs[2] = x0.z; trs[3] = x0.w;
         trs[4] = y0.x; trs[5] = y0.y; trs[6] = y0.z;
         trs[7] = y0.w; trs[8] = z0.x; trs[9] = z0.y;
         return;
     }
-    const float4* p1 = p0 + (int64_t)J * 3;
-    const float4 x1 = __ldg(p1), y1 = __ldg(p1 + 1), z1 = __ldg(p1 + 2);
     const float b = 1.0f - a;
     trs[0] = b * x0.x + a * x1.x; trs[1] = b * x0.y + a * x1.y; trs[2] = b * x0.z + a * x1.z;
     trs[7] = b * y0.w + a * y1.w; trs[8] = b * z0.x + a * z1.x; trs[9] = b * z0.y + a * z1.y;
@@ -166,7 +195,7 @@ __device__ __forceinline__ void sample_trs(const float4* __restrict__ keys, int 
     const float as = d < 0.0f ? -a : a;
     float qw = b * x0.w + as * x1.w, qx = b * y0.x + as * y1.x, qy = b * y0.y + as * y1.y,
           qz = b * y0.z + as * y1.z;
-    const float inv = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
+    const float inv = rsqrt_fast(qw * qw + qx * qx + qy * qy + qz * qz);
     trs[3] = qw * inv; trs[4] = qx * inv; trs[5] = qy * inv; trs[6] = qz * inv;
 }
 
@@ -181,48 +210,134 @@ __device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
     m[10] = (1.0f - 2.0f * (x * x + y * y)) * sz; m[11] = trs[2];
 }
 
-// Local pose of joint j for one character's layers (n_layers <= 8): blend of samples.
-__device__ __forceinline__ void stage1_local(const ChunkedArgs& a, const int4* __restrict__ lay, int j,
-                                             float* m) {
-    float acc[10], first[10];
-    float wsum = 0.0f;
-    const int nl = a.n_layers;
-    for (int l = 0; l < nl; ++l) {
-        const int4 L = __ldg(lay + l);
-        const float t = __int_as_float(L.y), w = __int_as_float(L.z);
-        int k0;
-        float fr;
-        key_index(t, a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
-        float s[10];
-        sample_trs(reinterpret_cast<const float4*>(a.keys), a.n_keys, a.J, L.x, j, k0, fr, s);
-        if (l == 0) {
+// Local poses of E tile elements at once (E independent (character, joint) pairs,
+// so each layer's 6 * E key loads are in flight together; PIPE also issues layer
+// l + 1's loads before layer l's arithmetic): sample every layer, blend (DESIGN.md
+// R22), TRS -> 3x4, store into the tile in smem.
+struct KeyPair {
+    float4 x0, y0, z0, x1, y1, z1;
+};
+
+// Keys are planar (float4 plane p of joint j at row * 3J + p * J + j): a warp's
+// loads of one plane over consecutive joints are contiguous.
+__device__ __forceinline__ KeyPair load_keys(const float4* __restrict__ keys, int4 d, int j, int J) {
+    const float4* p0 = keys + d.x + j;
+    const float4* p1 = p0 + d.y;
+    KeyPair k;
+    k.x0 = __ldg(p0); k.y0 = __ldg(p0 + J); k.z0 = __ldg(p0 + 2 * J);
+    k.x1 = __ldg(p1); k.y1 = __ldg(p1 + J); k.z1 = __ldg(p1 + 2 * J);
+    return k;
+}
+
+template <int E, bool PIPE>
+__device__ __forceinline__ void stage1_elems(const float4* __restrict__ keys, const int4* const* dsc,
+                                             const int* j, const bool* valid, int nl, int J, float* L,
+                                             const int* off) {
+    float acc[E][10], q0[E][4], wsum[E];
+    KeyPair kp[E];
+    int4 d[E];
+    if (PIPE) {
 #pragma unroll
-            for (int e = 0; e < 10; ++e) { first[e] = s[e]; acc[e] = w * s[e]; }
-        } else {
-            const float d = s[3] * first[3] + s[4] * first[4] + s[5] * first[5] + s[6] * first[6];
-            const float ws = d < 0.0f ? -w : w;
-#pragma unroll
-            for (int e = 0; e < 3; ++e) acc[e] += w * s[e];
-#pragma unroll
-            for (int e = 3; e < 7; ++e) acc[e] += ws * s[e];
-#pragma unroll
-            for (int e = 7; e < 10; ++e) acc[e] += w * s[e];
+        for (int e = 0; e < E; ++e) {
+            d[e] = valid[e] ? dsc[e][0] : make_int4(0, 0, 0, 0);
+            kp[e] = load_keys(keys, d[e], j[e], J);
         }
-        wsum += w;
     }
-    if (nl == 1) {
-        trs_to_m34(first, m);   // one layer: the sample itself (R22)
-        return;
+    for (int l = 0; l < nl; ++l) {
+        KeyPair cur[E];
+        int4 dc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (PIPE) {
+                cur[e] = kp[e];
+                dc[e] = d[e];
+                if (l + 1 < nl) {
+                    d[e] = valid[e] ? dsc[e][l + 1] : make_int4(0, 0, 0, 0);
+                    kp[e] = load_keys(keys, d[e], j[e], J);
+                }
+            } else {
+                dc[e] = valid[e] ? dsc[e][l] : make_int4(0, 0, 0, 0);
+                cur[e] = load_keys(keys, dc[e], j[e], J);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            float s[10];
+            sample_trs(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
+                       __int_as_float(dc[e].z), s);
+            const float w = __int_as_float(dc[e].w);
+            if (nl == 1) {   // one layer: the sample itself (R22)
+#pragma unroll
+                for (int c = 0; c < 10; ++c) acc[e][c] = s[c];
+            } else if (l == 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q0[e][c] = s[3 + c];
+#pragma unroll
+                for (int c = 0; c < 10; ++c) acc[e][c] = w * s[c];
+                wsum[e] = w;
+            } else {
+                const float dq = s[3] * q0[e][0] + s[4] * q0[e][1] + s[5] * q0[e][2] + s[6] * q0[e][3];
+                const float ws = dq < 0.0f ? -w : w;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[e][c] += w * s[c];
+#pragma unroll
+                for (int c = 3; c < 7; ++c) acc[e][c] += ws * s[c];
+#pragma unroll
+                for (int c = 7; c < 10; ++c) acc[e][c] += w * s[c];
+                wsum[e] += w;
+            }
+        }
     }
-    const float iw = 1.0f / wsum;
 #pragma unroll
-    for (int e = 0; e < 3; ++e) acc[e] *= iw;
+    for (int e = 0; e < E; ++e) {
+        if (!valid[e]) continue;
+        if (nl > 1) {
+            const float iw = rcp_fast(wsum[e]);
 #pragma unroll
-    for (int e = 7; e < 10; ++e) acc[e] *= iw;
-    const float inv = rsqrtf(acc[3] * acc[3] + acc[4] * acc[4] + acc[5] * acc[5] + acc[6] * acc[6]);
+            for (int c = 0; c < 3; ++c) acc[e][c] *= iw;
 #pragma unroll
-    for (int e = 3; e < 7; ++e) acc[e] *= inv;
-    trs_to_m34(acc, m);
+            for (int c = 7; c < 10; ++c) acc[e][c] *= iw;
+            const float inv = rsqrt_fast(acc[e][3] * acc[e][3] + acc[e][4] * acc[e][4] +
+                                     acc[e][5] * acc[e][5] + acc[e][6] * acc[e][6]);
+#pragma unroll
+            for (int c = 3; c < 7; ++c) acc[e][c] *= inv;
+        }
+        float m[12];
+        trs_to_m34(acc[e], m);
+        st3(L + off[e] * 12, m);
+    }
+}
+
+// Phase 0 over one tile: element o = (character o / J, joint o % J) of the tile,
+// consecutive elements on consecutive threads (coalesced key reads), E per thread
+// per pass.
+template <int E, bool PIPE>
+__device__ __forceinline__ void stage1_tile(const float4* __restrict__ keys, const int4* dsc_t, int nel,
+                                            int J, int nl, int t, int NC, float* L) {
+    // element o = cl * J + j, advanced by E * NC per pass without a division
+    const int step = E * NC, step_c = step / J, step_j = step - step_c * J;
+    int cl0 = t / J, j0 = t - (t / J) * J;
+    for (int o = t; o < nel; o += step) {
+        int off[E], j[E];
+        bool valid[E];
+        const int4* dsc[E];
+        int cl = cl0, jj = j0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            off[q] = o + q * NC;
+            valid[q] = off[q] < nel;
+            j[q] = valid[q] ? jj : 0;
+            dsc[q] = dsc_t + (valid[q] ? cl : 0) * nl;
+            if (q + 1 < E) {
+                jj += NC;
+                while (jj >= J) { jj -= J; ++cl; }
+            }
+        }
+        stage1_elems<E, PIPE>(keys, dsc, j, valid, nl, J, L, off);
+        cl0 += step_c;
+        j0 += step_j;
+        if (j0 >= J) { j0 -= J; ++cl0; }
+    }
 }
 
 // ================================================================== chunked kernel
@@ -249,6 +364,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     float* P = SB + NSS * tile_f;
     int32_t* s_round_off = reinterpret_cast<int32_t*>(P + (a.p_single ? 1 : 2) * a.nslots * 12);
     uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + a.R2 + 1);
+    int4* desc = reinterpret_cast<int4*>(smem + a.desc_off);   // Stage 1: [NS][C * n_layers]
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
@@ -267,7 +383,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
 
     if (warp == nwc) {
         // ------------------------------------------------------------ producer
-        if ((threadIdx.x & 31) != 0) return;
+        // (Stage 1: the whole warp writes the next tiles' layer descriptors)
+        const int lane = threadIdx.x & 31;
+        if (!PRO && lane != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
         // stage / S-buffer indices and mbarrier parities advance incrementally: no
         // 64-bit division in the loop
@@ -282,12 +400,32 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             for (uint32_t o = 0; o < bytes; o += piece)
                 bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
         };
+        // Stage 1: descriptors of tile `it`'s (character, layer) pairs into desc[stage],
+        // then full[stage] tells the consumers the stage is theirs
+        auto fill_desc = [&](int64_t it, int stage) {
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+            const int nl = a.n_layers;
+            const int n = (int)min((int64_t)a.C, a.n_chars - c0) * nl;
+            const int4* lay = reinterpret_cast<const int4*>(a.layers) + c0 * nl;
+            int4* d = desc + stage * a.C * nl;
+            for (int i = lane; i < n; i += 32) d[i] = layer_desc(a, __ldg(lay + i));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+        };
         if (!PRO)
             for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load(it, (int)it);
+        else
+            for (int64_t it = 0; it < my_tiles && it < NS; ++it) fill_desc(it, (int)it);
         int stage = 0, sb = 0;
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
             mbar_wait(&done[stage], phase);
+            if (PRO && lane != 0) {   // lanes 1..31: only the descriptor fill
+                __syncwarp();
+                if (it + NS < my_tiles) fill_desc(it + NS, stage);
+                if (++stage == NS) { stage = 0; phase ^= 1u; }
+                continue;
+            }
             const int64_t tile = blockIdx.x + it * gridDim.x;
             const int64_t c0 = tile * a.C;
             const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
@@ -306,12 +444,16 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             bulk_commit();
             bulk_wait_read<0>();                  // smem of this tile has been read out
             if (do_skin) mbar_arrive(&sfree[sb]);
-            if (PRO) mbar_arrive(&full[stage]);   // Stage 1 computes tiles in place: stage free
-            else if (it + NS < my_tiles) issue_load(it + NS, stage);
+            if (PRO) {   // Stage 1 computes tiles in place: the stage is free once read out
+                __syncwarp();
+                if (it + NS < my_tiles) fill_desc(it + NS, stage);
+            } else if (it + NS < my_tiles) {
+                issue_load(it + NS, stage);
+            }
             if (++stage == NS) { stage = 0; phase ^= 1u; }
             if (++sb == NSS) sb = 0;
         }
-        bulk_wait_all();
+        if (lane == 0) bulk_wait_all();
         return;
     }
 
@@ -361,28 +503,21 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
     for (int64_t it = 0; it < my_tiles; ++it) {
         float* L = LG + stage * tile_f;
         prof_mark(-1);
-        if (!PRO) {
-            mbar_wait(&full[stage], phase);
-        } else {
-            // phase 0 (Stage 1): this thread's joints' local poses, computed in place in
-            // the stage buffer once the producer has stored that stage's last tile
-            if (it >= NS) mbar_wait(&full[stage], phase ^ 1u);
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;
-                const int off = (int)(m[s] & 0xffff);
-                const int u = (int)((m[s] >> 16) & 0xffff);
-                const int64_t ch = c0 + off / a.J;
-                if (ch >= a.n_chars) continue;
-                const int4* lay = reinterpret_cast<const int4*>(a.layers) + ch * a.n_layers;
-                float lm[12];
-                stage1_local(a, lay, u, lm);
-                st3(L + off * 12, lm);
-            }
-        }
+        mbar_wait(&full[stage], phase);
         prof_mark(0);
+        if (PRO) {
+            // phase 0 (Stage 1): the tile's local poses, computed into the stage buffer
+            // by all consumer threads, consecutive elements on consecutive lanes
+            // (coalesced key reads)
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+            const int nel = (int)min((int64_t)a.C, a.n_chars - c0) * a.J;
+            const int nl = a.n_layers;
+            const int4* dsc_t = desc + stage * a.C * nl;
+            const float4* keys4 = reinterpret_cast<const float4*>(a.keys);
+            stage1_tile<HS_S1_E, HS_S1_PIPE != 0>(keys4, dsc_t, nel, a.J, nl, t, NC, L);
+            bar_consumers(NC);
+            prof_mark(8);   // phase 0 (Stage 1)
+        }
 
         // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
         float acc[12];

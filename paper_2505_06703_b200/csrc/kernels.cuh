@@ -31,6 +31,8 @@ struct ChunkedArgs {
     const void* layers;        // device [n_chars][n_layers] hs_layer (16 B)
     const float* keys;         // device [n_clips][n_keys][J][12] packed keys
     int32_t n_layers, n_keys, wrap;
+    int32_t desc_off;
+    int32_t s1_variant;        // Stage-1 phase-0 schedule (tuning aid)          // smem byte offset of the layer-descriptor ring ([stages][C * n_layers] int4)
     float fps, duration;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
