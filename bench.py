@@ -69,6 +69,9 @@ def parse_args(argv=None):
     ap.add_argument("--stage1", action="store_true",
                     help="fused Stage-1 prologue (hs_animate): 2 animation layers per character "
                          "sampled from 8 clips x 31 keys instead of resident local poses")
+    ap.add_argument("--launch", choices=["auto", "batch", "per-type"], default="auto",
+                    help="batch = all skeleton types in one hs_scan_batch launch (NEXT-3); "
+                         "auto = batch for small crowds only (see bench.py)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no checks, no e2e, no cpu baseline")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
@@ -120,12 +123,13 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(workload: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def ncu_traffic(workload: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary
+    (only when it was captured on this workload and launch)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        if d.get("workload") == workload:
+        if d.get("workload") == workload and d.get("kernel") == kernel:
             return float(d["dram_bytes_per_launch"]), d.get("source")
     except Exception:
         pass
@@ -285,17 +289,35 @@ def run_ours(args):
     torch.cuda.synchronize()
     joints_rank = sum(w["n"] * w["J"] for w in work)
 
+    # auto: one batch launch only when every type's crowd is small (under ~32 tiles per
+    # SM, where per-launch fill/drain and tails dominate; profiles/r01_next3_sweep.json);
+    # C5's crowds are thousands of tiles per SM, where per-type launches measured 3%
+    # faster (the multi-segment kernel's program switch costs registers)
+    small = all(-(-w["n"] // max(1, w["sk"].query("tile_chars"))) < 32 * 148 for w in work)
+    batch = args.launch == "batch" or (
+        args.launch == "auto" and small and not args.stage1 and args.algo == "auto"
+        and args.tile_ctas == 0 and len({w["sk"].query("chunk") for w in work}) == 1
+        and all(w["sk"].query("path") == 1 for w in work))
+    # launches per step: one hs_scan_batch over every type, or one call per type
+    launches = [("batch", list(range(len(work))))] if batch else [(w["name"], [t]) for t, w in
+                                                                   enumerate(work)]
+    batch_items = [(w["sk"], w["local"], w["g"], w["s"]) for w in work if w["n"]] if batch else None
+
     def step(events=None, k=0):
-        for t, w in enumerate(work):
+        for li, (_, members) in enumerate(launches):
             if events is not None:
-                events[t][0][k].record(stream)
-            if args.stage1:
-                hs.animate(w["sk"], w["cs"], w["layers"], w["g"], w["s"], stream=stream)
+                events[li][0][k].record(stream)
+            if batch:
+                hs.scan_batch(batch_items, stream=stream)
             else:
-                w["sk"].scan_into(w["local"], w["g"], w["s"], stream=stream, algo=args.algo,
-                                  tile_ctas=args.tile_ctas)
+                w = work[members[0]]
+                if args.stage1:
+                    hs.animate(w["sk"], w["cs"], w["layers"], w["g"], w["s"], stream=stream)
+                else:
+                    w["sk"].scan_into(w["local"], w["g"], w["s"], stream=stream, algo=args.algo,
+                                      tile_ctas=args.tile_ctas)
             if events is not None:
-                events[t][1][k].record(stream)
+                events[li][1][k].record(stream)
 
     # ---- correctness on sampled characters at full size (outside the timed region)
     step()
@@ -314,7 +336,7 @@ def run_ours(args):
         step()
     K = args.steps
     events = [[[torch.cuda.Event(enable_timing=True) for _ in range(K)] for _ in range(2)]
-              for _ in work]
+              for _ in launches]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(torch.cuda.current_device())
     if world > 1:
@@ -329,23 +351,32 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms_rank = start.elapsed_time(stop)
-    per_type_ms = [statistics.mean(events[t][0][k].elapsed_time(events[t][1][k]) for k in range(K))
-                   for t in range(len(work))]
+    per_launch_ms = [statistics.mean(events[li][0][k].elapsed_time(events[li][1][k]) for k in range(K))
+                     for li in range(len(launches))]
     ms, joints_total = reduce_over_ranks(ms_rank, joints_rank, world, dev)
     value = joints_total * K / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (largest byte share: tree1024's launch)
-    dom = max(range(len(work)), key=lambda t: work[t]["n"] * work[t]["J"])
+    # ---- roofline of the dominant kernel launch (largest byte share: the batch launch,
+    # else tree1024's)
     bpj = STAGE1_BYTES_PER_JOINT if args.stage1 else BYTES_PER_JOINT
     per_char_extra = 16 * STAGE1_LAYERS if args.stage1 else 0
-    dom_bytes = bpj * work[dom]["n"] * work[dom]["J"] + per_char_extra * work[dom]["n"]
-    achieved = dom_bytes / (per_type_ms[dom] / 1e3) / 1e9
+
+    def launch_bytes(li):
+        return sum(bpj * work[t]["n"] * work[t]["J"] + per_char_extra * work[t]["n"]
+                   for t in launches[li][1])
+
+    dom_l = max(range(len(launches)), key=launch_bytes)
+    dom = max(launches[dom_l][1], key=lambda t: work[t]["n"] * work[t]["J"])
+    dom_bytes = launch_bytes(dom_l)
+    achieved = dom_bytes / (per_launch_ms[dom_l] / 1e3) / 1e9
     peak, peak_src = measured_peaks()
     workload = WORKLOAD_NAME[args.config]
     if args.stage1:
         workload += (f" + fused Stage 1 ({STAGE1_LAYERS} layers per character, "
                      f"{STAGE1_CLIPS} clips x {STAGE1_KEYS} keys at {STAGE1_FPS:g} fps)")
-    traffic, traffic_src = ncu_traffic(workload)
+    kernel_name = (f"chunked_kernel{'<stage1>' if args.stage1 else ''} "
+                   f"({launches[dom_l][0]} launch)")
+    traffic, traffic_src = ncu_traffic(workload, kernel_name)
 
     e2e = None
     cpu = None
@@ -366,7 +397,8 @@ def run_ours(args):
                    "hbm_gbs": joints_total * bpj * K / (ms / 1e3) / 1e9 / world,
                    "hbm_gbs_note": "per GPU, algorithmic bytes / step time",
                    "l2": "inputs larger than L2 (no flush)", "algo": args.algo,
-                   "per_launch_ms": {w["name"]: per_type_ms[t] for t, w in enumerate(work)},
+                   "launch": "batch (one hs_scan_batch per step)" if batch else "one launch per type",
+                   "per_launch_ms": {name: per_launch_ms[li] for li, (name, _) in enumerate(launches)},
                    "chunk": work[dom]["sk"].query("chunk"),
                    "tile_chars": work[dom]["sk"].query("tile_chars"),
                    "stages": {w["name"]: w["sk"].query("stages") for w in work},
@@ -375,12 +407,11 @@ def run_ours(args):
                    "chunking": work[dom]["sk"].query("chunking")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"chunked_kernel{'<stage1>' if args.stage1 else ''} "
-                               f"({work[dom]['name']} launch)",
+                     "kernel": kernel_name,
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
                      "traffic_source": traffic_src},
         "clocks": sampler.summary(),
-        "gpu_launches": len(work) * K,
+        "gpu_launches": len(launches) * K,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": check,

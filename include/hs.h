@@ -133,6 +133,32 @@ hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars,
                      float* skin_out, void* cuda_stream, const hs_scan_opts* opts);
 
 /* ---------------------------------------------------------------------------
+ * Heterogeneous single launch ("varied
+ * hierarchies"): several crowds, each with its own skeleton, scanned by ONE kernel
+ * launch.  Their tiles form one global tile space over the persistent CTAs, which
+ * switch programs at segment boundaries, so the per-launch pipeline fill/drain and
+ * tails of separate hs_scan calls disappear.  Results are bitwise identical to
+ * calling hs_scan on each item in order (characters are chunked per character and
+ * the per-skeleton tile size is kept).
+ *   items     host array of n_items descriptors (read during the call only); each
+ *             item's buffers follow hs_scan's rules (device, 16-byte aligned, no
+ *             aliasing); distinct items must not overlap in memory.
+ *   n_items   0..HS_MAX_BATCH; items with n_chars == 0 are skipped.
+ * Every skeleton must be on the single-CTA path (HS_Q_PATH == HS_ALGO_CHUNKED), use
+ * the same chunk size (HS_Q_CHUNK) and live on the current device; otherwise
+ * HS_ERR_UNSUPPORTED / HS_ERR_WRONG_DEVICE and nothing is launched.
+ * ------------------------------------------------------------------------- */
+#define HS_MAX_BATCH 8
+typedef struct {
+    const hs_skeleton* skeleton;
+    const float* local;     /* device [n_chars][n_joints][3][4]                          */
+    int64_t n_chars;
+    float* global_out;      /* device, same shape                                        */
+    float* skin_out;        /* device, same shape, or NULL (no bind epilogue)             */
+} hs_batch_item;
+hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * Stage 1 fused ahead of the scan ("Sample
  * animation data and generate local pose in local space").
  * Per character and joint: sample each animation layer's clip at its time (keys

@@ -106,6 +106,7 @@ def lib():
     L.hs_clipset_create.argtypes = [vp, vp, i32, i32, ctypes.c_float, i32, ctypes.POINTER(vp)]
     L.hs_clipset_destroy.argtypes = [vp]
     L.hs_animate.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
+    L.hs_scan_batch.argtypes = [ctypes.POINTER(_BatchItem), i32, vp]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
@@ -251,6 +252,33 @@ class Skeleton:
         self._h = None
 
     __del__ = close
+
+
+MAX_BATCH = 8   # HS_MAX_BATCH
+
+
+class _BatchItem(ctypes.Structure):
+    _fields_ = [("skeleton", ctypes.c_void_p), ("local", ctypes.c_void_p), ("n_chars", ctypes.c_int64),
+                ("global_out", ctypes.c_void_p), ("skin_out", ctypes.c_void_p)]
+
+
+def scan_batch(items, stream=None):
+    """hs_scan_batch: one launch over several crowds (NEXT-3).  items: sequence of
+    (Skeleton, local, global_out, skin_out-or-None) CUDA tensors (or device pointers
+    as ints, then a fifth element n_chars)."""
+    import torch
+
+    def ptr(t):
+        return None if t is None else (t if isinstance(t, int) else t.data_ptr())
+
+    arr = (_BatchItem * max(1, len(items)))()
+    for i, it in enumerate(items):
+        sk, loc, g, s = it[:4]
+        n = it[4] if len(it) > 4 else loc.shape[0]
+        arr[i] = _BatchItem(sk.handle, ptr(loc), n, ptr(g), ptr(s))
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_scan_batch(arr, len(items), st), "hs_scan_batch")
 
 
 LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])

@@ -252,6 +252,87 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+static_assert(HS_MAX_BATCH <= hs::kMaxSegs, "one kernel segment per batch item");
+
+struct ChunkItem {
+    const hs_skeleton* sk;
+    const float* local;
+    int64_t n_chars;
+    float* gout;
+    float* sout;
+};
+
+// Segments + shared-memory layout of one chunked launch: stage and
+// S buffers sized for the largest tile, P for the largest anchor set, tables for the
+// largest program.  For one segment this is tile_smem_bytes() exactly.
+void chunked_layout(const ChunkItem* items, int n, int stages, int sbufs, hs::ChunkedArgs& a) {
+    int64_t tiles = 0;
+    int max_f = 0, p_floats = 0, r2_max = 0, rounds_max = 0, max_t = 0;
+    bool runs = false;
+    a.nseg = n;
+    for (int i = 0; i < n; ++i) {
+        const hs_skeleton* sk = items[i].sk;
+        const hs::TileProgram& tp = sk->tp;
+        hs::SegArgs& s = a.seg[i];
+        s.local = items[i].local; s.gout = items[i].gout; s.sout = items[i].sout; s.ib = sk->d_ib;
+        s.meta = sk->d_meta; s.p1len = sk->d_p1len; s.round_off = sk->d_round_off; s.rounds = sk->d_rounds;
+        s.n_chars = items[i].n_chars;
+        s.tile_base = tiles;
+        s.J = sk->plan.n; s.C = tp.C; s.F = tp.F; s.T = tp.T;
+        s.nslots = tp.nslots; s.R2 = tp.R2;
+        s.n_rounds_entries = (int32_t)tp.rounds.size();
+        s.p_single = tp.pingpong ? 0 : 1;
+        tiles += (items[i].n_chars + tp.C - 1) / tp.C;
+        max_f = std::max(max_f, tp.F);
+        p_floats = std::max(p_floats, (tp.pingpong ? 2 : 1) * tp.nslots * 12);
+        r2_max = std::max(r2_max, tp.R2);
+        rounds_max = std::max(rounds_max, (int)tp.rounds.size());
+        max_t = std::max(max_t, tp.T);
+        runs = runs || tp.has_runs;
+    }
+    a.total_tiles = tiles;
+    a.tile_f = max_f * 12;
+    a.p_floats = p_floats;
+    a.r2_max = r2_max;
+    a.stages = stages;
+    a.sbufs = sbufs;
+    const int64_t tables = ((int64_t)(r2_max + 1) * 4 + (int64_t)rounds_max * 4 + 15) / 16 * 16;
+    a.smem_bytes = 128 + (int64_t)(stages + sbufs) * max_f * 48 + (int64_t)p_floats * 4 + tables;
+    a.threads = ((max_t + 31) / 32) * 32 + 32;
+    a.has_runs = runs ? 1 : 0;
+    a.bulk_piece = 8192;   // 8 KB TMA bulk copies (measured +2% over one copy per tile)
+    if (const char* bp = std::getenv("HS_BULK_PIECE")) a.bulk_piece = std::atoi(bp) & ~15;  // tuning aid
+}
+
+// Launch one chunked program (with the HS_DEBUG_PROF phase profile when set).
+hs_status run_chunked(hs::ChunkedArgs& a, int K, cudaStream_t st) {
+    a.prof = nullptr;
+    if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
+        cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
+        cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
+    }
+    cudaError_t e = hs::launch_chunked(K, a, st);
+    if (e != cudaSuccess) {
+        char buf[256];
+        std::snprintf(buf, sizeof(buf), "chunked launch (K=%d threads=%d smem=%lld stages=%d sbufs=%d)",
+                      K, a.threads, (long long)a.smem_bytes, a.stages, a.sbufs);
+        return cuda_fail(e, buf);
+    }
+    if (a.prof) {
+        unsigned long long h[10];
+        cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const double n = h[5] ? (double)h[5] : 1.0;
+        std::fprintf(stderr,
+                     "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f stage1 %.0f phase1 %.0f phase2 %.0f "
+                     "wait_sbuf %.0f phase3 %.0f (thread 0: fold %.0f scan+lift %.0f)\n",
+                     a.seg[0].J, h[5], h[0] / n, h[8] / n, (h[1] + h[6] + h[7]) / n, h[2] / n, h[3] / n, h[4] / n,
+                     h[6] / n, h[7] / n);
+        cudaFree(a.prof);
+    }
+    return HS_OK;
+}
+
 hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, float* gout,
                     float* sout, cudaStream_t st, int algo, int max_rounds, int tile_ctas,
                     const hs_clipset* cs = nullptr, const void* layers = nullptr, int n_layers = 0) {
@@ -261,19 +342,10 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
     switch (algo) {
         case HS_ALGO_CHUNKED: {
             if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "skeleton does not fit the single-CTA path");
-            hs::ChunkedArgs a;
-            a.local = local; a.gout = gout; a.sout = sout; a.ib = sk->d_ib; a.n_chars = n_chars;
-            a.J = J; a.C = sk->tp.C; a.F = sk->tp.F; a.T = sk->tp.T;
-            a.nslots = sk->tp.nslots; a.R2 = sk->tp.R2;
-            a.meta = sk->d_meta; a.p1len = sk->d_p1len; a.round_off = sk->d_round_off;
-            a.rounds = sk->d_rounds; a.stages = sk->stages; a.sbufs = sk->sbufs;
-            a.n_rounds_entries = (int32_t)sk->tp.rounds.size();
-            a.has_runs = sk->tp.has_runs ? 1 : 0;
-            a.bulk_piece = 8192;   // 8 KB TMA bulk copies (measured +2% over one copy per tile)
-            if (const char* bp = std::getenv("HS_BULK_PIECE")) a.bulk_piece = std::atoi(bp) & ~15;  // tuning aid
-            a.smem_bytes = sk->smem; a.threads = sk->threads;
+            hs::ChunkedArgs a{};
+            const ChunkItem item{sk, local, n_chars, gout, sout};
+            chunked_layout(&item, 1, sk->stages, sk->sbufs, a);
             a.ctas_per_sm = tile_ctas;
-            a.p_single = sk->tp.pingpong ? 0 : 1;
             a.layers = layers;
             a.keys = cs ? cs->d_keys : nullptr;
             a.n_layers = n_layers;
@@ -287,7 +359,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 // a third stage is dropped if the ring does not fit beside it
                 for (;;) {
                     const int64_t base = hs::tile_smem_bytes(sk->tp, a.stages, a.sbufs);
-                    const int64_t need = base + (int64_t)a.stages * a.C * n_layers * 16;
+                    const int64_t need = base + (int64_t)a.stages * sk->tp.C * n_layers * 16;
                     if (need <= sk->smem_optin) {
                         a.desc_off = (int32_t)base;
                         a.smem_bytes = need;
@@ -296,32 +368,10 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                     if (a.stages <= 2)
                         return fail(HS_ERR_UNSUPPORTED, "no shared memory left for the Stage-1 descriptors");
                     --a.stages;
+                    chunked_layout(&item, 1, a.stages, a.sbufs, a);
                 }
             }
-            a.prof = nullptr;
-            if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
-                cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
-                cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
-            }
-            e = hs::launch_chunked(sk->K, a, st);
-            if (e != cudaSuccess) {
-                char buf[256];
-                std::snprintf(buf, sizeof(buf), "chunked launch (K=%d threads=%d smem=%lld stages=%d sbufs=%d)",
-                              sk->K, a.threads, (long long)a.smem_bytes, a.stages, a.sbufs);
-                return cuda_fail(e, buf);
-            }
-            if (a.prof) {
-                unsigned long long h[10];
-                cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                const double n = h[5] ? (double)h[5] : 1.0;
-                std::fprintf(stderr,
-                             "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f stage1 %.0f phase1 %.0f phase2 %.0f "
-                             "wait_sbuf %.0f phase3 %.0f (thread 0: fold %.0f scan+lift %.0f)\n",
-                             J, h[5], h[0] / n, h[8] / n, (h[1] + h[6] + h[7]) / n, h[2] / n, h[3] / n, h[4] / n,
-                             h[6] / n, h[7] / n);
-                cudaFree(a.prof);
-            }
+            if (hs_status r = run_chunked(a, sk->K, st); r != HS_OK) return r;
             break;
         }
         case HS_ALGO_DOUBLING:
@@ -426,6 +476,48 @@ hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars,
     if (dev != sk->device) return fail(HS_ERR_WRONG_DEVICE, "handle belongs to another device");
     return scan_impl(sk, local, n_chars, global_out, skin_out, static_cast<cudaStream_t>(cuda_stream),
                      algo, max_rounds, tile_ctas);
+}
+
+hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_stream) {
+    if (n_items < 0 || n_items > HS_MAX_BATCH) return fail(HS_ERR_INVALID_ARG, "n_items must be in 0..HS_MAX_BATCH");
+    if (n_items > 0 && !items) return fail(HS_ERR_INVALID_ARG, "items is null");
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    ChunkItem segs[HS_MAX_BATCH];
+    int n = 0, K = 0, stages = 3, sbufs = 2, optin = 0;
+    for (int32_t i = 0; i < n_items; ++i) {
+        const hs_batch_item& it = items[i];
+        const hs_skeleton* sk = it.skeleton;
+        if (!sk) return fail(HS_ERR_INVALID_ARG, "item skeleton is null");
+        if (it.n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+        if (it.n_chars == 0) continue;
+        if (!it.local || !it.global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+        if (!aligned16(it.local) || !aligned16(it.global_out) || (it.skin_out && !aligned16(it.skin_out)))
+            return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+        if (it.local == it.global_out ||
+            (it.skin_out && (it.local == it.skin_out || it.global_out == it.skin_out)))
+            return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
+        if (it.n_chars > (INT64_MAX / 64) / sk->plan.n) return fail(HS_ERR_INVALID_ARG, "size overflow");
+        if (dev != sk->device) return fail(HS_ERR_WRONG_DEVICE, "handle belongs to another device");
+        if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "batched skeletons must fit the single-CTA path");
+        if (K && sk->K != K) return fail(HS_ERR_UNSUPPORTED, "batched skeletons must share the chunk size K");
+        K = sk->K;
+        stages = std::min(stages, sk->stages);
+        sbufs = std::min(sbufs, sk->sbufs);
+        optin = sk->smem_optin;
+        segs[n++] = ChunkItem{sk, it.local, it.n_chars, it.global_out, it.skin_out};
+    }
+    if (n == 0) return HS_OK;
+    hs::ChunkedArgs a{};
+    for (;;) {   // the common layout of the largest tile / anchor set / program
+        chunked_layout(segs, n, stages, sbufs, a);
+        if (a.smem_bytes <= optin) break;
+        if (sbufs > 1) --sbufs;
+        else if (stages > 2) { --stages; sbufs = 2; }
+        else return fail(HS_ERR_UNSUPPORTED, "batched programs do not fit shared memory together");
+    }
+    return run_chunked(a, K, static_cast<cudaStream_t>(cuda_stream));
 }
 
 hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_clips, int32_t n_keys,

@@ -175,8 +175,9 @@ __device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
     int k0;
     float fr;
     key_index(__int_as_float(L.y), a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
-    const int row = (L.x * a.n_keys + k0) * a.J * 3;
-    return make_int4(row, fr != 0.0f ? a.J * 3 : 0, __float_as_int(fr), L.z);
+    const int J = a.seg[0].J;
+    const int row = (L.x * a.n_keys + k0) * J * 3;
+    return make_int4(row, fr != 0.0f ? J * 3 : 0, __float_as_int(fr), L.z);
 }
 
 // Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
@@ -351,28 +352,58 @@ __device__ __forceinline__ void stage1_tile(const float4* __restrict__ keys, con
 //            segment head's parent, writes G in place over L, and S = G (x) IB
 //            (IB held in registers) into the S buffer;
 // then the producer bulk-stores G and S and refills the stage.
-template <int K, bool RUNS, bool PRO>
-__global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
+// Kernel modes: one segment (hs_scan), one segment with the Stage-1 prologue
+// (hs_animate), or several segments in one launch (hs_scan_batch, NEXT-3).
+enum : int { kModeScan = 0, kModeStage1 = 1, kModeMulti = 2 };
+
+// Producer-side view of the segment a tile belongs to; advanced only when the tile
+// index crosses into the next segment (tiles of a CTA only move forward).
+struct SegCursor {
+    int s;
+    int64_t next_base, base, n_chars;
+    int J, C;
+    const float* local;
+    float* gout;
+    float* sout;
+    __device__ __forceinline__ void load(const ChunkedArgs& a, int i) {
+        const SegArgs& S = a.seg[i];
+        s = i;
+        base = S.tile_base; n_chars = S.n_chars; J = S.J; C = S.C;
+        local = S.local; gout = S.gout; sout = S.sout;
+        next_base = i + 1 < a.nseg ? a.seg[i + 1].tile_base : INT64_MAX;
+    }
+    __device__ __forceinline__ void seek(const ChunkedArgs& a, int64_t g) {
+        if (g >= next_base) {
+            int i = s + 1;
+            while (i + 1 < a.nseg && g >= a.seg[i + 1].tile_base) ++i;
+            load(a, i);
+        }
+    }
+};
+
+template <int K, bool RUNS, int MODE>
+__global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__ ChunkedArgs a) {
+    constexpr bool PRO = MODE == kModeStage1;
+    constexpr bool MULTI = MODE == kModeMulti;
     extern __shared__ __align__(128) unsigned char smem[];
     const int NS = a.stages, NSS = a.sbufs;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* done = full + 4;
     uint64_t* sfree = done + 4;
     float* LG = reinterpret_cast<float*>(smem + 128);
-    const int64_t tile_f = (int64_t)a.F * 12;
+    const int64_t tile_f = a.tile_f;
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
-    int32_t* s_round_off = reinterpret_cast<int32_t*>(P + (a.p_single ? 1 : 2) * a.nslots * 12);
-    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + a.R2 + 1);
+    int32_t* s_round_off = reinterpret_cast<int32_t*>(P + a.p_floats);
+    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + a.r2_max + 1);
     int4* desc = reinterpret_cast<int4*>(smem + a.desc_off);   // Stage 1: [NS][C * n_layers]
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
     const int warp = threadIdx.x >> 5;
-    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
+    const int64_t ntiles = a.total_tiles;
     const int64_t my_tiles =
         blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const bool do_skin = a.sout != nullptr;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
@@ -388,26 +419,31 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
         if (!PRO && lane != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
         // stage / S-buffer indices and mbarrier parities advance incrementally: no
-        // 64-bit division in the loop
+        // 64-bit division in the loop; segment cursors for the loads (run NS tiles
+        // ahead) and for the stores
+        SegCursor ld, st;
+        ld.load(a, 0);
+        st.load(a, 0);
         auto issue_load = [&](int64_t it, int stage) {
-            const int64_t tile = blockIdx.x + it * gridDim.x;
-            const int64_t c0 = tile * a.C;
-            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
-            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+            const int64_t g = blockIdx.x + it * gridDim.x;
+            if (MULTI) ld.seek(a, g);
+            const int64_t c0 = (g - ld.base) * ld.C;
+            const int64_t nc = min((int64_t)ld.C, ld.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * ld.J * 48);
             mbar_expect_tx(&full[stage], bytes);
-            const char* src = reinterpret_cast<const char*>(a.local + c0 * a.J * 12);
+            const char* src = reinterpret_cast<const char*>(ld.local + c0 * ld.J * 12);
             char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
             for (uint32_t o = 0; o < bytes; o += piece)
                 bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
         };
-        // Stage 1: descriptors of tile `it`'s (character, layer) pairs into desc[stage],
-        // then full[stage] tells the consumers the stage is theirs
+        // Stage 1 (one segment): descriptors of tile `it`'s (character, layer) pairs
+        // into desc[stage], then full[stage] tells the consumers the stage is theirs
         auto fill_desc = [&](int64_t it, int stage) {
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
+            const int64_t c0 = (blockIdx.x + it * gridDim.x) * st.C;
             const int nl = a.n_layers;
-            const int n = (int)min((int64_t)a.C, a.n_chars - c0) * nl;
+            const int n = (int)min((int64_t)st.C, st.n_chars - c0) * nl;
             const int4* lay = reinterpret_cast<const int4*>(a.layers) + c0 * nl;
-            int4* d = desc + stage * a.C * nl;
+            int4* d = desc + stage * st.C * nl;
             for (int i = lane; i < n; i += 32) d[i] = layer_desc(a, __ldg(lay + i));
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[stage]);
@@ -426,24 +462,26 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
                 if (++stage == NS) { stage = 0; phase ^= 1u; }
                 continue;
             }
-            const int64_t tile = blockIdx.x + it * gridDim.x;
-            const int64_t c0 = tile * a.C;
-            const int64_t nc = min((int64_t)a.C, a.n_chars - c0);
-            const uint32_t bytes = (uint32_t)(nc * a.J * 48);
+            const int64_t g = blockIdx.x + it * gridDim.x;
+            if (MULTI) st.seek(a, g);
+            const bool do_skin = st.sout != nullptr;
+            const int64_t c0 = (g - st.base) * st.C;
+            const int64_t nc = min((int64_t)st.C, st.n_chars - c0);
+            const uint32_t bytes = (uint32_t)(nc * st.J * 48);
             {
-                char* g = reinterpret_cast<char*>(a.gout + c0 * a.J * 12);
+                char* gp = reinterpret_cast<char*>(st.gout + c0 * st.J * 12);
                 const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
-                char* s = do_skin ? reinterpret_cast<char*>(a.sout + c0 * a.J * 12) : nullptr;
+                char* sp = do_skin ? reinterpret_cast<char*>(st.sout + c0 * st.J * 12) : nullptr;
                 const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
                 for (uint32_t o = 0; o < bytes; o += piece) {
                     const uint32_t nb = min(piece, bytes - o);
-                    bulk_s2g(g + o, sg + o, nb);
-                    if (do_skin) bulk_s2g(s + o, ss + o, nb);
+                    bulk_s2g(gp + o, sg + o, nb);
+                    if (do_skin) bulk_s2g(sp + o, ss + o, nb);
                 }
             }
             bulk_commit();
             bulk_wait_read<0>();                  // smem of this tile has been read out
-            if (do_skin) mbar_arrive(&sfree[sb]);
+            mbar_arrive(&sfree[sb]);              // (also when this segment has no skin output)
             if (PRO) {   // Stage 1 computes tiles in place: the stage is free once read out
                 __syncwarp();
                 if (it + NS < my_tiles) fill_desc(it + NS, stage);
@@ -459,35 +497,55 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
 
     // ---------------------------------------------------------------- consumers
     const int t = threadIdx.x;
-    const bool active = t < a.T;
     uint64_t m[K];
     float ibr[K][12];
     int p1 = 0, run_back = 0, run_anchor = -1;
-    if (active) {
-        const int info = a.p1len[t];
-        p1 = info & 0xff;
-        run_back = (info >> 8) & 0xff;
-        run_anchor = (int)((uint32_t)info >> 16) - 1;
+    // the current segment's program (MULTI: reloaded when a tile crosses into the next
+    // segment; otherwise loaded once)
+    int cseg = 0;
+    int64_t next_base = INT64_MAX;
+    int J = 0, C = 0, S2 = 0, R2 = 0, p_single = 0;
+    int64_t nch = 0, tbase = 0;
+    bool do_skin = false;
+    auto load_program = [&](int s) {
+        const SegArgs& S = a.seg[s];
+        J = S.J; C = S.C; S2 = S.nslots; R2 = S.R2; p_single = S.p_single;
+        nch = S.n_chars; tbase = S.tile_base; do_skin = S.sout != nullptr;
+        next_base = s + 1 < a.nseg ? a.seg[s + 1].tile_base : INT64_MAX;
+        p1 = 0; run_back = 0; run_anchor = -1;
+        if (t < S.T) {
+            const int info = S.p1len[t];
+            p1 = info & 0xff;
+            run_back = (info >> 8) & 0xff;
+            run_anchor = (int)((uint32_t)info >> 16) - 1;
 #pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = a.meta[(int64_t)t * K + s];
-    } else {
+            for (int s2 = 0; s2 < K; ++s2) m[s2] = S.meta[(int64_t)t * K + s2];
+        } else {
 #pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
-    }
-    if (do_skin) {
-#pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const int src = (int)(int16_t)(m[s] >> 32);
-            const int ibu = (int)((m[s] >> 16) & 0xffff);
-            if (src != kSrcNone) ldg3(a.ib + (int64_t)ibu * 12, ibr[s]);
+            for (int s2 = 0; s2 < K; ++s2) m[s2] = (uint64_t)(uint16_t)(int16_t)kSrcNone << 32;
         }
+        if (do_skin) {
+#pragma unroll
+            for (int s2 = 0; s2 < K; ++s2) {
+                const int src = (int)(int16_t)(m[s2] >> 32);
+                const int ibu = (int)((m[s2] >> 16) & 0xffff);
+                if (src != kSrcNone) ldg3(S.ib + (int64_t)ibu * 12, ibr[s2]);
+            }
+        }
+        // phase-2 tables: identical for every tile of the segment, staged per CTA (the
+        // previous tile ended with a consumer barrier, so nobody still reads them)
+        for (int i = t; i <= S.R2; i += NC) s_round_off[i] = __ldg(S.round_off + i);
+        for (int i = t; i < S.n_rounds_entries; i += NC) s_rounds[i] = __ldg(S.rounds + i);
+        bar_consumers(NC);
+    };
+    if (my_tiles > 0) {
+        if (MULTI) {
+            int s0 = 0;
+            while (s0 + 1 < a.nseg && (int64_t)blockIdx.x >= a.seg[s0 + 1].tile_base) ++s0;
+            cseg = s0;
+        }
+        load_program(cseg);
     }
-    // longest run prefix in this warp: the scan needs ceil(log2(max + 1)) steps
-    const int warp_maxrb = RUNS ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
-    // phase-2 tables: identical for every tile, staged once per CTA
-    for (int i = t; i <= a.R2; i += NC) s_round_off[i] = __ldg(a.round_off + i);
-    for (int i = t; i < a.n_rounds_entries; i += NC) s_rounds[i] = __ldg(a.rounds + i);
-    bar_consumers(NC);
 
     // debug phase profile (HS_DEBUG_PROF): consumer thread 0 accumulates clock64 deltas
     long long prof_last = 0;
@@ -498,189 +556,217 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const ChunkedArgs a) {
             prof_last = now;
         }
     };
+    // per-segment values in the tile loop, read from the kernel parameters with the
+    // (CTA-uniform) segment index, so loop bounds and branches stay uniform
+#define SEGV(field, var) (a.seg[MULTI ? cseg : 0].field)
+#define SKIN (a.seg[MULTI ? cseg : 0].sout != nullptr)
     int stage = 0, sb = 0;
     uint32_t phase = 0, sphase = 0;   // full[] parity; sfree[] parity of the S buffer's last use
-    for (int64_t it = 0; it < my_tiles; ++it) {
-        float* L = LG + stage * tile_f;
-        prof_mark(-1);
-        mbar_wait(&full[stage], phase);
-        prof_mark(0);
-        if (PRO) {
-            // phase 0 (Stage 1): the tile's local poses, computed into the stage buffer
-            // by all consumer threads, consecutive elements on consecutive lanes
-            // (coalesced key reads)
-            const int64_t c0 = (blockIdx.x + it * gridDim.x) * a.C;
-            const int nel = (int)min((int64_t)a.C, a.n_chars - c0) * a.J;
-            const int nl = a.n_layers;
-            const int4* dsc_t = desc + stage * a.C * nl;
-            const float4* keys4 = reinterpret_cast<const float4*>(a.keys);
-            stage1_tile<HS_S1_E, HS_S1_PIPE != 0>(keys4, dsc_t, nel, a.J, nl, t, NC, L);
-            bar_consumers(NC);
-            prof_mark(8);   // phase 0 (Stage 1)
+    // tiles of this CTA, grouped by segment: the program switch sits outside the hot
+    // loop (MULTI only; one group otherwise)
+    int64_t it = 0;
+    while (it < my_tiles) {
+        int64_t it_end = my_tiles;
+        if (MULTI) {
+            const int64_t g0 = blockIdx.x + it * gridDim.x;
+            if (g0 >= next_base) {   // first tile in a later segment: switch programs
+                int s = cseg + 1;
+                while (s + 1 < a.nseg && g0 >= a.seg[s + 1].tile_base) ++s;
+                cseg = s;
+                load_program(s);
+            }
+            if (next_base != INT64_MAX)
+                it_end = min(it_end, (next_base - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
         }
+        for (; it < it_end; ++it) {
+            const int64_t g = blockIdx.x + it * gridDim.x;
+            float* L = LG + stage * tile_f;
+            prof_mark(-1);
+            mbar_wait(&full[stage], phase);
+            prof_mark(0);
+            if (PRO) {
+                // phase 0 (Stage 1): the tile's local poses, computed into the stage buffer
+                // by all consumer threads, consecutive elements on consecutive lanes
+                // (coalesced key reads)
+                const int64_t c0 = (g - SEGV(tile_base, tbase_g)) * SEGV(C, C_g);
+                const int nel = (int)min((int64_t)SEGV(C, C_g), SEGV(n_chars, nch_g) - c0) * SEGV(J, J_g);
+                const int nl = a.n_layers;
+                const int4* dsc_t = desc + stage * SEGV(C, C_g) * nl;
+                const float4* keys4 = reinterpret_cast<const float4*>(a.keys);
+                stage1_tile<HS_S1_E, HS_S1_PIPE != 0>(keys4, dsc_t, nel, SEGV(J, J_g), nl, t, NC, L);
+                bar_consumers(NC);
+                prof_mark(8);   // phase 0 (Stage 1)
+            }
 
-        // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
-        float acc[12];
-        if (p1 > 0) {
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                if (s < p1) {
-                    const int off = (int)(m[s] & 0xffff);
+            // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
+            float acc[12];
+            if (p1 > 0) {
+    #pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    if (s < p1) {
+                        const int off = (int)(m[s] & 0xffff);
+                        const int src = (int)(int16_t)(m[s] >> 32);
+                        const int own = (int)(int16_t)(m[s] >> 48);
+                        float l[12];
+                        ld3(L + off * 12, l);
+                        if (src == kSrcPrev) {
+                            float tmp[12];
+                            compose(acc, l, tmp);
+    #pragma unroll
+                            for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                        } else {
+    #pragma unroll
+                            for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                        }
+                        if (own >= 0) st3(P + own * 12, acc);
+                    }
+                }
+            }
+            prof_mark(6);   // phase-1 fold of thread 0 (before any barrier)
+            // phase 2a: heavy paths longer than K sit on consecutive lanes (runs); a
+            // segmented warp-shuffle scan joins their pieces (Hillis-Steele over lanes,
+            // parent on the left), then each run lane lifts its anchors by its exclusive
+            // prefix.  No CTA barrier: runs never cross a warp.
+            float excl[12];
+            // longest run prefix in this warp: the scan needs ceil(log2(max + 1)) steps
+            // (reduced per tile so the compiler sees a warp-uniform bound: no divergence
+            // guards around the shuffles)
+            const int warp_maxrb = RUNS ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
+            if (RUNS && warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
+                for (int d = 1; d <= warp_maxrb; d <<= 1) {
+                    float u[12];
+    #pragma unroll
+                    for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
+                    if (run_back >= d) {
+                        float w[12];
+                        compose(u, acc, w);
+    #pragma unroll
+                        for (int e = 0; e < 12; ++e) acc[e] = w[e];
+                    }
+                }
+    #pragma unroll
+                for (int e = 0; e < 12; ++e) excl[e] = __shfl_up_sync(0xffffffffu, acc[e], 1);
+                if (run_back > 0) {
+    #pragma unroll
+                    for (int s = 0; s < K; ++s) {
+                        const int own = (int)(int16_t)(m[s] >> 48);
+                        if (own >= 0) {
+                            float x[12], y[12];
+                            ld3(P + own * 12, x);
+                            compose(excl, x, y);
+                            st3(P + own * 12, y);
+                        }
+                    }
+                }
+            }
+            prof_mark(7);   // phase-2a scan + lift of thread 0's warp
+            bar_consumers(NC);
+
+            prof_mark(1);
+            // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
+            // snapshot semantics: ping-pong P, or a single P with every read of a round
+            // before any of its writes (entries held in registers, <= 4 per thread).
+            // Descriptors (slot | dst buf | self buf | link location) come from smem.
+            for (int r = 0, nr = SEGV(R2, R2_g); r < nr; ++r) {
+                const int eb = s_round_off[r], e1 = s_round_off[r + 1];
+                if (!SEGV(p_single, psingle_g)) {
+                    for (int e = eb + t; e < e1; e += NC) {
+                        const uint32_t w = s_rounds[e];
+                        const int slot = (int)(w & 0x3fff);
+                        const int dst = slot + ((w >> 14) & 1) * SEGV(nslots, S2_g),
+                                  self = slot + ((w >> 15) & 1) * SEGV(nslots, S2_g),
+                                  link = (int)(w >> 16);
+                        float x[12], y[12], z[12];
+                        ld3(P + link * 12, x);
+                        ld3(P + self * 12, y);
+                        compose(x, y, z);
+                        st3(P + dst * 12, z);
+                    }
+                    bar_consumers(NC);
+                } else {
+                    float z[4][12];
+                    int dst[4];
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = eb + t + q * NC;
+                        dst[q] = -1;
+                        if (e < e1) {
+                            const uint32_t w = s_rounds[e];
+                            float x[12], y[12];
+                            ld3(P + (int)(w >> 16) * 12, x);
+                            ld3(P + (int)(w & 0x3fff) * 12, y);
+                            compose(x, y, z[q]);
+                            dst[q] = (int)(w & 0x3fff);
+                        }
+                    }
+                    bar_consumers(NC);
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (dst[q] >= 0) st3(P + dst[q] * 12, z[q]);
+                    bar_consumers(NC);
+                }
+            }
+            prof_mark(2);
+
+            // phase 3: final fold, G in place, S into the S buffer
+            float* S = SB + sb * tile_f;
+            if (SKIN && it >= NSS) mbar_wait(&sfree[sb], sphase);
+            prof_mark(3);
+            {
+                float acc[12];
+    #pragma unroll
+                for (int s = 0; s < K; ++s) {
                     const int src = (int)(int16_t)(m[s] >> 32);
-                    const int own = (int)(int16_t)(m[s] >> 48);
+                    if (src == kSrcNone) continue;
+                    const int off = (int)(m[s] & 0xffff);
                     float l[12];
                     ld3(L + off * 12, l);
                     if (src == kSrcPrev) {
                         float tmp[12];
                         compose(acc, l, tmp);
-#pragma unroll
+    #pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
-                    } else {
-#pragma unroll
+                    } else if (src == kSrcRoot) {
+    #pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                    }
-                    if (own >= 0) st3(P + own * 12, acc);
-                }
-            }
-        }
-        prof_mark(6);   // phase-1 fold of thread 0 (before any barrier)
-        // phase 2a: heavy paths longer than K sit on consecutive lanes (runs); a
-        // segmented warp-shuffle scan joins their pieces (Hillis-Steele over lanes,
-        // parent on the left), then each run lane lifts its anchors by its exclusive
-        // prefix.  No CTA barrier: runs never cross a warp.
-        float excl[12];
-        if (RUNS && warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
-            for (int d = 1; d <= warp_maxrb; d <<= 1) {
-                float u[12];
-#pragma unroll
-                for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
-                if (run_back >= d) {
-                    float w[12];
-                    compose(u, acc, w);
-#pragma unroll
-                    for (int e = 0; e < 12; ++e) acc[e] = w[e];
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < 12; ++e) excl[e] = __shfl_up_sync(0xffffffffu, acc[e], 1);
-            if (run_back > 0) {
-#pragma unroll
-                for (int s = 0; s < K; ++s) {
-                    const int own = (int)(int16_t)(m[s] >> 48);
-                    if (own >= 0) {
-                        float x[12], y[12];
-                        ld3(P + own * 12, x);
-                        compose(excl, x, y);
-                        st3(P + own * 12, y);
-                    }
-                }
-            }
-        }
-        prof_mark(7);   // phase-2a scan + lift of thread 0's warp
-        bar_consumers(NC);
-
-        prof_mark(1);
-        // phase 2: pointer jumping over anchors (Alg. 2 on the anchor forest) with
-        // snapshot semantics: ping-pong P, or a single P with every read of a round
-        // before any of its writes (entries held in registers, <= 4 per thread).
-        // Descriptors (slot | dst buf | self buf | link location) come from smem.
-        const int S2 = a.nslots;
-        for (int r = 0; r < a.R2; ++r) {
-            const int eb = s_round_off[r], e1 = s_round_off[r + 1];
-            if (!a.p_single) {
-                for (int e = eb + t; e < e1; e += NC) {
-                    const uint32_t w = s_rounds[e];
-                    const int slot = (int)(w & 0x3fff);
-                    const int dst = slot + ((w >> 14) & 1) * S2, self = slot + ((w >> 15) & 1) * S2,
-                              link = (int)(w >> 16);
-                    float x[12], y[12], z[12];
-                    ld3(P + link * 12, x);
-                    ld3(P + self * 12, y);
-                    compose(x, y, z);
-                    st3(P + dst * 12, z);
-                }
-                bar_consumers(NC);
-            } else {
-                float z[4][12];
-                int dst[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int e = eb + t + q * NC;
-                    dst[q] = -1;
-                    if (e < e1) {
-                        const uint32_t w = s_rounds[e];
-                        float x[12], y[12];
-                        ld3(P + (int)(w >> 16) * 12, x);
-                        ld3(P + (int)(w & 0x3fff) * 12, y);
-                        compose(x, y, z[q]);
-                        dst[q] = (int)(w & 0x3fff);
-                    }
-                }
-                bar_consumers(NC);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (dst[q] >= 0) st3(P + dst[q] * 12, z[q]);
-                bar_consumers(NC);
-            }
-        }
-        prof_mark(2);
-
-        // phase 3: final fold, G in place, S into the S buffer
-        float* S = SB + sb * tile_f;
-        if (do_skin && it >= NSS) mbar_wait(&sfree[sb], sphase);
-        prof_mark(3);
-        {
-            float acc[12];
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                const int src = (int)(int16_t)(m[s] >> 32);
-                if (src == kSrcNone) continue;
-                const int off = (int)(m[s] & 0xffff);
-                float l[12];
-                ld3(L + off * 12, l);
-                if (src == kSrcPrev) {
-                    float tmp[12];
-                    compose(acc, l, tmp);
-#pragma unroll
-                    for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
-                } else if (src == kSrcRoot) {
-#pragma unroll
-                    for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                } else if (RUNS && src == kSrcRun) {
-                    // first joint of a run lane: parent = previous lane's tail, whose
-                    // global pose is P[run anchor] (x) (exclusive scan of the run)
-                    float base[12];
-                    if (run_anchor >= 0) {
-                        float pa[12];
-                        ld3(P + run_anchor * 12, pa);
-                        compose(pa, excl, base);
+                    } else if (RUNS && src == kSrcRun) {
+                        // first joint of a run lane: parent = previous lane's tail, whose
+                        // global pose is P[run anchor] (x) (exclusive scan of the run)
+                        float base[12];
+                        if (run_anchor >= 0) {
+                            float pa[12];
+                            ld3(P + run_anchor * 12, pa);
+                            compose(pa, excl, base);
+                        } else {
+    #pragma unroll
+                            for (int e = 0; e < 12; ++e) base[e] = excl[e];
+                        }
+                        compose(base, l, acc);
                     } else {
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) base[e] = excl[e];
+                        float pa[12];
+                        ld3(P + src * 12, pa);
+                        compose(pa, l, acc);
                     }
-                    compose(base, l, acc);
-                } else {
-                    float pa[12];
-                    ld3(P + src * 12, pa);
-                    compose(pa, l, acc);
-                }
-                st3(L + off * 12, acc);
-                if (do_skin) {
-                    float sk[12];
-                    compose(acc, ibr[s], sk);
-                    st3(S + off * 12, sk);
+                    st3(L + off * 12, acc);
+                    if (SKIN) {
+                        float sk[12];
+                        compose(acc, ibr[s], sk);
+                        st3(S + off * 12, sk);
+                    }
                 }
             }
+            fence_proxy_async();
+            bar_consumers(NC);
+            if (t == 0) mbar_arrive(&done[stage]);
+            prof_mark(4);
+            if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
+            if (++stage == NS) { stage = 0; phase ^= 1u; }
+            if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }   // parity of use q-1
         }
-        fence_proxy_async();
-        bar_consumers(NC);
-        if (t == 0) mbar_arrive(&done[stage]);
-        prof_mark(4);
-        if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
-        if (++stage == NS) { stage = 0; phase ^= 1u; }
-        if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }   // parity of use q-1
     }
 }
+#undef SEGV
+#undef SKIN
 
 // ================================================================== doubling (Alg. 2)
 // One CTA per group of C characters, one thread per (character, joint) in USER
@@ -871,22 +957,29 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
     }
 }
 
-template <int K>
-void* chunked_ptr(bool runs, bool pro) {
-    if (pro)
-        return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true, true>)
-                    : reinterpret_cast<void*>(&chunked_kernel<K, false, true>);
-    return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true, false>)
-                : reinterpret_cast<void*>(&chunked_kernel<K, false, false>);
+template <int K, int MODE>
+void* chunked_ptr_m(bool runs) {
+    return runs ? reinterpret_cast<void*>(&chunked_kernel<K, true, MODE>)
+                : reinterpret_cast<void*>(&chunked_kernel<K, false, MODE>);
 }
 
-void* chunked_fn(int K, bool runs, bool pro) {
+template <int K>
+void* chunked_ptr(bool runs, int mode) {
+    switch (mode) {
+        case kModeScan: return chunked_ptr_m<K, kModeScan>(runs);
+        case kModeStage1: return chunked_ptr_m<K, kModeStage1>(runs);
+        case kModeMulti: return chunked_ptr_m<K, kModeMulti>(runs);
+        default: return nullptr;
+    }
+}
+
+void* chunked_fn(int K, bool runs, int mode) {
     switch (K) {
-        case 3: return chunked_ptr<3>(runs, pro);
-        case 5: return chunked_ptr<5>(runs, pro);
-        case 7: return chunked_ptr<7>(runs, pro);
-        case 9: return chunked_ptr<9>(runs, pro);
-        case 11: return chunked_ptr<11>(runs, pro);
+        case 3: return chunked_ptr<3>(runs, mode);
+        case 5: return chunked_ptr<5>(runs, mode);
+        case 7: return chunked_ptr<7>(runs, mode);
+        case 9: return chunked_ptr<9>(runs, mode);
+        case 11: return chunked_ptr<11>(runs, mode);
         default: return nullptr;
     }
 }
@@ -913,8 +1006,8 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
     for (bool runs : {false, true})
-        for (bool pro : {false, true}) {
-            void* fn = chunked_fn(K, runs, pro);
+        for (int mode : {(int)kModeScan, (int)kModeStage1, (int)kModeMulti}) {
+            void* fn = chunked_fn(K, runs, mode);
             if (!fn) return cudaErrorInvalidValue;
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
             if (e != cudaSuccess) return e;
@@ -923,7 +1016,7 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
 }
 
 int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes) {
-    void* fn = chunked_fn(K, runs, false);
+    void* fn = chunked_fn(K, runs, kModeScan);
     int nb = 0;
     if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
                    cudaSuccess)
@@ -932,9 +1025,11 @@ int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes)
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    void* fn = chunked_fn(K, a.has_runs != 0, a.layers != nullptr);
+    const int mode = a.layers != nullptr ? kModeStage1 : (a.nseg > 1 ? kModeMulti : kModeScan);
+    if (mode == kModeStage1 && a.nseg != 1) return cudaErrorInvalidValue;
+    void* fn = chunked_fn(K, a.has_runs != 0, mode);
     if (!fn) return cudaErrorInvalidValue;
-    const int64_t ntiles = (a.n_chars + a.C - 1) / a.C;
+    const int64_t ntiles = a.total_tiles;
     int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm
                                    : max_chunked_blocks_per_sm(K, a.has_runs != 0, a.threads, a.smem_bytes);
     int64_t grid = (int64_t)sm_count() * per_sm;

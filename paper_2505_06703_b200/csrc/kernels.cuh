@@ -6,33 +6,48 @@
 
 namespace hs {
 
-// Persistent TMA tile kernel (HS_ALGO_CHUNKED), DESIGN.md §5.1.
-struct ChunkedArgs {
+// Persistent TMA tile kernel (HS_ALGO_CHUNKED), DESIGN.md §5.1.  One launch runs
+// up to kMaxSegs segments (a skeleton's crowd each, NEXT-3): their tiles form one
+// global tile space, CTA b taking tiles b, b + grid, ...; a CTA switches programs
+// when its tile crosses into the next segment.
+constexpr int kMaxSegs = 8;
+
+struct SegArgs {
     const float* local;        // [n_chars][J][12]
     float* gout;               // [n_chars][J][12]
     float* sout;               // [n_chars][J][12] or nullptr (no bind epilogue)
     const float* ib;           // [J][12] user order (used when sout != nullptr)
-    int64_t n_chars;
-    int32_t J, C, F, T;        // joints, chars per tile, joints per tile, compute threads
-    int32_t nslots, R2;
     const uint64_t* meta;      // [T][K]
     const int32_t* p1len;      // [T]: phase-1 length | run_back << 8 | (run anchor + 1) << 16
     const int32_t* round_off;  // [R2+1]
     const uint32_t* rounds;    // phase-2 descriptors (copied to smem by each CTA)
+    int64_t n_chars;
+    int64_t tile_base;         // first global tile of this segment
+    int32_t J, C, F, T;        // joints, chars per tile, joints per tile, compute threads
+    int32_t nslots, R2;
     int32_t n_rounds_entries;
+    int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
+};
+
+struct ChunkedArgs {
+    SegArgs seg[kMaxSegs];
+    int32_t nseg;
+    int64_t total_tiles;
+    int32_t tile_f;            // floats per stage / S buffer: 12 x max F
+    int32_t p_floats;          // floats of the P region (max over segments)
+    int32_t r2_max;            // max R2 (table layout)
     int32_t stages, sbufs;
     int64_t smem_bytes;
     int32_t threads;           // consumer warps * 32 + 32 (producer warp)
     int32_t ctas_per_sm;       // 0 = occupancy maximum
-    int32_t has_runs;          // lanes joined by the warp-shuffle scan (CHUNK_RUNS programs)
+    int32_t has_runs;          // some segment's lanes are joined by the warp-shuffle scan
     int32_t bulk_piece;        // bytes per TMA bulk copy (0 = one copy per tile and buffer)
-    int32_t p_single;          // 1 = single P buffer, all reads of a round before its writes
-    // Stage-1 prologue (hs_animate): layers != nullptr replaces the local-pose input
+    // Stage-1 prologue (hs_animate, one segment): layers != nullptr replaces the
+    // local-pose input
     const void* layers;        // device [n_chars][n_layers] hs_layer (16 B)
-    const float* keys;         // device [n_clips][n_keys][J][12] packed keys
+    const float* keys;         // device [n_clips][n_keys][3][J] planar float4 keys
     int32_t n_layers, n_keys, wrap;
-    int32_t desc_off;
-    int32_t s1_variant;        // Stage-1 phase-0 schedule (tuning aid)          // smem byte offset of the layer-descriptor ring ([stages][C * n_layers] int4)
+    int32_t desc_off;          // smem byte offset of the layer-descriptor ring ([stages][C * n_layers] int4)
     float fps, duration;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
