@@ -75,6 +75,9 @@ def lib():
         L.hsg_clips.restype = None
         L.hsg_layers.argtypes = [u64, u64, u64, u64, u64, u64, ctypes.c_float, ctypes.c_void_p]
         L.hsg_layers.restype = None
+        L.hsg_mesh.argtypes = [u64, u64, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.hsg_mesh.restype = None
         _lib = L
     return _lib
 
@@ -216,3 +219,15 @@ def layers(seed: int, n_chars: int, n_layers: int, n_clips: int, time_span: floa
     if n_chars:
         lib().hsg_layers(seed, type_, char0, n_chars, n_layers, n_clips, time_span, out.ctypes.data)
     return out
+
+
+# --- NEXT-4: synthetic skinned meshes --------------------------------------------------
+def mesh(seed: int, parents, V: int, type_: int = 0):
+    """(pos [V, 3] f32, joints [V, 4] i32, weights [V, 4] f32) for a skeleton."""
+    par = np.ascontiguousarray(parents, np.int32)
+    pos = np.empty((V, 3), np.float32)
+    joints = np.empty((V, 4), np.int32)
+    weights = np.empty((V, 4), np.float32)
+    lib().hsg_mesh(seed, type_, par.ctypes.data, len(par), V, pos.ctypes.data, joints.ctypes.data,
+                   weights.ctypes.data)
+    return pos, joints, weights

@@ -285,3 +285,31 @@ void hsg_layers(uint64_t seed, uint64_t type, uint64_t char0, uint64_t n_chars, 
             memcpy(p, &clip, 4); memcpy(p + 4, &tm, 4); memcpy(p + 8, &wt, 4); memcpy(p + 12, &pad, 4);
         }
 }
+
+/* Synthetic skinned mesh for a skeleton (NEXT-4; "Mesh Face Number
+ * 1000-3000"): V vertices, stream 8*(type + 64) + 7, counter (0, V, vertex, k).
+ * Rest position uniform in [-1, 1]^3.  Influences: a home joint floor(u0 J), its
+ * parent and grandparent (the joint itself at a root), and a uniform random joint;
+ * weights u + 0.05 normalised in fp64 and rounded to fp32; with probability 0.3 the
+ * fourth weight is 0 (fewer than four influences). */
+void hsg_mesh(uint64_t seed, uint64_t type, const int32_t* parents, int32_t J, int32_t V,
+              float* pos, int32_t* joints, float* weights) {
+    const uint64_t s = 8 * (type + 64) + 7;
+    for (int32_t v = 0; v < V; ++v) {
+#define U(k) hsg_u(seed, s, 0, (uint64_t)V, (uint64_t)v, (k))
+        for (int e = 0; e < 3; ++e) pos[3 * v + e] = (float)(2.0 * U(e) - 1.0);
+        int32_t j0 = (int32_t)floor(U(3) * (double)J);
+        if (j0 >= J) j0 = J - 1;
+        const int32_t j1 = parents[j0] >= 0 ? parents[j0] : j0;
+        const int32_t j2 = parents[j1] >= 0 ? parents[j1] : j1;
+        int32_t j3 = (int32_t)floor(U(4) * (double)J);
+        if (j3 >= J) j3 = J - 1;
+        double w[4], sum = 0.0;
+        for (int k = 0; k < 4; ++k) w[k] = U(5 + k) + 0.05;
+        if (U(9) < 0.3) w[3] = 0.0;
+        for (int k = 0; k < 4; ++k) sum += w[k];
+        joints[4 * v + 0] = j0; joints[4 * v + 1] = j1; joints[4 * v + 2] = j2; joints[4 * v + 3] = j3;
+        for (int k = 0; k < 4; ++k) weights[4 * v + k] = (float)(w[k] / sum);
+#undef U
+    }
+}

@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "stage1.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "stage1.c"), os.path.join(_HERE, "lbs.c")]
 
 STATUS = {0: "ok", 2: "empty", 3: "out_of_range", 4: "cycle", 6: "nomem"}
 
@@ -68,6 +68,8 @@ def lib():
                                   ctypes.c_int32, vp, ctypes.c_int32, vp, ctypes.c_int64, vp, vp, vp,
                                   ctypes.c_int]
         L.orc_animate.restype = ctypes.c_int
+        L.orc_skin_vertices.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp]
+        L.orc_skin_vertices.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -208,3 +210,24 @@ def animate(parents, keys, fps: float, wrap: int, layers, inv_bind=None, nthread
     if st:
         raise OracleError(st)
     return (g, s, loc) if return_local else (g, s)
+
+
+# ---------------------------------------------------------------- LBS (NEXT-4)
+def skin_vertices(skin, pos, joints, weights) -> np.ndarray:
+    """Linear blend skinning in fp64.  skin: [n_chars, J, 3, 4] (or [J, 3, 4]) skin
+    matrices; pos [V, 3], joints [V, 4], weights [V, 4].  Returns [n_chars, V, 3]."""
+    S = np.ascontiguousarray(skin, np.float64)
+    squeeze = S.ndim == 3
+    if squeeze:
+        S = S[None]
+    n, J = S.shape[0], S.shape[1]
+    p = np.ascontiguousarray(pos, np.float32)
+    jt = np.ascontiguousarray(joints, np.int32)
+    w = np.ascontiguousarray(weights, np.float32)
+    V = p.shape[0]
+    out = np.empty((n, V, 3), np.float64)
+    st = lib().orc_skin_vertices(S.ctypes.data, n, J, V, p.ctypes.data, jt.ctypes.data, w.ctypes.data,
+                                 out.ctypes.data)
+    if st:
+        raise OracleError(st)
+    return out[0] if squeeze else out
