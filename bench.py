@@ -69,6 +69,9 @@ def parse_args(argv=None):
     ap.add_argument("--stage1", action="store_true",
                     help="fused Stage-1 prologue (hs_animate): 2 animation layers per character "
                          "sampled from 8 clips x 31 keys instead of resident local poses")
+    ap.add_argument("--skin-mesh", type=int, default=0, metavar="V",
+                    help="NEXT-4: fuse linear blend skinning of a V-vertex synthetic mesh per "
+                         "character (hs_scan_skin); 0 = off")
     ap.add_argument("--launch", choices=["auto", "batch", "per-type"], default="auto",
                     help="batch = all skeleton types in one hs_scan_batch launch (NEXT-3); "
                          "auto = batch for small crowds only (see bench.py)")
@@ -284,6 +287,10 @@ def run_ours(args):
                 assert rc == 0, f"generator launch failed: {rc}"
             item["local"] = local
             item["g"] = torch.empty_like(local)
+            if args.skin_mesh:
+                item["mesh_np"] = hsgen.mesh(200 + type_, par, args.skin_mesh, type_=type_)
+                item["mesh"] = hs.Mesh(sk, *item["mesh_np"])
+                item["verts"] = torch.empty((n, args.skin_mesh, 3), dtype=torch.float32, device=dev)
         item["s"] = torch.empty_like(item["g"])
         work.append(item)
     torch.cuda.synchronize()
@@ -295,7 +302,7 @@ def run_ours(args):
     # faster (the multi-segment kernel's program switch costs registers)
     small = all(-(-w["n"] // max(1, w["sk"].query("tile_chars"))) < 32 * 148 for w in work)
     batch = args.launch == "batch" or (
-        args.launch == "auto" and small and not args.stage1 and args.algo == "auto"
+        args.launch == "auto" and small and not args.stage1 and not args.skin_mesh and args.algo == "auto"
         and args.tile_ctas == 0 and len({w["sk"].query("chunk") for w in work}) == 1
         and all(w["sk"].query("path") == 1 for w in work))
     # launches per step: one hs_scan_batch over every type, or one call per type
@@ -313,6 +320,8 @@ def run_ours(args):
                 w = work[members[0]]
                 if args.stage1:
                     hs.animate(w["sk"], w["cs"], w["layers"], w["g"], w["s"], stream=stream)
+                elif args.skin_mesh:
+                    hs.scan_skin(w["sk"], w["mesh"], w["local"], w["g"], w["s"], w["verts"], stream=stream)
                 else:
                     w["sk"].scan_into(w["local"], w["g"], w["s"], stream=stream, algo=args.algo,
                                       tile_ctas=args.tile_ctas)
@@ -359,7 +368,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel launch (largest byte share: the batch launch,
     # else tree1024's)
     bpj = STAGE1_BYTES_PER_JOINT if args.stage1 else BYTES_PER_JOINT
-    per_char_extra = 16 * STAGE1_LAYERS if args.stage1 else 0
+    per_char_extra = 16 * STAGE1_LAYERS if args.stage1 else 12 * args.skin_mesh
 
     def launch_bytes(li):
         return sum(bpj * work[t]["n"] * work[t]["J"] + per_char_extra * work[t]["n"]
@@ -371,10 +380,12 @@ def run_ours(args):
     achieved = dom_bytes / (per_launch_ms[dom_l] / 1e3) / 1e9
     peak, peak_src = measured_peaks()
     workload = WORKLOAD_NAME[args.config]
+    if args.skin_mesh:
+        workload += f" + fused LBS ({args.skin_mesh}-vertex mesh per character)"
     if args.stage1:
         workload += (f" + fused Stage 1 ({STAGE1_LAYERS} layers per character, "
                      f"{STAGE1_CLIPS} clips x {STAGE1_KEYS} keys at {STAGE1_FPS:g} fps)")
-    kernel_name = (f"chunked_kernel{'<stage1>' if args.stage1 else ''} "
+    kernel_name = (f"chunked_kernel{'<stage1>' if args.stage1 else '<lbs>' if args.skin_mesh else ''} "
                    f"({launches[dom_l][0]} launch)")
     traffic, traffic_src = ncu_traffic(workload, kernel_name)
 
@@ -382,7 +393,7 @@ def run_ours(args):
     cpu = None
     if not (args.no_e2e or args.profile):
         e2e = run_e2e(work, args, hs, torch, dist, world)
-    if not (args.no_cpu or args.profile) and rank == 0 and world == 1:
+    if not (args.no_cpu or args.profile or args.skin_mesh) and rank == 0 and world == 1:
         cpu = run_cpu_baseline(args)
 
     if rank != 0:
@@ -394,6 +405,9 @@ def run_ours(args):
         "config": {"workload": workload,
                    "characters_per_gpu": {w["name"]: w["n"] for w in work},
                    "joints_total": joints_total, "bytes_per_joint": bpj,
+                   **({"vertices_per_char": args.skin_mesh,
+                       "vertices_per_s": value * sum(w["n"] for w in work) * args.skin_mesh / joints_rank,
+                       "bytes_per_vertex": 12} if args.skin_mesh else {}),
                    "hbm_gbs": joints_total * bpj * K / (ms / 1e3) / 1e9 / world,
                    "hbm_gbs_note": "per GPU, algorithmic bytes / step time",
                    "l2": "inputs larger than L2 (no flush)", "algo": args.algo,
@@ -448,12 +462,17 @@ def sampled_parity(work, rank, per_type=24):
         worst = max(worst, eg, es)
         out[w["name"]] = {"chars": len(idx), "max_err_global": eg, "max_err_skin": es,
                           "gen_elements_differing": gen_mismatch}
+        if "verts" in w:   # NEXT-4: vertices vs the oracle's LBS of its own skin pose
+            ev = float(np.abs(w["verts"][idx].cpu().numpy() - oracle.skin_vertices(S, *w["mesh_np"])).max())
+            out[w["name"]]["max_err_verts"] = ev
+            out["verts_tolerance"] = 4e-4   # (|p|_1 + 1) x 1e-4, tests/test_gpu_lbs.py
+            out["verts_pass"] = out.get("verts_pass", True) and ev <= 4e-4
     # Stage 1 adds fp32 rounding of each computed local pose, carried down the root
     # path: max(1e-4, 4e-9 L^2) with L = 300 here
     tol = 3.6e-4 if any("keys" in w for w in work) else 1e-4
     out["tolerance"] = tol
     out["worst"] = worst
-    out["pass"] = worst <= tol
+    out["pass"] = worst <= tol and out.get("verts_pass", True)
     if not out["pass"]:
         print(f"PARITY FAILURE: {out}", file=sys.stderr)
     return out
@@ -508,6 +527,8 @@ def run_e2e(work, args, hs, torch, dist, world):
     that step's local poses H2D from pinned memory and reads global + skin back D2H."""
     if args.stage1:
         return run_e2e_stage1(work, args, hs, torch, dist, world)
+    if args.skin_mesh:   # the host-buffer pipeline has no LBS entry point
+        return None
     pl = hs.Pipeline(batch_bytes=256 << 20)
     slices = []
     h2d = d2h = 0

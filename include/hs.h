@@ -159,6 +159,34 @@ typedef struct {
 hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * Linear blend skinning fused after the bind epilogue (
+ * PAPER.md:96 "compute animation simulation, Hierarchy-Scan, skinning and rendering
+ * in the GPU", PAPER.md:240 meshes of 1000-3000 faces).  The paper gives no formula;
+ * DESIGN.md reading R24: per character c and vertex v,
+ *     verts[c][v] = sum_{k<4} w[v][k] * S[c][j[v][k]] (p[v], 1)
+ * with S = G (x) IB the skin pose, weights used as given, positions only.  The skin
+ * palette of a tile never leaves shared memory (skin_out may be NULL).
+ * ------------------------------------------------------------------------- */
+typedef struct hs_mesh hs_mesh;
+
+/* pos: host fp32 [n_vertices][3] rest positions (bind space); joints: host int32
+ * [n_vertices][4] influencing joints (user labels, each in [0, n_joints)); weights:
+ * host fp32 [n_vertices][4] (a 0 weight disables an influence).  Copied to the
+ * current device.  Errors: HS_ERR_INVALID_ARG (null, n_vertices outside 1..2^24),
+ * HS_ERR_OUT_OF_RANGE (a joint index), HS_ERR_UNSUPPORTED (n_joints > 65535). */
+hs_status hs_mesh_create(const hs_skeleton* sk, int32_t n_vertices, const float* pos, const int32_t* joints,
+                         const float* weights, hs_mesh** out);
+hs_status hs_mesh_destroy(hs_mesh* mesh);
+
+/* hs_scan (G, and S when skin_out != NULL) plus skinned vertex positions:
+ *   verts_out  device fp32 [n_chars][n_vertices][3], 4-byte aligned, not aliasing
+ *              the other buffers.
+ * Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise); the mesh must have been
+ * created for this skeleton (HS_ERR_INVALID_ARG). */
+hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
+                       float* global_out, float* skin_out, float* verts_out, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * Stage 1 fused ahead of the scan ("Sample
  * animation data and generate local pose in local space").
  * Per character and joint: sample each animation layer's clip at its time (keys

@@ -107,6 +107,9 @@ def lib():
     L.hs_clipset_destroy.argtypes = [vp]
     L.hs_animate.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
     L.hs_scan_batch.argtypes = [ctypes.POINTER(_BatchItem), i32, vp]
+    L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
+    L.hs_mesh_destroy.argtypes = [vp]
+    L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
@@ -279,6 +282,54 @@ def scan_batch(items, stream=None):
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
     _check(lib().hs_scan_batch(arr, len(items), st), "hs_scan_batch")
+
+
+class Mesh:
+    """Skinned mesh for one skeleton (hs_mesh_create): pos [V, 3] f32, joints [V, 4]
+    int32, weights [V, 4] f32 (NEXT-4)."""
+
+    def __init__(self, sk: "Skeleton", pos, joints, weights):
+        p = np.ascontiguousarray(pos, np.float32)
+        j = np.ascontiguousarray(joints, np.int32)
+        w = np.ascontiguousarray(weights, np.float32)
+        V = p.shape[0]
+        if p.shape != (V, 3) or j.shape != (V, 4) or w.shape != (V, 4):
+            raise ValueError("pos [V, 3], joints [V, 4], weights [V, 4]")
+        h = ctypes.c_void_p()
+        _check(lib().hs_mesh_create(sk.handle, V, p.ctypes.data, j.ctypes.data, w.ctypes.data,
+                                    ctypes.byref(h)), "hs_mesh_create")
+        self._h, self.n_vertices = h, V
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.hs_mesh_destroy(self._h)
+        self._h = None
+
+    __del__ = close
+
+
+def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None, verts_out=None,
+              stream=None, skin: bool = False):
+    """hs_scan_skin: scan + bind + linear blend skinning.  Returns (global, skin-or-None,
+    verts [N, V, 3])."""
+    import torch
+    n = local.shape[0]
+    if global_out is None:
+        global_out = torch.empty_like(local)
+    if skin_out is None and skin:
+        skin_out = torch.empty_like(local)
+    if verts_out is None:
+        verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=local.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_scan_skin(sk.handle, mesh.handle, local.data_ptr(), n, global_out.data_ptr(),
+                              None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st),
+           "hs_scan_skin")
+    return global_out, skin_out, verts_out
 
 
 LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])

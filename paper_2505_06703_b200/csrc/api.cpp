@@ -84,6 +84,14 @@ struct hs_clipset {
     float* d_keys = nullptr;   // [n_clips][n_keys][3][n_joints] float4: {t,qw} {qxyz,sx} {sy,sz,0,0}
 };
 
+struct hs_mesh {
+    int device = 0;
+    int32_t n_joints = 0, n_verts = 0;
+    float4* d_a = nullptr;     // [V] (px, py, pz, w0)
+    float4* d_b = nullptr;     // [V] (w1, w2, w3, 0)
+    int2* d_j = nullptr;       // [V] packed 16-bit joint indices
+};
+
 struct hs_pipeline {
     int device = 0;
     int64_t batch_bytes = 0;
@@ -518,6 +526,79 @@ hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_
         else return fail(HS_ERR_UNSUPPORTED, "batched programs do not fit shared memory together");
     }
     return run_chunked(a, K, static_cast<cudaStream_t>(cuda_stream));
+}
+
+hs_status hs_mesh_create(const hs_skeleton* sk, int32_t n_vertices, const float* pos, const int32_t* joints,
+                         const float* weights, hs_mesh** out) {
+    if (!sk || !pos || !joints || !weights || !out) return fail(HS_ERR_INVALID_ARG, "null argument");
+    if (n_vertices < 1 || n_vertices > (1 << 24)) return fail(HS_ERR_INVALID_ARG, "n_vertices must be in 1..2^24");
+    const int32_t J = sk->plan.n;
+    if (J > 65535) return fail(HS_ERR_UNSUPPORTED, "meshes need n_joints <= 65535");
+    const size_t V = (size_t)n_vertices;
+    std::vector<float4> A(V), B(V);
+    std::vector<int2> Jt(V);
+    for (size_t v = 0; v < V; ++v) {
+        for (int k = 0; k < 4; ++k) {
+            const int32_t j = joints[4 * v + k];
+            if (j < 0 || j >= J) return fail(HS_ERR_OUT_OF_RANGE, "mesh joint index out of range");
+        }
+        A[v] = make_float4(pos[3 * v], pos[3 * v + 1], pos[3 * v + 2], weights[4 * v]);
+        B[v] = make_float4(weights[4 * v + 1], weights[4 * v + 2], weights[4 * v + 3], 0.f);
+        Jt[v] = make_int2((int)((uint32_t)joints[4 * v] | ((uint32_t)joints[4 * v + 1] << 16)),
+                          (int)((uint32_t)joints[4 * v + 2] | ((uint32_t)joints[4 * v + 3] << 16)));
+    }
+    hs_mesh* m = new (std::nothrow) hs_mesh();
+    if (!m) return fail(HS_ERR_OOM, "host allocation failed");
+    cudaGetDevice(&m->device);
+    m->n_joints = J;
+    m->n_verts = n_vertices;
+    cudaError_t e;
+    if ((e = upload(&m->d_a, A.data(), V)) != cudaSuccess || (e = upload(&m->d_b, B.data(), V)) != cudaSuccess ||
+        (e = upload(&m->d_j, Jt.data(), V)) != cudaSuccess) {
+        hs_mesh_destroy(m);
+        return cuda_fail(e, "mesh upload");
+    }
+    *out = m;
+    return HS_OK;
+}
+
+hs_status hs_mesh_destroy(hs_mesh* m) {
+    if (!m) return HS_OK;
+    cudaFree(m->d_a);
+    cudaFree(m->d_b);
+    cudaFree(m->d_j);
+    delete m;
+    return HS_OK;
+}
+
+hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
+                       float* global_out, float* skin_out, float* verts_out, void* cuda_stream) {
+    if (!sk || !mesh) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!local || !global_out || !verts_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (!aligned16(local) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)) ||
+        (reinterpret_cast<uintptr_t>(verts_out) & 3))
+        return fail(HS_ERR_INVALID_ARG, "pose buffers must be 16-byte aligned, vertices 4-byte");
+    if (local == global_out || (skin_out && (local == skin_out || global_out == skin_out)) ||
+        verts_out == local || verts_out == global_out || verts_out == skin_out)
+        return fail(HS_ERR_INVALID_ARG, "output aliases an input or another output");
+    if (mesh->n_joints != sk->plan.n) return fail(HS_ERR_INVALID_ARG, "mesh built for another skeleton");
+    if (n_chars > (INT64_MAX / 64) / std::max(sk->plan.n, mesh->n_verts))
+        return fail(HS_ERR_INVALID_ARG, "size overflow");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != sk->device || dev != mesh->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "hs_scan_skin needs a single-CTA skeleton");
+    hs::ChunkedArgs a{};
+    const ChunkItem item{sk, local, n_chars, global_out, skin_out};
+    chunked_layout(&item, 1, sk->stages, sk->sbufs, a);
+    a.mesh_a = mesh->d_a;
+    a.mesh_b = mesh->d_b;
+    a.mesh_j = mesh->d_j;
+    a.verts = verts_out;
+    a.n_verts = mesh->n_verts;
+    return run_chunked(a, sk->K, static_cast<cudaStream_t>(cuda_stream));
 }
 
 hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_clips, int32_t n_keys,

@@ -353,8 +353,9 @@ __device__ __forceinline__ void stage1_tile(const float4* __restrict__ keys, con
 //            (IB held in registers) into the S buffer;
 // then the producer bulk-stores G and S and refills the stage.
 // Kernel modes: one segment (hs_scan), one segment with the Stage-1 prologue
-// (hs_animate), or several segments in one launch (hs_scan_batch, NEXT-3).
-enum : int { kModeScan = 0, kModeStage1 = 1, kModeMulti = 2 };
+// (hs_animate), several segments in one launch (hs_scan_batch, NEXT-3), or one
+// segment with the linear-blend-skinning epilogue (hs_scan_skin, NEXT-4).
+enum : int { kModeScan = 0, kModeStage1 = 1, kModeMulti = 2, kModeSkin = 3 };
 
 // Producer-side view of the segment a tile belongs to; advanced only when the tile
 // index crosses into the next segment (tiles of a CTA only move forward).
@@ -385,6 +386,7 @@ template <int K, bool RUNS, int MODE>
 __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__ ChunkedArgs a) {
     constexpr bool PRO = MODE == kModeStage1;
     constexpr bool MULTI = MODE == kModeMulti;
+    constexpr bool LBS = MODE == kModeSkin;
     extern __shared__ __align__(128) unsigned char smem[];
     const int NS = a.stages, NSS = a.sbufs;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
     auto load_program = [&](int s) {
         const SegArgs& S = a.seg[s];
         J = S.J; C = S.C; S2 = S.nslots; R2 = S.R2; p_single = S.p_single;
-        nch = S.n_chars; tbase = S.tile_base; do_skin = S.sout != nullptr;
+        nch = S.n_chars; tbase = S.tile_base; do_skin = LBS || S.sout != nullptr;
         next_base = s + 1 < a.nseg ? a.seg[s + 1].tile_base : INT64_MAX;
         p1 = 0; run_back = 0; run_anchor = -1;
         if (t < S.T) {
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
     // per-segment values in the tile loop, read from the kernel parameters with the
     // (CTA-uniform) segment index, so loop bounds and branches stay uniform
 #define SEGV(field, var) (a.seg[MULTI ? cseg : 0].field)
-#define SKIN (a.seg[MULTI ? cseg : 0].sout != nullptr)
+#define SKIN (LBS || a.seg[MULTI ? cseg : 0].sout != nullptr)
     int stage = 0, sb = 0;
     uint32_t phase = 0, sphase = 0;   // full[] parity; sfree[] parity of the S buffer's last use
     // tiles of this CTA, grouped by segment: the program switch sits outside the hot
@@ -758,6 +760,58 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             fence_proxy_async();
             bar_consumers(NC);
             if (t == 0) mbar_arrive(&done[stage]);
+            if (LBS) {
+                // linear blend skinning (R24): the tile's skin palette is in
+                // the S buffer; vertex v of character c = sum_k w_k S[c][j_k] (p_v, 1).
+                // Consecutive vertices on consecutive lanes (planar mesh arrays, L2-
+                // resident, coalesced stores); the producer's bulk store of S only reads
+                // the buffer.
+                const SegArgs& S0 = a.seg[0];
+                const int64_t c0 = (g - S0.tile_base) * S0.C;
+                const int V = a.n_verts, Jn = S0.J;
+                const int nct = (int)min((int64_t)S0.C, S0.n_chars - c0);   // characters in the tile
+                const float* Sb = SB + sb * tile_f;
+                float* vout = a.verts + c0 * V * 3;
+                // vertex-major: mesh records of two vertices per thread loaded up front,
+                // then every character of the tile (independent palette reads and
+                // stores: ILP, no division)
+                for (int v0 = t; v0 < V; v0 += 2 * NC) {
+                    float4 pa[2], pb[2];
+                    int js[2][4];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int v = min(v0 + u * NC, V - 1);
+                        pa[u] = __ldg(a.mesh_a + v);
+                        pb[u] = __ldg(a.mesh_b + v);
+                        const int2 jj = __ldg(a.mesh_j + v);
+                        js[u][0] = (jj.x & 0xffff) * 12; js[u][1] = (int)((uint32_t)jj.x >> 16) * 12;
+                        js[u][2] = (jj.y & 0xffff) * 12; js[u][3] = (int)((uint32_t)jj.y >> 16) * 12;
+                    }
+                    for (int cl = 0; cl < nct; ++cl) {
+                        const float* Sc = Sb + cl * Jn * 12;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int v = v0 + u * NC;
+                            if (v >= V) continue;
+                            const float ws[4] = {pa[u].w, pb[u].x, pb[u].y, pb[u].z};
+                            float x = 0.f, y = 0.f, z = 0.f;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                float m[12];
+                                ld3(Sc + js[u][q], m);
+                                const float px = fmaf(m[0], pa[u].x, fmaf(m[1], pa[u].y, fmaf(m[2], pa[u].z, m[3])));
+                                const float py = fmaf(m[4], pa[u].x, fmaf(m[5], pa[u].y, fmaf(m[6], pa[u].z, m[7])));
+                                const float pz = fmaf(m[8], pa[u].x, fmaf(m[9], pa[u].y, fmaf(m[10], pa[u].z, m[11])));
+                                x = fmaf(ws[q], px, x);
+                                y = fmaf(ws[q], py, y);
+                                z = fmaf(ws[q], pz, z);
+                            }
+                            float* d = vout + ((int64_t)cl * V + v) * 3;
+                            d[0] = x; d[1] = y; d[2] = z;
+                        }
+                    }
+                }
+            }
             prof_mark(4);
             if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
             if (++stage == NS) { stage = 0; phase ^= 1u; }
@@ -969,6 +1023,7 @@ void* chunked_ptr(bool runs, int mode) {
         case kModeScan: return chunked_ptr_m<K, kModeScan>(runs);
         case kModeStage1: return chunked_ptr_m<K, kModeStage1>(runs);
         case kModeMulti: return chunked_ptr_m<K, kModeMulti>(runs);
+        case kModeSkin: return chunked_ptr_m<K, kModeSkin>(runs);
         default: return nullptr;
     }
 }
@@ -1006,7 +1061,7 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
     if (e != cudaSuccess) return e;
     if (smem_bytes > optin) return cudaErrorInvalidValue;
     for (bool runs : {false, true})
-        for (int mode : {(int)kModeScan, (int)kModeStage1, (int)kModeMulti}) {
+        for (int mode : {(int)kModeScan, (int)kModeStage1, (int)kModeMulti, (int)kModeSkin}) {
             void* fn = chunked_fn(K, runs, mode);
             if (!fn) return cudaErrorInvalidValue;
             e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
@@ -1025,8 +1080,11 @@ int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes)
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
-    const int mode = a.layers != nullptr ? kModeStage1 : (a.nseg > 1 ? kModeMulti : kModeScan);
-    if (mode == kModeStage1 && a.nseg != 1) return cudaErrorInvalidValue;
+    const int mode = a.layers != nullptr ? kModeStage1
+                     : a.verts != nullptr ? kModeSkin
+                     : (a.nseg > 1 ? kModeMulti : kModeScan);
+    if ((mode == kModeStage1 || mode == kModeSkin) && a.nseg != 1) return cudaErrorInvalidValue;
+    if (a.layers != nullptr && a.verts != nullptr) return cudaErrorInvalidValue;
     void* fn = chunked_fn(K, a.has_runs != 0, mode);
     if (!fn) return cudaErrorInvalidValue;
     const int64_t ntiles = a.total_tiles;

@@ -49,6 +49,12 @@ struct ChunkedArgs {
     int32_t n_layers, n_keys, wrap;
     int32_t desc_off;          // smem byte offset of the layer-descriptor ring ([stages][C * n_layers] int4)
     float fps, duration;
+    // LBS epilogue (hs_scan_skin, one segment): verts != nullptr adds vertex skinning
+    const float4* mesh_a;      // [V] (px, py, pz, w0)
+    const float4* mesh_b;      // [V] (w1, w2, w3, 0)
+    const int2* mesh_j;        // [V] (j0 | j1 << 16, j2 | j3 << 16)
+    float* verts;              // [n_chars][V][3]
+    int32_t n_verts;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);

@@ -1,0 +1,121 @@
+"""GPU parity of the fused linear-blend-skinning epilogue (hs_scan_skin; SURVEY.md §8(f)
+NEXT-4, R24) against the fp64 oracle (oracle.scan -> oracle.skin_vertices).
+
+Tolerance: a skinned vertex is sum_k w_k (S_k (p, 1)) with sum w = 1 and |p_i| <= 1,
+so an error e in each skin-matrix element moves it by at most (|p|_1 + 1) e <= 4e with
+the north-star e = 1e-4 -> 4e-4, plus the fp32 rounding of the blend itself (~1e-6).
+Against the LBS of the GPU's own skin output the bound is that rounding only: a few
+fp32 ulps of the vertex magnitude, 2e-6 x (1 + max |v|).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import hsgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2505_06703_b200 as hs  # noqa: E402
+
+TOL_VERTS = 4e-4
+TOL_SELF = 2e-6   # x (1 + max |v|)
+
+
+def run(par, loc, ib, mesh, skin=True, **create):
+    sk = hs.Skeleton(par, ib, **create)
+    m = hs.Mesh(sk, *mesh)
+    x = torch.from_numpy(loc).cuda()
+    g, s, v = hs.scan_skin(sk, m, x, skin=skin)
+    torch.cuda.synchronize()
+    g2, s2 = sk.scan(x)
+    torch.cuda.synchronize()
+    out = (g.cpu().numpy(), None if s is None else s.cpu().numpy(), v.cpu().numpy(),
+           g2.cpu().numpy(), s2.cpu().numpy())
+    return out
+
+
+@pytest.mark.parametrize("name,n,V", [("hum32", 100, 700), ("hum64", 300, 1000), ("chain256", 60, 1500),
+                                      ("tree1024", 24, 2000)])
+def test_lbs_parity(name, n, V):
+    par = hsgen.skeleton(name)
+    J = len(par)
+    loc = hsgen.local_poses(21, J, n)
+    ib = hsgen.inv_bind(22, J)
+    mesh = hsgen.mesh(23, par, V)
+    g, s, v, g2, s2 = run(par, loc, ib, mesh)
+    # the scan outputs are the plain hs_scan ones, bit for bit
+    assert np.array_equal(g, g2) and np.array_equal(s, s2)
+    G, S = oracle.scan(par, loc, ib)
+    want = oracle.skin_vertices(S, *mesh)
+    err = float(np.abs(v - want).max())
+    self_err = float(np.abs(v - oracle.skin_vertices(s.astype(np.float64), *mesh)).max())
+    print(f"{name}: verts vs oracle {err:.2e}, vs LBS of the GPU skin {self_err:.2e}")
+    assert err <= TOL_VERTS and self_err <= TOL_SELF * (1 + float(np.abs(want).max()))
+
+
+def test_lbs_without_skin_output_matches():
+    par = hsgen.skeleton("hum64")
+    loc = hsgen.local_poses(31, 64, 50)
+    ib = hsgen.inv_bind(32, 64)
+    mesh = hsgen.mesh(33, par, 900)
+    _, s_none, v_none, _, _ = run(par, loc, ib, mesh, skin=False)
+    _, _, v_skin, _, _ = run(par, loc, ib, mesh, skin=True)
+    assert s_none is None and np.array_equal(v_none, v_skin)
+
+
+def test_lbs_exact_family_bitwise():
+    # exact poses (signed permutations, integer translations), positions in {-1, 0, 1}
+    # and dyadic weights: every product and sum is exact in fp32
+    par = hsgen.skeleton("tree1024")
+    J = len(par)
+    loc = hsgen.exact_poses(41, J, 5)
+    ib = hsgen.exact_inv_bind(42, J)
+    pos, jt, _ = hsgen.mesh(43, par, 1200)
+    pos = np.sign(np.round(pos * 1.4)).astype(np.float32)
+    w = np.tile(np.array([0.5, 0.25, 0.125, 0.125], np.float32), (len(pos), 1))
+    _, s, v, _, _ = run(par, loc, ib, (pos, jt, w))
+    G, S = oracle.scan(par, loc, ib)
+    assert np.array_equal(s.astype(np.float64), S)
+    assert np.array_equal(v.astype(np.float64), oracle.skin_vertices(S, pos, jt, w))
+
+
+def test_lbs_bind_pose_returns_rest_positions():
+    # locals = the bind pose's locals -> S = I -> every vertex at its rest position
+    par = hsgen.skeleton("hum64")
+    bind_local = hsgen.local_poses(51, 64, 1)[0]
+    G, _ = oracle.scan(par, bind_local[None])
+    ib = np.empty((64, 3, 4), np.float32)
+    for j in range(64):
+        H = np.eye(4)
+        H[:3] = G[0, j]
+        ib[j] = np.linalg.inv(H)[:3].astype(np.float32)
+    mesh = hsgen.mesh(52, par, 800)
+    _, _, v, _, _ = run(par, np.repeat(bind_local[None], 3, 0), ib, mesh)
+    assert np.abs(v - mesh[0][None].astype(np.float64)).max() < 1e-4
+
+
+def test_lbs_errors():
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    pos, jt, w = hsgen.mesh(61, hsgen.skeleton("hum32"), 10)
+    bad = jt.copy()
+    bad[3, 2] = 32
+    with pytest.raises(hs.HSError) as e:
+        hs.Mesh(sk, pos, bad, w)
+    assert e.value.status == hs.HS_ERR_OUT_OF_RANGE
+    other = hs.Skeleton(hsgen.skeleton("hum64"))
+    m_other = hs.Mesh(other, *hsgen.mesh(62, hsgen.skeleton("hum64"), 10))
+    x = torch.zeros((2, 32, 3, 4), device="cuda")
+    with pytest.raises(hs.HSError) as e:
+        hs.scan_skin(sk, m_other, x)
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    big = hs.Skeleton(hsgen.random_tree(9, 4096, 64))
+    m_big = hs.Mesh(big, *hsgen.mesh(63, hsgen.random_tree(9, 4096, 64), 10))
+    with pytest.raises(hs.HSError) as e:
+        hs.scan_skin(big, m_big, torch.zeros((1, 4096, 3, 4), device="cuda"))
+    assert e.value.status == hs.HS_ERR_UNSUPPORTED
