@@ -82,8 +82,45 @@ def full_capture(rep, out_path, tag, n_joints, workload):
               open("profiles/ncu_traffic.json", "w"), indent=1)
 
 
+def kernel_summary(rep, out_path, title, alg_bytes):
+    """Key counters of one captured launch (no ncu_traffic.json update)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, u, v = rows[0], rows[1], rows[2]
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "lts__t_sectors_srcunit_tex_op_read.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__shared_mem_per_block_dynamic", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smsp__inst_executed.sum"]
+    lines = [f"# {title}", f"# algorithmic HBM bytes per launch: {alg_bytes / 1e9:.3f} GB", ""]
+    for k in keys:
+        if k in h:
+            i = h.index(k)
+            lines.append(f"{k:75s} {v[i]:>18s} {u[i]}")
+    stalls = sorted(((h[i], float(v[i])) for i in range(len(h))
+                     if "average_warps_issue_stalled" in h[i] and "per_issue_active" in h[i]),
+                    key=lambda z: -z[1])
+    lines += ["", "# warp stall reasons (warps stalled per issued instruction)"]
+    lines += [f"{k:75s} {x:8.3f}" for k, x in stalls if x > 0.01]
+    open(out_path, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
 if __name__ == "__main__":
     tag = sys.argv[1]
+    if len(sys.argv) > 2 and sys.argv[2] == "stage1":
+        kernel_summary(f"gpurun_out/prof_stage1_{tag}.ncu-rep", f"profiles/{tag}_ncu_stage1_tree1024.txt",
+                       f"{tag}: ncu --set full, hs_animate tree1024 x 50,000 characters, 2 layers "
+                       "(tools/stage1_one.py, 3rd launch)", 50_000 * (1024 * 96 + 32))
+        sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[2] == "lbs":
+        kernel_summary(f"gpurun_out/prof_lbs_{tag}.ncu-rep", f"profiles/{tag}_ncu_lbs_tree1024.txt",
+                       f"{tag}: ncu --set full, hs_scan_skin tree1024 x 20,000 characters, 1000-vertex "
+                       "mesh (tools/lbs_one.py, 3rd launch)", 20_000 * (1024 * 144 + 1000 * 12))
+        sys.exit(0)
     launches(f"gpurun_out/launches_{tag}.csv", f"profiles/{tag}_launches.txt", tag)
     full_capture(f"gpurun_out/prof_tree_{tag}.ncu-rep", f"profiles/{tag}_ncu_tree1024.txt", tag,
                  333333 * 1024, "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU")
