@@ -214,9 +214,27 @@ typedef struct {
 } hs_layer;
 
 /* layers: device [n_chars][n_layers] hs_layer (n_layers 1..8), 16-byte aligned; outputs
- * as hs_scan.  Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise). */
+ * as hs_scan.  Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise).  Same as
+ * hs_animate_ex with opts == NULL. */
 hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
                      int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream);
+
+/* How Stage 1 meets the scan.  FUSED: computed in shared memory inside the scan
+ * kernel (96 B/joint of HBM traffic).  TWO_PASS: a streaming Stage-1 kernel writes the
+ * local poses of a batch of characters to a workspace (stream-ordered cudaMallocAsync,
+ * workspace_bytes, default 1 GiB) and the plain scan reads them back (192 B/joint),
+ * which hides the key-load latency better.  AUTO = TWO_PASS (measured faster on B200,
+ * DESIGN.md §5.1b).  Both produce bitwise the same local poses, hence the same output. */
+typedef enum { HS_ANIMATE_AUTO = 0, HS_ANIMATE_FUSED = 1, HS_ANIMATE_TWO_PASS = 2 } hs_animate_mode;
+typedef struct {
+    int32_t mode;             /* hs_animate_mode                                        */
+    int32_t reserved0;        /* must be 0                                              */
+    int64_t workspace_bytes;  /* TWO_PASS batch workspace (0 = 1 GiB; >= one character) */
+    int64_t reserved[2];      /* must be 0                                              */
+} hs_animate_opts;
+hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                        int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
+                        const hs_animate_opts* opts);
 
 /* Destroy a handle (NULL-safe).  The caller guarantees no hs_scan using it is
  * still in flight.  Frees its device tables with cudaFree (device-synchronising). */

@@ -106,6 +106,7 @@ def lib():
     L.hs_clipset_create.argtypes = [vp, vp, i32, i32, ctypes.c_float, i32, ctypes.POINTER(vp)]
     L.hs_clipset_destroy.argtypes = [vp]
     L.hs_animate.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
+    L.hs_animate_ex.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp, ctypes.POINTER(_AnimateOpts)]
     L.hs_scan_batch.argtypes = [ctypes.POINTER(_BatchItem), i32, vp]
     L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
     L.hs_mesh_destroy.argtypes = [vp]
@@ -260,6 +261,14 @@ class Skeleton:
 MAX_BATCH = 8   # HS_MAX_BATCH
 
 
+ANIMATE_MODE = {"auto": 0, "fused": 1, "two_pass": 2}
+
+
+class _AnimateOpts(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64), ("reserved", ctypes.c_int64 * 2)]
+
+
 class _BatchItem(ctypes.Structure):
     _fields_ = [("skeleton", ctypes.c_void_p), ("local", ctypes.c_void_p), ("n_chars", ctypes.c_int64),
                 ("global_out", ctypes.c_void_p), ("skin_out", ctypes.c_void_p)]
@@ -361,7 +370,7 @@ class ClipSet:
 
 
 def animate(sk: "Skeleton", clips: ClipSet, layers, global_out=None, skin_out=None, stream=None,
-            skin: bool = True):
+            skin: bool = True, mode: str = "auto", workspace_bytes: int = 0):
     """Stage 1 + Hierarchy-Scan + Bind (hs_animate).  layers: CUDA tensor [N, n_layers, 4]
     int32 / float32 bit pattern of hs_layer, or a numpy LAYER_DTYPE array (copied)."""
     import torch
@@ -375,8 +384,10 @@ def animate(sk: "Skeleton", clips: ClipSet, layers, global_out=None, skin_out=No
         skin_out = torch.empty_like(global_out)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    _check(lib().hs_animate(sk.handle, clips.handle, layers.data_ptr(), nl, n, global_out.data_ptr(),
-                            None if skin_out is None else skin_out.data_ptr(), st), "hs_animate")
+    opts = _AnimateOpts(ANIMATE_MODE[mode], 0, workspace_bytes)
+    _check(lib().hs_animate_ex(sk.handle, clips.handle, layers.data_ptr(), nl, n, global_out.data_ptr(),
+                               None if skin_out is None else skin_out.data_ptr(), st, ctypes.byref(opts)),
+           "hs_animate")
     return global_out, skin_out
 
 

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -81,7 +82,7 @@ struct hs_clipset {
     int device = 0;
     int32_t n_clips = 0, n_keys = 0, n_joints = 0, wrap = 0;
     float fps = 0.f, duration = 0.f;
-    float* d_keys = nullptr;   // [n_clips][n_keys][3][n_joints] float4: {t,qw} {qxyz,sx} {sy,sz,0,0}
+    float* d_keys = nullptr;   // [n_clips][n_keys] rows of 10 * Jp floats (see hs_clipset_create)
 };
 
 struct hs_mesh {
@@ -260,6 +261,32 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Stream-ordered workspaces (split path, two-pass Stage 1) come from a library-owned
+// pool per device that keeps its memory (release threshold = max): after the first
+// frame a workspace costs no driver allocation.  The process's default pool and
+// PyTorch's allocator are left alone.
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
+    static cudaMemPool_t pools[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, st);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = pool;
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pools[dev], st);
+}
+
 static_assert(HS_MAX_BATCH <= hs::kMaxSegs, "one kernel segment per batch item");
 
 struct ChunkItem {
@@ -407,7 +434,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             batch = std::min(batch, n_chars);
             float* ws = nullptr;
             if (sp.nslots > 0) {
-                e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)(2 * batch * per_char), st);
+                e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(2 * batch * per_char), st);
                 if (e != cudaSuccess) return cuda_fail(e, "split workspace");
             }
             float* pg = ws;
@@ -607,22 +634,25 @@ hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_
     if (n_clips <= 0 || n_keys <= 0 || !(fps > 0.f) || wrap < 0 || wrap > 1)
         return fail(HS_ERR_INVALID_ARG, "n_clips, n_keys, fps must be positive; wrap 0 or 1");
     const int32_t J = sk->plan.n;
-    if ((int64_t)n_clips * n_keys * J * 3 >= ((int64_t)1 << 31))   // int32 float4 indices
+    const int64_t Jp = J + (J & 1);   // planes padded to 16 bytes
+    if ((int64_t)n_clips * n_keys * Jp * 10 >= ((int64_t)1 << 31))   // int32 float offsets
         return fail(HS_ERR_INVALID_ARG, "clip set too large");
     hs_clipset* cs = new (std::nothrow) hs_clipset();
     if (!cs) return fail(HS_ERR_OOM, "host allocation failed");
     cudaGetDevice(&cs->device);
     cs->n_clips = n_clips; cs->n_keys = n_keys; cs->n_joints = J; cs->wrap = wrap; cs->fps = fps;
     cs->duration = (float)(n_keys - 1) / fps;   // same fp32 operation as the oracle (R20)
-    // planar float4 layout: per (clip, key) row, plane p in {0,1,2} holds joint j's
-    // float4 p at [row][p][j] — consecutive joints on consecutive lanes read 512
-    // contiguous bytes per warp load
-    std::vector<float> packed((size_t)n_clips * n_keys * J * 12, 0.f);
+    // planar layout, 40 B per (key, joint): per (clip, key) row of 10 * Jp floats,
+    // [Jp][4] {t, qw} | [Jp][4] {q.xyz, sx} | [Jp][2] {sy, sz} — consecutive joints on
+    // consecutive lanes read contiguous bytes
+    std::vector<float> packed((size_t)n_clips * n_keys * Jp * 10, 0.f);
     for (size_t row = 0; row < (size_t)n_clips * n_keys; ++row)
         for (int32_t j = 0; j < J; ++j) {
             const float* s = keys + (row * J + j) * 10;
-            for (int e = 0; e < 10; ++e)   // t0 t1 t2 qw | qx qy qz sx | sy sz 0 0
-                packed[((row * 3 + e / 4) * J + j) * 4 + e % 4] = s[e];
+            float* r = packed.data() + row * Jp * 10;
+            for (int e = 0; e < 4; ++e) r[(size_t)j * 4 + e] = s[e];
+            for (int e = 0; e < 4; ++e) r[(size_t)Jp * 4 + (size_t)j * 4 + e] = s[4 + e];
+            for (int e = 0; e < 2; ++e) r[(size_t)Jp * 8 + (size_t)j * 2 + e] = s[8 + e];
         }
     cudaError_t e = upload(&cs->d_keys, packed.data(), packed.size());
     if (e != cudaSuccess) { delete cs; return cuda_fail(e, "clip upload"); }
@@ -637,10 +667,20 @@ hs_status hs_clipset_destroy(hs_clipset* cs) {
     return HS_OK;
 }
 
-hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
-                     int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream) {
+hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                        int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
+                        const hs_animate_opts* opts) {
     if (!sk || !cs) return fail(HS_ERR_INVALID_ARG, "null handle");
     if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    int mode = HS_ANIMATE_AUTO;
+    int64_t ws_bytes = (int64_t)1 << 30;
+    if (opts) {
+        if (opts->mode < HS_ANIMATE_AUTO || opts->mode > HS_ANIMATE_TWO_PASS || opts->reserved0 ||
+            opts->reserved[0] || opts->reserved[1] || opts->workspace_bytes < 0)
+            return fail(HS_ERR_INVALID_ARG, "invalid hs_animate_opts");
+        mode = opts->mode;
+        if (opts->workspace_bytes) ws_bytes = opts->workspace_bytes;
+    }
     if (n_chars == 0) return HS_OK;
     if (!layers || !global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
     if (n_layers < 1 || n_layers > 8) return fail(HS_ERR_INVALID_ARG, "n_layers must be in 1..8");
@@ -652,8 +692,43 @@ hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* la
     cudaGetDevice(&dev);
     if (dev != sk->device || dev != cs->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
     if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "hs_animate needs a single-CTA skeleton");
-    return scan_impl(sk, nullptr, n_chars, global_out, skin_out, static_cast<cudaStream_t>(cuda_stream),
-                     HS_ALGO_CHUNKED, -1, 0, cs, layers, n_layers);
+    const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (mode == HS_ANIMATE_FUSED)
+        return scan_impl(sk, nullptr, n_chars, global_out, skin_out, st, HS_ALGO_CHUNKED, -1, 0, cs, layers,
+                         n_layers);
+    // two-pass (and AUTO, measured faster on B200: DESIGN.md §5.1b): Stage 1 streams the
+    // local poses of a batch of characters into a stream-ordered workspace, then the
+    // plain chunked scan reads them back
+    const int32_t J = sk->plan.n;
+    const int64_t per_char = (int64_t)J * 48;
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(n_chars, ws_bytes / per_char));
+    float* ws = nullptr;
+    cudaError_t e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(batch * per_char), st);
+    if (e != cudaSuccess) return cuda_fail(e, "Stage-1 workspace");
+    hs::ChunkedArgs s1{};
+    const ChunkItem one{sk, nullptr, n_chars, global_out, skin_out};
+    chunked_layout(&one, 1, sk->stages, sk->sbufs, s1);
+    s1.layers = layers;
+    s1.keys = cs->d_keys;
+    s1.n_layers = n_layers;
+    s1.n_keys = cs->n_keys;
+    s1.wrap = cs->wrap;
+    s1.fps = cs->fps;
+    s1.duration = cs->duration;
+    hs_status r = HS_OK;
+    for (int64_t c0 = 0; c0 < n_chars && r == HS_OK; c0 += batch) {
+        const int64_t nb = std::min(batch, n_chars - c0);
+        if ((e = hs::launch_stage1(s1, c0, nb, ws, st)) != cudaSuccess) { r = cuda_fail(e, "Stage-1 launch"); break; }
+        r = scan_impl(sk, ws, nb, global_out + c0 * J * 12, skin_out ? skin_out + c0 * J * 12 : nullptr, st,
+                      HS_ALGO_CHUNKED, -1, 0);
+    }
+    cudaFreeAsync(ws, st);
+    return r;
+}
+
+hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                     int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream) {
+    return hs_animate_ex(sk, cs, layers, n_layers, n_chars, global_out, skin_out, cuda_stream, nullptr);
 }
 
 hs_status hs_scan(const hs_skeleton* sk, const float* local, int64_t n_chars, float* global_out,

@@ -130,7 +130,8 @@ __device__ __forceinline__ void bar_consumers(int nthreads) {
 // Keyframe sampling, layer blending and TRS -> 3x4 (
 // DESIGN.md readings R19-R23), fused ahead of the scan: the local pose is computed
 // in shared memory instead of being read from HBM.  Keys on the device are packed
-// per (clip, key) row as three planar float4 arrays over joints: {tx,ty,tz,qw} {qx,qy,qz,sx} {sy,sz,-,-}.
+// per (clip, key) row as planar arrays over joints: float4 {tx,ty,tz,qw}, float4
+// {qx,qy,qz,sx}, float2 {sy,sz} (40 B per key and joint, see load_keys).
 // The time -> key decision uses the oracle's exact fp32 operation sequence.
 __device__ __forceinline__ void key_index(float t, int n_keys, float fps, float duration, int wrap,
                                           int& k0, float& a) {
@@ -175,14 +176,14 @@ __device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
     int k0;
     float fr;
     key_index(__int_as_float(L.y), a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
-    const int J = a.seg[0].J;
-    const int row = (L.x * a.n_keys + k0) * J * 3;
-    return make_int4(row, fr != 0.0f ? J * 3 : 0, __float_as_int(fr), L.z);
+    const int Jp = a.seg[0].J + (a.seg[0].J & 1);   // joints padded to even (16-byte planes)
+    const int row = (L.x * a.n_keys + k0) * Jp * 10;
+    return make_int4(row, fr != 0.0f ? Jp * 10 : 0, __float_as_int(fr), L.z);
 }
 
 // Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
-__device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float4 z0, float4 x1, float4 y1,
-                                           float4 z1, float a, float* trs) {
+__device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, float4 x1, float4 y1,
+                                           float2 z1, float a, float* trs) {
     if (a == 0.0f) {   // on a key: that key exactly (R21)
         trs[0] = x0.x; trs[1] = x0.y; trs[2] = x0.z; trs[3] = x0.w;
         trs[4] = y0.x; trs[5] = y0.y; trs[6] = y0.z;
@@ -216,23 +217,30 @@ __device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
 // l + 1's loads before layer l's arithmetic): sample every layer, blend (DESIGN.md
 // R22), TRS -> 3x4, store into the tile in smem.
 struct KeyPair {
-    float4 x0, y0, z0, x1, y1, z1;
+    float4 x0, y0, x1, y1;
+    float2 z0, z1;
 };
 
-// Keys are planar (float4 plane p of joint j at row * 3J + p * J + j): a warp's
-// loads of one plane over consecutive joints are contiguous.
-__device__ __forceinline__ KeyPair load_keys(const float4* __restrict__ keys, int4 d, int j, int J) {
-    const float4* p0 = keys + d.x + j;
-    const float4* p1 = p0 + d.y;
+// Keys are planar, 40 bytes per (key, joint): per (clip, key) row of 10 * Jp floats
+// (Jp = joints padded to even), plane 0 = float4 {t, qw}, plane 1 = float4 {q.xyz, sx},
+// plane 2 = float2 {sy, sz}; a warp's loads of one plane over consecutive joints are
+// contiguous.  d.x = the row's float offset, d.y = the step to key k0 + 1 (0: one key).
+__device__ __forceinline__ KeyPair load_keys(const float* __restrict__ keys, int4 d, int j, int Jp) {
+    const float* p0 = keys + d.x;
+    const float* p1 = p0 + d.y;
     KeyPair k;
-    k.x0 = __ldg(p0); k.y0 = __ldg(p0 + J); k.z0 = __ldg(p0 + 2 * J);
-    k.x1 = __ldg(p1); k.y1 = __ldg(p1 + J); k.z1 = __ldg(p1 + 2 * J);
+    k.x0 = __ldg(reinterpret_cast<const float4*>(p0) + j);
+    k.y0 = __ldg(reinterpret_cast<const float4*>(p0 + 4 * Jp) + j);
+    k.z0 = __ldg(reinterpret_cast<const float2*>(p0 + 8 * Jp) + j);
+    k.x1 = __ldg(reinterpret_cast<const float4*>(p1) + j);
+    k.y1 = __ldg(reinterpret_cast<const float4*>(p1 + 4 * Jp) + j);
+    k.z1 = __ldg(reinterpret_cast<const float2*>(p1 + 8 * Jp) + j);
     return k;
 }
 
 template <int E, bool PIPE>
-__device__ __forceinline__ void stage1_elems(const float4* __restrict__ keys, const int4* const* dsc,
-                                             const int* j, const bool* valid, int nl, int J, float* L,
+__device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, const int4* const* dsc,
+                                             const int* j, const bool* valid, int nl, int Jp, float* L,
                                              const int* off) {
     float acc[E][10], q0[E][4], wsum[E];
     KeyPair kp[E];
@@ -241,7 +249,7 @@ __device__ __forceinline__ void stage1_elems(const float4* __restrict__ keys, co
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             d[e] = valid[e] ? dsc[e][0] : make_int4(0, 0, 0, 0);
-            kp[e] = load_keys(keys, d[e], j[e], J);
+            kp[e] = load_keys(keys, d[e], j[e], Jp);
         }
     }
     for (int l = 0; l < nl; ++l) {
@@ -254,11 +262,11 @@ __device__ __forceinline__ void stage1_elems(const float4* __restrict__ keys, co
                 dc[e] = d[e];
                 if (l + 1 < nl) {
                     d[e] = valid[e] ? dsc[e][l + 1] : make_int4(0, 0, 0, 0);
-                    kp[e] = load_keys(keys, d[e], j[e], J);
+                    kp[e] = load_keys(keys, d[e], j[e], Jp);
                 }
             } else {
                 dc[e] = valid[e] ? dsc[e][l] : make_int4(0, 0, 0, 0);
-                cur[e] = load_keys(keys, dc[e], j[e], J);
+                cur[e] = load_keys(keys, dc[e], j[e], Jp);
             }
         }
 #pragma unroll
@@ -313,7 +321,7 @@ __device__ __forceinline__ void stage1_elems(const float4* __restrict__ keys, co
 // consecutive elements on consecutive threads (coalesced key reads), E per thread
 // per pass.
 template <int E, bool PIPE>
-__device__ __forceinline__ void stage1_tile(const float4* __restrict__ keys, const int4* dsc_t, int nel,
+__device__ __forceinline__ void stage1_tile(const float* __restrict__ keys, const int4* dsc_t, int nel,
                                             int J, int nl, int t, int NC, float* L) {
     // element o = cl * J + j, advanced by E * NC per pass without a division
     const int step = E * NC, step_c = step / J, step_j = step - step_c * J;
@@ -334,7 +342,7 @@ __device__ __forceinline__ void stage1_tile(const float4* __restrict__ keys, con
                 while (jj >= J) { jj -= J; ++cl; }
             }
         }
-        stage1_elems<E, PIPE>(keys, dsc, j, valid, nl, J, L, off);
+        stage1_elems<E, PIPE>(keys, dsc, j, valid, nl, J + (J & 1), L, off);
         cl0 += step_c;
         j0 += step_j;
         if (j0 >= J) { j0 -= J; ++cl0; }
@@ -594,8 +602,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 const int nel = (int)min((int64_t)SEGV(C, C_g), SEGV(n_chars, nch_g) - c0) * SEGV(J, J_g);
                 const int nl = a.n_layers;
                 const int4* dsc_t = desc + stage * SEGV(C, C_g) * nl;
-                const float4* keys4 = reinterpret_cast<const float4*>(a.keys);
-                stage1_tile<HS_S1_E, HS_S1_PIPE != 0>(keys4, dsc_t, nel, SEGV(J, J_g), nl, t, NC, L);
+                stage1_tile<HS_S1_E, HS_S1_PIPE != 0>(a.keys, dsc_t, nel, SEGV(J, J_g), nl, t, NC, L);
                 bar_consumers(NC);
                 prof_mark(8);   // phase 0 (Stage 1)
             }
@@ -821,6 +828,37 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
 }
 #undef SEGV
 #undef SKIN
+
+// ================================================================== Stage 1, two-pass
+// The same per-element Stage-1 arithmetic as the fused prologue (layer_desc +
+// stage1_elems: bitwise the same local poses), as a high-occupancy streaming kernel
+// that writes the local poses to a workspace for a plain chunked scan.  One thread
+// per (character, joint) element, consecutive joints on consecutive lanes.
+__global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ ChunkedArgs a, int64_t c0,
+                                                     int64_t n_chars, float* __restrict__ local) {
+    extern __shared__ int4 sd[];   // layer descriptors of the block's characters
+    const int J = a.seg[0].J, nl = a.n_layers;
+    const int64_t n = n_chars * J;
+    const int4* lay = reinterpret_cast<const int4*>(a.layers);
+    for (int64_t e0 = (int64_t)blockIdx.x * 256; e0 < n; e0 += (int64_t)gridDim.x * 256) {
+        const int64_t cfirst = e0 / J;
+        const int nc = (int)((min(n, e0 + 256) - 1) / J - cfirst + 1);
+        __syncthreads();   // the previous block-tile's readers are done
+        for (int i = threadIdx.x; i < nc * nl; i += blockDim.x)
+            sd[i] = layer_desc(a, __ldg(lay + (c0 + cfirst) * nl + i));
+        __syncthreads();
+        const int64_t e = e0 + threadIdx.x;
+        if (e < n) {
+            const int rel = (int)(e - cfirst * J);
+            const int cl = rel / J;
+            const int j[1] = {rel - cl * J};
+            const int4* dp[1] = {sd + cl * nl};
+            const bool valid[1] = {true};
+            const int off[1] = {0};
+            stage1_elems<1, false>(a.keys, dp, j, valid, nl, J + (J & 1), local + e * 12, off);
+        }
+    }
+}
 
 // ================================================================== doubling (Alg. 2)
 // One CTA per group of C characters, one thread per (character, joint) in USER
@@ -1096,6 +1134,24 @@ cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
     ChunkedArgs args = a;
     void* params[] = {&args};
     return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(a.threads), params, (size_t)a.smem_bytes, st);
+}
+
+cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st) {
+    const int64_t n = n_chars * a.seg[0].J;
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;   // grid-stride, 8 CTAs of 256 per SM
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ChunkedArgs args = a;
+    void* params[] = {&args, &c0, &n_chars, &local};
+    const size_t smem = (size_t)(256 / a.seg[0].J + 2) * a.n_layers * sizeof(int4);
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<void*>(&stage1_kernel),
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaLaunchKernel(reinterpret_cast<void*>(&stage1_kernel), dim3((unsigned)blocks), dim3(256), params,
+                            smem, st);
 }
 
 cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,

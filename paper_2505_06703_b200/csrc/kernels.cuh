@@ -45,7 +45,7 @@ struct ChunkedArgs {
     // Stage-1 prologue (hs_animate, one segment): layers != nullptr replaces the
     // local-pose input
     const void* layers;        // device [n_chars][n_layers] hs_layer (16 B)
-    const float* keys;         // device [n_clips][n_keys][3][J] planar float4 keys
+    const float* keys;         // device [n_clips][n_keys] rows of 10 * Jp floats (planar keys)
     int32_t n_layers, n_keys, wrap;
     int32_t desc_off;          // smem byte offset of the layer-descriptor ring ([stages][C * n_layers] int4)
     float fps, duration;
@@ -58,6 +58,9 @@ struct ChunkedArgs {
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
+// Stage 1 alone (two-pass hs_animate): local poses of characters [c0, c0 + n_chars)
+// of a.layers into local ([n_chars][J][12]).
+cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st);
 cudaError_t prepare_chunked(int K, int64_t smem_bytes);   // sets the dynamic smem attribute
 int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes);
 

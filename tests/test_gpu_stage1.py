@@ -37,10 +37,10 @@ def hsgen_order(par):
     return oracle.kahn_order(par)
 
 
-def run(par, keys, fps, wrap, lay, ib=None, **create):
+def run(par, keys, fps, wrap, lay, ib=None, mode="auto", **create):
     sk = hs.Skeleton(par, ib, **create)
     cs = hs.ClipSet(sk, keys, fps, wrap)
-    g, s = hs.animate(sk, cs, lay)
+    g, s = hs.animate(sk, cs, lay, mode=mode)
     torch.cuda.synchronize()
     return g.cpu().numpy(), s.cpu().numpy()
 
@@ -48,13 +48,14 @@ def run(par, keys, fps, wrap, lay, ib=None, **create):
 @pytest.mark.parametrize("name,n_layers,wrap", [("hum64", 2, 1), ("chain256", 3, 0),
                                                 ("tree1024", 2, 1), ("hum32", 1, 1),
                                                 ("tree1024", 1, 0)])
-def test_animate_parity(name, n_layers, wrap):
+@pytest.mark.parametrize("mode", ["fused", "two_pass"])
+def test_animate_parity(name, n_layers, wrap, mode):
     par = hsgen.skeleton(name)
     J = len(par)
     keys = hsgen.clips(11, J, 4, 31)
     lay = hsgen.layers(11, 97, n_layers, 4, 1.6)     # times beyond the 1 s duration: wrap
     ib = hsgen.inv_bind(11, J)
-    g, s = run(par, keys, 30.0, wrap, lay, ib)
+    g, s = run(par, keys, 30.0, wrap, lay, ib, mode=mode)
     G, S = oracle.animate(par, keys, 30.0, wrap, lay, ib)
     eg, es = float(np.abs(g - G).max()), float(np.abs(s - S).max())
     tol = stage1_tol(levels(par))
@@ -127,3 +128,30 @@ def test_animate_errors():
     other = hs.Skeleton(hsgen.skeleton("hum64"))
     with pytest.raises(hs.HSError):
         hs.animate(other, cs, torch.zeros((4, 1, 4), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("name,n_layers", [("hum64", 3), ("chain256", 1), ("tree1024", 2)])
+def test_fused_and_two_pass_bitwise_equal(name, n_layers):
+    """Both Stage-1 placements compute the same local poses (same device code) and the
+    same scan, so they agree bit for bit; a 3-character workspace forces many batches."""
+    par = hsgen.skeleton(name)
+    J = len(par)
+    keys = hsgen.clips(9, J, 4, 17)
+    lay = hsgen.layers(10, 101, n_layers, 4, 2.0)
+    sk = hs.Skeleton(par, hsgen.inv_bind(11, J))
+    cs = hs.ClipSet(sk, keys, 24.0, 1)
+    g1, s1 = hs.animate(sk, cs, lay, mode="fused")
+    g2, s2 = hs.animate(sk, cs, lay, mode="two_pass", workspace_bytes=3 * J * 48)
+    g3, s3 = hs.animate(sk, cs, lay)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(s1, s2) and torch.equal(g1, g3) and torch.equal(s1, s3)
+
+
+def test_animate_opts_errors():
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    cs = hs.ClipSet(sk, hsgen.clips(1, 32, 1, 3), 10.0, 1)
+    lay = torch.zeros((4, 1, 4), dtype=torch.int32, device="cuda")
+    for bad in (dict(mode="fused", workspace_bytes=-1),):
+        with pytest.raises(hs.HSError) as e:
+            hs.animate(sk, cs, lay, **bad)
+        assert e.value.status == hs.HS_ERR_INVALID_ARG
