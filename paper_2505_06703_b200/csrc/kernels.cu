@@ -834,28 +834,45 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
 // stage1_elems: bitwise the same local poses), as a high-occupancy streaming kernel
 // that writes the local poses to a workspace for a plain chunked scan.  One thread
 // per (character, joint) element, consecutive joints on consecutive lanes.
+#ifndef HS_S1K_PER_THREAD
+#define HS_S1K_PER_THREAD 8
+#endif
+#ifndef HS_S1K_UNROLL
+#define HS_S1K_UNROLL 1
+#endif
+constexpr int kStage1PerThread = HS_S1K_PER_THREAD;   // elements per thread between descriptor refreshes
+constexpr int kStage1Unroll = HS_S1K_UNROLL;
+
 __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ ChunkedArgs a, int64_t c0,
                                                      int64_t n_chars, float* __restrict__ local) {
     extern __shared__ int4 sd[];   // layer descriptors of the block's characters
     const int J = a.seg[0].J, nl = a.n_layers;
     const int64_t n = n_chars * J;
     const int4* lay = reinterpret_cast<const int4*>(a.layers);
-    for (int64_t e0 = (int64_t)blockIdx.x * 256; e0 < n; e0 += (int64_t)gridDim.x * 256) {
+    constexpr int kTile = 256 * kStage1PerThread;   // elements per block iteration
+    for (int64_t e0 = (int64_t)blockIdx.x * kTile; e0 < n; e0 += (int64_t)gridDim.x * kTile) {
         const int64_t cfirst = e0 / J;
-        const int nc = (int)((min(n, e0 + 256) - 1) / J - cfirst + 1);
+        const int nc = (int)((min(n, e0 + kTile) - 1) / J - cfirst + 1);
         __syncthreads();   // the previous block-tile's readers are done
         for (int i = threadIdx.x; i < nc * nl; i += blockDim.x)
             sd[i] = layer_desc(a, __ldg(lay + (c0 + cfirst) * nl + i));
         __syncthreads();
-        const int64_t e = e0 + threadIdx.x;
-        if (e < n) {
-            const int rel = (int)(e - cfirst * J);
-            const int cl = rel / J;
-            const int j[1] = {rel - cl * J};
+        // element rel = cl * J + j of the block-tile, advanced by 256 without division
+        int rel = (int)(e0 - cfirst * J) + threadIdx.x;
+        int cl = rel / J, jj = rel - cl * J;
+        const int sc = 256 / J, sj = 256 - sc * J;
+#pragma unroll kStage1Unroll
+        for (int q = 0; q < kStage1PerThread; ++q) {
+            const int64_t e = e0 + q * 256 + threadIdx.x;
+            if (e >= n) break;
+            const int j[1] = {jj};
             const int4* dp[1] = {sd + cl * nl};
             const bool valid[1] = {true};
             const int off[1] = {0};
             stage1_elems<1, false>(a.keys, dp, j, valid, nl, J + (J & 1), local + e * 12, off);
+            cl += sc;
+            jj += sj;
+            if (jj >= J) { jj -= J; ++cl; }
         }
     }
 }
@@ -1138,13 +1155,13 @@ cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {
 
 cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st) {
     const int64_t n = n_chars * a.seg[0].J;
-    int64_t blocks = (n + 255) / 256;
+    int64_t blocks = (n + 256 * kStage1PerThread - 1) / (256 * kStage1PerThread);
     const int64_t cap = (int64_t)sm_count() * 8;   // grid-stride, 8 CTAs of 256 per SM
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ChunkedArgs args = a;
     void* params[] = {&args, &c0, &n_chars, &local};
-    const size_t smem = (size_t)(256 / a.seg[0].J + 2) * a.n_layers * sizeof(int4);
+    const size_t smem = (size_t)(256 * kStage1PerThread / a.seg[0].J + 2) * a.n_layers * sizeof(int4);
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<void*>(&stage1_kernel),
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Profiling target: a few hs_animate launches on one skeleton (default tree1024, 50k
-characters, 2 layers) — small enough to run under ncu --set full."""
+characters, 2 layers) — small enough to run under ncu --set full.  HS_ANIMATE_MODE =
+fused (default) | two_pass."""
 import os
 import sys
 
@@ -21,7 +22,8 @@ lay = hsgen.layers(5, n, 2, 8, 1.5, type_=2)
 layers = torch.from_numpy(lay.view(np.int32).reshape(n, 2, 4)).cuda()
 g = torch.empty((n, J, 3, 4), device="cuda")
 s = torch.empty_like(g)
+mode = os.environ.get("HS_ANIMATE_MODE", "fused")
 for _ in range(4):
-    hs.animate(sk, cs, layers, g, s)
+    hs.animate(sk, cs, layers, g, s, mode=mode)
 torch.cuda.synchronize()
 print("ok", name, n)

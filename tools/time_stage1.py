@@ -23,7 +23,7 @@ for name in ["hum64", "chain256", "tree1024"]:
     layers = torch.from_numpy(lay.view(np.int32).reshape(n, 2, 4)).cuda()
     g = torch.empty((n, J, 3, 4), device="cuda")
     s = torch.empty_like(g)
-    for mode, ws in (("fused", 0), ("two_pass", 0), ("two_pass_256M", 256 << 20)):
+    for mode, ws in (("fused", 0), ("two_pass", 0), ("two_pass_256M", 256 << 20), ("two_pass_48M", 48 << 20)):
         m = mode[:8]
         for _ in range(3):
             hs.animate(sk, cs, layers, g, s, mode=m, workspace_bytes=ws)
@@ -37,5 +37,5 @@ for name in ["hum64", "chain256", "tree1024"]:
             ts.append(e0.elapsed_time(e1))
         res[f"{name} {mode}"] = round(statistics.median(ts), 3)
 print(os.environ.get("HS_LIB", "default"), res, flush=True)
-for mode in ("fused", "two_pass", "two_pass_256M"):
+for mode in ("fused", "two_pass", "two_pass_256M", "two_pass_48M"):
     print(mode, "total", round(sum(v for k, v in res.items() if k.endswith(mode)), 3), flush=True)
