@@ -573,7 +573,7 @@ def run_e2e(work, args, hs, torch, dist, world):
     return {"value": joints * args.e2e_steps / dt, "unit": "joints/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "sample": f"1/{args.e2e_frac} of each type's characters per GPU, pinned host buffers, "
-                      f"hs_scan_host (256 MiB batches, 3 streams)",
+                      f"hs_scan_host (batches ramping from 8 MB to 256 MiB, 3 streams)",
             "matches_device_path": same}
 
 

@@ -921,10 +921,12 @@ hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_lo
     const int64_t per_char = (int64_t)sk->plan.n * 48;
     const int64_t batch = pl->batch_bytes / per_char;
     if (batch < 1) return fail(HS_ERR_INVALID_ARG, "pipeline batch smaller than one character");
-    int64_t b = 0;
-    for (int64_t c0 = 0; c0 < n_chars; c0 += batch, ++b) {
+    // batches ramp up geometrically from ~8 MB: the copy engine that reads back (the
+    // larger direction) idles only for the first, small H2D instead of a full batch
+    int64_t b = 0, cur = std::max<int64_t>(1, std::min<int64_t>(batch, ((int64_t)8 << 20) / per_char));
+    for (int64_t c0 = 0, nb = 0; c0 < n_chars; c0 += nb, ++b, cur = std::min(batch, 2 * cur)) {
         const int i = (int)(b % 3);
-        const int64_t nb = std::min(batch, n_chars - c0);
+        nb = std::min(cur, n_chars - c0);
         const size_t bytes = (size_t)(nb * per_char);
         const int64_t foff = c0 * sk->plan.n * 12;
         cudaError_t e = cudaMemcpyAsync(pl->d_in[i], h_local + foff, bytes, cudaMemcpyHostToDevice, pl->st[i]);
