@@ -730,7 +730,34 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                     const int off = (int)(m[s] & 0xffff);
                     float l[12];
                     ld3(L + off * 12, l);
-                    if (src == kSrcPrev) {
+                    if (RUNS) {
+                        // the parent's global pose as the left operand, then ONE compose
+                        // for every lane (lanes of a runs program mix sources at the same
+                        // slot; divergent compose paths cost tree1024 4 %): the previous
+                        // joint of the chunk, the identity at a root (I (x) l == l
+                        // exactly for finite l), an anchor's final, or a run lane's
+                        // P[run anchor] (x) exclusive scan
+                        float left[12];
+                        if (src == kSrcPrev) {
+    #pragma unroll
+                            for (int e = 0; e < 12; ++e) left[e] = acc[e];
+                        } else if (src == kSrcRoot) {
+    #pragma unroll
+                            for (int e = 0; e < 12; ++e) left[e] = (e == 0 || e == 5 || e == 10) ? 1.0f : 0.0f;
+                        } else if (src == kSrcRun) {
+                            if (run_anchor >= 0) {
+                                float pa[12];
+                                ld3(P + run_anchor * 12, pa);
+                                compose(pa, excl, left);
+                            } else {
+    #pragma unroll
+                                for (int e = 0; e < 12; ++e) left[e] = excl[e];
+                            }
+                        } else {
+                            ld3(P + src * 12, left);
+                        }
+                        compose(left, l, acc);
+                    } else if (src == kSrcPrev) {
                         float tmp[12];
                         compose(acc, l, tmp);
     #pragma unroll
@@ -738,19 +765,6 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                     } else if (src == kSrcRoot) {
     #pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = l[e];
-                    } else if (RUNS && src == kSrcRun) {
-                        // first joint of a run lane: parent = previous lane's tail, whose
-                        // global pose is P[run anchor] (x) (exclusive scan of the run)
-                        float base[12];
-                        if (run_anchor >= 0) {
-                            float pa[12];
-                            ld3(P + run_anchor * 12, pa);
-                            compose(pa, excl, base);
-                        } else {
-    #pragma unroll
-                            for (int e = 0; e < 12; ++e) base[e] = excl[e];
-                        }
-                        compose(base, l, acc);
                     } else {
                         float pa[12];
                         ld3(P + src * 12, pa);
