@@ -217,8 +217,7 @@ typedef struct {
 } hs_layer;
 
 /* layers: device [n_chars][n_layers] hs_layer (n_layers 1..8), 16-byte aligned; outputs
- * as hs_scan.  Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise).  Same as
- * hs_animate_ex with opts == NULL. */
+ * as hs_scan.  Same as hs_animate_ex with opts == NULL (two-pass: any skeleton). */
 hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
                      int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream);
 
@@ -226,8 +225,10 @@ hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* la
  * kernel (96 B/joint of HBM traffic).  TWO_PASS: a streaming Stage-1 kernel writes the
  * local poses of a batch of characters to a workspace (stream-ordered cudaMallocAsync,
  * workspace_bytes, default 1 GiB) and the plain scan reads them back (192 B/joint),
- * which hides the key-load latency better.  AUTO = TWO_PASS (measured faster on B200,
- * DESIGN.md §5.1b).  Both produce bitwise the same local poses, hence the same output. */
+ * which hides the key-load latency better, and works for multi-CTA skeletons too
+ * (FUSED needs a single-CTA skeleton: HS_ERR_UNSUPPORTED otherwise).  AUTO = TWO_PASS
+ * (measured faster on B200).  Both produce bitwise the same local
+ * poses, hence the same output. */
 typedef enum { HS_ANIMATE_AUTO = 0, HS_ANIMATE_FUSED = 1, HS_ANIMATE_TWO_PASS = 2 } hs_animate_mode;
 typedef struct {
     int32_t mode;             /* hs_animate_mode                                        */

@@ -691,11 +691,12 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
     int dev = -1;
     cudaGetDevice(&dev);
     if (dev != sk->device || dev != cs->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
-    if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "hs_animate needs a single-CTA skeleton");
     const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    if (mode == HS_ANIMATE_FUSED)
+    if (mode == HS_ANIMATE_FUSED) {
+        if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "the fused Stage 1 needs a single-CTA skeleton");
         return scan_impl(sk, nullptr, n_chars, global_out, skin_out, st, HS_ALGO_CHUNKED, -1, 0, cs, layers,
                          n_layers);
+    }
     // two-pass (and AUTO, measured faster on B200: DESIGN.md §5.1b): Stage 1 streams the
     // local poses of a batch of characters into a stream-ordered workspace, then the
     // plain chunked scan reads them back
@@ -705,9 +706,10 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
     float* ws = nullptr;
     cudaError_t e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(batch * per_char), st);
     if (e != cudaSuccess) return cuda_fail(e, "Stage-1 workspace");
-    hs::ChunkedArgs s1{};
-    const ChunkItem one{sk, nullptr, n_chars, global_out, skin_out};
-    chunked_layout(&one, 1, sk->stages, sk->sbufs, s1);
+    hs::ChunkedArgs s1{};   // the Stage-1 kernel reads only seg[0].J and the Stage-1 fields
+    s1.nseg = 1;
+    s1.seg[0].J = J;
+    s1.seg[0].n_chars = n_chars;
     s1.layers = layers;
     s1.keys = cs->d_keys;
     s1.n_layers = n_layers;
@@ -720,7 +722,7 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
         const int64_t nb = std::min(batch, n_chars - c0);
         if ((e = hs::launch_stage1(s1, c0, nb, ws, st)) != cudaSuccess) { r = cuda_fail(e, "Stage-1 launch"); break; }
         r = scan_impl(sk, ws, nb, global_out + c0 * J * 12, skin_out ? skin_out + c0 * J * 12 : nullptr, st,
-                      HS_ALGO_CHUNKED, -1, 0);
+                      HS_ALGO_AUTO, -1, 0);   // single-CTA or multi-CTA path
     }
     cudaFreeAsync(ws, st);
     return r;

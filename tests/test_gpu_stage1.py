@@ -155,3 +155,24 @@ def test_animate_opts_errors():
         with pytest.raises(hs.HSError) as e:
             hs.animate(sk, cs, lay, **bad)
         assert e.value.status == hs.HS_ERR_INVALID_ARG
+
+
+def test_two_pass_on_multi_cta_skeleton():
+    """The two-pass placement feeds any skeleton, including the multi-CTA path (the
+    fused prologue needs one CTA and says so)."""
+    par = hsgen.random_tree(21, 3000, 80)
+    J = len(par)
+    keys = hsgen.clips(22, J, 3, 9)
+    lay = hsgen.layers(23, 5, 2, 3, 1.0)
+    ib = hsgen.inv_bind(24, J)
+    sk = hs.Skeleton(par, ib)
+    assert sk.query("path") == 3   # HS_ALGO_SPLIT
+    cs = hs.ClipSet(sk, keys, 30.0, 1)
+    g, s = hs.animate(sk, cs, lay)
+    torch.cuda.synchronize()
+    G, S = oracle.animate(par, keys, 30.0, 1, lay, ib)
+    tol = stage1_tol(levels(par))
+    assert np.abs(g.cpu().numpy() - G).max() <= tol and np.abs(s.cpu().numpy() - S).max() <= tol
+    with pytest.raises(hs.HSError) as e:
+        hs.animate(sk, cs, lay, mode="fused")
+    assert e.value.status == hs.HS_ERR_UNSUPPORTED
