@@ -414,7 +414,9 @@ def run_ours(args):
                    "hbm_gbs": joints_total * bpj * K / (ms / 1e3) / 1e9 / world,
                    "hbm_gbs_note": "per GPU, algorithmic bytes / step time",
                    "hbm_frac_of_8tbs": joints_total * bpj * K / (ms / 1e3) / 8e12 / world,
-                   "l2": "inputs larger than L2 (no flush)", "algo": args.algo,
+                   "l2": ("inputs larger than L2 (no flush)" if joints_total * 48 / world > 126e6 else
+                          "L2-resident working set (launch-bound config, reported for parity only)"),
+                   "algo": args.algo,
                    "launch": "batch (one hs_scan_batch per step)" if batch else "one launch per type",
                    "per_launch_ms": {name: per_launch_ms[li] for li, (name, _) in enumerate(launches)},
                    "chunk": work[dom]["sk"].query("chunk"),
