@@ -118,7 +118,10 @@ typedef enum {
                                recursive anchor scan, phase-3 kernel.  Available when the
                                skeleton does not fit one CTA or was created with force_split  */
     HS_ALGO_GATEAU = 4,     /* Alg. 1: thread per joint walks every ancestor   */
-    HS_ALGO_LEAF = 5        /* KIYA leaf walk: thread per leaf fills its root path */
+    HS_ALGO_LEAF = 5,       /* KIYA leaf walk: thread per leaf fills its root path */
+    HS_ALGO_BLOCKED = 6     /* Alg. 3 literally: 64-joint blocks, in-block
+                               doubling clamped to the block, then the MaxParentOutBlock walk;
+                               n_joints <= 1024                                                */
 } hs_algo;
 
 typedef struct {

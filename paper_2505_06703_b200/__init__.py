@@ -32,7 +32,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
 HS_OK, HS_ERR_INVALID_ARG, HS_ERR_EMPTY, HS_ERR_OUT_OF_RANGE, HS_ERR_CYCLE, HS_ERR_CUDA, \
     HS_ERR_OOM, HS_ERR_WRONG_DEVICE, HS_ERR_UNSUPPORTED = range(9)
 # hs_algo
-ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf": 5}
+ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf": 5, "blocked": 6}
 # hs_query
 QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "tile_chars": 5,
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,

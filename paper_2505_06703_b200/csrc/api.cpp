@@ -68,6 +68,9 @@ struct hs_skeleton {
     float* d_ib = nullptr;
     int32_t* d_parents = nullptr;
     int32_t* d_lift = nullptr;
+    int32_t* d_blk_lift = nullptr;    // Alg. 3 comparison kernel: in-block lift [RB][n]
+    int32_t* d_blk_mpob = nullptr;    //   and MaxParentOutBlock [n], user labels
+    int32_t blk_rounds = 0;
     uint64_t* d_meta = nullptr;
     int32_t* d_p1len = nullptr;
     int32_t* d_round_off = nullptr;
@@ -110,6 +113,8 @@ void free_skeleton(hs_skeleton* sk) {
     cudaFree(sk->d_ib);
     cudaFree(sk->d_parents);
     cudaFree(sk->d_lift);
+    cudaFree(sk->d_blk_lift);
+    cudaFree(sk->d_blk_mpob);
     cudaFree(sk->d_meta);
     cudaFree(sk->d_p1len);
     cudaFree(sk->d_round_off);
@@ -205,6 +210,15 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
         (e = upload(&sk->d_lift, P.lift.data(), P.lift.size())) != cudaSuccess) {
         free_skeleton(sk);
         return cuda_fail(e, "upload skeleton tables");
+    }
+    {   // the paper's 64-joint blocks for the Alg. 3 comparison kernel
+        std::vector<int32_t> lb, mp;
+        hs::blocked_tables(P, 64, lb, mp, sk->blk_rounds);
+        if ((e = upload(&sk->d_blk_lift, lb.data(), lb.size())) != cudaSuccess ||
+            (e = upload(&sk->d_blk_mpob, mp.data(), mp.size())) != cudaSuccess) {
+            free_skeleton(sk);
+            return cuda_fail(e, "upload block tables");
+        }
     }
     // root -> leaf paths for the KIYA leaf kernel (comparison algorithm)
     {
@@ -413,6 +427,11 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             if (J > 1024) return fail(HS_ERR_UNSUPPORTED, "doubling kernel needs n_joints <= 1024");
             e = hs::launch_doubling(local, gout, sout, sk->d_ib, sk->d_lift, J, sk->plan.R, max_rounds,
                                     n_chars, st);
+            break;
+        case HS_ALGO_BLOCKED:
+            if (J > 1024) return fail(HS_ERR_UNSUPPORTED, "blocked kernel needs n_joints <= 1024");
+            e = hs::launch_blocked(local, gout, sout, sk->d_ib, sk->d_blk_lift, sk->d_blk_mpob, J, sk->blk_rounds,
+                                   n_chars, st);
             break;
         case HS_ALGO_GATEAU:
             e = hs::launch_gateau(local, gout, sout, sk->d_ib, sk->d_parents, J, n_chars, st);

@@ -891,6 +891,68 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
     }
 }
 
+// ================================================================== blocked (Alg. 3)
+// The paper's Alg. 3 literally, a comparison kernel: one thread
+// per (character, joint) in USER order, B = 64-joint blocks over the internal
+// topological order.  Stage A: pointer jumping along in-block parents only (ceil
+// log2 B rounds on a ping-pong snapshot; reading R8 clamps the hops to the block).
+// Stage B: walk MaxParentOutBlock, G = A[mpob] (x) G, on the stage-A snapshot
+// (reading R9 walks the variable).  "6 + n/64" composes per thread.
+__global__ void __launch_bounds__(1024) blocked_kernel(const float* __restrict__ local,
+                                                       float* __restrict__ gout,
+                                                       float* __restrict__ sout,
+                                                       const float* __restrict__ ib,
+                                                       const int32_t* __restrict__ lb,
+                                                       const int32_t* __restrict__ mpob, int J, int C,
+                                                       int RB, int64_t n_chars) {
+    extern __shared__ __align__(16) float sm[];
+    const int F = C * J;
+    float* buf0 = sm;
+    float* buf1 = sm + F * 12;
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int nc = (int)min((int64_t)C, n_chars - c0);
+    const int f = threadIdx.x;
+    const int cl = f / J, u = f - cl * J;
+    const bool valid = f < F && cl < nc;
+    float v[12];
+    if (valid) ldg3(local + (c0 * J + f) * 12, v);
+    if (f < F) st3(buf0 + f * 12, v);
+    __syncthreads();
+    float* cur = buf0;
+    float* nxt = buf1;
+    for (int r = 0; r < RB; ++r) {   // stage A
+        if (f < F) {
+            const int anc = __ldg(lb + (int64_t)r * J + u);
+            if (anc >= 0) {
+                float x[12], y[12];
+                ld3(cur + (cl * J + anc) * 12, x);
+                compose(x, v, y);
+#pragma unroll
+                for (int e = 0; e < 12; ++e) v[e] = y[e];
+            }
+            st3(nxt + f * 12, v);
+        }
+        __syncthreads();
+        float* tmp = cur; cur = nxt; nxt = tmp;
+    }
+    if (valid) {   // stage B on the stage-A snapshot `cur`
+        for (int m = __ldg(mpob + u); m >= 0; m = __ldg(mpob + m)) {
+            float x[12], y[12];
+            ld3(cur + (cl * J + m) * 12, x);
+            compose(x, v, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) v[e] = y[e];
+        }
+        st3(gout + (c0 * J + f) * 12, v);
+        if (sout) {
+            float b[12], s[12];
+            ldg3(ib + (int64_t)u * 12, b);
+            compose(v, b, s);
+            st3(sout + (c0 * J + f) * 12, s);
+        }
+    }
+}
+
 // ================================================================== doubling (Alg. 2)
 // One CTA per group of C characters, one thread per (character, joint) in USER
 // order (pointer jumping is order-agnostic).  Round r: V[j] <- V[anc_r(j)] (x) V[j]
@@ -1201,6 +1263,22 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
     const int64_t blocks = (n_chars + C - 1) / C;
     doubling_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lift, J, C, rounds,
                                                            n_chars);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blocked(const float* local, float* gout, float* sout, const float* ib, const int32_t* lb,
+                           const int32_t* mpob, int32_t J, int32_t RB, int64_t n_chars, cudaStream_t st) {
+    if (J > 1024) return cudaErrorInvalidValue;
+    int C = 1024 / J;
+    if (C < 1) C = 1;
+    const size_t smem = (size_t)2 * C * J * 48;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 1024 * 48);
+        attr = true;
+    }
+    const int64_t blocks = (n_chars + C - 1) / C;
+    blocked_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lb, mpob, J, C, RB, n_chars);
     return cudaGetLastError();
 }
 

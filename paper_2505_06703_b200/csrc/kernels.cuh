@@ -69,6 +69,11 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
                             const int32_t* lift, int32_t J, int32_t R, int32_t rounds,
                             int64_t n_chars, cudaStream_t st);
 
+// Alg. 3 literally: 64-joint blocks, clamped in-block doubling, then
+// the MaxParentOutBlock walk (comparison kernel).
+cudaError_t launch_blocked(const float* local, float* gout, float* sout, const float* ib, const int32_t* lb,
+                           const int32_t* mpob, int32_t J, int32_t RB, int64_t n_chars, cudaStream_t st);
+
 // Alg. 1: thread per joint walks all ancestors.
 cudaError_t launch_gateau(const float* local, float* gout, float* sout, const float* ib,
                           const int32_t* parents, int32_t J, int64_t n_chars, cudaStream_t st);

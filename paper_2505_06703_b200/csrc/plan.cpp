@@ -555,6 +555,26 @@ void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vec
     }
 }
 
+void blocked_tables(const Plan& p, int B, std::vector<int32_t>& lb, std::vector<int32_t>& mpob, int& RB) {
+    RB = 0;
+    while ((1 << RB) < B) ++RB;
+    const int32_t n = p.n;
+    std::vector<int32_t> block_of, mi;
+    block_layout(p, B, block_of, mi);
+    lb.assign((size_t)std::max(RB, 1) * n, -1);
+    mpob.assign(n, -1);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t q = p.ipar[i];
+        lb[p.order[i]] = (q >= 0 && q / B == i / B) ? p.order[q] : -1;
+        mpob[p.order[i]] = mi[i] >= 0 ? p.order[mi[i]] : -1;
+    }
+    for (int r = 1; r < RB; ++r)
+        for (int32_t u = 0; u < n; ++u) {
+            const int32_t a = lb[(size_t)(r - 1) * n + u];
+            lb[(size_t)r * n + u] = a >= 0 ? lb[(size_t)(r - 1) * n + a] : -1;
+        }
+}
+
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs) {
     const int64_t tileb = (int64_t)tp.F * 48, pb = (tp.pingpong ? 2LL : 1LL) * tp.nslots * 48;
     const int64_t tables = ((int64_t)(tp.R2 + 1) * 4 + (int64_t)tp.rounds.size() * 4 + 15) / 16 * 16;

@@ -97,6 +97,12 @@ SplitProgram build_split_program(const Plan& p, int K);
 // The paper's block layout for block size B over INTERNAL positions (exports).
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);
 
+// Tables of the literal Alg. 3 comparison kernel, in USER labels:
+// lb[r][u] = 2^r-th ancestor of u along in-block parents (stage A, clamped to u's
+// block: DESIGN.md reading R8), mpob[u] = MaxParentOutBlock(u) (stage B walk,
+// reading R9); RB = ceil(log2 B) stage-A rounds.
+void blocked_tables(const Plan& p, int B, std::vector<int32_t>& lb, std::vector<int32_t>& mpob, int& RB);
+
 // Shared-memory bytes of the chunked kernel for a tile program and stage counts
 // (tiles, skin buffers, anchor buffers, and the phase-2 tables staged in smem).
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs);

@@ -87,7 +87,7 @@ def test_exact_family_bitwise(name, create):
     assert np.array_equal(g, G) and np.array_equal(s, S)
 
 
-@pytest.mark.parametrize("algo", ["doubling", "gateau", "leaf"])
+@pytest.mark.parametrize("algo", ["doubling", "gateau", "leaf", "blocked"])
 @pytest.mark.parametrize("name", ["hum64", "chain256", "tree1024"])
 def test_exact_family_comparison_algorithms(algo, name):
     par = hsgen.skeleton(name)
@@ -170,7 +170,7 @@ def test_dyadic_translation_chain_bitwise():
     assert np.array_equal(g[..., 3], np.cumsum(t, axis=1))
 
 
-@pytest.mark.parametrize("algo", ["auto", "doubling", "gateau", "leaf"])
+@pytest.mark.parametrize("algo", ["auto", "doubling", "gateau", "leaf", "blocked"])
 def test_single_joint_and_all_roots(algo):
     for par in ([-1], [-1] * 10):
         local = hsgen.local_poses(40, len(par), 33)

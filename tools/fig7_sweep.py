@@ -11,7 +11,8 @@ bone levels > 30, the performance of our solution is significantly better"
 
 Here, on one B200, every algorithm runs through the same C ABI (hs_scan_ex) on the
 same seeded crowd: `chunked` (this build's kernel), `doubling` (Alg. 2 verbatim),
-`gateau` (Alg. 1), `leaf` (KIYA).  Skeletons: SPEC random_tree with
+`blocked` (Alg. 3 literally: 64-joint blocks, clamped in-block doubling, then the
+MaxParentOutBlock walk), `gateau` (Alg. 1), `leaf` (KIYA).  Skeletons: SPEC random_tree with
 300 joints and max level = depth.  Each cell is checked against the fp64 oracle on
 sampled characters, then timed with CUDA events (median of 20 after 5 warm-ups).
 """
@@ -31,7 +32,7 @@ import numpy as np  # noqa: E402
 import hsgen  # noqa: E402
 import oracle  # noqa: E402
 
-ALGOS = ["chunked", "doubling", "gateau", "leaf"]
+ALGOS = ["chunked", "doubling", "blocked", "gateau", "leaf"]
 
 
 def main(argv=None):
@@ -40,7 +41,7 @@ def main(argv=None):
     ap.add_argument("--joints", type=int, default=300)
     ap.add_argument("--depths", default="15,30,45,60,90,120")
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_fig7_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01d_fig7_sweep.json"))
     args = ap.parse_args(argv)
 
     import torch
@@ -98,8 +99,8 @@ def main(argv=None):
         f.write("# Fig. 7-shaped depth sweep on one B200 (ms per frame; lower is better)\n\n")
         f.write(f"{args.chars} characters x {args.joints} joints (SPEC random_tree, max level = depth), "
                 "3x4 fp32 poses, G and S written; oracle parity checked per cell.\n\n")
-        f.write("| depth | mean level | chunked (this build) | Alg. 2 doubling | Gateau (Alg. 1) | KIYA leaf |\n")
-        f.write("|---|---|---|---|---|---|\n")
+        f.write("| depth | mean level | chunked (this build) | Alg. 2 doubling | Alg. 3 blocked | Gateau (Alg. 1) | KIYA leaf |\n")
+        f.write("|---|---|---|---|---|---|---|\n")
         for r in rows:
             f.write(f"| {r['depth']} | {r['mean_level']:.1f} | " +
                     " | ".join(f"{r[a]['ms']:.3f}" for a in ALGOS) + " |\n")
