@@ -38,7 +38,7 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--types", type=int, default=8)
     ap.add_argument("--chars", default="64,512,4096,32768")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_next3_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01d_next3_sweep.json"))
     args = ap.parse_args(argv)
     # 8 skeleton types: the templates plus SPEC random trees of 100-1000 joints
     pars = [hsgen.skeleton("hum32"), hsgen.skeleton("hum64"), hsgen.skeleton("chain256"),
