@@ -431,7 +431,10 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": dom_bytes, "peak_source": peak_src,
                      "traffic_source": traffic_src},
         "clocks": sampler.summary(),
-        "gpu_launches": len(launches) * K,
+        # our kernels per step x K: one per hs_scan / hs_scan_skin / batch; the two-pass
+        # hs_animate launches a Stage-1 kernel and a scan per 1 GiB workspace batch
+        "gpu_launches": K * (sum(2 * -(-w["n"] // max(1, (1 << 30) // (w["J"] * 48))) for w in work)
+                             if args.stage1 else len(launches)),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": check,
