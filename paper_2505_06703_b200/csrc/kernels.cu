@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             // phase 1: in-chunk fold, publish anchors (buffer 0 of P)
             float acc[12];
             if (p1 > 0) {
-    #pragma unroll
+#pragma unroll
                 for (int s = 0; s < K; ++s) {
                     if (s < p1) {
                         const int off = (int)(m[s] & 0xffff);
@@ -621,10 +621,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         if (src == kSrcPrev) {
                             float tmp[12];
                             compose(acc, l, tmp);
-    #pragma unroll
+#pragma unroll
                             for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
                         } else {
-    #pragma unroll
+#pragma unroll
                             for (int e = 0; e < 12; ++e) acc[e] = l[e];
                         }
                         if (own >= 0) st3(P + own * 12, acc);
@@ -644,19 +644,19 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             if (RUNS && warp_maxrb > 0) {   // warp-uniform: this warp holds run lanes
                 for (int d = 1; d <= warp_maxrb; d <<= 1) {
                     float u[12];
-    #pragma unroll
+#pragma unroll
                     for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
                     if (run_back >= d) {
                         float w[12];
                         compose(u, acc, w);
-    #pragma unroll
+#pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = w[e];
                     }
                 }
-    #pragma unroll
+#pragma unroll
                 for (int e = 0; e < 12; ++e) excl[e] = __shfl_up_sync(0xffffffffu, acc[e], 1);
                 if (run_back > 0) {
-    #pragma unroll
+#pragma unroll
                     for (int s = 0; s < K; ++s) {
                         const int own = (int)(int16_t)(m[s] >> 48);
                         if (own >= 0) {
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 } else {
                     float z[4][12];
                     int dst[4];
-    #pragma unroll
+#pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int e = eb + t + q * NC;
                         dst[q] = -1;
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         }
                     }
                     bar_consumers(NC);
-    #pragma unroll
+#pragma unroll
                     for (int q = 0; q < 4; ++q)
                         if (dst[q] >= 0) st3(P + dst[q] * 12, z[q]);
                     bar_consumers(NC);
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             prof_mark(3);
             {
                 float acc[12];
-    #pragma unroll
+#pragma unroll
                 for (int s = 0; s < K; ++s) {
                     const int src = (int)(int16_t)(m[s] >> 32);
                     if (src == kSrcNone) continue;
@@ -739,10 +739,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         // P[run anchor] (x) exclusive scan
                         float left[12];
                         if (src == kSrcPrev) {
-    #pragma unroll
+#pragma unroll
                             for (int e = 0; e < 12; ++e) left[e] = acc[e];
                         } else if (src == kSrcRoot) {
-    #pragma unroll
+#pragma unroll
                             for (int e = 0; e < 12; ++e) left[e] = (e == 0 || e == 5 || e == 10) ? 1.0f : 0.0f;
                         } else if (src == kSrcRun) {
                             if (run_anchor >= 0) {
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                                 ld3(P + run_anchor * 12, pa);
                                 compose(pa, excl, left);
                             } else {
-    #pragma unroll
+#pragma unroll
                                 for (int e = 0; e < 12; ++e) left[e] = excl[e];
                             }
                         } else {
@@ -760,10 +760,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                     } else if (src == kSrcPrev) {
                         float tmp[12];
                         compose(acc, l, tmp);
-    #pragma unroll
+#pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
                     } else if (src == kSrcRoot) {
-    #pragma unroll
+#pragma unroll
                         for (int e = 0; e < 12; ++e) acc[e] = l[e];
                     } else {
                         float pa[12];
