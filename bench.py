@@ -362,8 +362,9 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms_rank = start.elapsed_time(stop)
-    per_launch_ms = [statistics.mean(events[li][0][k].elapsed_time(events[li][1][k]) for k in range(K))
-                     for li in range(len(launches))]
+    launch_ms = [[events[li][0][k].elapsed_time(events[li][1][k]) for k in range(K)]
+                 for li in range(len(launches))]
+    per_launch_ms = [statistics.mean(x) for x in launch_ms]
     ms, joints_total = reduce_over_ranks(ms_rank, joints_rank, world, dev)
     value = joints_total * K / (ms / 1e3)
 
@@ -419,6 +420,9 @@ def run_ours(args):
                    "algo": args.algo,
                    "launch": "batch (one hs_scan_batch per step)" if batch else "one launch per type",
                    "per_launch_ms": {name: per_launch_ms[li] for li, (name, _) in enumerate(launches)},
+                   "per_launch_ms_median": {name: statistics.median(launch_ms[li])
+                                            for li, (name, _) in enumerate(launches)},
+                   "per_launch_ms_min": {name: min(launch_ms[li]) for li, (name, _) in enumerate(launches)},
                    "chunk": work[dom]["sk"].query("chunk"),
                    "tile_chars": work[dom]["sk"].query("tile_chars"),
                    "stages": {w["name"]: w["sk"].query("stages") for w in work},
