@@ -497,7 +497,7 @@ def run_e2e_stage1(work, args, hs, torch, dist, world):
     stream = torch.cuda.current_stream()
     slices, h2d, d2h, joints = [], 0, 0, 0
     for w in work:
-        m = max(1, w["n"] // args.e2e_frac) if w["n"] else 0
+        m = max(1, w["n"] // e2e_fraction(args, world)) if w["n"] else 0
         if m == 0:
             continue
         hl = w["layers"][:m].cpu().pin_memory()
@@ -531,8 +531,15 @@ def run_e2e_stage1(work, args, hs, torch, dist, world):
         joints *= world
     return {"value": joints * args.e2e_steps / dt, "unit": "joints/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "sample": f"1/{args.e2e_frac} of each type's characters per GPU: layers H2D (pinned), "
+            "sample": f"1/{e2e_fraction(args, world)} of each type's characters per GPU: layers H2D (pinned), "
                       "hs_animate, global + skin D2H (pinned)"}
+
+
+def e2e_fraction(args, world):
+    """Sample fraction of each rank's crowd for the e2e leg: pinned host buffers are
+    ~8 GB per rank at 1/8, so under N ranks the fraction shrinks by N (host memory
+    is shared by all ranks of the node; each GPU keeps its own PCIe link busy)."""
+    return args.e2e_frac * max(1, world)
 
 
 def run_e2e(work, args, hs, torch, dist, world):
@@ -547,7 +554,7 @@ def run_e2e(work, args, hs, torch, dist, world):
     h2d = d2h = 0
     joints = 0
     for w in work:
-        m = max(1, w["n"] // args.e2e_frac) if w["n"] else 0
+        m = max(1, w["n"] // e2e_fraction(args, world)) if w["n"] else 0
         if m == 0:
             continue
         hl = torch.empty((m, w["J"], 3, 4), dtype=torch.float32, pin_memory=True)
@@ -581,7 +588,7 @@ def run_e2e(work, args, hs, torch, dist, world):
     pl.close()
     return {"value": joints * args.e2e_steps / dt, "unit": "joints/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "sample": f"1/{args.e2e_frac} of each type's characters per GPU, pinned host buffers, "
+            "sample": f"1/{e2e_fraction(args, world)} of each type's characters per GPU, pinned host buffers, "
                       f"hs_scan_host (batches ramping from 8 MB to 256 MiB, 3 streams)",
             "matches_device_path": same}
 
