@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <stdexcept>
 
@@ -223,6 +224,84 @@ void order_lists(std::vector<std::vector<int32_t>>& lists, const std::vector<int
     for (int32_t i : perm) lists.push_back(out[i]);
 }
 
+// Bank-conflict-aware arrangement of the movable (packed) lanes.  A lane's list is
+// a concatenation of pieces; the piece order inside a lane is free (each piece
+// starts at an anchor or a root) and decides which joint the lane touches at each
+// slot.  The cost is the swap_search model: per quarter-warp group of 8 lanes and
+// per slot, the largest number of lanes whose joints share a 16-byte bank group
+// (pos mod 8).  Simulated annealing over (a) swaps of two lanes between groups and
+// (b) random piece orders of one lane, from a fixed seed (plans are reproducible);
+// the best arrangement seen is kept.
+void anneal_lists(std::vector<std::vector<int32_t>>& lists, const std::vector<char>& movable,
+                  const std::vector<int32_t>& pos, const std::vector<int32_t>& par, int K) {
+    const int n = (int)lists.size();
+    std::vector<int> mov;
+    for (int i = 0; i < n; ++i) if (movable[i]) mov.push_back(i);
+    if (mov.size() < 2) return;
+    auto key = [&](const std::vector<int32_t>& l, int s) { return s < (int)l.size() ? (pos[l[s]] & 7) : -1; };
+    auto group_cost = [&](int g) {
+        int cost = 0;
+        for (int s = 0; s < K; ++s) {
+            int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, m = 0;
+            for (int i = 8 * g; i < std::min(n, 8 * g + 8); ++i) {
+                const int k = key(lists[i], s);
+                if (k >= 0) m = std::max(m, ++cnt[k]);
+            }
+            cost += m;
+        }
+        return cost;
+    };
+    auto pieces_of = [&](const std::vector<int32_t>& l) {
+        std::vector<std::vector<int32_t>> pc;
+        for (size_t k = 0; k < l.size(); ++k) {
+            if (k == 0 || par[l[k]] != l[k - 1]) pc.emplace_back();
+            pc.back().push_back(l[k]);
+        }
+        return pc;
+    };
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() {   // splitmix64
+        uint64_t z = (rng += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    };
+    auto uni = [&]() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); };
+    int cur = 0;
+    for (int g = 0; g < (n + 7) / 8; ++g) cur += group_cost(g);
+    int best = cur;
+    std::vector<std::vector<int32_t>> best_lists = lists;
+    const long iters = std::min<long>(400000, 2000L * (long)mov.size());
+    const double t0 = 1.5, t1 = 0.02;
+    for (long it = 0; it < iters; ++it) {
+        const double temp = t0 * std::pow(t1 / t0, (double)it / (double)iters);
+        const int i = mov[next() % mov.size()];
+        if (uni() < 0.5) {   // swap two lanes of different groups
+            const int j = mov[next() % mov.size()];
+            if (i / 8 == j / 8) continue;
+            const int before = group_cost(i / 8) + group_cost(j / 8);
+            std::swap(lists[i], lists[j]);
+            const int delta = group_cost(i / 8) + group_cost(j / 8) - before;
+            if (delta <= 0 || uni() < std::exp(-delta / temp)) cur += delta;
+            else std::swap(lists[i], lists[j]);
+        } else {             // reorder the pieces of one lane
+            auto pc = pieces_of(lists[i]);
+            if (pc.size() < 2) continue;
+            for (size_t k = pc.size() - 1; k > 0; --k) std::swap(pc[k], pc[next() % (k + 1)]);
+            std::vector<int32_t> cand;
+            for (auto& p : pc) cand.insert(cand.end(), p.begin(), p.end());
+            const int before = group_cost(i / 8);
+            std::vector<int32_t> old = lists[i];
+            lists[i] = cand;
+            const int delta = group_cost(i / 8) - before;
+            if (delta <= 0 || uni() < std::exp(-delta / temp)) cur += delta;
+            else lists[i] = old;
+        }
+        if (cur < best) { best = cur; best_lists = lists; }
+    }
+    lists.swap(best_lists);
+}
+
 }  // namespace
 
 ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const std::vector<int32_t>* pos,
@@ -270,6 +349,7 @@ ChunkDecomp decompose(const std::vector<int32_t>& par, int K, int mode, const st
             std::vector<std::vector<int32_t>> out;
             for (int32_t i : perm) out.push_back(d.lists[i]);
             d.lists.swap(out);
+            anneal_lists(d.lists, movable, *pos, par, K);
         }
     } else {
         d.lists = pack_pieces(heavy_pieces(par, K), K);
