@@ -187,10 +187,30 @@ hs_status hs_mesh_destroy(hs_mesh* mesh);
 /* hs_scan (G, and S when skin_out != NULL) plus skinned vertex positions:
  *   verts_out  device fp32 [n_chars][n_vertices][3], 4-byte aligned, not aliasing
  *              the other buffers.
- * Single-CTA skeletons only (HS_ERR_UNSUPPORTED otherwise); the mesh must have been
- * created for this skeleton (HS_ERR_INVALID_ARG). */
+ * The mesh must have been created for this skeleton (HS_ERR_INVALID_ARG).  Same as
+ * hs_scan_skin_ex with opts == NULL. */
 hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
                        float* global_out, float* skin_out, float* verts_out, void* cuda_stream);
+
+/* Where skinning runs.  FUSED: in the scan kernel after the bind epilogue, the
+ * palette never leaves shared memory (single-CTA skeletons only).  TWO_PASS: the
+ * scan writes S (to skin_out, or to a stream-ordered pooled workspace of
+ * workspace_bytes, default 1 GiB, in batches) and a skinning kernel with several
+ * CTAs per SM reads it back (+48 B/joint of HBM; any skeleton whose palette fits
+ * shared memory, n_joints <= 4842).  AUTO = FUSED on single-CTA skeletons (both
+ * placements measured equal on B200: shared-memory bound), else
+ * TWO_PASS.  Both compute each vertex with the same device code: bitwise equal
+ * results. */
+typedef enum { HS_SKIN_AUTO = 0, HS_SKIN_FUSED = 1, HS_SKIN_TWO_PASS = 2 } hs_skin_mode;
+typedef struct {
+    int32_t mode;             /* hs_skin_mode                                            */
+    int32_t reserved0;        /* must be 0                                               */
+    int64_t workspace_bytes;  /* TWO_PASS with skin_out == NULL (0 = 1 GiB)             */
+    int64_t reserved[2];      /* must be 0                                               */
+} hs_skin_opts;
+hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
+                          float* global_out, float* skin_out, float* verts_out, void* cuda_stream,
+                          const hs_skin_opts* opts);
 
 /* ---------------------------------------------------------------------------
  * Stage 1 fused ahead of the scan ("Sample

@@ -111,6 +111,7 @@ def lib():
     L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
     L.hs_mesh_destroy.argtypes = [vp]
     L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
+    L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_AnimateOpts)]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
@@ -321,8 +322,11 @@ class Mesh:
     __del__ = close
 
 
+SKIN_MODE = {"auto": 0, "fused": 1, "two_pass": 2}
+
+
 def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None, verts_out=None,
-              stream=None, skin: bool = False):
+              stream=None, skin: bool = False, mode: str = "auto", workspace_bytes: int = 0):
     """hs_scan_skin: scan + bind + linear blend skinning.  Returns (global, skin-or-None,
     verts [N, V, 3])."""
     import torch
@@ -335,9 +339,10 @@ def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None,
         verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=local.device)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    _check(lib().hs_scan_skin(sk.handle, mesh.handle, local.data_ptr(), n, global_out.data_ptr(),
-                              None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st),
-           "hs_scan_skin")
+    opts = _AnimateOpts(SKIN_MODE[mode], 0, workspace_bytes)   # same layout as hs_skin_opts
+    _check(lib().hs_scan_skin_ex(sk.handle, mesh.handle, local.data_ptr(), n, global_out.data_ptr(),
+                                 None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st,
+                                 ctypes.byref(opts)), "hs_scan_skin")
     return global_out, skin_out, verts_out
 
 

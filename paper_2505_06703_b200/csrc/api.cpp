@@ -617,10 +617,20 @@ hs_status hs_mesh_destroy(hs_mesh* m) {
     return HS_OK;
 }
 
-hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
-                       float* global_out, float* skin_out, float* verts_out, void* cuda_stream) {
+hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
+                          float* global_out, float* skin_out, float* verts_out, void* cuda_stream,
+                          const hs_skin_opts* opts) {
     if (!sk || !mesh) return fail(HS_ERR_INVALID_ARG, "null handle");
     if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    int mode = HS_SKIN_AUTO;
+    int64_t ws_bytes = (int64_t)1 << 30;
+    if (opts) {
+        if (opts->mode < HS_SKIN_AUTO || opts->mode > HS_SKIN_TWO_PASS || opts->reserved0 || opts->reserved[0] ||
+            opts->reserved[1] || opts->workspace_bytes < 0)
+            return fail(HS_ERR_INVALID_ARG, "invalid hs_skin_opts");
+        mode = opts->mode;
+        if (opts->workspace_bytes) ws_bytes = opts->workspace_bytes;
+    }
     if (n_chars == 0) return HS_OK;
     if (!local || !global_out || !verts_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
     if (!aligned16(local) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)) ||
@@ -635,16 +645,49 @@ hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* 
     int dev = -1;
     cudaGetDevice(&dev);
     if (dev != sk->device || dev != mesh->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
-    if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "hs_scan_skin needs a single-CTA skeleton");
-    hs::ChunkedArgs a{};
-    const ChunkItem item{sk, local, n_chars, global_out, skin_out};
-    chunked_layout(&item, 1, sk->stages, sk->sbufs, a);
-    a.mesh_a = mesh->d_a;
-    a.mesh_b = mesh->d_b;
-    a.mesh_j = mesh->d_j;
-    a.verts = verts_out;
-    a.n_verts = mesh->n_verts;
-    return run_chunked(a, sk->K, static_cast<cudaStream_t>(cuda_stream));
+    const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const int32_t J = sk->plan.n;
+    // AUTO: the fused epilogue where it exists (measured as fast as two-pass on B200:
+    // both are bound by the palette's shared-memory reads), else two-pass
+    if (mode == HS_SKIN_AUTO) mode = sk->chunked ? HS_SKIN_FUSED : HS_SKIN_TWO_PASS;
+    if (mode == HS_SKIN_FUSED) {
+        if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "the fused LBS epilogue needs a single-CTA skeleton");
+        hs::ChunkedArgs a{};
+        const ChunkItem item{sk, local, n_chars, global_out, skin_out};
+        chunked_layout(&item, 1, sk->stages, sk->sbufs, a);
+        a.mesh_a = mesh->d_a;
+        a.mesh_b = mesh->d_b;
+        a.mesh_j = mesh->d_j;
+        a.verts = verts_out;
+        a.n_verts = mesh->n_verts;
+        return run_chunked(a, sk->K, st);
+    }
+    // two-pass: the scan writes S (to skin_out, or to a pooled workspace in
+    // batches when the caller does not want S), then lbs_kernel skins from it
+    if ((int64_t)J * 48 > 227 * 1024) return fail(HS_ERR_UNSUPPORTED, "palette does not fit shared memory");
+    const int64_t per_char = (int64_t)J * 48;
+    const int64_t batch = skin_out ? n_chars : std::max<int64_t>(1, std::min<int64_t>(n_chars, ws_bytes / per_char));
+    float* ws = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (!skin_out && (e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(batch * per_char), st)) != cudaSuccess)
+        return cuda_fail(e, "LBS workspace");
+    hs_status r = HS_OK;
+    for (int64_t c0 = 0; c0 < n_chars && r == HS_OK; c0 += batch) {
+        const int64_t nb = std::min(batch, n_chars - c0);
+        float* sb = skin_out ? skin_out + c0 * J * 12 : ws;
+        r = scan_impl(sk, local + c0 * J * 12, nb, global_out + c0 * J * 12, sb, st, HS_ALGO_AUTO, -1, 0);
+        if (r == HS_OK &&
+            (e = hs::launch_lbs(sb, nb, J, mesh->d_a, mesh->d_b, mesh->d_j, mesh->n_verts,
+                                verts_out + c0 * (int64_t)mesh->n_verts * 3, st)) != cudaSuccess)
+            r = cuda_fail(e, "LBS launch");
+    }
+    if (ws) cudaFreeAsync(ws, st);
+    return r;
+}
+
+hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
+                       float* global_out, float* skin_out, float* verts_out, void* cuda_stream) {
+    return hs_scan_skin_ex(sk, mesh, local, n_chars, global_out, skin_out, verts_out, cuda_stream, nullptr);
 }
 
 hs_status hs_clipset_create(const hs_skeleton* sk, const float* keys, int32_t n_clips, int32_t n_keys,

@@ -7,6 +7,7 @@
 // contraction (BASELINE.json north_star); the path is HBM-bound.
 #include "kernels.cuh"
 
+#include <algorithm>
 #include <cstdint>
 
 #ifndef HS_S1_E
@@ -347,6 +348,32 @@ __device__ __forceinline__ void stage1_tile(const float* __restrict__ keys, cons
         j0 += step_j;
         if (j0 >= J) { j0 -= J; ++cl0; }
     }
+}
+
+// ================================================================== LBS (NEXT-4)
+// One skinned vertex (R24): sum_k w_k S[j_k] (p, 1) with the character's
+// skin palette `pal` ([J][12], shared memory); joints pre-multiplied by 12.  The
+// fused epilogue and the two-pass kernel share it, so their vertices are bitwise equal.
+__device__ __forceinline__ void lbs_vertex(const float* pal, float4 pa, float4 pb, const int* js, float* d) {
+    const float ws[4] = {pa.w, pb.x, pb.y, pb.z};
+    float x = 0.f, y = 0.f, z = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float m[12];
+        ld3(pal + js[q], m);
+        const float px = fmaf(m[0], pa.x, fmaf(m[1], pa.y, fmaf(m[2], pa.z, m[3])));
+        const float py = fmaf(m[4], pa.x, fmaf(m[5], pa.y, fmaf(m[6], pa.z, m[7])));
+        const float pz = fmaf(m[8], pa.x, fmaf(m[9], pa.y, fmaf(m[10], pa.z, m[11])));
+        x = fmaf(ws[q], px, x);
+        y = fmaf(ws[q], py, y);
+        z = fmaf(ws[q], pz, z);
+    }
+    d[0] = x; d[1] = y; d[2] = z;
+}
+
+__device__ __forceinline__ void mesh_joints(int2 jj, int* js) {
+    js[0] = (jj.x & 0xffff) * 12; js[1] = (int)((uint32_t)jj.x >> 16) * 12;
+    js[2] = (jj.y & 0xffff) * 12; js[3] = (int)((uint32_t)jj.y >> 16) * 12;
 }
 
 // ================================================================== chunked kernel
@@ -804,31 +831,14 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         const int v = min(v0 + u * NC, V - 1);
                         pa[u] = __ldg(a.mesh_a + v);
                         pb[u] = __ldg(a.mesh_b + v);
-                        const int2 jj = __ldg(a.mesh_j + v);
-                        js[u][0] = (jj.x & 0xffff) * 12; js[u][1] = (int)((uint32_t)jj.x >> 16) * 12;
-                        js[u][2] = (jj.y & 0xffff) * 12; js[u][3] = (int)((uint32_t)jj.y >> 16) * 12;
+                        mesh_joints(__ldg(a.mesh_j + v), js[u]);
                     }
                     for (int cl = 0; cl < nct; ++cl) {
                         const float* Sc = Sb + cl * Jn * 12;
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
                             const int v = v0 + u * NC;
-                            if (v >= V) continue;
-                            const float ws[4] = {pa[u].w, pb[u].x, pb[u].y, pb[u].z};
-                            float x = 0.f, y = 0.f, z = 0.f;
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                float m[12];
-                                ld3(Sc + js[u][q], m);
-                                const float px = fmaf(m[0], pa[u].x, fmaf(m[1], pa[u].y, fmaf(m[2], pa[u].z, m[3])));
-                                const float py = fmaf(m[4], pa[u].x, fmaf(m[5], pa[u].y, fmaf(m[6], pa[u].z, m[7])));
-                                const float pz = fmaf(m[8], pa[u].x, fmaf(m[9], pa[u].y, fmaf(m[10], pa[u].z, m[11])));
-                                x = fmaf(ws[q], px, x);
-                                y = fmaf(ws[q], py, y);
-                                z = fmaf(ws[q], pz, z);
-                            }
-                            float* d = vout + ((int64_t)cl * V + v) * 3;
-                            d[0] = x; d[1] = y; d[2] = z;
+                            if (v < V) lbs_vertex(Sc, pa[u], pb[u], js[u], vout + ((int64_t)cl * V + v) * 3);
                         }
                     }
                 }
@@ -949,6 +959,32 @@ __global__ void __launch_bounds__(1024) blocked_kernel(const float* __restrict__
             ldg3(ib + (int64_t)u * 12, b);
             compose(v, b, s);
             st3(sout + (c0 * J + f) * 12, s);
+        }
+    }
+}
+
+// ================================================================== LBS, two-pass
+// Skinning from skin poses in HBM: one CTA per character (grid-stride), its palette
+// staged in shared memory (J x 48 B), then consecutive vertices on consecutive
+// threads.  Several CTAs per SM (vs the scan kernel's one) hide the palette-read
+// latency; costs one extra 48 B/joint read of S.
+__global__ void __launch_bounds__(256) lbs_kernel(const float* __restrict__ S, int64_t n_chars, int J,
+                                                  const float4* __restrict__ mesh_a,
+                                                  const float4* __restrict__ mesh_b,
+                                                  const int2* __restrict__ mesh_j, int V,
+                                                  float* __restrict__ verts) {
+    extern __shared__ float4 pal4[];
+    const float* pal = reinterpret_cast<const float*>(pal4);
+    for (int64_t c = blockIdx.x; c < n_chars; c += gridDim.x) {
+        __syncthreads();   // the previous character's readers are done
+        const float4* src = reinterpret_cast<const float4*>(S + c * J * 12);
+        for (int i = threadIdx.x; i < J * 3; i += blockDim.x) pal4[i] = __ldcs(src + i);
+        __syncthreads();
+        float* vout = verts + c * V * 3;
+        for (int v = threadIdx.x; v < V; v += blockDim.x) {
+            int js[4];
+            mesh_joints(__ldg(mesh_j + v), js);
+            lbs_vertex(pal, __ldg(mesh_a + v), __ldg(mesh_b + v), js, vout + (int64_t)v * 3);
         }
     }
 }
@@ -1245,6 +1281,23 @@ cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, flo
     }
     return cudaLaunchKernel(reinterpret_cast<void*>(&stage1_kernel), dim3((unsigned)blocks), dim3(256), params,
                             smem, st);
+}
+
+cudaError_t launch_lbs(const float* S, int64_t n_chars, int32_t J, const float4* mesh_a, const float4* mesh_b,
+                       const int2* mesh_j, int32_t V, float* verts, cudaStream_t st) {
+    const size_t smem = (size_t)J * 48;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<void*>(&lbs_kernel),
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lbs_kernel, 256, smem);
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    if (grid > n_chars) grid = n_chars;
+    if (grid < 1) grid = 1;
+    lbs_kernel<<<(unsigned)grid, 256, smem, st>>>(S, n_chars, J, mesh_a, mesh_b, mesh_j, V, verts);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_doubling(const float* local, float* gout, float* sout, const float* ib,

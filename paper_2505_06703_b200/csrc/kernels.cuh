@@ -58,6 +58,9 @@ struct ChunkedArgs {
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
+// Linear blend skinning from skin poses in HBM (two-pass hs_scan_skin): S [n_chars][J][12].
+cudaError_t launch_lbs(const float* S, int64_t n_chars, int32_t J, const float4* mesh_a, const float4* mesh_b,
+                       const int2* mesh_j, int32_t V, float* verts, cudaStream_t st);
 // Stage 1 alone (two-pass hs_animate): local poses of characters [c0, c0 + n_chars)
 // of a.layers into local ([n_chars][J][12]).
 cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st);

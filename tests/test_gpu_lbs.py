@@ -27,11 +27,11 @@ TOL_VERTS = 4e-4
 TOL_SELF = 2e-6   # x (1 + max |v|)
 
 
-def run(par, loc, ib, mesh, skin=True, **create):
+def run(par, loc, ib, mesh, skin=True, mode="auto", **create):
     sk = hs.Skeleton(par, ib, **create)
     m = hs.Mesh(sk, *mesh)
     x = torch.from_numpy(loc).cuda()
-    g, s, v = hs.scan_skin(sk, m, x, skin=skin)
+    g, s, v = hs.scan_skin(sk, m, x, skin=skin, mode=mode)
     torch.cuda.synchronize()
     g2, s2 = sk.scan(x)
     torch.cuda.synchronize()
@@ -40,15 +40,16 @@ def run(par, loc, ib, mesh, skin=True, **create):
     return out
 
 
+@pytest.mark.parametrize("mode", ["fused", "two_pass"])
 @pytest.mark.parametrize("name,n,V", [("hum32", 100, 700), ("hum64", 300, 1000), ("chain256", 60, 1500),
                                       ("tree1024", 24, 2000)])
-def test_lbs_parity(name, n, V):
+def test_lbs_parity(name, n, V, mode):
     par = hsgen.skeleton(name)
     J = len(par)
     loc = hsgen.local_poses(21, J, n)
     ib = hsgen.inv_bind(22, J)
     mesh = hsgen.mesh(23, par, V)
-    g, s, v, g2, s2 = run(par, loc, ib, mesh)
+    g, s, v, g2, s2 = run(par, loc, ib, mesh, mode=mode)
     # the scan outputs are the plain hs_scan ones, bit for bit
     assert np.array_equal(g, g2) and np.array_equal(s, s2)
     G, S = oracle.scan(par, loc, ib)
@@ -117,5 +118,36 @@ def test_lbs_errors():
     big = hs.Skeleton(hsgen.random_tree(9, 4096, 64))
     m_big = hs.Mesh(big, *hsgen.mesh(63, hsgen.random_tree(9, 4096, 64), 10))
     with pytest.raises(hs.HSError) as e:
-        hs.scan_skin(big, m_big, torch.zeros((1, 4096, 3, 4), device="cuda"))
+        hs.scan_skin(big, m_big, torch.zeros((1, 4096, 3, 4), device="cuda"), mode="fused")
     assert e.value.status == hs.HS_ERR_UNSUPPORTED
+
+
+def test_fused_and_two_pass_bitwise_equal():
+    """Both placements run the same per-vertex code on the same skin palette; the
+    two-pass path without skin_out batches through a 3-character workspace."""
+    for name, n, V in (("hum64", 77, 900), ("tree1024", 9, 1500)):
+        par = hsgen.skeleton(name)
+        J = len(par)
+        sk = hs.Skeleton(par, hsgen.inv_bind(71, J))
+        m = hs.Mesh(sk, *hsgen.mesh(72, par, V))
+        x = torch.from_numpy(hsgen.local_poses(73, J, n)).cuda()
+        g1, s1, v1 = hs.scan_skin(sk, m, x, skin=True, mode="fused")
+        g2, s2, v2 = hs.scan_skin(sk, m, x, skin=True, mode="two_pass")
+        g3, _, v3 = hs.scan_skin(sk, m, x, skin=False, mode="two_pass", workspace_bytes=3 * J * 48)
+        torch.cuda.synchronize()
+        assert torch.equal(g1, g2) and torch.equal(s1, s2) and torch.equal(v1, v2)
+        assert torch.equal(g1, g3) and torch.equal(v1, v3)
+
+
+def test_two_pass_lbs_on_multi_cta_skeleton():
+    par = hsgen.random_tree(81, 3000, 70)
+    J = len(par)
+    loc = hsgen.local_poses(82, J, 3)
+    ib = hsgen.inv_bind(83, J)
+    mesh = hsgen.mesh(84, par, 600)
+    sk = hs.Skeleton(par, ib)
+    assert sk.query("path") == 3
+    _, s, v = hs.scan_skin(sk, hs.Mesh(sk, *mesh), torch.from_numpy(loc).cuda(), skin=True)
+    torch.cuda.synchronize()
+    G, S = oracle.scan(par, loc, ib)
+    assert np.abs(v.cpu().numpy() - oracle.skin_vertices(S, *mesh)).max() <= TOL_VERTS

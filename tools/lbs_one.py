@@ -19,7 +19,8 @@ mesh = hs.Mesh(sk, *hsgen.mesh(202, par, 1000, type_=2))
 x = torch.from_numpy(hsgen.local_poses(5, J, n, type_=2)).cuda()
 g, s = torch.empty_like(x), torch.empty_like(x)
 v = torch.empty((n, 1000, 3), device="cuda")
+mode = os.environ.get("HS_SKIN_MODE", "auto")
 for _ in range(4):
-    hs.scan_skin(sk, mesh, x, g, s, v)
+    hs.scan_skin(sk, mesh, x, g, s, v, mode=mode)
 torch.cuda.synchronize()
 print("ok", name, n)
