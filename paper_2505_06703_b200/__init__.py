@@ -111,7 +111,7 @@ def lib():
     L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
     L.hs_mesh_destroy.argtypes = [vp]
     L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
-    L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_AnimateOpts)]
+    L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_SkinOpts)]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
@@ -265,7 +265,12 @@ MAX_BATCH = 8   # HS_MAX_BATCH
 ANIMATE_MODE = {"auto": 0, "fused": 1, "two_pass": 2}
 
 
-class _AnimateOpts(ctypes.Structure):
+class _AnimateOpts(ctypes.Structure):   # hs_animate_opts
+    _fields_ = [("mode", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64), ("reserved", ctypes.c_int64 * 2)]
+
+
+class _SkinOpts(ctypes.Structure):   # hs_skin_opts
     _fields_ = [("mode", ctypes.c_int32), ("reserved0", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_int64), ("reserved", ctypes.c_int64 * 2)]
 
@@ -339,7 +344,7 @@ def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None,
         verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=local.device)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    opts = _AnimateOpts(SKIN_MODE[mode], 0, workspace_bytes)   # same layout as hs_skin_opts
+    opts = _SkinOpts(SKIN_MODE[mode], 0, workspace_bytes)
     _check(lib().hs_scan_skin_ex(sk.handle, mesh.handle, local.data_ptr(), n, global_out.data_ptr(),
                                  None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st,
                                  ctypes.byref(opts)), "hs_scan_skin")
