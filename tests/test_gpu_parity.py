@@ -239,13 +239,14 @@ def test_determinism_and_character_independence():
     assert np.array_equal(ga[50:], gb)
 
 
-def test_host_pipeline_matches_device_path():
+@pytest.mark.parametrize("batch_chars", [700, 5000])   # fixed batches / the 8 MB ramp (682, 1364, ...)
+def test_host_pipeline_matches_device_path(batch_chars):
     par = hsgen.skeleton("chain256")
     ib = hsgen.inv_bind(3, 256)
     local = hsgen.local_poses(46, 256, 3000)
     g_dev, s_dev = gpu_scan(par, local, ib)
     sk = hs.Skeleton(par, ib)
-    pl = hs.Pipeline(batch_bytes=256 * 48 * 700)  # several batches + a ragged one
+    pl = hs.Pipeline(batch_bytes=256 * 48 * batch_chars)  # several batches + a ragged one
     hl = torch.from_numpy(local).pin_memory()
     hg = torch.empty_like(hl).pin_memory()
     hsk = torch.empty_like(hl).pin_memory()
