@@ -350,6 +350,12 @@ typedef struct hs_pipeline hs_pipeline;
 hs_status hs_pipeline_create(int64_t batch_bytes, hs_pipeline** out);
 hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_local,
                        int64_t n_chars, float* h_global, float* h_skin);
+
+/* The same over several crowds (any skeletons): items hold HOST pointers here
+ * (local, global_out and skin_out all required), n_items >= 0.  One pipeline runs
+ * through every item's characters, so the copy engines do not drain between skeleton
+ * types.  Errors as hs_scan_host. */
+hs_status hs_scan_host_batch(hs_pipeline* pl, const hs_batch_item* items, int32_t n_items);
 hs_status hs_pipeline_destroy(hs_pipeline* pl);
 
 #ifdef __cplusplus

@@ -114,6 +114,7 @@ def lib():
     L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_SkinOpts)]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.hs_scan_host_batch.argtypes = [vp, ctypes.POINTER(_BatchItem), i32]
     L.hs_pipeline_destroy.argtypes = [vp]
     for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
               "hs_skeleton_query", "hs_plan_create", "hs_plan_create_ex", "hs_plan_query", "hs_plan_export",
@@ -418,6 +419,17 @@ class Pipeline:
             n_chars = h_local.shape[0]
         _check(lib().hs_scan_host(self._h, sk.handle, ptr(h_local), n_chars, ptr(h_global),
                                   ptr(h_skin)), "hs_scan_host")
+
+    def scan_host_batch(self, items):
+        """hs_scan_host_batch: items = [(Skeleton, h_local, h_global, h_skin), ...] on the
+        host; one pipeline over all of them."""
+        def ptr(t):
+            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+
+        arr = (_BatchItem * max(1, len(items)))()
+        for i, (sk, hl, hg, hsk) in enumerate(items):
+            arr[i] = _BatchItem(sk.handle, ptr(hl), hl.shape[0], ptr(hg), ptr(hsk))
+        _check(lib().hs_scan_host_batch(self._h, arr, len(items)), "hs_scan_host_batch")
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -973,41 +973,64 @@ hs_status hs_pipeline_create(int64_t batch_bytes, hs_pipeline** out) {
     return HS_OK;
 }
 
-hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_local, int64_t n_chars,
-                       float* h_global, float* h_skin) {
-    if (!pl || !sk) return fail(HS_ERR_INVALID_ARG, "null handle");
-    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
-    if (n_chars == 0) return HS_OK;
-    if (!h_local || !h_global || !h_skin) return fail(HS_ERR_INVALID_ARG, "null buffer");
+hs_status hs_scan_host_batch(hs_pipeline* pl, const hs_batch_item* items, int32_t n_items) {
+    if (!pl) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_items < 0 || (n_items > 0 && !items)) return fail(HS_ERR_INVALID_ARG, "bad item list");
     int dev = -1;
     cudaGetDevice(&dev);
-    if (dev != sk->device || dev != pl->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
-    const int64_t per_char = (int64_t)sk->plan.n * 48;
-    const int64_t batch = pl->batch_bytes / per_char;
-    if (batch < 1) return fail(HS_ERR_INVALID_ARG, "pipeline batch smaller than one character");
-    // batches ramp up geometrically from ~8 MB: the copy engine that reads back (the
-    // larger direction) idles only for the first, small H2D instead of a full batch
-    int64_t b = 0, cur = std::max<int64_t>(1, std::min<int64_t>(batch, ((int64_t)8 << 20) / per_char));
-    for (int64_t c0 = 0, nb = 0; c0 < n_chars; c0 += nb, ++b, cur = std::min(batch, 2 * cur)) {
-        const int i = (int)(b % 3);
-        nb = std::min(cur, n_chars - c0);
-        const size_t bytes = (size_t)(nb * per_char);
-        const int64_t foff = c0 * sk->plan.n * 12;
-        cudaError_t e = cudaMemcpyAsync(pl->d_in[i], h_local + foff, bytes, cudaMemcpyHostToDevice, pl->st[i]);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D");
-        hs_status s = scan_impl(sk, pl->d_in[i], nb, pl->d_g[i], pl->d_s[i], pl->st[i], HS_ALGO_AUTO, -1, 0);
-        if (s != HS_OK) return s;
-        if ((e = cudaMemcpyAsync(h_global + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
-                cudaSuccess ||
-            (e = cudaMemcpyAsync(h_skin + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
-                cudaSuccess)
-            return cuda_fail(e, "D2H");
+    if (dev != pl->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    for (int32_t k = 0; k < n_items; ++k) {
+        const hs_batch_item& it = items[k];
+        if (!it.skeleton) return fail(HS_ERR_INVALID_ARG, "null skeleton");
+        if (it.n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+        if (it.n_chars && (!it.local || !it.global_out || !it.skin_out)) return fail(HS_ERR_INVALID_ARG, "null buffer");
+        if (it.skeleton->device != dev) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+        if (pl->batch_bytes / ((int64_t)it.skeleton->plan.n * 48) < 1)
+            return fail(HS_ERR_INVALID_ARG, "pipeline batch smaller than one character");
+    }
+    // one pipeline over every item's characters: the 3 streams rotate across items
+    // without draining in between; batches ramp up geometrically from ~8 MB at the
+    // start, so the read-back copy engine (the larger direction) idles only for the
+    // first small upload
+    int64_t b = 0, ramp = (int64_t)8 << 20;
+    for (int32_t k = 0; k < n_items; ++k) {
+        const hs_batch_item& it = items[k];
+        const hs_skeleton* sk = it.skeleton;
+        const int64_t per_char = (int64_t)sk->plan.n * 48;
+        const int64_t batch = pl->batch_bytes / per_char;
+        for (int64_t c0 = 0, nb = 0; c0 < it.n_chars; c0 += nb, ++b) {
+            const int i = (int)(b % 3);
+            const int64_t cur = std::max<int64_t>(1, std::min<int64_t>(batch, ramp / per_char));
+            ramp = std::min<int64_t>(2 * ramp, pl->batch_bytes);
+            nb = std::min(cur, it.n_chars - c0);
+            const size_t bytes = (size_t)(nb * per_char);
+            const int64_t foff = c0 * sk->plan.n * 12;
+            cudaError_t e = cudaMemcpyAsync(pl->d_in[i], it.local + foff, bytes, cudaMemcpyHostToDevice, pl->st[i]);
+            if (e != cudaSuccess) return cuda_fail(e, "H2D");
+            hs_status s = scan_impl(sk, pl->d_in[i], nb, pl->d_g[i], pl->d_s[i], pl->st[i], HS_ALGO_AUTO, -1, 0);
+            if (s != HS_OK) return s;
+            if ((e = cudaMemcpyAsync(it.global_out + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                    cudaSuccess ||
+                (e = cudaMemcpyAsync(it.skin_out + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                    cudaSuccess)
+                return cuda_fail(e, "D2H");
+        }
     }
     for (int i = 0; i < 3; ++i) {
         cudaError_t e = cudaStreamSynchronize(pl->st[i]);
         if (e != cudaSuccess) return cuda_fail(e, "pipeline sync");
     }
     return HS_OK;
+}
+
+hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_local, int64_t n_chars,
+                       float* h_global, float* h_skin) {
+    if (!pl || !sk) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!h_local || !h_global || !h_skin) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    const hs_batch_item it{sk, h_local, n_chars, h_global, h_skin};
+    return hs_scan_host_batch(pl, &it, 1);
 }
 
 hs_status hs_pipeline_destroy(hs_pipeline* pl) {

@@ -254,6 +254,23 @@ def test_host_pipeline_matches_device_path(batch_chars):
     assert np.array_equal(hg.numpy(), g_dev) and np.array_equal(hsk.numpy(), s_dev)
 
 
+def test_host_pipeline_batch_over_types():
+    items, want = [], []
+    for name, n in (("hum64", 900), ("chain256", 300), ("tree1024", 40)):
+        par = hsgen.skeleton(name)
+        J = len(par)
+        ib = hsgen.inv_bind(5, J)
+        local = hsgen.local_poses(47, J, n)
+        want.append(gpu_scan(par, local, ib))
+        hl = torch.from_numpy(local).pin_memory()
+        items.append((hs.Skeleton(par, ib), hl, torch.empty_like(hl).pin_memory(),
+                      torch.empty_like(hl).pin_memory()))
+    pl = hs.Pipeline(batch_bytes=1 << 20)
+    pl.scan_host_batch(items)
+    for (_, _, hg, hsk), (g, s) in zip(items, want):
+        assert np.array_equal(hg.numpy(), g) and np.array_equal(hsk.numpy(), s)
+
+
 # ------------------------------------------------------------------ ABI error behaviour
 def test_abi_errors():
     sk = hs.Skeleton(hsgen.skeleton("hum32"))
