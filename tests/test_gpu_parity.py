@@ -326,3 +326,25 @@ def test_fig7_shape_depth_sweep():
         assert res[(depth, "auto")] < res[(depth, "leaf")]
     assert res[(120, "gateau")] > 2.5 * res[(15, "gateau")]       # ancestor walks grow with depth
     assert res[(120, "auto")] < 2.0 * res[(15, "auto")]            # ours does not
+
+
+def test_large_crowd_int64_offsets():
+    """Buffers beyond 2^31 floats (9.2 GB each): characters near the end are addressed
+    with 64-bit offsets on every path the kernel takes (TMA loads/stores, tiles)."""
+    par = hsgen.skeleton("hum32")
+    J, n = 32, 6_000_000                       # 6e6 x 32 x 12 floats = 2.3e9 > 2^31
+    x = torch.empty((n, J, 3, 4), device="cuda")
+    assert hsgen.lib_cuda().hsg_cuda_local_poses(91, 0, J, 0, n, x.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream) == 0
+    ib = hsgen.inv_bind(92, J)
+    sk = hs.Skeleton(par, ib)
+    g, s = torch.empty_like(x), torch.empty_like(x)
+    sk.scan_into(x, g, s)
+    torch.cuda.synchronize()
+    idx = np.array([0, 1, n // 2, n - 3, n - 2, n - 1])
+    loc = np.concatenate([hsgen.local_poses(91, J, 1, char0=int(i)) for i in idx])
+    assert np.array_equal(loc, x[idx].cpu().numpy())    # device generator == host generator
+    G, S = oracle.scan(par, loc, ib)
+    assert np.abs(g[idx].cpu().numpy() - G).max() <= TOL and np.abs(s[idx].cpu().numpy() - S).max() <= TOL
+    del x, g, s
+    torch.cuda.empty_cache()
