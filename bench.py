@@ -409,6 +409,7 @@ def run_ours(args):
         "config": {"workload": workload,
                    "characters_per_gpu": {w["name"]: w["n"] for w in work},
                    "joints_total": joints_total, "bytes_per_joint": bpj,
+                   "characters_per_s": value * sum(w["n"] for w in work) / joints_rank if joints_rank else 0.0,
                    **({"vertices_per_char": args.skin_mesh,
                        "vertices_per_s": value * sum(w["n"] for w in work) * args.skin_mesh / joints_rank,
                        "bytes_per_vertex": 12} if args.skin_mesh else {}),
