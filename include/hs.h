@@ -164,6 +164,20 @@ typedef struct {
 } hs_batch_item;
 hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_stream);
 
+/* Per-character topology ("and/or per-character topology"):
+ * every character has its own skeleton, so nothing is planned ahead.  Pointer jumping
+ * with the parent pointers themselves (Alg. 2, with the Eq. 2 lift
+ * built on the fly): ceil(log2 L) rounds per character group.
+ *   parents   device int32 [n_chars][n_joints], character-local labels, -1 = root,
+ *             any order; an entry outside [-1, n_joints) is treated as a root; a cycle
+ *             gives undefined values but the launch terminates (bounded rounds).
+ *   local     device fp32 [n_chars][n_joints][3][4] (16-byte aligned)
+ *   inv_bind  device fp32 [n_chars][n_joints][3][4] per-character inverse binds, or
+ *             NULL (skin = global)
+ *   n_joints  1..1024 (HS_ERR_UNSUPPORTED above); outputs as hs_scan. */
+hs_status hs_scan_varied(const int32_t* parents, const float* local, const float* inv_bind, int32_t n_joints,
+                         int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream);
+
 /* ---------------------------------------------------------------------------
  * Linear blend skinning fused after the bind epilogue (
  * PAPER.md:96 "compute animation simulation, Hierarchy-Scan, skinning and rendering

@@ -108,6 +108,7 @@ def lib():
     L.hs_animate.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
     L.hs_animate_ex.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp, ctypes.POINTER(_AnimateOpts)]
     L.hs_scan_batch.argtypes = [ctypes.POINTER(_BatchItem), i32, vp]
+    L.hs_scan_varied.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp]
     L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
     L.hs_mesh_destroy.argtypes = [vp]
     L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
@@ -350,6 +351,25 @@ def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None,
                                  None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st,
                                  ctypes.byref(opts)), "hs_scan_skin")
     return global_out, skin_out, verts_out
+
+
+def scan_varied(parents, local, inv_bind=None, global_out=None, skin_out=None, stream=None,
+                skin: bool = True):
+    """hs_scan_varied: per-character topology.  parents: CUDA int32 [N, J]; local: CUDA
+    float32 [N, J, 3, 4]; inv_bind: CUDA float32 [N, J, 3, 4] or None."""
+    import torch
+    n, J = parents.shape
+    if global_out is None:
+        global_out = torch.empty_like(local)
+    if skin_out is None and skin:
+        skin_out = torch.empty_like(local)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_scan_varied(parents.data_ptr(), local.data_ptr(),
+                                None if inv_bind is None else inv_bind.data_ptr(), J, n,
+                                global_out.data_ptr(), None if skin_out is None else skin_out.data_ptr(), st),
+           "hs_scan_varied")
+    return global_out, skin_out
 
 
 LAYER_DTYPE = np.dtype([("clip", "<i4"), ("time", "<f4"), ("weight", "<f4"), ("pad", "<i4")])

@@ -532,6 +532,24 @@ hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars,
                      algo, max_rounds, tile_ctas);
 }
 
+hs_status hs_scan_varied(const int32_t* parents, const float* local, const float* inv_bind, int32_t n_joints,
+                         int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream) {
+    if (n_chars < 0 || n_joints < 0) return fail(HS_ERR_INVALID_ARG, "negative size");
+    if (n_chars == 0 || n_joints == 0) return n_joints == 0 && n_chars > 0 ? fail(HS_ERR_EMPTY, "n_joints == 0")
+                                                                          : HS_OK;
+    if (n_joints > 1024) return fail(HS_ERR_UNSUPPORTED, "per-character topology needs n_joints <= 1024");
+    if (!parents || !local || !global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (!aligned16(local) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)) ||
+        (inv_bind && !aligned16(inv_bind)) || (reinterpret_cast<uintptr_t>(parents) & 3))
+        return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned (parents 4-byte)");
+    if (local == global_out || (skin_out && (local == skin_out || global_out == skin_out)))
+        return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
+    if (n_chars > (INT64_MAX / 64) / n_joints) return fail(HS_ERR_INVALID_ARG, "size overflow");
+    const cudaError_t e = hs::launch_varied(parents, local, inv_bind, n_joints, n_chars, global_out, skin_out,
+                                            static_cast<cudaStream_t>(cuda_stream));
+    return e == cudaSuccess ? HS_OK : cuda_fail(e, "varied-topology launch");
+}
+
 hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_stream) {
     if (n_items < 0 || n_items > HS_MAX_BATCH) return fail(HS_ERR_INVALID_ARG, "n_items must be in 0..HS_MAX_BATCH");
     if (n_items > 0 && !items) return fail(HS_ERR_INVALID_ARG, "items is null");

@@ -901,6 +901,77 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
     }
 }
 
+// ================================================================== varied topology
+// NEXT-3's per-character topology: every character brings its own parent array
+// (4 B/joint more input), so nothing can be planned per skeleton.  One thread per
+// (character, joint), C = 1024 / J characters per CTA; pointer jumping WITH the
+// parent pointers (Alg. 2 with the Eq. 2 lift built on the fly): V[i] <- V[p[i]] (x)
+// V[i], p[i] <- p[p[i]] on ping-pong snapshots until no pointer is left (at most
+// ceil(log2 J) + 1 rounds, so a malformed array still terminates).
+__global__ void __launch_bounds__(1024) varied_kernel(const int32_t* __restrict__ parents,
+                                                      const float* __restrict__ local,
+                                                      const float* __restrict__ ib, int J, int C,
+                                                      int64_t n_chars, int max_rounds,
+                                                      float* __restrict__ gout, float* __restrict__ sout) {
+    extern __shared__ __align__(16) float sm[];
+    const int F = C * J;
+    float* v0 = sm;
+    float* v1 = sm + F * 12;
+    int32_t* q0 = reinterpret_cast<int32_t*>(sm + 2 * F * 12);
+    int32_t* q1 = q0 + F;
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int nc = (int)min((int64_t)C, n_chars - c0);
+    const int f = threadIdx.x;
+    const int cl = f / J;
+    const bool valid = f < F && cl < nc;
+    float v[12];
+    int p = -1;
+    if (valid) {
+        ldg3(local + (c0 * J + f) * 12, v);
+        p = __ldg(parents + c0 * J + f);
+        if (p < -1 || p >= J) p = -1;   // out of range: treated as a root (documented)
+    }
+    if (f < F) { st3(v0 + f * 12, v); q0[f] = p; }
+    float* vc = v0;
+    float* vn = v1;
+    int32_t* qc = q0;
+    int32_t* qn = q1;
+    __syncthreads();
+    for (int r = 0; r < max_rounds; ++r) {
+        if (!__syncthreads_or(p >= 0)) break;
+        if (f < F) {
+            if (p >= 0) {
+                float x[12], y[12];
+                ld3(vc + (cl * J + p) * 12, x);
+                compose(x, v, y);
+#pragma unroll
+                for (int e = 0; e < 12; ++e) v[e] = y[e];
+                p = qc[cl * J + p];
+            }
+            st3(vn + f * 12, v);
+            qn[f] = p;
+        }
+        __syncthreads();
+        float* tv = vc; vc = vn; vn = tv;
+        int32_t* tq = qc; qc = qn; qn = tq;
+    }
+    if (valid) {
+        st3(gout + (c0 * J + f) * 12, v);
+        if (sout) {
+            float s[12];
+            if (ib) {
+                float b[12];
+                ldg3(ib + (c0 * J + f) * 12, b);
+                compose(v, b, s);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 12; ++e) s[e] = v[e];
+            }
+            st3(sout + (c0 * J + f) * 12, s);
+        }
+    }
+}
+
 // ================================================================== blocked (Alg. 3)
 // The paper's Alg. 3 literally, a comparison kernel: one thread
 // per (character, joint) in USER order, B = 64-joint blocks over the internal
@@ -1316,6 +1387,25 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
     const int64_t blocks = (n_chars + C - 1) / C;
     doubling_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lift, J, C, rounds,
                                                            n_chars);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_varied(const int32_t* parents, const float* local, const float* ib, int32_t J,
+                          int64_t n_chars, float* gout, float* sout, cudaStream_t st) {
+    if (J < 1 || J > 1024) return cudaErrorInvalidValue;
+    const int C = std::max(1, 1024 / J);
+    int rounds = 1;
+    while ((1 << (rounds - 1)) < J) ++rounds;   // ceil(log2 J) + 1: enough for any forest
+    const size_t smem = (size_t)C * J * (2 * 48 + 2 * 4);
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(varied_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   1024 * (2 * 48 + 2 * 4));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t blocks = (n_chars + C - 1) / C;
+    varied_kernel<<<(unsigned)blocks, C * J, smem, st>>>(parents, local, ib, J, C, n_chars, rounds, gout, sout);
     return cudaGetLastError();
 }
 

@@ -77,6 +77,11 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
 cudaError_t launch_blocked(const float* local, float* gout, float* sout, const float* ib, const int32_t* lb,
                            const int32_t* mpob, int32_t J, int32_t RB, int64_t n_chars, cudaStream_t st);
 
+// Per-character topology (NEXT-3): parents [n_chars][J] (character-local labels),
+// inverse binds [n_chars][J][12] or nullptr (skin = global); J <= 1024.
+cudaError_t launch_varied(const int32_t* parents, const float* local, const float* ib, int32_t J,
+                          int64_t n_chars, float* gout, float* sout, cudaStream_t st);
+
 // Alg. 1: thread per joint walks all ancestors.
 cudaError_t launch_gateau(const float* local, float* gout, float* sout, const float* ib,
                           const int32_t* parents, int32_t J, int64_t n_chars, cudaStream_t st);
