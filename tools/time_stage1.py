@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Tuning aid: per-launch time of hs_animate (fused Stage 1) on the C5 skeletons at
-bench size (median of 10 launches after 3 warm-ups, CUDA events)."""
+"""Tuning aid: per-call time of hs_animate on the C5 skeletons at bench size, fused and
+two-pass placements and workspace sizes (median of 10 after 3 warm-ups, CUDA events)."""
 import os
 import statistics
 import sys
