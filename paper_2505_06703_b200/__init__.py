@@ -358,7 +358,13 @@ def scan_varied(parents, local, inv_bind=None, global_out=None, skin_out=None, s
     """hs_scan_varied: per-character topology.  parents: CUDA int32 [N, J]; local: CUDA
     float32 [N, J, 3, 4]; inv_bind: CUDA float32 [N, J, 3, 4] or None."""
     import torch
+    if parents.dtype != torch.int32 or local.dtype != torch.float32:
+        raise TypeError("parents must be int32 and local float32 CUDA tensors")
+    if not (parents.is_contiguous() and local.is_contiguous()) or (inv_bind is not None and not inv_bind.is_contiguous()):
+        raise ValueError("tensors must be contiguous")
     n, J = parents.shape
+    if tuple(local.shape) != (n, J, 3, 4):
+        raise ValueError(f"local must be [{n}, {J}, 3, 4]")
     if global_out is None:
         global_out = torch.empty_like(local)
     if skin_out is None and skin:
