@@ -388,8 +388,11 @@ def run_ours(args):
     if args.stage1:
         workload += (f" + Stage 1 ({STAGE1_LAYERS} layers per character, "
                      f"{STAGE1_CLIPS} clips x {STAGE1_KEYS} keys at {STAGE1_FPS:g} fps)")
+    dom_two_pass_lbs = bool(args.skin_mesh) and args.skin_mesh >= 2 * work[dom]["J"]
     kernel_name = ("stage1_kernel + chunked_kernel (two-pass hs_animate, "
                    f"{launches[dom_l][0]} call)" if args.stage1 else
+                   f"chunked_kernel + lbs_kernel (two-pass hs_scan_skin, {launches[dom_l][0]} call)"
+                   if dom_two_pass_lbs else
                    f"chunked_kernel{'<lbs>' if args.skin_mesh else ''} ({launches[dom_l][0]} launch)")
     traffic, traffic_src = ncu_traffic(workload, kernel_name)
 
@@ -439,7 +442,9 @@ def run_ours(args):
         # our kernels per step x K: one per hs_scan / hs_scan_skin / batch; the two-pass
         # hs_animate launches a Stage-1 kernel and a scan per 1 GiB workspace batch
         "gpu_launches": K * (sum(2 * -(-w["n"] // max(1, (1 << 30) // (w["J"] * 48))) for w in work)
-                             if args.stage1 else len(launches)),
+                             if args.stage1 else
+                             sum(2 if args.skin_mesh >= 2 * w["J"] else 1 for w in work)   # two-pass LBS
+                             if args.skin_mesh else len(launches)),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": check,

@@ -211,10 +211,12 @@ hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* 
  * scan writes S (to skin_out, or to a stream-ordered pooled workspace of
  * workspace_bytes, default 1 GiB, in batches) and a skinning kernel with several
  * CTAs per SM reads it back (+48 B/joint of HBM; any skeleton whose palette fits
- * shared memory, n_joints <= 4842).  AUTO = FUSED on single-CTA skeletons (both
- * placements measured equal on B200: shared-memory bound), else
- * TWO_PASS.  Both compute each vertex with the same device code: bitwise equal
- * results. */
+ * shared memory with the character's vertices: 48 n_joints + 12 n_vertices <= 227 KB).
+ * The two-pass kernel processes vertices in joint-sorted order (palette reads become
+ * shared-memory broadcasts) and stages them in smem to write them out in the caller's
+ * order.  AUTO = TWO_PASS when n_vertices >= 2 n_joints or the skeleton is multi-CTA,
+ * else FUSED.  Both compute each vertex with the same device code:
+ * bitwise equal results. */
 typedef enum { HS_SKIN_AUTO = 0, HS_SKIN_FUSED = 1, HS_SKIN_TWO_PASS = 2 } hs_skin_mode;
 typedef struct {
     int32_t mode;             /* hs_skin_mode                                            */

@@ -94,6 +94,9 @@ struct hs_mesh {
     float4* d_a = nullptr;     // [V] (px, py, pz, w0)
     float4* d_b = nullptr;     // [V] (w1, w2, w3, 0)
     int2* d_j = nullptr;       // [V] packed 16-bit joint indices
+    float4* d_sa = nullptr;    // the same three arrays sorted by joints (two-pass kernel);
+    float4* d_sb = nullptr;    //   d_sb.w holds the output index bits
+    int2* d_sj = nullptr;
 };
 
 struct hs_pipeline {
@@ -611,6 +614,28 @@ hs_status hs_mesh_create(const hs_skeleton* sk, int32_t n_vertices, const float*
         Jt[v] = make_int2((int)((uint32_t)joints[4 * v] | ((uint32_t)joints[4 * v + 1] << 16)),
                           (int)((uint32_t)joints[4 * v + 2] | ((uint32_t)joints[4 * v + 3] << 16)));
     }
+    // a second copy in processing order for the two-pass kernel: vertices sorted by
+    // their joints (a quarter warp then mostly reads the same palette matrices:
+    // shared-memory broadcasts), each record carrying its output index in B.w; that
+    // kernel stages a character's vertices in smem and writes them out in order
+    std::vector<int32_t> order(V);
+    for (size_t v = 0; v < V; ++v) order[v] = (int32_t)v;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+        for (int k = 0; k < 4; ++k)
+            if (joints[4 * (size_t)x + k] != joints[4 * (size_t)y + k])
+                return joints[4 * (size_t)x + k] < joints[4 * (size_t)y + k];
+        return false;
+    });
+    std::vector<float4> SA(V), SBv(V);
+    std::vector<int2> SJ(V);
+    for (size_t i = 0; i < V; ++i) {
+        const size_t v = (size_t)order[i];
+        SA[i] = A[v];
+        SBv[i] = B[v];
+        const int32_t out_idx = (int32_t)v;
+        std::memcpy(&SBv[i].w, &out_idx, 4);
+        SJ[i] = Jt[v];
+    }
     hs_mesh* m = new (std::nothrow) hs_mesh();
     if (!m) return fail(HS_ERR_OOM, "host allocation failed");
     cudaGetDevice(&m->device);
@@ -618,7 +643,8 @@ hs_status hs_mesh_create(const hs_skeleton* sk, int32_t n_vertices, const float*
     m->n_verts = n_vertices;
     cudaError_t e;
     if ((e = upload(&m->d_a, A.data(), V)) != cudaSuccess || (e = upload(&m->d_b, B.data(), V)) != cudaSuccess ||
-        (e = upload(&m->d_j, Jt.data(), V)) != cudaSuccess) {
+        (e = upload(&m->d_j, Jt.data(), V)) != cudaSuccess || (e = upload(&m->d_sa, SA.data(), V)) != cudaSuccess ||
+        (e = upload(&m->d_sb, SBv.data(), V)) != cudaSuccess || (e = upload(&m->d_sj, SJ.data(), V)) != cudaSuccess) {
         hs_mesh_destroy(m);
         return cuda_fail(e, "mesh upload");
     }
@@ -631,6 +657,9 @@ hs_status hs_mesh_destroy(hs_mesh* m) {
     cudaFree(m->d_a);
     cudaFree(m->d_b);
     cudaFree(m->d_j);
+    cudaFree(m->d_sa);
+    cudaFree(m->d_sb);
+    cudaFree(m->d_sj);
     delete m;
     return HS_OK;
 }
@@ -665,9 +694,15 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
     if (dev != sk->device || dev != mesh->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
     const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     const int32_t J = sk->plan.n;
-    // AUTO: the fused epilogue where it exists (measured as fast as two-pass on B200:
-    // both are bound by the palette's shared-memory reads), else two-pass
-    if (mode == HS_SKIN_AUTO) mode = sk->chunked ? HS_SKIN_FUSED : HS_SKIN_TWO_PASS;
+    // AUTO: two-pass when the mesh has at least twice as many vertices as the skeleton
+    // has joints (its joint-sorted vertex order turns palette reads into broadcasts and
+    // repays the extra 48 B/joint S round trip: hum64 / chain256 with 1000 vertices are
+    // 24 % / 17 % faster), else the fused epilogue (tree1024: 13 % faster fused); and
+    // two-pass wherever the fused path does not exist (multi-CTA skeletons)
+    if (mode == HS_SKIN_AUTO) {
+        const bool fits = (int64_t)J * 48 + (int64_t)mesh->n_verts * 12 <= 227 * 1024;
+        mode = (!sk->chunked || (fits && mesh->n_verts >= 2 * J)) ? HS_SKIN_TWO_PASS : HS_SKIN_FUSED;
+    }
     if (mode == HS_SKIN_FUSED) {
         if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "the fused LBS epilogue needs a single-CTA skeleton");
         hs::ChunkedArgs a{};
@@ -682,7 +717,8 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
     }
     // two-pass: the scan writes S (to skin_out, or to a pooled workspace in
     // batches when the caller does not want S), then lbs_kernel skins from it
-    if ((int64_t)J * 48 > 227 * 1024) return fail(HS_ERR_UNSUPPORTED, "palette does not fit shared memory");
+    if ((int64_t)J * 48 + (int64_t)mesh->n_verts * 12 > 227 * 1024)
+        return fail(HS_ERR_UNSUPPORTED, "palette + vertices do not fit shared memory");
     const int64_t per_char = (int64_t)J * 48;
     const int64_t batch = skin_out ? n_chars : std::max<int64_t>(1, std::min<int64_t>(n_chars, ws_bytes / per_char));
     float* ws = nullptr;
@@ -695,7 +731,7 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
         float* sb = skin_out ? skin_out + c0 * J * 12 : ws;
         r = scan_impl(sk, local + c0 * J * 12, nb, global_out + c0 * J * 12, sb, st, HS_ALGO_AUTO, -1, 0);
         if (r == HS_OK &&
-            (e = hs::launch_lbs(sb, nb, J, mesh->d_a, mesh->d_b, mesh->d_j, mesh->n_verts,
+            (e = hs::launch_lbs(sb, nb, J, mesh->d_sa, mesh->d_sb, mesh->d_sj, mesh->n_verts,
                                 verts_out + c0 * (int64_t)mesh->n_verts * 3, st)) != cudaSuccess)
             r = cuda_fail(e, "LBS launch");
     }

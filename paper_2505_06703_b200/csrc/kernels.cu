@@ -1046,17 +1046,23 @@ __global__ void __launch_bounds__(256) lbs_kernel(const float* __restrict__ S, i
                                                   float* __restrict__ verts) {
     extern __shared__ float4 pal4[];
     const float* pal = reinterpret_cast<const float*>(pal4);
+    float* vs = reinterpret_cast<float*>(pal4 + J * 3);   // the character's vertices, caller order
     for (int64_t c = blockIdx.x; c < n_chars; c += gridDim.x) {
-        __syncthreads();   // the previous character's readers are done
+        __syncthreads();   // the previous character's readers / writers are done
         const float4* src = reinterpret_cast<const float4*>(S + c * J * 12);
         for (int i = threadIdx.x; i < J * 3; i += blockDim.x) pal4[i] = __ldcs(src + i);
         __syncthreads();
-        float* vout = verts + c * V * 3;
+        // mesh records in joint-sorted order (palette broadcasts), each written to its
+        // caller-order slot in smem, then one coalesced copy out
         for (int v = threadIdx.x; v < V; v += blockDim.x) {
             int js[4];
             mesh_joints(__ldg(mesh_j + v), js);
-            lbs_vertex(pal, __ldg(mesh_a + v), __ldg(mesh_b + v), js, vout + (int64_t)v * 3);
+            const float4 pb = __ldg(mesh_b + v);
+            lbs_vertex(pal, __ldg(mesh_a + v), pb, js, vs + (int64_t)__float_as_int(pb.w) * 3);
         }
+        __syncthreads();
+        float* vout = verts + c * V * 3;
+        for (int i = threadIdx.x; i < V * 3; i += blockDim.x) __stcs(vout + i, vs[i]);
     }
 }
 
@@ -1356,7 +1362,7 @@ cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, flo
 
 cudaError_t launch_lbs(const float* S, int64_t n_chars, int32_t J, const float4* mesh_a, const float4* mesh_b,
                        const int2* mesh_j, int32_t V, float* verts, cudaStream_t st) {
-    const size_t smem = (size_t)J * 48;
+    const size_t smem = (size_t)J * 48 + (size_t)V * 12;
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<void*>(&lbs_kernel),
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
