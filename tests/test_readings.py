@@ -76,3 +76,40 @@ def test_alg3_unclamped_double_counts_and_r8_r9_are_eq1():
     clamped = blocked(clamp=True)
     assert unclamped[100] == 128.0                      # SURVEY §8(c) row 8 scratch value
     assert np.array_equal(clamped, np.arange(1, N + 1))
+
+
+def test_alg4_radix8_reading_is_eq1():
+    """Reading R10 of Alg. 4: 7 serial in-block composes over the
+    ancestors at distances 1..7, then 7 composes with that snapshot at distances 8, 16,
+    ..., 56 (14 in all), then the MaxParentOutBlock walk — Eq. 1 on the chain."""
+    B = 64
+
+    def inblock(j, k):
+        a = ancestor(j, k)
+        return a if a >= 0 and a // B == j // B else -1
+
+    ones = np.ones(N)
+    a1 = ones.copy()
+    for j in range(N):                  # stage A1: serial, distances 1..7
+        for k in range(1, 8):
+            a = inblock(j, k)
+            if a >= 0:
+                a1[j] += ones[a]
+    A = a1.copy()
+    for j in range(N):                  # stage A2: radix-8 strides on the A1 snapshot
+        for k in range(8, 64, 8):
+            a = inblock(j, k)
+            if a >= 0:
+                A[j] += a1[a]
+    out = A.copy()
+    for j in range(N):                  # stage B as Alg. 3
+        m = PARENT[j]
+        while m >= 0 and m // B == j // B:
+            m = PARENT[m]
+        while m >= 0:
+            out[j] += A[m]
+            mm = PARENT[m]
+            while mm >= 0 and mm // B == m // B:
+                mm = PARENT[mm]
+            m = mm
+    assert np.array_equal(out, np.arange(1, N + 1))
