@@ -278,6 +278,20 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Common checks of a scan's pose buffers (hs_scan rules): non-null input and global
+// output, 16-byte alignment, no aliasing between input and outputs, sizes in int64.
+hs_status check_pose_buffers(const float* local, int64_t n_chars, int32_t n_joints, const float* gout,
+                             const float* sout) {
+    if (!local || !gout) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (!aligned16(local) || !aligned16(gout) || (sout && !aligned16(sout)))
+        return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+    if (local == gout || (sout && (local == sout || gout == sout)))
+        return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
+    if (n_chars > (INT64_MAX / 64) / std::max<int32_t>(n_joints, 1))
+        return fail(HS_ERR_INVALID_ARG, "size overflow");
+    return HS_OK;
+}
+
 // Stream-ordered workspaces (split path, two-pass Stage 1) come from a library-owned
 // pool per device that keeps its memory (release threshold = max): after the first
 // frame a workspace costs no driver allocation.  The process's default pool and
@@ -511,12 +525,7 @@ hs_status hs_scan_ex(const hs_skeleton* sk, const float* local, int64_t n_chars,
     if (!sk) return fail(HS_ERR_INVALID_ARG, "skeleton is null");
     if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
     if (n_chars == 0) return HS_OK;
-    if (!local || !global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
-    if (!aligned16(local) || !aligned16(global_out) || (skin_out && !aligned16(skin_out)))
-        return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
-    if (local == global_out || (skin_out && (local == skin_out || global_out == skin_out)))
-        return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
-    if (n_chars > (INT64_MAX / 64) / sk->plan.n) return fail(HS_ERR_INVALID_ARG, "size overflow");
+    if (hs_status r = check_pose_buffers(local, n_chars, sk->plan.n, global_out, skin_out); r != HS_OK) return r;
     int algo = HS_ALGO_AUTO, max_rounds = -1, tile_ctas = 0;
     if (opts) {
         algo = opts->algo;
@@ -567,13 +576,9 @@ hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_
         if (!sk) return fail(HS_ERR_INVALID_ARG, "item skeleton is null");
         if (it.n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
         if (it.n_chars == 0) continue;
-        if (!it.local || !it.global_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
-        if (!aligned16(it.local) || !aligned16(it.global_out) || (it.skin_out && !aligned16(it.skin_out)))
-            return fail(HS_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
-        if (it.local == it.global_out ||
-            (it.skin_out && (it.local == it.skin_out || it.global_out == it.skin_out)))
-            return fail(HS_ERR_INVALID_ARG, "output aliases an input or the other output");
-        if (it.n_chars > (INT64_MAX / 64) / sk->plan.n) return fail(HS_ERR_INVALID_ARG, "size overflow");
+        if (hs_status r = check_pose_buffers(it.local, it.n_chars, sk->plan.n, it.global_out, it.skin_out);
+            r != HS_OK)
+            return r;
         if (dev != sk->device) return fail(HS_ERR_WRONG_DEVICE, "handle belongs to another device");
         if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "batched skeletons must fit the single-CTA path");
         if (K && sk->K != K) return fail(HS_ERR_UNSUPPORTED, "batched skeletons must share the chunk size K");
