@@ -21,8 +21,8 @@ _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libhs.so")
 # A/B experiments may point the binding at another in-tree build of the same sources.
 _LOAD_PATH = os.environ.get("HS_LIB", LIB_PATH)
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu")]
-_DEPS = _SOURCES + [os.path.join(_HERE, "csrc", f) for f in ("plan.hpp", "kernels.cuh")] + [
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu", "kernels_aux.cu")]
+_DEPS = _SOURCES + [os.path.join(_HERE, "csrc", f) for f in ("plan.hpp", "kernels.cuh", "device_util.cuh")] + [
     os.path.join(_ROOT, "include", "hs.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

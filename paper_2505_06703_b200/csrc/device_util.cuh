@@ -1,0 +1,380 @@
+// device_util.cuh — device helpers shared by the sm_100a kernels (kernels.cu,
+// kernels_aux.cu): 3x4 algebra, shared-memory / TMA / mbarrier primitives, the
+// Stage-1 sampling and blending functions (NEXT-1) and the LBS vertex (NEXT-4).
+// Everything is __device__ __forceinline__ in an unnamed namespace (one copy per TU).
+#pragma once
+
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstdint>
+
+#ifndef HS_S1_E
+#define HS_S1_E 1      // Stage-1 elements per thread per pass
+#endif
+#ifndef HS_S1_PIPE
+#define HS_S1_PIPE 0   // issue layer l + 1's key loads before layer l's arithmetic
+#endif
+
+namespace hs {
+namespace {
+
+
+enum : int { kSrcRoot = -1, kSrcPrev = -2, kSrcNone = -3, kSrcRun = -4 };
+
+// ------------------------------------------------------------------ 3x4 algebra
+struct M34 {
+    float v[12];
+};
+
+__device__ __forceinline__ void compose(const float* __restrict__ a, const float* __restrict__ b,
+                                        float* __restrict__ c) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float x = a[4 * r + 0] * b[k];
+            x = fmaf(a[4 * r + 1], b[4 + k], x);
+            c[4 * r + k] = fmaf(a[4 * r + 2], b[8 + k], x);
+        }
+        float t = fmaf(a[4 * r + 0], b[3], a[4 * r + 3]);
+        t = fmaf(a[4 * r + 1], b[7], t);
+        c[4 * r + 3] = fmaf(a[4 * r + 2], b[11], t);
+    }
+}
+
+__device__ __forceinline__ void ld3(const float* p, float* v) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float4 a = q[0], b = q[1], c = q[2];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
+}
+
+__device__ __forceinline__ void st3(float* p, const float* v) {
+    float4* q = reinterpret_cast<float4*>(p);
+    q[0] = make_float4(v[0], v[1], v[2], v[3]);
+    q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    q[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
+__device__ __forceinline__ void ldg3(const float* p, float* v) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    v[8] = c.x; v[9] = c.y; v[10] = c.z; v[11] = c.w;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) {
+    }
+}
+// 1D bulk copy global -> shared, completion signalled on an mbarrier (TMA, UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// 1D bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_consumers(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// ================================================================== Stage 1 (NEXT-1)
+// Keyframe sampling, layer blending and TRS -> 3x4 (
+// DESIGN.md readings R19-R23), fused ahead of the scan: the local pose is computed
+// in shared memory instead of being read from HBM.  Keys on the device are packed
+// per (clip, key) row as planar arrays over joints: float4 {tx,ty,tz,qw}, float4
+// {qx,qy,qz,sx}, float2 {sy,sz} (40 B per key and joint, see load_keys).
+// The time -> key decision uses the oracle's exact fp32 operation sequence.
+__device__ __forceinline__ void key_index(float t, int n_keys, float fps, float duration, int wrap,
+                                          int& k0, float& a) {
+    if (n_keys <= 1) { k0 = 0; a = 0.0f; return; }
+    float tt;
+    if (wrap == 1) {
+        const float q = floorf(__fdiv_rn(t, duration));
+        tt = __fsub_rn(t, __fmul_rn(q, duration));
+        if (tt < 0.0f) tt = 0.0f;
+    } else {
+        tt = t < 0.0f ? 0.0f : (t > duration ? duration : t);
+    }
+    const float u = __fmul_rn(tt, fps);
+    const float kf = floorf(u);
+    float frac = __fsub_rn(u, kf);
+    int ki = (int)kf;
+    if (ki >= n_keys - 1) { ki = n_keys - 1; frac = 0.0f; }
+    if (ki < 0) { ki = 0; frac = 0.0f; }
+    k0 = ki;
+    a = frac;
+}
+
+// MUFU approximations (rel. error ~2^-22): a unit quaternion's norm and the weight
+// sum are far from denormal, so the IEEE fix-up paths of rsqrtf / '/' buy nothing.
+__device__ __forceinline__ float rsqrt_fast(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Layer descriptor of one (character, layer) of a tile, written by the producer
+// warp ahead of the consumers (smem ring, one slot per stage):
+//   x = float4 index of key k0 of the layer's clip at joint 0,
+//   y = float4 offset from key k0 to key k0 + 1 (0 when frac == 0: one key),
+//   z = frac (fp32 bits), w = weight (fp32 bits).
+__device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
+    int k0;
+    float fr;
+    key_index(__int_as_float(L.y), a.n_keys, a.fps, a.duration, a.wrap, k0, fr);
+    const int Jp = a.seg[0].J + (a.seg[0].J & 1);   // joints padded to even (16-byte planes)
+    const int row = (L.x * a.n_keys + k0) * Jp * 10;
+    return make_int4(row, fr != 0.0f ? Jp * 10 : 0, __float_as_int(fr), L.z);
+}
+
+// Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
+__device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, float4 x1, float4 y1,
+                                           float2 z1, float a, float* trs) {
+    if (a == 0.0f) {   // on a key: that key exactly (R21)
+        trs[0] = x0.x; trs[1] = x0.y; trs[2] = x0.z; trs[3] = x0.w;
+        trs[4] = y0.x; trs[5] = y0.y; trs[6] = y0.z;
+        trs[7] = y0.w; trs[8] = z0.x; trs[9] = z0.y;
+        return;
+    }
+    const float b = 1.0f - a;
+    trs[0] = b * x0.x + a * x1.x; trs[1] = b * x0.y + a * x1.y; trs[2] = b * x0.z + a * x1.z;
+    trs[7] = b * y0.w + a * y1.w; trs[8] = b * z0.x + a * z1.x; trs[9] = b * z0.y + a * z1.y;
+    const float d = x0.w * x1.w + y0.x * y1.x + y0.y * y1.y + y0.z * y1.z;
+    const float as = d < 0.0f ? -a : a;
+    float qw = b * x0.w + as * x1.w, qx = b * y0.x + as * y1.x, qy = b * y0.y + as * y1.y,
+          qz = b * y0.z + as * y1.z;
+    const float inv = rsqrt_fast(qw * qw + qx * qx + qy * qy + qz * qz);
+    trs[3] = qw * inv; trs[4] = qx * inv; trs[5] = qy * inv; trs[6] = qz * inv;
+}
+
+__device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
+    const float w = trs[3], x = trs[4], y = trs[5], z = trs[6];
+    const float sx = trs[7], sy = trs[8], sz = trs[9];
+    m[0] = (1.0f - 2.0f * (y * y + z * z)) * sx; m[1] = 2.0f * (x * y - w * z) * sy;
+    m[2] = 2.0f * (x * z + w * y) * sz;          m[3] = trs[0];
+    m[4] = 2.0f * (x * y + w * z) * sx;          m[5] = (1.0f - 2.0f * (x * x + z * z)) * sy;
+    m[6] = 2.0f * (y * z - w * x) * sz;          m[7] = trs[1];
+    m[8] = 2.0f * (x * z - w * y) * sx;          m[9] = 2.0f * (y * z + w * x) * sy;
+    m[10] = (1.0f - 2.0f * (x * x + y * y)) * sz; m[11] = trs[2];
+}
+
+// Local poses of E tile elements at once (E independent (character, joint) pairs,
+// so each layer's 6 * E key loads are in flight together; PIPE also issues layer
+// l + 1's loads before layer l's arithmetic): sample every layer, blend (DESIGN.md
+// R22), TRS -> 3x4, store into the tile in smem.
+struct KeyPair {
+    float4 x0, y0, x1, y1;
+    float2 z0, z1;
+};
+
+// Keys are planar, 40 bytes per (key, joint): per (clip, key) row of 10 * Jp floats
+// (Jp = joints padded to even), plane 0 = float4 {t, qw}, plane 1 = float4 {q.xyz, sx},
+// plane 2 = float2 {sy, sz}; a warp's loads of one plane over consecutive joints are
+// contiguous.  d.x = the row's float offset, d.y = the step to key k0 + 1 (0: one key).
+__device__ __forceinline__ KeyPair load_keys(const float* __restrict__ keys, int4 d, int j, int Jp) {
+    const float* p0 = keys + d.x;
+    const float* p1 = p0 + d.y;
+    KeyPair k;
+    k.x0 = __ldg(reinterpret_cast<const float4*>(p0) + j);
+    k.y0 = __ldg(reinterpret_cast<const float4*>(p0 + 4 * Jp) + j);
+    k.z0 = __ldg(reinterpret_cast<const float2*>(p0 + 8 * Jp) + j);
+    k.x1 = __ldg(reinterpret_cast<const float4*>(p1) + j);
+    k.y1 = __ldg(reinterpret_cast<const float4*>(p1 + 4 * Jp) + j);
+    k.z1 = __ldg(reinterpret_cast<const float2*>(p1 + 8 * Jp) + j);
+    return k;
+}
+
+template <int E, bool PIPE>
+__device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, const int4* const* dsc,
+                                             const int* j, const bool* valid, int nl, int Jp, float* L,
+                                             const int* off) {
+    float acc[E][10], q0[E][4], wsum[E];
+    KeyPair kp[E];
+    int4 d[E];
+    if (PIPE) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            d[e] = valid[e] ? dsc[e][0] : make_int4(0, 0, 0, 0);
+            kp[e] = load_keys(keys, d[e], j[e], Jp);
+        }
+    }
+    for (int l = 0; l < nl; ++l) {
+        KeyPair cur[E];
+        int4 dc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (PIPE) {
+                cur[e] = kp[e];
+                dc[e] = d[e];
+                if (l + 1 < nl) {
+                    d[e] = valid[e] ? dsc[e][l + 1] : make_int4(0, 0, 0, 0);
+                    kp[e] = load_keys(keys, d[e], j[e], Jp);
+                }
+            } else {
+                dc[e] = valid[e] ? dsc[e][l] : make_int4(0, 0, 0, 0);
+                cur[e] = load_keys(keys, dc[e], j[e], Jp);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            float s[10];
+            sample_trs(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
+                       __int_as_float(dc[e].z), s);
+            const float w = __int_as_float(dc[e].w);
+            if (nl == 1) {   // one layer: the sample itself (R22)
+#pragma unroll
+                for (int c = 0; c < 10; ++c) acc[e][c] = s[c];
+            } else if (l == 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q0[e][c] = s[3 + c];
+#pragma unroll
+                for (int c = 0; c < 10; ++c) acc[e][c] = w * s[c];
+                wsum[e] = w;
+            } else {
+                const float dq = s[3] * q0[e][0] + s[4] * q0[e][1] + s[5] * q0[e][2] + s[6] * q0[e][3];
+                const float ws = dq < 0.0f ? -w : w;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[e][c] += w * s[c];
+#pragma unroll
+                for (int c = 3; c < 7; ++c) acc[e][c] += ws * s[c];
+#pragma unroll
+                for (int c = 7; c < 10; ++c) acc[e][c] += w * s[c];
+                wsum[e] += w;
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (!valid[e]) continue;
+        if (nl > 1) {
+            const float iw = rcp_fast(wsum[e]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[e][c] *= iw;
+#pragma unroll
+            for (int c = 7; c < 10; ++c) acc[e][c] *= iw;
+            const float inv = rsqrt_fast(acc[e][3] * acc[e][3] + acc[e][4] * acc[e][4] +
+                                     acc[e][5] * acc[e][5] + acc[e][6] * acc[e][6]);
+#pragma unroll
+            for (int c = 3; c < 7; ++c) acc[e][c] *= inv;
+        }
+        float m[12];
+        trs_to_m34(acc[e], m);
+        st3(L + off[e] * 12, m);
+    }
+}
+
+// Phase 0 over one tile: element o = (character o / J, joint o % J) of the tile,
+// consecutive elements on consecutive threads (coalesced key reads), E per thread
+// per pass.
+template <int E, bool PIPE>
+__device__ __forceinline__ void stage1_tile(const float* __restrict__ keys, const int4* dsc_t, int nel,
+                                            int J, int nl, int t, int NC, float* L) {
+    // element o = cl * J + j, advanced by E * NC per pass without a division
+    const int step = E * NC, step_c = step / J, step_j = step - step_c * J;
+    int cl0 = t / J, j0 = t - (t / J) * J;
+    for (int o = t; o < nel; o += step) {
+        int off[E], j[E];
+        bool valid[E];
+        const int4* dsc[E];
+        int cl = cl0, jj = j0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            off[q] = o + q * NC;
+            valid[q] = off[q] < nel;
+            j[q] = valid[q] ? jj : 0;
+            dsc[q] = dsc_t + (valid[q] ? cl : 0) * nl;
+            if (q + 1 < E) {
+                jj += NC;
+                while (jj >= J) { jj -= J; ++cl; }
+            }
+        }
+        stage1_elems<E, PIPE>(keys, dsc, j, valid, nl, J + (J & 1), L, off);
+        cl0 += step_c;
+        j0 += step_j;
+        if (j0 >= J) { j0 -= J; ++cl0; }
+    }
+}
+
+// ================================================================== LBS (NEXT-4)
+// One skinned vertex (R24): sum_k w_k S[j_k] (p, 1) with the character's
+// skin palette `pal` ([J][12], shared memory); joints pre-multiplied by 12.  The
+// fused epilogue and the two-pass kernel share it, so their vertices are bitwise equal.
+__device__ __forceinline__ void lbs_vertex(const float* pal, float4 pa, float4 pb, const int* js, float* d) {
+    const float ws[4] = {pa.w, pb.x, pb.y, pb.z};
+    float x = 0.f, y = 0.f, z = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float m[12];
+        ld3(pal + js[q], m);
+        const float px = fmaf(m[0], pa.x, fmaf(m[1], pa.y, fmaf(m[2], pa.z, m[3])));
+        const float py = fmaf(m[4], pa.x, fmaf(m[5], pa.y, fmaf(m[6], pa.z, m[7])));
+        const float pz = fmaf(m[8], pa.x, fmaf(m[9], pa.y, fmaf(m[10], pa.z, m[11])));
+        x = fmaf(ws[q], px, x);
+        y = fmaf(ws[q], py, y);
+        z = fmaf(ws[q], pz, z);
+    }
+    d[0] = x; d[1] = y; d[2] = z;
+}
+
+__device__ __forceinline__ void mesh_joints(int2 jj, int* js) {
+    js[0] = (jj.x & 0xffff) * 12; js[1] = (int)((uint32_t)jj.x >> 16) * 12;
+    js[2] = (jj.y & 0xffff) * 12; js[3] = (int)((uint32_t)jj.y >> 16) * 12;
+}
+
+}  // namespace
+}  // namespace hs

@@ -57,6 +57,7 @@ struct ChunkedArgs {
     int32_t n_verts;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
+int sm_count();   // SMs of the current device (cached)
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 // Linear blend skinning from skin poses in HBM (two-pass hs_scan_skin): S [n_chars][J][12].
 cudaError_t launch_lbs(const float* S, int64_t n_chars, int32_t J, const float4* mesh_a, const float4* mesh_b,
