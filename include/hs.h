@@ -228,6 +228,17 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
                           float* global_out, float* skin_out, float* verts_out, void* cuda_stream,
                           const hs_skin_opts* opts);
 
+/* Skinning alone, from skin poses already on the device (e.g. hs_animate's skin_out):
+ *   skin     device fp32 [n_chars][n_joints][3][4] (16-byte aligned), n_joints = the
+ *            mesh's skeleton
+ *   verts_out device fp32 [n_chars][n_vertices][3] (4-byte aligned)
+ * The two-pass LBS kernel (joint-sorted vertices, smem-staged output; the palette and
+ * the vertices must fit shared memory: HS_ERR_UNSUPPORTED otherwise).  Together with
+ * hs_animate this runs the paper's whole GPU pipeline: simulation,
+ * Hierarchy-Scan, bind, skinning. */
+hs_status hs_skin_vertices(const hs_mesh* mesh, const float* skin, int64_t n_chars, float* verts_out,
+                           void* cuda_stream);
+
 /* ---------------------------------------------------------------------------
  * Stage 1 fused ahead of the scan ("Sample
  * animation data and generate local pose in local space").

@@ -112,6 +112,7 @@ def lib():
     L.hs_mesh_create.argtypes = [vp, i32, vp, vp, vp, ctypes.POINTER(vp)]
     L.hs_mesh_destroy.argtypes = [vp]
     L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
+    L.hs_skin_vertices.argtypes = [vp, vp, i64, vp, vp]
     L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_SkinOpts)]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
@@ -327,6 +328,18 @@ class Mesh:
         self._h = None
 
     __del__ = close
+
+
+def skin_vertices(mesh: Mesh, skin, verts_out=None, stream=None):
+    """hs_skin_vertices: LBS from skin poses on the device (CUDA float32 [N, J, 3, 4])."""
+    import torch
+    n = skin.shape[0]
+    if verts_out is None:
+        verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=skin.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_skin_vertices(mesh.handle, skin.data_ptr(), n, verts_out.data_ptr(), st), "hs_skin_vertices")
+    return verts_out
 
 
 SKIN_MODE = {"auto": 0, "fused": 1, "two_pass": 2}

@@ -744,6 +744,26 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
     return r;
 }
 
+hs_status hs_skin_vertices(const hs_mesh* mesh, const float* skin, int64_t n_chars, float* verts_out,
+                           void* cuda_stream) {
+    if (!mesh) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!skin || !verts_out) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (!aligned16(skin) || (reinterpret_cast<uintptr_t>(verts_out) & 3))
+        return fail(HS_ERR_INVALID_ARG, "skin must be 16-byte aligned, vertices 4-byte");
+    if (n_chars > (INT64_MAX / 64) / std::max(mesh->n_joints, mesh->n_verts))
+        return fail(HS_ERR_INVALID_ARG, "size overflow");
+    if ((int64_t)mesh->n_joints * 48 + (int64_t)mesh->n_verts * 12 > 227 * 1024)
+        return fail(HS_ERR_UNSUPPORTED, "palette + vertices do not fit shared memory");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != mesh->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    const cudaError_t e = hs::launch_lbs(skin, n_chars, mesh->n_joints, mesh->d_sa, mesh->d_sb, mesh->d_sj,
+                                         mesh->n_verts, verts_out, static_cast<cudaStream_t>(cuda_stream));
+    return e == cudaSuccess ? HS_OK : cuda_fail(e, "LBS launch");
+}
+
 hs_status hs_scan_skin(const hs_skeleton* sk, const hs_mesh* mesh, const float* local, int64_t n_chars,
                        float* global_out, float* skin_out, float* verts_out, void* cuda_stream) {
     return hs_scan_skin_ex(sk, mesh, local, n_chars, global_out, skin_out, verts_out, cuda_stream, nullptr);

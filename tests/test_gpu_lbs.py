@@ -151,3 +151,31 @@ def test_two_pass_lbs_on_multi_cta_skeleton():
     torch.cuda.synchronize()
     G, S = oracle.scan(par, loc, ib)
     assert np.abs(v.cpu().numpy() - oracle.skin_vertices(S, *mesh)).max() <= TOL_VERTS
+
+
+def test_full_pipeline_animate_then_skin_vertices():
+    """The paper's whole GPU pipeline: Stage 1 -> scan -> bind (hs_animate),
+    then skinning from the skin poses (hs_skin_vertices), against the fp64 oracles."""
+    par = hsgen.skeleton("hum64")
+    J = 64
+    keys = hsgen.clips(91, J, 4, 13)
+    lay = hsgen.layers(92, 40, 2, 4, 1.2)
+    ib = hsgen.inv_bind(93, J)
+    mesh = hsgen.mesh(94, par, 800)
+    sk = hs.Skeleton(par, ib)
+    cs = hs.ClipSet(sk, keys, 30.0, 1)
+    m = hs.Mesh(sk, *mesh)
+    g, s = hs.animate(sk, cs, lay)
+    v = hs.skin_vertices(m, s)
+    torch.cuda.synchronize()
+    G, S = oracle.animate(par, keys, 30.0, 1, lay, ib)
+    want = oracle.skin_vertices(S, *mesh)
+    assert np.abs(v.cpu().numpy() - want).max() <= TOL_VERTS
+    # and bitwise equal to the LBS of the GPU skin poses computed by hs_scan_skin's kernel
+    x = torch.from_numpy(np.ascontiguousarray(
+        np.stack([oracle.animate(par, keys, 30.0, 1, lay[c:c + 1], None, return_local=True)[2][0]
+                  for c in range(2)]).astype(np.float32))).cuda()
+    _, s2, v2 = hs.scan_skin(sk, m, x, skin=True, mode="two_pass")
+    v3 = hs.skin_vertices(m, s2)
+    torch.cuda.synchronize()
+    assert torch.equal(v2, v3)
