@@ -281,6 +281,10 @@ def run_ours(args):
             item["lay_np"] = lay
             item["layers"] = torch.from_numpy(lay.view(np.int32).reshape(n, STAGE1_LAYERS, 4)).to(dev)
             item["g"] = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
+            if args.skin_mesh:   # the whole pipeline: Stage 1 -> scan -> bind -> skinning
+                item["mesh_np"] = hsgen.mesh(200 + type_, par, args.skin_mesh, type_=type_)
+                item["mesh"] = hs.Mesh(sk, *item["mesh_np"])
+                item["verts"] = torch.empty((n, args.skin_mesh, 3), dtype=torch.float32, device=dev)
         else:
             local = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
             if n:
@@ -322,6 +326,8 @@ def run_ours(args):
                 w = work[members[0]]
                 if args.stage1:
                     hs.animate(w["sk"], w["cs"], w["layers"], w["g"], w["s"], stream=stream)
+                    if args.skin_mesh:
+                        hs.skin_vertices(w["mesh"], w["s"], w["verts"], stream=stream)
                 elif args.skin_mesh:
                     hs.scan_skin(w["sk"], w["mesh"], w["local"], w["g"], w["s"], w["verts"], stream=stream)
                 else:
@@ -371,7 +377,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel launch (largest byte share: the batch launch,
     # else tree1024's)
     bpj = STAGE1_BYTES_PER_JOINT if args.stage1 else BYTES_PER_JOINT
-    per_char_extra = 16 * STAGE1_LAYERS if args.stage1 else 12 * args.skin_mesh
+    per_char_extra = (16 * STAGE1_LAYERS if args.stage1 else 0) + 12 * args.skin_mesh
 
     def launch_bytes(li):
         return sum(bpj * work[t]["n"] * work[t]["J"] + per_char_extra * work[t]["n"]
@@ -384,13 +390,14 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     workload = WORKLOAD_NAME[args.config]
     if args.skin_mesh:
-        workload += f" + fused LBS ({args.skin_mesh}-vertex mesh per character)"
+        workload += f" + LBS ({args.skin_mesh}-vertex mesh per character)"
     if args.stage1:
         workload += (f" + Stage 1 ({STAGE1_LAYERS} layers per character, "
                      f"{STAGE1_CLIPS} clips x {STAGE1_KEYS} keys at {STAGE1_FPS:g} fps)")
     dom_two_pass_lbs = bool(args.skin_mesh) and args.skin_mesh >= 2 * work[dom]["J"]
-    kernel_name = ("stage1_kernel + chunked_kernel (two-pass hs_animate, "
-                   f"{launches[dom_l][0]} call)" if args.stage1 else
+    kernel_name = (f"stage1_kernel + chunked_kernel{' + lbs_kernel' if args.skin_mesh else ''} (two-pass "
+                   f"hs_animate{' + hs_skin_vertices' if args.skin_mesh else ''}, {launches[dom_l][0]} call)"
+                   if args.stage1 else
                    f"chunked_kernel + lbs_kernel (two-pass hs_scan_skin, {launches[dom_l][0]} call)"
                    if dom_two_pass_lbs else
                    f"chunked_kernel{'<lbs>' if args.skin_mesh else ''} ({launches[dom_l][0]} launch)")
@@ -441,7 +448,8 @@ def run_ours(args):
         "clocks": sampler.summary(),
         # our kernels per step x K: one per hs_scan / hs_scan_skin / batch; the two-pass
         # hs_animate launches a Stage-1 kernel and a scan per 1 GiB workspace batch
-        "gpu_launches": K * (sum(2 * -(-w["n"] // max(1, (1 << 30) // (w["J"] * 48))) for w in work)
+        "gpu_launches": K * (sum(2 * -(-w["n"] // max(1, (1 << 30) // (w["J"] * 48))) + (1 if args.skin_mesh else 0)
+                                 for w in work)
                              if args.stage1 else
                              sum(2 if args.skin_mesh >= 2 * w["J"] else 1 for w in work)   # two-pass LBS
                              if args.skin_mesh else len(launches)),
@@ -552,10 +560,10 @@ def run_e2e(work, args, hs, torch, dist, world):
     """Same metric through the public host-buffer API (hs_scan_host_batch): every step
     copies that step's local poses H2D from pinned memory and reads global + skin back
     D2H."""
-    if args.stage1:
-        return run_e2e_stage1(work, args, hs, torch, dist, world)
     if args.skin_mesh:   # the host-buffer pipeline has no LBS entry point
         return None
+    if args.stage1:
+        return run_e2e_stage1(work, args, hs, torch, dist, world)
     pl = hs.Pipeline(batch_bytes=256 << 20)
     slices = []
     h2d = d2h = 0
