@@ -324,10 +324,11 @@ def run_ours(args):
                 hs.scan_batch(batch_items, stream=stream)
             else:
                 w = work[members[0]]
-                if args.stage1:
+                if args.stage1 and args.skin_mesh:   # the whole pipeline in one call
+                    hs.animate_skin(w["sk"], w["cs"], w["layers"], w["mesh"], w["g"], w["s"], w["verts"],
+                                    stream=stream)
+                elif args.stage1:
                     hs.animate(w["sk"], w["cs"], w["layers"], w["g"], w["s"], stream=stream)
-                    if args.skin_mesh:
-                        hs.skin_vertices(w["mesh"], w["s"], w["verts"], stream=stream)
                 elif args.skin_mesh:
                     hs.scan_skin(w["sk"], w["mesh"], w["local"], w["g"], w["s"], w["verts"], stream=stream)
                 else:
@@ -395,8 +396,8 @@ def run_ours(args):
         workload += (f" + Stage 1 ({STAGE1_LAYERS} layers per character, "
                      f"{STAGE1_CLIPS} clips x {STAGE1_KEYS} keys at {STAGE1_FPS:g} fps)")
     dom_two_pass_lbs = bool(args.skin_mesh) and args.skin_mesh >= 2 * work[dom]["J"]
-    kernel_name = (f"stage1_kernel + chunked_kernel{' + lbs_kernel' if args.skin_mesh else ''} (two-pass "
-                   f"hs_animate{' + hs_skin_vertices' if args.skin_mesh else ''}, {launches[dom_l][0]} call)"
+    kernel_name = (f"stage1_kernel + chunked_kernel{'<lbs>' if args.skin_mesh else ''} (two-pass "
+                   f"{'hs_animate_skin' if args.skin_mesh else 'hs_animate'}, {launches[dom_l][0]} call)"
                    if args.stage1 else
                    f"chunked_kernel + lbs_kernel (two-pass hs_scan_skin, {launches[dom_l][0]} call)"
                    if dom_two_pass_lbs else

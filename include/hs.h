@@ -290,6 +290,14 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
                         int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
                         const hs_animate_opts* opts);
 
+/* The paper's whole GPU pipeline in one call: Stage 1 (two-pass
+ * placement), Hierarchy-Scan, bind and linear blend skinning of `mesh` (hs_mesh
+ * below; the scan + skinning of each Stage-1 batch runs as hs_scan_skin with AUTO
+ * placement).  Outputs as hs_animate plus verts_out [n_chars][n_vertices][3]. */
+hs_status hs_animate_skin(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                          int64_t n_chars, const hs_mesh* mesh, float* global_out, float* skin_out,
+                          float* verts_out, void* cuda_stream);
+
 /* Destroy a handle (NULL-safe).  The caller guarantees no hs_scan using it is
  * still in flight.  Frees its device tables with cudaFree (device-synchronising). */
 hs_status hs_destroy(hs_skeleton* sk);

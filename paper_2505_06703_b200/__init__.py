@@ -113,6 +113,7 @@ def lib():
     L.hs_mesh_destroy.argtypes = [vp]
     L.hs_scan_skin.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
     L.hs_skin_vertices.argtypes = [vp, vp, i64, vp, vp]
+    L.hs_animate_skin.argtypes = [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]
     L.hs_scan_skin_ex.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, ctypes.POINTER(_SkinOpts)]
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
@@ -439,6 +440,28 @@ def animate(sk: "Skeleton", clips: ClipSet, layers, global_out=None, skin_out=No
                                None if skin_out is None else skin_out.data_ptr(), st, ctypes.byref(opts)),
            "hs_animate")
     return global_out, skin_out
+
+
+def animate_skin(sk: "Skeleton", clips: "ClipSet", layers, mesh: "Mesh", global_out=None, skin_out=None,
+                 verts_out=None, stream=None, skin: bool = False):
+    """hs_animate_skin: Stage 1 -> scan -> bind -> skinning.  Returns (global, skin, verts)."""
+    import torch
+    if isinstance(layers, np.ndarray):
+        layers = torch.from_numpy(np.ascontiguousarray(layers).view(np.int32).reshape(
+            layers.shape[0], layers.shape[1], 4)).cuda()
+    n, nl = layers.shape[0], layers.shape[1]
+    if global_out is None:
+        global_out = torch.empty((n, sk.n_joints, 3, 4), dtype=torch.float32, device=layers.device)
+    if skin_out is None and skin:
+        skin_out = torch.empty_like(global_out)
+    if verts_out is None:
+        verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=layers.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else (
+        stream if isinstance(stream, int) else stream.cuda_stream)
+    _check(lib().hs_animate_skin(sk.handle, clips.handle, layers.data_ptr(), nl, n, mesh.handle,
+                                 global_out.data_ptr(), None if skin_out is None else skin_out.data_ptr(),
+                                 verts_out.data_ptr(), st), "hs_animate_skin")
+    return global_out, skin_out, verts_out
 
 
 class Pipeline:

@@ -808,9 +808,9 @@ hs_status hs_clipset_destroy(hs_clipset* cs) {
     return HS_OK;
 }
 
-hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
-                        int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
-                        const hs_animate_opts* opts) {
+static hs_status animate_impl(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                       int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
+                       const hs_animate_opts* opts, const hs_mesh* mesh, float* verts_out) {
     if (!sk || !cs) return fail(HS_ERR_INVALID_ARG, "null handle");
     if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
     int mode = HS_ANIMATE_AUTO;
@@ -833,6 +833,8 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
     cudaGetDevice(&dev);
     if (dev != sk->device || dev != cs->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
     const cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (mesh && mode == HS_ANIMATE_FUSED)
+        return fail(HS_ERR_UNSUPPORTED, "Stage 1 + skinning runs the two-pass placement");
     if (mode == HS_ANIMATE_FUSED) {
         if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "the fused Stage 1 needs a single-CTA skeleton");
         return scan_impl(sk, nullptr, n_chars, global_out, skin_out, st, HS_ALGO_CHUNKED, -1, 0, cs, layers,
@@ -862,11 +864,32 @@ hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void*
     for (int64_t c0 = 0; c0 < n_chars && r == HS_OK; c0 += batch) {
         const int64_t nb = std::min(batch, n_chars - c0);
         if ((e = hs::launch_stage1(s1, c0, nb, ws, st)) != cudaSuccess) { r = cuda_fail(e, "Stage-1 launch"); break; }
-        r = scan_impl(sk, ws, nb, global_out + c0 * J * 12, skin_out ? skin_out + c0 * J * 12 : nullptr, st,
-                      HS_ALGO_AUTO, -1, 0);   // single-CTA or multi-CTA path
+        if (mesh)   // scan + bind + skinning of the batch (fused or two-pass LBS, AUTO)
+            r = hs_scan_skin_ex(sk, mesh, ws, nb, global_out + c0 * J * 12,
+                                skin_out ? skin_out + c0 * J * 12 : nullptr,
+                                verts_out + c0 * (int64_t)mesh->n_verts * 3, cuda_stream, nullptr);
+        else
+            r = scan_impl(sk, ws, nb, global_out + c0 * J * 12, skin_out ? skin_out + c0 * J * 12 : nullptr,
+                          st, HS_ALGO_AUTO, -1, 0);   // single-CTA or multi-CTA path
     }
     cudaFreeAsync(ws, st);
     return r;
+}
+
+hs_status hs_animate_ex(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                        int64_t n_chars, float* global_out, float* skin_out, void* cuda_stream,
+                        const hs_animate_opts* opts) {
+    return animate_impl(sk, cs, layers, n_layers, n_chars, global_out, skin_out, cuda_stream, opts, nullptr,
+                        nullptr);
+}
+
+hs_status hs_animate_skin(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,
+                          int64_t n_chars, const hs_mesh* mesh, float* global_out, float* skin_out,
+                          float* verts_out, void* cuda_stream) {
+    if (!mesh || !verts_out) return fail(HS_ERR_INVALID_ARG, "null mesh or vertex buffer");
+    if (mesh->n_joints != (sk ? sk->plan.n : -1)) return fail(HS_ERR_INVALID_ARG, "mesh built for another skeleton");
+    return animate_impl(sk, cs, layers, n_layers, n_chars, global_out, skin_out, cuda_stream, nullptr, mesh,
+                        verts_out);
 }
 
 hs_status hs_animate(const hs_skeleton* sk, const hs_clipset* cs, const void* layers, int32_t n_layers,

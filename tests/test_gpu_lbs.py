@@ -179,3 +179,24 @@ def test_full_pipeline_animate_then_skin_vertices():
     v3 = hs.skin_vertices(m, s2)
     torch.cuda.synchronize()
     assert torch.equal(v2, v3)
+
+
+def test_animate_skin_one_call_matches_two_calls():
+    """hs_animate_skin (Stage 1 -> scan -> bind -> LBS in one call) equals hs_animate followed
+    by the same skinning placement, bit for bit, and stays within the oracle bounds."""
+    for name, V in (("hum64", 700), ("tree1024", 900)):
+        par = hsgen.skeleton(name)
+        J = len(par)
+        keys = hsgen.clips(95, J, 3, 11)
+        lay = hsgen.layers(96, 7, 2, 3, 1.0)
+        ib = hsgen.inv_bind(97, J)
+        mesh = hsgen.mesh(98, par, V)
+        sk = hs.Skeleton(par, ib)
+        cs = hs.ClipSet(sk, keys, 30.0, 1)
+        m = hs.Mesh(sk, *mesh)
+        g, s, v = hs.animate_skin(sk, cs, lay, m, skin=True)
+        g2, s2 = hs.animate(sk, cs, lay)
+        torch.cuda.synchronize()
+        assert torch.equal(g, g2) and torch.equal(s, s2)
+        G, S = oracle.animate(par, keys, 30.0, 1, lay, ib)
+        assert np.abs(v.cpu().numpy() - oracle.skin_vertices(S, *mesh)).max() <= TOL_VERTS
