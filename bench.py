@@ -303,7 +303,7 @@ def run_ours(args):
     joints_rank = sum(w["n"] * w["J"] for w in work)
 
     # auto: one batch launch only when every type's crowd is small (under ~32 tiles per
-    # SM, where per-launch fill/drain and tails dominate; profiles/r01d_next3_sweep.json);
+    # SM, where per-launch fill/drain and tails dominate; profiles/r01f_next3_sweep.json);
     # C5's crowds are thousands of tiles per SM, where per-type launches measured 3%
     # faster (the multi-segment kernel's program switch costs registers)
     small = all(-(-w["n"] // max(1, w["sk"].query("tile_chars"))) < 32 * 148 for w in work)
