@@ -391,6 +391,12 @@ hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_lo
  * through every item's characters, so the copy engines do not drain between skeleton
  * types.  Errors as hs_scan_host. */
 hs_status hs_scan_host_batch(hs_pipeline* pl, const hs_batch_item* items, int32_t n_items);
+
+/* Stage 1 + scan + bind from HOST buffers: h_layers [n_chars][n_layers] hs_layer (host),
+ * outputs as hs_scan_host.  Per batch: layers up, hs_animate (two-pass) on the device,
+ * global and skin poses back. */
+hs_status hs_animate_host(hs_pipeline* pl, const hs_skeleton* sk, const hs_clipset* cs, const void* h_layers,
+                          int32_t n_layers, int64_t n_chars, float* h_global, float* h_skin);
 hs_status hs_pipeline_destroy(hs_pipeline* pl);
 
 #ifdef __cplusplus

@@ -118,6 +118,7 @@ def lib():
     L.hs_pipeline_create.argtypes = [i64, ctypes.POINTER(vp)]
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_scan_host_batch.argtypes = [vp, ctypes.POINTER(_BatchItem), i32]
+    L.hs_animate_host.argtypes = [vp, vp, vp, vp, i32, i64, vp, vp]
     L.hs_pipeline_destroy.argtypes = [vp]
     for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
               "hs_skeleton_query", "hs_plan_create", "hs_plan_create_ex", "hs_plan_query", "hs_plan_export",
@@ -481,6 +482,16 @@ class Pipeline:
             n_chars = h_local.shape[0]
         _check(lib().hs_scan_host(self._h, sk.handle, ptr(h_local), n_chars, ptr(h_global),
                                   ptr(h_skin)), "hs_scan_host")
+
+    def animate_host(self, sk: Skeleton, clips: "ClipSet", h_layers, h_global, h_skin):
+        """hs_animate_host: host layer states [N, n_layers] (LAYER_DTYPE array or an int32
+        [N, n_layers, 4] tensor, pinned for full PCIe rate) -> fills h_global, h_skin."""
+        def ptr(t):
+            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+
+        n, nl = h_layers.shape[0], h_layers.shape[1]
+        _check(lib().hs_animate_host(self._h, sk.handle, clips.handle, ptr(h_layers), nl, n, ptr(h_global),
+                                     ptr(h_skin)), "hs_animate_host")
 
     def scan_host_batch(self, items):
         """hs_scan_host_batch: items = [(Skeleton, h_local, h_global, h_skin), ...] on the

@@ -1135,6 +1135,51 @@ hs_status hs_scan_host(hs_pipeline* pl, const hs_skeleton* sk, const float* h_lo
     return hs_scan_host_batch(pl, &it, 1);
 }
 
+hs_status hs_animate_host(hs_pipeline* pl, const hs_skeleton* sk, const hs_clipset* cs, const void* h_layers,
+                          int32_t n_layers, int64_t n_chars, float* h_global, float* h_skin) {
+    if (!pl || !sk || !cs) return fail(HS_ERR_INVALID_ARG, "null handle");
+    if (n_chars < 0) return fail(HS_ERR_INVALID_ARG, "n_chars < 0");
+    if (n_chars == 0) return HS_OK;
+    if (!h_layers || !h_global || !h_skin) return fail(HS_ERR_INVALID_ARG, "null buffer");
+    if (n_layers < 1 || n_layers > 8) return fail(HS_ERR_INVALID_ARG, "n_layers must be in 1..8");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != sk->device || dev != pl->device) return fail(HS_ERR_WRONG_DEVICE, "device mismatch");
+    const int32_t J = sk->plan.n;
+    const int64_t per_char = (int64_t)J * 48, lay_bytes = (int64_t)n_layers * 16;
+    const int64_t batch = pl->batch_bytes / std::max(per_char, lay_bytes);
+    if (batch < 1) return fail(HS_ERR_INVALID_ARG, "pipeline batch smaller than one character");
+    hs_animate_opts o{};
+    o.mode = HS_ANIMATE_TWO_PASS;
+    o.workspace_bytes = batch * per_char;
+    // layers up (16 B per layer), Stage 1 + scan + bind on the device, poses back; the
+    // 3 streams rotate and the batches ramp up from ~8 MB as in hs_scan_host
+    int64_t b = 0, ramp = (int64_t)8 << 20;
+    for (int64_t c0 = 0, nb = 0; c0 < n_chars; c0 += nb, ++b) {
+        const int i = (int)(b % 3);
+        const int64_t cur = std::max<int64_t>(1, std::min<int64_t>(batch, ramp / per_char));
+        ramp = std::min<int64_t>(2 * ramp, pl->batch_bytes);
+        nb = std::min(cur, n_chars - c0);
+        cudaError_t e = cudaMemcpyAsync(pl->d_in[i], static_cast<const char*>(h_layers) + c0 * lay_bytes,
+                                        (size_t)(nb * lay_bytes), cudaMemcpyHostToDevice, pl->st[i]);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+        hs_status s = hs_animate_ex(sk, cs, pl->d_in[i], n_layers, nb, pl->d_g[i], pl->d_s[i], pl->st[i], &o);
+        if (s != HS_OK) return s;
+        const size_t bytes = (size_t)(nb * per_char);
+        const int64_t foff = c0 * J * 12;
+        if ((e = cudaMemcpyAsync(h_global + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(h_skin + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
+                cudaSuccess)
+            return cuda_fail(e, "D2H");
+    }
+    for (int i = 0; i < 3; ++i) {
+        cudaError_t e = cudaStreamSynchronize(pl->st[i]);
+        if (e != cudaSuccess) return cuda_fail(e, "pipeline sync");
+    }
+    return HS_OK;
+}
+
 hs_status hs_pipeline_destroy(hs_pipeline* pl) {
     if (!pl) return HS_OK;
     for (int i = 0; i < 3; ++i) {

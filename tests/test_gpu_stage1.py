@@ -176,3 +176,37 @@ def test_two_pass_on_multi_cta_skeleton():
     with pytest.raises(hs.HSError) as e:
         hs.animate(sk, cs, lay, mode="fused")
     assert e.value.status == hs.HS_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("name,n", [("hum64", 5000), ("tree1024", 300)])
+def test_animate_host_pipeline(name, n):
+    """hs_animate_host (host layers in, host poses out, batched over 3 streams with a small
+    pipeline so many batches run) equals hs_animate on the device bit for bit, and the
+    oracle within the Stage-1 bound on sampled characters."""
+    par = hsgen.skeleton(name)
+    J = len(par)
+    keys = hsgen.clips(31, J, 4, 15)
+    lay = hsgen.layers(32, n, 2, 4, 1.5)
+    ib = hsgen.inv_bind(33, J)
+    sk = hs.Skeleton(par, ib)
+    cs = hs.ClipSet(sk, keys, 30.0, 1)
+    hl = torch.from_numpy(np.ascontiguousarray(lay).view(np.int32).reshape(n, 2, 4)).pin_memory()
+    hg = torch.full((n, J, 3, 4), float("nan"), pin_memory=True)
+    hsk = torch.full_like(hg, float("nan"), pin_memory=True)
+    pl = hs.Pipeline(batch_bytes=2 << 20)
+    pl.animate_host(sk, cs, hl, hg, hsk)
+    g, s = hs.animate(sk, cs, lay)
+    torch.cuda.synchronize()
+    assert torch.equal(hg, g.cpu()) and torch.equal(hsk, s.cpu())
+    # a numpy LAYER_DTYPE array works as the host buffer too
+    hg2, hs2 = np.empty((n, J, 3, 4), np.float32), np.empty((n, J, 3, 4), np.float32)
+    pl.animate_host(sk, cs, np.ascontiguousarray(lay), hg2, hs2)
+    assert np.array_equal(hg2, hg.numpy()) and np.array_equal(hs2, hsk.numpy())
+    idx = np.linspace(0, n - 1, 7).astype(int)
+    G, S = oracle.animate(par, keys, 30.0, 1, lay[idx], ib)
+    tol = stage1_tol(levels(par))
+    assert np.abs(hg.numpy()[idx] - G).max() <= tol and np.abs(hsk.numpy()[idx] - S).max() <= tol
+    with pytest.raises(hs.HSError) as e:
+        pl.animate_host(sk, cs, hl[:, :0], hg, hsk)
+    assert e.value.status == hs.HS_ERR_INVALID_ARG
+    pl.close()
