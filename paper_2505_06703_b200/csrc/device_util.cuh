@@ -182,6 +182,18 @@ __device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
     return make_int4(row, fr != 0.0f ? Jp * 10 : 0, __float_as_int(fr), L.z);
 }
 
+// Every product and sum below is an explicit __fmul_rn / __fadd_rn / fmaf: the
+// compiler's FMA contraction otherwise depends on the surrounding code (an unrolled
+// layer loop contracts differently from a rolled one), and the fused and two-pass
+// placements must produce the same local poses bit for bit.
+__device__ __forceinline__ float lerp_rn(float b, float x0, float a, float x1) {
+    return fmaf(a, x1, __fmul_rn(b, x0));
+}
+__device__ __forceinline__ float dot4_rn(float a0, float a1, float a2, float a3, float b0, float b1, float b2,
+                                         float b3) {
+    return fmaf(a3, b3, fmaf(a2, b2, fmaf(a1, b1, __fmul_rn(a0, b0))));
+}
+
 // Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
 __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, float4 x1, float4 y1,
                                            float2 z1, float a, float* trs) {
@@ -191,26 +203,32 @@ __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, floa
         trs[7] = y0.w; trs[8] = z0.x; trs[9] = z0.y;
         return;
     }
-    const float b = 1.0f - a;
-    trs[0] = b * x0.x + a * x1.x; trs[1] = b * x0.y + a * x1.y; trs[2] = b * x0.z + a * x1.z;
-    trs[7] = b * y0.w + a * y1.w; trs[8] = b * z0.x + a * z1.x; trs[9] = b * z0.y + a * z1.y;
-    const float d = x0.w * x1.w + y0.x * y1.x + y0.y * y1.y + y0.z * y1.z;
+    const float b = __fsub_rn(1.0f, a);
+    trs[0] = lerp_rn(b, x0.x, a, x1.x); trs[1] = lerp_rn(b, x0.y, a, x1.y); trs[2] = lerp_rn(b, x0.z, a, x1.z);
+    trs[7] = lerp_rn(b, y0.w, a, y1.w); trs[8] = lerp_rn(b, z0.x, a, z1.x); trs[9] = lerp_rn(b, z0.y, a, z1.y);
+    const float d = dot4_rn(x0.w, y0.x, y0.y, y0.z, x1.w, y1.x, y1.y, y1.z);
     const float as = d < 0.0f ? -a : a;
-    float qw = b * x0.w + as * x1.w, qx = b * y0.x + as * y1.x, qy = b * y0.y + as * y1.y,
-          qz = b * y0.z + as * y1.z;
-    const float inv = rsqrt_fast(qw * qw + qx * qx + qy * qy + qz * qz);
-    trs[3] = qw * inv; trs[4] = qx * inv; trs[5] = qy * inv; trs[6] = qz * inv;
+    const float qw = lerp_rn(b, x0.w, as, x1.w), qx = lerp_rn(b, y0.x, as, y1.x),
+                qy = lerp_rn(b, y0.y, as, y1.y), qz = lerp_rn(b, y0.z, as, y1.z);
+    const float inv = rsqrt_fast(dot4_rn(qw, qx, qy, qz, qw, qx, qy, qz));
+    trs[3] = __fmul_rn(qw, inv); trs[4] = __fmul_rn(qx, inv); trs[5] = __fmul_rn(qy, inv);
+    trs[6] = __fmul_rn(qz, inv);
 }
 
 __device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
     const float w = trs[3], x = trs[4], y = trs[5], z = trs[6];
     const float sx = trs[7], sy = trs[8], sz = trs[9];
-    m[0] = (1.0f - 2.0f * (y * y + z * z)) * sx; m[1] = 2.0f * (x * y - w * z) * sy;
-    m[2] = 2.0f * (x * z + w * y) * sz;          m[3] = trs[0];
-    m[4] = 2.0f * (x * y + w * z) * sx;          m[5] = (1.0f - 2.0f * (x * x + z * z)) * sy;
-    m[6] = 2.0f * (y * z - w * x) * sz;          m[7] = trs[1];
-    m[8] = 2.0f * (x * z - w * y) * sx;          m[9] = 2.0f * (y * z + w * x) * sy;
-    m[10] = (1.0f - 2.0f * (x * x + y * y)) * sz; m[11] = trs[2];
+    // 1 - 2 (u^2 + v^2) and 2 (u v -/+ w t), each rounded in one fixed order
+    auto diag = [](float u, float v) { return fmaf(-2.0f, fmaf(u, u, __fmul_rn(v, v)), 1.0f); };
+    auto offd = [](float u, float v, float p, float q, float sgn) {
+        return __fmul_rn(2.0f, fmaf(sgn * p, q, __fmul_rn(u, v)));
+    };
+    m[0] = __fmul_rn(diag(y, z), sx);               m[1] = __fmul_rn(offd(x, y, w, z, -1.0f), sy);
+    m[2] = __fmul_rn(offd(x, z, w, y, 1.0f), sz);   m[3] = trs[0];
+    m[4] = __fmul_rn(offd(x, y, w, z, 1.0f), sx);   m[5] = __fmul_rn(diag(x, z), sy);
+    m[6] = __fmul_rn(offd(y, z, w, x, -1.0f), sz);  m[7] = trs[1];
+    m[8] = __fmul_rn(offd(x, z, w, y, -1.0f), sx);  m[9] = __fmul_rn(offd(y, z, w, x, 1.0f), sy);
+    m[10] = __fmul_rn(diag(x, y), sz);              m[11] = trs[2];
 }
 
 // Local poses of E tile elements at once (E independent (character, joint) pairs,
@@ -239,26 +257,44 @@ __device__ __forceinline__ KeyPair load_keys(const float* __restrict__ keys, int
     return k;
 }
 
-template <int E, bool PIPE>
+// NLT > 0: the layer count is a compile-time constant (the layer loop unrolls, so
+// every layer's key loads can be issued before the first layer's arithmetic).
+template <int E, bool PIPE, int NLT = 0>
 __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, const int4* const* dsc,
-                                             const int* j, const bool* valid, int nl, int Jp, float* L,
+                                             const int* j, const bool* valid, int nl_rt, int Jp, float* L,
                                              const int* off) {
+    const int nl = NLT > 0 ? NLT : nl_rt;
     float acc[E][10], q0[E][4], wsum[E];
     KeyPair kp[E];
     int4 d[E];
-    if (PIPE) {
+    constexpr int kPre = NLT > 0 ? NLT : 1;
+    KeyPair pre[kPre][E];
+    int4 pd[kPre][E];
+    if (NLT > 0) {   // every layer's descriptors and keys in flight at once
+#pragma unroll
+        for (int l = 0; l < kPre; ++l)
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                pd[l][e] = valid[e] ? dsc[e][l] : make_int4(0, 0, 0, 0);
+                pre[l][e] = load_keys(keys, pd[l][e], j[e], Jp);
+            }
+    } else if (PIPE) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             d[e] = valid[e] ? dsc[e][0] : make_int4(0, 0, 0, 0);
             kp[e] = load_keys(keys, d[e], j[e], Jp);
         }
     }
+#pragma unroll(kPre)
     for (int l = 0; l < nl; ++l) {
         KeyPair cur[E];
         int4 dc[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            if (PIPE) {
+            if (NLT > 0) {
+                cur[e] = pre[l][e];
+                dc[e] = pd[l][e];
+            } else if (PIPE) {
                 cur[e] = kp[e];
                 dc[e] = d[e];
                 if (l + 1 < nl) {
@@ -283,18 +319,18 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
 #pragma unroll
                 for (int c = 0; c < 4; ++c) q0[e][c] = s[3 + c];
 #pragma unroll
-                for (int c = 0; c < 10; ++c) acc[e][c] = w * s[c];
+                for (int c = 0; c < 10; ++c) acc[e][c] = __fmul_rn(w, s[c]);
                 wsum[e] = w;
             } else {
-                const float dq = s[3] * q0[e][0] + s[4] * q0[e][1] + s[5] * q0[e][2] + s[6] * q0[e][3];
+                const float dq = dot4_rn(s[3], s[4], s[5], s[6], q0[e][0], q0[e][1], q0[e][2], q0[e][3]);
                 const float ws = dq < 0.0f ? -w : w;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) acc[e][c] += w * s[c];
+                for (int c = 0; c < 3; ++c) acc[e][c] = fmaf(w, s[c], acc[e][c]);
 #pragma unroll
-                for (int c = 3; c < 7; ++c) acc[e][c] += ws * s[c];
+                for (int c = 3; c < 7; ++c) acc[e][c] = fmaf(ws, s[c], acc[e][c]);
 #pragma unroll
-                for (int c = 7; c < 10; ++c) acc[e][c] += w * s[c];
-                wsum[e] += w;
+                for (int c = 7; c < 10; ++c) acc[e][c] = fmaf(w, s[c], acc[e][c]);
+                wsum[e] = __fadd_rn(wsum[e], w);
             }
         }
     }
@@ -304,13 +340,13 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
         if (nl > 1) {
             const float iw = rcp_fast(wsum[e]);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[e][c] *= iw;
+            for (int c = 0; c < 3; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
 #pragma unroll
-            for (int c = 7; c < 10; ++c) acc[e][c] *= iw;
-            const float inv = rsqrt_fast(acc[e][3] * acc[e][3] + acc[e][4] * acc[e][4] +
-                                     acc[e][5] * acc[e][5] + acc[e][6] * acc[e][6]);
+            for (int c = 7; c < 10; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
+            const float inv = rsqrt_fast(dot4_rn(acc[e][3], acc[e][4], acc[e][5], acc[e][6], acc[e][3],
+                                                 acc[e][4], acc[e][5], acc[e][6]));
 #pragma unroll
-            for (int c = 3; c < 7; ++c) acc[e][c] *= inv;
+            for (int c = 3; c < 7; ++c) acc[e][c] = __fmul_rn(acc[e][c], inv);
         }
         float m[12];
         trs_to_m34(acc[e], m);

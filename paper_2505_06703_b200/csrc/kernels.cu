@@ -8,6 +8,8 @@
 //
 // This file: the chunked kernel (the hot path) and its launcher;
 // the other kernels live in kernels_aux.cu, shared device helpers in device_util.cuh.
+#include <mutex>
+
 #include "device_util.cuh"
 
 namespace hs {
@@ -550,12 +552,35 @@ cudaError_t prepare_chunked(int K, int64_t smem_bytes) {
 }
 
 int max_chunked_blocks_per_sm(int K, bool runs, int threads, int64_t smem_bytes) {
+    // the occupancy query costs a few microseconds of host time per launch: remember
+    // each (device, kernel, block shape) answer (a handful of shapes per process)
+    struct Entry {
+        int dev;
+        const void* fn;
+        int threads;
+        int64_t smem;
+        int nb;
+    };
+    static Entry cache[64];
+    static int n_cached = 0;
+    static std::mutex mu;
     void* fn = chunked_fn(K, runs, kModeScan);
+    if (!fn) return 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (int i = 0; i < n_cached; ++i)
+            if (cache[i].dev == dev && cache[i].fn == fn && cache[i].threads == threads && cache[i].smem == smem_bytes)
+                return cache[i].nb;
+    }
     int nb = 0;
-    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) !=
-                   cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, (size_t)smem_bytes) != cudaSuccess)
         return 1;
-    return nb > 0 ? nb : 1;
+    nb = nb > 0 ? nb : 1;
+    std::lock_guard<std::mutex> lock(mu);
+    if (n_cached < 64) cache[n_cached++] = Entry{dev, fn, threads, smem_bytes, nb};
+    return nb;
 }
 
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st) {

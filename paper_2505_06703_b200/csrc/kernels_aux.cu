@@ -18,13 +18,25 @@ namespace {
 #ifndef HS_S1K_UNROLL
 #define HS_S1K_UNROLL 1
 #endif
+#ifndef HS_S1K_TMA_STORE
+#define HS_S1K_TMA_STORE 1
+#endif
+#ifndef HS_S1K_SPECIALISE
+#define HS_S1K_SPECIALISE 1
+#endif
 constexpr int kStage1PerThread = HS_S1K_PER_THREAD;   // elements per thread between descriptor refreshes
 constexpr int kStage1Unroll = HS_S1K_UNROLL;
 
+template <int NLT>
 __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ ChunkedArgs a, int64_t c0,
                                                      int64_t n_chars, float* __restrict__ local) {
     extern __shared__ int4 sd[];   // layer descriptors of the block's characters
-    const int J = a.seg[0].J, nl = a.n_layers;
+    __shared__ __align__(128) float stg[(HS_S1K_TMA_STORE ? 2 : 1) * 256 * 12];   // warps' local poses before the store
+#if HS_S1K_TMA_STORE
+    int it = 0;   // store-buffer parity
+#endif
+    const int J = a.seg[0].J, nl = NLT > 0 ? NLT : a.n_layers;
+    const int lane = threadIdx.x & 31;
     const int64_t n = n_chars * J;
     const int4* lay = reinterpret_cast<const int4*>(a.layers);
     constexpr int kTile = 256 * kStage1PerThread;   // elements per block iteration
@@ -41,18 +53,50 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
         const int sc = 256 / J, sj = 256 - sc * J;
 #pragma unroll kStage1Unroll
         for (int q = 0; q < kStage1PerThread; ++q) {
-            const int64_t e = e0 + q * 256 + threadIdx.x;
-            if (e >= n) break;
-            const int j[1] = {jj};
-            const int4* dp[1] = {sd + cl * nl};
-            const bool valid[1] = {true};
+            const int64_t wbase = e0 + q * 256 + (threadIdx.x & ~31);   // the warp's first element
+            if (wbase >= n) break;                                      // warp-uniform
+            const bool ok = wbase + lane < n;
+            const int j[1] = {ok ? jj : 0};
+            const int4* dp[1] = {sd + (ok ? cl : 0) * nl};
+            const bool valid[1] = {ok};
             const int off[1] = {0};
-            stage1_elems<1, false>(a.keys, dp, j, valid, nl, J + (J & 1), local + e * 12, off);
+#if HS_S1K_TMA_STORE
+            // the warp's 32 local poses are 1536 contiguous bytes: staged in smem (two
+            // buffers per warp) and written by one TMA bulk store, so the LSU carries
+            // only the key loads; the store of two iterations ago must have been read
+            float* sbuf = stg + (it & 1) * 256 * 12;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            stage1_elems<1, false, NLT>(a.keys, dp, j, valid, nl, J + (J & 1), sbuf + threadIdx.x * 12, off);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                bulk_s2g(local + wbase * 12, sbuf + (threadIdx.x & ~31) * 12,
+                         (uint32_t)(48 * min((int64_t)32, n - wbase)));
+                bulk_commit();
+            }
+            ++it;
+#else
+            stage1_elems<1, false, NLT>(a.keys, dp, j, valid, nl, J + (J & 1), stg + threadIdx.x * 12, off);
+            __syncwarp();
+            // the warp's 32 local poses are 1536 contiguous bytes: write them as 96
+            // lane-consecutive float4 (whole sectors) instead of 3 x 32 strided ones
+            const int nv3 = 3 * (int)min((int64_t)32, n - wbase);
+            const float4* src = reinterpret_cast<const float4*>(stg + (threadIdx.x & ~31) * 12);
+            float4* dst = reinterpret_cast<float4*>(local + wbase * 12);
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                if (lane + 32 * i < nv3) dst[lane + 32 * i] = src[lane + 32 * i];
+            __syncwarp();
+#endif
             cl += sc;
             jj += sj;
             if (jj >= J) { jj -= J; ++cl; }
         }
     }
+#if HS_S1K_TMA_STORE
+    if (lane == 0) bulk_wait_all();   // smem stays valid until the last store has read it
+#endif
 }
 
 // ================================================================== varied topology
@@ -420,13 +464,17 @@ cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, flo
     ChunkedArgs args = a;
     void* params[] = {&args, &c0, &n_chars, &local};
     const size_t smem = (size_t)(256 * kStage1PerThread / a.seg[0].J + 2) * a.n_layers * sizeof(int4);
+    // one, two and three layers (the common blends) get the unrolled layer loop
+    const void* fn = !HS_S1K_SPECIALISE ? reinterpret_cast<const void*>(&stage1_kernel<0>)
+                     : a.n_layers == 1   ? reinterpret_cast<const void*>(&stage1_kernel<1>)
+                     : a.n_layers == 2 ? reinterpret_cast<const void*>(&stage1_kernel<2>)
+                     : a.n_layers == 3 ? reinterpret_cast<const void*>(&stage1_kernel<3>)
+                                       : reinterpret_cast<const void*>(&stage1_kernel<0>);
     if (smem > 48 * 1024) {
-        const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<void*>(&stage1_kernel),
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    return cudaLaunchKernel(reinterpret_cast<void*>(&stage1_kernel), dim3((unsigned)blocks), dim3(256), params,
-                            smem, st);
+    return cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(256), params, smem, st);
 }
 
 cudaError_t launch_lbs(const float* S, int64_t n_chars, int32_t J, const float4* mesh_a, const float4* mesh_b,
