@@ -374,8 +374,7 @@ void chunked_layout(const ChunkItem* items, int n, int stages, int sbufs, hs::Ch
 // Launch one chunked program (with the HS_DEBUG_PROF phase profile when set).
 hs_status run_chunked(hs::ChunkedArgs& a, int K, cudaStream_t st) {
     a.prof = nullptr;
-    static const bool prof = std::getenv("HS_DEBUG_PROF") != nullptr;   // read once per process
-    if (prof) {   // debug aid: per-phase cycle split, synchronising
+    if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
         cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
         cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
     }
