@@ -331,6 +331,14 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value)
 const char* hs_status_string(hs_status s);
 const char* hs_last_error(void);
 
+/* Workspaces (two-pass hs_animate / hs_scan_skin, the multi-CTA path) come from a
+ * library-owned stream-ordered pool per device that keeps its memory between calls,
+ * so steady-state frames allocate nothing.  hs_workspace_trim returns the pool's
+ * unused memory of the CURRENT device to the driver (outstanding work keeps what it
+ * holds); *held_bytes (may be NULL) receives what the pool still reserves.  Safe to
+ * call at any time; HS_OK if the pool was never created. */
+hs_status hs_workspace_trim(int64_t* held_bytes);
+
 /* ---------------------------------------------------------------------------
  * Host-only topology plan (no CUDA calls): the preprocessor hs_skeleton_create
  * runs, exposed for tests and tools.  Exports are in USER labels unless noted.

@@ -119,6 +119,7 @@ def lib():
     L.hs_scan_host.argtypes = [vp, vp, vp, i64, vp, vp]
     L.hs_scan_host_batch.argtypes = [vp, ctypes.POINTER(_BatchItem), i32]
     L.hs_animate_host.argtypes = [vp, vp, vp, vp, i32, i64, vp, vp]
+    L.hs_workspace_trim.argtypes = [ctypes.POINTER(ctypes.c_int64)]
     L.hs_pipeline_destroy.argtypes = [vp]
     for f in ("hs_skeleton_create", "hs_skeleton_create_ex", "hs_scan", "hs_scan_ex", "hs_destroy",
               "hs_skeleton_query", "hs_plan_create", "hs_plan_create_ex", "hs_plan_query", "hs_plan_export",
@@ -463,6 +464,14 @@ def animate_skin(sk: "Skeleton", clips: "ClipSet", layers, mesh: "Mesh", global_
                                  global_out.data_ptr(), None if skin_out is None else skin_out.data_ptr(),
                                  verts_out.data_ptr(), st), "hs_animate_skin")
     return global_out, skin_out, verts_out
+
+
+def workspace_trim() -> int:
+    """hs_workspace_trim: return the workspace pool's unused memory on the current device
+    to the driver; returns the bytes the pool still reserves."""
+    held = ctypes.c_int64(0)
+    _check(lib().hs_workspace_trim(ctypes.byref(held)), "hs_workspace_trim")
+    return held.value
 
 
 class Pipeline:

@@ -296,9 +296,12 @@ hs_status check_pose_buffers(const float* local, int64_t n_chars, int32_t n_join
 // pool per device that keeps its memory (release threshold = max): after the first
 // frame a workspace costs no driver allocation.  The process's default pool and
 // PyTorch's allocator are left alone.
+cudaMemPool_t g_pools[64] = {};
+std::mutex g_pools_mu;
+
 cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
-    static cudaMemPool_t pools[64] = {};
-    static std::mutex mu;
+    cudaMemPool_t* pools = g_pools;
+    std::mutex& mu = g_pools_mu;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -1177,6 +1180,25 @@ hs_status hs_animate_host(hs_pipeline* pl, const hs_skeleton* sk, const hs_clips
     for (int i = 0; i < 3; ++i) {
         cudaError_t e = cudaStreamSynchronize(pl->st[i]);
         if (e != cudaSuccess) return cuda_fail(e, "pipeline sync");
+    }
+    return HS_OK;
+}
+
+hs_status hs_workspace_trim(int64_t* held_bytes) {
+    if (held_bytes) *held_bytes = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return HS_OK;
+    std::lock_guard<std::mutex> lock(g_pools_mu);
+    cudaMemPool_t pool = g_pools[dev];
+    if (!pool) return HS_OK;
+    if ((e = cudaMemPoolTrimTo(pool, 0)) != cudaSuccess) return cuda_fail(e, "cudaMemPoolTrimTo");
+    if (held_bytes) {
+        uint64_t v = 0;
+        if ((e = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v)) != cudaSuccess)
+            return cuda_fail(e, "cudaMemPoolGetAttribute");
+        *held_bytes = (int64_t)v;
     }
     return HS_OK;
 }

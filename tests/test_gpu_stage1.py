@@ -210,3 +210,19 @@ def test_animate_host_pipeline(name, n):
         pl.animate_host(sk, cs, hl[:, :0], hg, hsk)
     assert e.value.status == hs.HS_ERR_INVALID_ARG
     pl.close()
+
+
+def test_workspace_trim_releases_the_pool():
+    """The two-pass workspace pool keeps its memory between calls (no per-frame driver
+    allocation) until hs_workspace_trim hands the unused part back."""
+    par = hsgen.skeleton("hum64")
+    sk = hs.Skeleton(par, hsgen.inv_bind(41, 64))
+    cs = hs.ClipSet(sk, hsgen.clips(42, 64, 2, 5), 30.0, 1)
+    lay = hsgen.layers(43, 5000, 1, 2, 1.0)
+    g1, s1 = hs.animate(sk, cs, lay, mode="two_pass")
+    torch.cuda.synchronize()
+    assert hs.workspace_trim() == 0          # nothing outstanding: everything released
+    g2, s2 = hs.animate(sk, cs, lay, mode="two_pass")   # the pool grows again on demand
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(s1, s2)
+    assert hs.workspace_trim() == 0
