@@ -57,3 +57,13 @@ def test_enums_and_limits(c_layout):
     assert c_layout["HS_MAX_BATCH"] == [hs.MAX_BATCH]
     assert c_layout["HS_ALGO_BLOCKED"] == [hs.ALGO["blocked"]]
     assert c_layout["HS_ERR_UNSUPPORTED"] == [hs.HS_ERR_UNSUPPORTED]
+
+
+def test_c_client_builds_against_the_header():
+    """include/hs.h is plain C11 (no C++ in the ABI): the example client compiles with
+    -Wall -Wextra -Werror and links against libhs.so (running it needs a GPU:
+    tests/test_gpu_parity.py::test_c_client_runs)."""
+    import __graft_entry__ as ge
+    hs.build()
+    out = ge.build_examples()
+    assert os.path.exists(out) and os.access(out, os.X_OK)

@@ -379,3 +379,15 @@ def test_scan_and_animate_capture_into_a_cuda_graph():
     torch.cuda.synchronize()
     assert torch.equal(g, g_ref) and torch.equal(s, s_ref)
     assert torch.equal(ga, ga_ref) and torch.equal(sa, sa_ref)
+
+
+def test_c_client_runs():
+    """examples/hs_demo.c: a plain C program using only the C ABI (skeleton, host-buffer
+    pipeline, query) checks 1000 characters against its own float64 walk."""
+    import subprocess
+
+    import __graft_entry__ as ge
+    out = ge.build_examples()
+    r = subprocess.run([out], capture_output=True, text=True, timeout=120)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "max |err|" in r.stdout
