@@ -100,9 +100,14 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
 }
 
 // ================================================================== varied topology
+#ifndef HS_VARIED_THREADS
+#define HS_VARIED_THREADS 64
+#endif
 // NEXT-3's per-character topology: every character brings its own parent array
 // (4 B/joint more input), so nothing can be planned per skeleton.  One thread per
-// (character, joint), C = 1024 / J characters per CTA; pointer jumping WITH the
+// (character, joint), C = max(1, 64 / J) characters per CTA — one character per CTA
+// from J = 64 up, so each barrier spans one character's threads only (1024-thread
+// CTAs of 16 hum64 characters were 1.7x slower); pointer jumping WITH the
 // parent pointers (Alg. 2 with the Eq. 2 lift built on the fly): V[i] <- V[p[i]] (x)
 // V[i], p[i] <- p[p[i]] on ping-pong snapshots until no pointer is left (at most
 // ceil(log2 J) + 1 rounds, so a malformed array still terminates).
@@ -134,9 +139,10 @@ __global__ void __launch_bounds__(1024) varied_kernel(const int32_t* __restrict_
     float* vn = v1;
     int32_t* qc = q0;
     int32_t* qn = q1;
-    __syncthreads();
-    for (int r = 0; r < max_rounds; ++r) {
-        if (!__syncthreads_or(p >= 0)) break;
+    // one barrier per round: the OR of "a pointer is left" rides on the barrier that
+    // publishes the round's snapshot
+    int any = __syncthreads_or(p >= 0);
+    for (int r = 0; r < max_rounds && any; ++r) {
         if (f < F) {
             if (p >= 0) {
                 float x[12], y[12];
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(1024) varied_kernel(const int32_t* __restrict_
             st3(vn + f * 12, v);
             qn[f] = p;
         }
-        __syncthreads();
+        any = __syncthreads_or(p >= 0);
         float* tv = vc; vc = vn; vn = tv;
         int32_t* tq = qc; qc = qn; qn = tq;
     }
@@ -516,7 +522,7 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
 cudaError_t launch_varied(const int32_t* parents, const float* local, const float* ib, int32_t J,
                           int64_t n_chars, float* gout, float* sout, cudaStream_t st) {
     if (J < 1 || J > 1024) return cudaErrorInvalidValue;
-    const int C = std::max(1, 1024 / J);
+    const int C = std::max(1, HS_VARIED_THREADS / J);   // characters per CTA
     int rounds = 1;
     while ((1 << (rounds - 1)) < J) ++rounds;   // ceil(log2 J) + 1: enough for any forest
     const size_t smem = (size_t)C * J * (2 * 48 + 2 * 4);
