@@ -12,8 +12,13 @@
 
 #include "device_util.cuh"
 
+#ifndef HS_LBS_U
+#define HS_LBS_U 2
+#endif
+
 namespace hs {
 namespace {
+constexpr int kLbsU = HS_LBS_U;   // vertices per thread in flight in the fused LBS epilogue
 
 // ================================================================== chunked kernel
 // Persistent, warp-specialised.  Warps 0..nwc-1 compute; warp nwc is the TMA
@@ -462,11 +467,11 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 // vertex-major: mesh records of two vertices per thread loaded up front,
                 // then every character of the tile (independent palette reads and
                 // stores: ILP, no division)
-                for (int v0 = t; v0 < V; v0 += 2 * NC) {
-                    float4 pa[2], pb[2];
-                    int js[2][4];
+                for (int v0 = t; v0 < V; v0 += kLbsU * NC) {
+                    float4 pa[kLbsU], pb[kLbsU];
+                    int js[kLbsU][4];
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
+                    for (int u = 0; u < kLbsU; ++u) {
                         const int v = min(v0 + u * NC, V - 1);
                         pa[u] = __ldg(a.mesh_a + v);
                         pb[u] = __ldg(a.mesh_b + v);
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                     for (int cl = 0; cl < nct; ++cl) {
                         const float* Sc = Sb + cl * Jn * 12;
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
+                        for (int u = 0; u < kLbsU; ++u) {
                             const int v = v0 + u * NC;
                             if (v < V) lbs_vertex(Sc, pa[u], pb[u], js[u], vout + ((int64_t)cl * V + v) * 3);
                         }
