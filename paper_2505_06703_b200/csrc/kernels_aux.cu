@@ -504,8 +504,7 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
                             const int32_t* lift, int32_t J, int32_t R, int32_t rounds,
                             int64_t n_chars, cudaStream_t st) {
     if (J > 1024) return cudaErrorInvalidValue;
-    int C = 1024 / J;
-    if (C < 1) C = 1;
+    const int C = std::max(1, HS_VARIED_THREADS / J);   // one character per CTA from J = 64 up
     if (rounds < 0 || rounds > R) rounds = R;
     const size_t smem = (size_t)2 * C * J * 48;
     static bool attr = false;
@@ -541,8 +540,7 @@ cudaError_t launch_varied(const int32_t* parents, const float* local, const floa
 cudaError_t launch_blocked(const float* local, float* gout, float* sout, const float* ib, const int32_t* lb,
                            const int32_t* mpob, int32_t J, int32_t RB, int64_t n_chars, cudaStream_t st) {
     if (J > 1024) return cudaErrorInvalidValue;
-    int C = 1024 / J;
-    if (C < 1) C = 1;
+    const int C = std::max(1, HS_VARIED_THREADS / J);   // one character per CTA from J = 64 up
     const size_t smem = (size_t)2 * C * J * 48;
     static bool attr = false;
     if (!attr) {
