@@ -56,6 +56,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB_PATH
 
 
+def build_variant(name: str, defines) -> str:
+    """Compile the same sources with extra -D flags into build/<name> (tuning and
+    profiling builds, e.g. the HS_PROF_HOOKS=1 phase-profile build) and return the path."""
+    out = os.path.join(_ROOT, "build", name)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    if not os.path.exists(out) or any(os.path.getmtime(out) < os.path.getmtime(d) for d in _DEPS):
+        subprocess.run(["nvcc", *NVCC_FLAGS, *defines, *_SOURCES, "-o", out], check=True, cwd=_HERE)
+    return out
+
+
+def use_library(path: str) -> None:
+    """Load another build of the library (before the first lib() call)."""
+    global _LOAD_PATH
+    if _lib is not None and _LOAD_PATH != path:
+        raise RuntimeError("the library is already loaded")
+    _LOAD_PATH = path
+
+
 class HSError(RuntimeError):
     def __init__(self, status: int, where: str):
         self.status = status

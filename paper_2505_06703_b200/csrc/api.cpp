@@ -392,6 +392,7 @@ hs_status run_chunked(hs::ChunkedArgs& a, int K, cudaStream_t st) {
         unsigned long long h[10];
         cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
+        if (!h[5]) std::fprintf(stderr, "[hs prof] no samples: build with -DHS_PROF_HOOKS=1 (tools/prof_scan.py does)\n");
         const double n = h[5] ? (double)h[5] : 1.0;
         std::fprintf(stderr,
                      "[hs prof] J=%d tiles=%llu cycles/tile: wait_full %.0f stage1 %.0f phase1 %.0f phase2 %.0f "

@@ -12,6 +12,9 @@
 
 #include "device_util.cuh"
 
+#ifndef HS_PROF_HOOKS
+#define HS_PROF_HOOKS 0   // 1: the HS_DEBUG_PROF phase profile (tools/prof_*.py build it); its checks cost ~3 %
+#endif
 #ifndef HS_LBS_U
 #define HS_LBS_U 2
 #endif
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
     // debug phase profile (HS_DEBUG_PROF): consumer thread 0 accumulates clock64 deltas
     long long prof_last = 0;
     auto prof_mark = [&](int slot) {
-        if (a.prof && t == 0) {
+        if (HS_PROF_HOOKS && a.prof && t == 0) {
             const long long now = clock64();
             if (slot >= 0) atomicAdd(a.prof + slot, (unsigned long long)(now - prof_last));
             prof_last = now;
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 }
             }
             prof_mark(4);
-            if (a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
+            if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 5, 1ull);
             if (++stage == NS) { stage = 0; phase ^= 1u; }
             if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }   // parity of use q-1
         }

@@ -10,6 +10,9 @@ import torch  # noqa: E402
 import hsgen  # noqa: E402
 import paper_2505_06703_b200 as hs  # noqa: E402
 
+# the phase-profile hooks are compiled out of the product build (they cost ~3 %)
+hs.use_library(hs.build_variant("libhs_prof.so", ["-DHS_PROF_HOOKS=1"]))
+
 for name, n, seed, type_, ib_seed in hsgen.CONFIGS[5]:
     par = hsgen.skeleton(name)
     J = len(par)

@@ -11,6 +11,9 @@ import torch  # noqa: E402
 import hsgen  # noqa: E402
 import paper_2505_06703_b200 as hs  # noqa: E402
 
+# the phase-profile hooks are compiled out of the product build (they cost ~3 %)
+hs.use_library(hs.build_variant("libhs_prof.so", ["-DHS_PROF_HOOKS=1"]))
+
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 333_333
 for name in sys.argv[2:] or ["hum64", "chain256", "tree1024"]:
     par = hsgen.skeleton(name)
