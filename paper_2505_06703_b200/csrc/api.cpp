@@ -1080,6 +1080,13 @@ hs_status hs_pipeline_create(int64_t batch_bytes, hs_pipeline** out) {
     return HS_OK;
 }
 
+// An error in the middle of a host pipeline returns only after the copies already
+// queued on its streams have finished: they read and write the caller's host buffers.
+static hs_status drain_fail(hs_pipeline* pl, hs_status s) {
+    for (int i = 0; i < 3; ++i) cudaStreamSynchronize(pl->st[i]);
+    return s;
+}
+
 hs_status hs_scan_host_batch(hs_pipeline* pl, const hs_batch_item* items, int32_t n_items) {
     if (!pl) return fail(HS_ERR_INVALID_ARG, "null handle");
     if (n_items < 0 || (n_items > 0 && !items)) return fail(HS_ERR_INVALID_ARG, "bad item list");
@@ -1113,14 +1120,14 @@ hs_status hs_scan_host_batch(hs_pipeline* pl, const hs_batch_item* items, int32_
             const size_t bytes = (size_t)(nb * per_char);
             const int64_t foff = c0 * sk->plan.n * 12;
             cudaError_t e = cudaMemcpyAsync(pl->d_in[i], it.local + foff, bytes, cudaMemcpyHostToDevice, pl->st[i]);
-            if (e != cudaSuccess) return cuda_fail(e, "H2D");
+            if (e != cudaSuccess) return drain_fail(pl, cuda_fail(e, "H2D"));
             hs_status s = scan_impl(sk, pl->d_in[i], nb, pl->d_g[i], pl->d_s[i], pl->st[i], HS_ALGO_AUTO, -1, 0);
-            if (s != HS_OK) return s;
+            if (s != HS_OK) return drain_fail(pl, s);
             if ((e = cudaMemcpyAsync(it.global_out + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
                     cudaSuccess ||
                 (e = cudaMemcpyAsync(it.skin_out + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
                     cudaSuccess)
-                return cuda_fail(e, "D2H");
+                return drain_fail(pl, cuda_fail(e, "D2H"));
         }
     }
     for (int i = 0; i < 3; ++i) {
@@ -1167,16 +1174,16 @@ hs_status hs_animate_host(hs_pipeline* pl, const hs_skeleton* sk, const hs_clips
         nb = std::min(cur, n_chars - c0);
         cudaError_t e = cudaMemcpyAsync(pl->d_in[i], static_cast<const char*>(h_layers) + c0 * lay_bytes,
                                         (size_t)(nb * lay_bytes), cudaMemcpyHostToDevice, pl->st[i]);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+        if (e != cudaSuccess) return drain_fail(pl, cuda_fail(e, "H2D"));
         hs_status s = hs_animate_ex(sk, cs, pl->d_in[i], n_layers, nb, pl->d_g[i], pl->d_s[i], pl->st[i], &o);
-        if (s != HS_OK) return s;
+        if (s != HS_OK) return drain_fail(pl, s);
         const size_t bytes = (size_t)(nb * per_char);
         const int64_t foff = c0 * J * 12;
         if ((e = cudaMemcpyAsync(h_global + foff, pl->d_g[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
                 cudaSuccess ||
             (e = cudaMemcpyAsync(h_skin + foff, pl->d_s[i], bytes, cudaMemcpyDeviceToHost, pl->st[i])) !=
                 cudaSuccess)
-            return cuda_fail(e, "D2H");
+            return drain_fail(pl, cuda_fail(e, "D2H"));
     }
     for (int i = 0; i < 3; ++i) {
         cudaError_t e = cudaStreamSynchronize(pl->st[i]);
