@@ -8,6 +8,7 @@
 //
 // This file: the chunked kernel (the hot path) and its launcher;
 // the other kernels live in kernels_aux.cu, shared device helpers in device_util.cuh.
+#include <atomic>
 #include <mutex>
 
 #include "device_util.cuh"
@@ -530,15 +531,17 @@ void* chunked_fn(int K, bool runs, int mode) {
 
 }  // namespace
 
-static int g_sms = 0;
-int sm_count() {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
+int sm_count() {   // of the current device, queried once per device
+    static std::atomic<int> sms[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = sms[dev].load(std::memory_order_relaxed);
+    if (n <= 0) {
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        sms[dev].store(n, std::memory_order_relaxed);
     }
-    return g_sms;
+    return n;
 }
 
 cudaError_t prepare_chunked(int K, int64_t smem_bytes) {

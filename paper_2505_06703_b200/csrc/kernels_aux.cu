@@ -2,6 +2,8 @@
 // kernel (two-pass hs_animate), the two-pass LBS kernel, the per-character-topology
 // scan, the paper's comparison algorithms (Alg. 1 Gateau, Alg. 2 doubling, Alg. 3
 // blocked, KIYA leaf walk) and the multi-CTA split path.  DESIGN.md §5.
+#include <atomic>
+
 #include "device_util.cuh"
 
 namespace hs {
@@ -459,6 +461,19 @@ __global__ void split_p3_kernel(const float* __restrict__ local, float* __restri
     }
 }
 
+// cudaFuncSetAttribute applies to the current device only: raise a kernel's dynamic
+// shared-memory limit once per (kernel, device), remembered in a per-kernel bitmask.
+cudaError_t raise_smem_once(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
+
 }  // namespace
 
 cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st) {
@@ -507,11 +522,10 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
     const int C = std::max(1, HS_VARIED_THREADS / J);   // one character per CTA from J = 64 up
     if (rounds < 0 || rounds > R) rounds = R;
     const size_t smem = (size_t)2 * C * J * 48;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(doubling_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 1024 * 48);
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&doubling_kernel), 2 * 1024 * 48, attr);
+        e != cudaSuccess)
+        return e;
     const int64_t blocks = (n_chars + C - 1) / C;
     doubling_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lift, J, C, rounds,
                                                            n_chars);
@@ -525,13 +539,11 @@ cudaError_t launch_varied(const int32_t* parents, const float* local, const floa
     int rounds = 1;
     while ((1 << (rounds - 1)) < J) ++rounds;   // ceil(log2 J) + 1: enough for any forest
     const size_t smem = (size_t)C * J * (2 * 48 + 2 * 4);
-    static bool attr = false;
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(varied_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   1024 * (2 * 48 + 2 * 4));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&varied_kernel),
+                                              1024 * (2 * 48 + 2 * 4), attr);
+        e != cudaSuccess)
+        return e;
     const int64_t blocks = (n_chars + C - 1) / C;
     varied_kernel<<<(unsigned)blocks, C * J, smem, st>>>(parents, local, ib, J, C, n_chars, rounds, gout, sout);
     return cudaGetLastError();
@@ -542,11 +554,10 @@ cudaError_t launch_blocked(const float* local, float* gout, float* sout, const f
     if (J > 1024) return cudaErrorInvalidValue;
     const int C = std::max(1, HS_VARIED_THREADS / J);   // one character per CTA from J = 64 up
     const size_t smem = (size_t)2 * C * J * 48;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 1024 * 48);
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&blocked_kernel), 2 * 1024 * 48, attr);
+        e != cudaSuccess)
+        return e;
     const int64_t blocks = (n_chars + C - 1) / C;
     blocked_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lb, mpob, J, C, RB, n_chars);
     return cudaGetLastError();
