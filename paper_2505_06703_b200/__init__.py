@@ -148,6 +148,40 @@ def lib():
     return L
 
 
+def _dev(t, name: str, need: int = 0, dtypes=("float32",)):
+    """Device pointer of an argument: None, a raw device pointer (int, trusted), or a
+    contiguous CUDA tensor of an accepted dtype holding at least `need` elements."""
+    if t is None or isinstance(t, int):
+        return t
+    if not getattr(t, "is_cuda", False):
+        raise TypeError(f"{name} must be a CUDA tensor (or a device pointer as int)")
+    if str(t.dtype).replace("torch.", "") not in dtypes:
+        raise TypeError(f"{name} must be {' or '.join(dtypes)}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() < need:
+        raise ValueError(f"{name} holds {t.numel()} elements, needs {need}")
+    return t.data_ptr()
+
+
+def _host(t, name: str, need_bytes: int = 0):
+    """Host pointer of a contiguous CPU tensor or C-contiguous numpy array (pinned memory
+    gives the full PCIe rate) of at least `need_bytes` bytes."""
+    if hasattr(t, "data_ptr"):
+        if t.is_cuda:
+            raise TypeError(f"{name} must be a host (CPU) tensor")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        n, p = t.numel() * t.element_size(), t.data_ptr()
+    else:
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+        n, p = t.nbytes, t.ctypes.data
+    if n < need_bytes:
+        raise ValueError(f"{name} holds {n} bytes, needs {need_bytes}")
+    return p
+
+
 def _check(status: int, where: str):
     if status != HS_OK:
         raise HSError(status, where)
@@ -243,18 +277,16 @@ class Skeleton:
         """hs_scan_ex on caller-owned CUDA tensors (or raw device pointers as ints)."""
         import torch
 
-        def ptr(t):
-            return None if t is None else (t if isinstance(t, int) else t.data_ptr())
-
         if n_chars is None:
             n_chars = local.shape[0]
+        need = n_chars * self.n_joints * 12
+        pl, pg, ps = _dev(local, "local", need), _dev(global_out, "global_out", need), _dev(skin_out, "skin_out", need)
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         elif not isinstance(stream, int):
             stream = stream.cuda_stream
         opts = _ScanOpts(ALGO[algo], max_rounds, tile_ctas)
-        _check(lib().hs_scan_ex(self._h, ptr(local), n_chars, ptr(global_out), ptr(skin_out),
-                                stream, ctypes.byref(opts)), "hs_scan")
+        _check(lib().hs_scan_ex(self._h, pl, n_chars, pg, ps, stream, ctypes.byref(opts)), "hs_scan")
 
     def scan(self, local, *, skin: bool = True, algo: str = "auto", max_rounds: int = -1,
              tile_ctas: int = 0):
@@ -310,14 +342,13 @@ def scan_batch(items, stream=None):
     as ints, then a fifth element n_chars)."""
     import torch
 
-    def ptr(t):
-        return None if t is None else (t if isinstance(t, int) else t.data_ptr())
-
     arr = (_BatchItem * max(1, len(items)))()
     for i, it in enumerate(items):
         sk, loc, g, s = it[:4]
         n = it[4] if len(it) > 4 else loc.shape[0]
-        arr[i] = _BatchItem(sk.handle, ptr(loc), n, ptr(g), ptr(s))
+        need = n * sk.n_joints * 12
+        arr[i] = _BatchItem(sk.handle, _dev(loc, f"items[{i}].local", need), n,
+                            _dev(g, f"items[{i}].global_out", need), _dev(s, f"items[{i}].skin_out", need))
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
     _check(lib().hs_scan_batch(arr, len(items), st), "hs_scan_batch")
@@ -359,7 +390,8 @@ def skin_vertices(mesh: Mesh, skin, verts_out=None, stream=None):
         verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=skin.device)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    _check(lib().hs_skin_vertices(mesh.handle, skin.data_ptr(), n, verts_out.data_ptr(), st), "hs_skin_vertices")
+    _check(lib().hs_skin_vertices(mesh.handle, _dev(skin, "skin"), n,
+                                  _dev(verts_out, "verts_out", n * mesh.n_vertices * 3), st), "hs_skin_vertices")
     return verts_out
 
 
@@ -381,8 +413,10 @@ def scan_skin(sk: "Skeleton", mesh: Mesh, local, global_out=None, skin_out=None,
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
     opts = _SkinOpts(SKIN_MODE[mode], 0, workspace_bytes)
-    _check(lib().hs_scan_skin_ex(sk.handle, mesh.handle, local.data_ptr(), n, global_out.data_ptr(),
-                                 None if skin_out is None else skin_out.data_ptr(), verts_out.data_ptr(), st,
+    need = n * sk.n_joints * 12
+    _check(lib().hs_scan_skin_ex(sk.handle, mesh.handle, _dev(local, "local", need), n,
+                                 _dev(global_out, "global_out", need), _dev(skin_out, "skin_out", need),
+                                 _dev(verts_out, "verts_out", n * mesh.n_vertices * 3), st,
                                  ctypes.byref(opts)), "hs_scan_skin")
     return global_out, skin_out, verts_out
 
@@ -405,9 +439,10 @@ def scan_varied(parents, local, inv_bind=None, global_out=None, skin_out=None, s
         skin_out = torch.empty_like(local)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    _check(lib().hs_scan_varied(parents.data_ptr(), local.data_ptr(),
-                                None if inv_bind is None else inv_bind.data_ptr(), J, n,
-                                global_out.data_ptr(), None if skin_out is None else skin_out.data_ptr(), st),
+    need = n * J * 12
+    _check(lib().hs_scan_varied(_dev(parents, "parents", n * J, ("int32",)), _dev(local, "local", need),
+                                _dev(inv_bind, "inv_bind", need), J, n,
+                                _dev(global_out, "global_out", need), _dev(skin_out, "skin_out", need), st),
            "hs_scan_varied")
     return global_out, skin_out
 
@@ -456,8 +491,10 @@ def animate(sk: "Skeleton", clips: ClipSet, layers, global_out=None, skin_out=No
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
     opts = _AnimateOpts(ANIMATE_MODE[mode], 0, workspace_bytes)
-    _check(lib().hs_animate_ex(sk.handle, clips.handle, layers.data_ptr(), nl, n, global_out.data_ptr(),
-                               None if skin_out is None else skin_out.data_ptr(), st, ctypes.byref(opts)),
+    need = n * sk.n_joints * 12
+    _check(lib().hs_animate_ex(sk.handle, clips.handle, _dev(layers, "layers", n * nl * 4, ("int32", "float32")),
+                               nl, n, _dev(global_out, "global_out", need), _dev(skin_out, "skin_out", need), st,
+                               ctypes.byref(opts)),
            "hs_animate")
     return global_out, skin_out
 
@@ -478,9 +515,11 @@ def animate_skin(sk: "Skeleton", clips: "ClipSet", layers, mesh: "Mesh", global_
         verts_out = torch.empty((n, mesh.n_vertices, 3), dtype=torch.float32, device=layers.device)
     st = torch.cuda.current_stream().cuda_stream if stream is None else (
         stream if isinstance(stream, int) else stream.cuda_stream)
-    _check(lib().hs_animate_skin(sk.handle, clips.handle, layers.data_ptr(), nl, n, mesh.handle,
-                                 global_out.data_ptr(), None if skin_out is None else skin_out.data_ptr(),
-                                 verts_out.data_ptr(), st), "hs_animate_skin")
+    need = n * sk.n_joints * 12
+    _check(lib().hs_animate_skin(sk.handle, clips.handle, _dev(layers, "layers", n * nl * 4, ("int32", "float32")),
+                                 nl, n, mesh.handle, _dev(global_out, "global_out", need),
+                                 _dev(skin_out, "skin_out", need),
+                                 _dev(verts_out, "verts_out", n * mesh.n_vertices * 3), st), "hs_animate_skin")
     return global_out, skin_out, verts_out
 
 
@@ -502,33 +541,31 @@ class Pipeline:
 
     def scan_host(self, sk: Skeleton, h_local, h_global, h_skin, n_chars: int | None = None):
         """Host tensors/arrays (pinned for full PCIe rate) -> fills h_global, h_skin."""
-        def ptr(t):
-            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
-
         if n_chars is None:
             n_chars = h_local.shape[0]
-        _check(lib().hs_scan_host(self._h, sk.handle, ptr(h_local), n_chars, ptr(h_global),
-                                  ptr(h_skin)), "hs_scan_host")
+        need = n_chars * sk.n_joints * 48
+        _check(lib().hs_scan_host(self._h, sk.handle, _host(h_local, "h_local", need), n_chars,
+                                  _host(h_global, "h_global", need), _host(h_skin, "h_skin", need)),
+               "hs_scan_host")
 
     def animate_host(self, sk: Skeleton, clips: "ClipSet", h_layers, h_global, h_skin):
         """hs_animate_host: host layer states [N, n_layers] (LAYER_DTYPE array or an int32
         [N, n_layers, 4] tensor, pinned for full PCIe rate) -> fills h_global, h_skin."""
-        def ptr(t):
-            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
-
         n, nl = h_layers.shape[0], h_layers.shape[1]
-        _check(lib().hs_animate_host(self._h, sk.handle, clips.handle, ptr(h_layers), nl, n, ptr(h_global),
-                                     ptr(h_skin)), "hs_animate_host")
+        need = n * sk.n_joints * 48
+        _check(lib().hs_animate_host(self._h, sk.handle, clips.handle, _host(h_layers, "h_layers", n * nl * 16),
+                                     nl, n, _host(h_global, "h_global", need), _host(h_skin, "h_skin", need)),
+               "hs_animate_host")
 
     def scan_host_batch(self, items):
         """hs_scan_host_batch: items = [(Skeleton, h_local, h_global, h_skin), ...] on the
         host; one pipeline over all of them."""
-        def ptr(t):
-            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
-
         arr = (_BatchItem * max(1, len(items)))()
         for i, (sk, hl, hg, hsk) in enumerate(items):
-            arr[i] = _BatchItem(sk.handle, ptr(hl), hl.shape[0], ptr(hg), ptr(hsk))
+            n = hl.shape[0]
+            need = n * sk.n_joints * 48
+            arr[i] = _BatchItem(sk.handle, _host(hl, f"items[{i}].h_local", need), n,
+                                _host(hg, f"items[{i}].h_global", need), _host(hsk, f"items[{i}].h_skin", need))
         _check(lib().hs_scan_host_batch(self._h, arr, len(items)), "hs_scan_host_batch")
 
     def close(self):

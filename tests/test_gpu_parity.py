@@ -391,3 +391,28 @@ def test_c_client_runs():
     r = subprocess.run([out], capture_output=True, text=True, timeout=120)
     print(r.stdout, r.stderr)
     assert r.returncode == 0 and "max |err|" in r.stdout
+
+
+def test_binding_rejects_bad_buffers_before_the_abi():
+    """The binding checks what the C ABI cannot (pointer residency, dtype, contiguity,
+    size) and raises before any kernel could touch a wrong buffer."""
+    sk = hs.Skeleton(hsgen.skeleton("hum32"))
+    x = torch.zeros((4, 32, 3, 4), device="cuda")
+    g = torch.empty_like(x)
+    with pytest.raises(TypeError):
+        sk.scan_into(x.cpu(), g)                                   # host tensor as device input
+    with pytest.raises(TypeError):
+        sk.scan_into(x.double(), g)                                # wrong dtype
+    with pytest.raises(ValueError):
+        sk.scan_into(x, torch.empty((4, 32, 4, 3), device="cuda").transpose(2, 3))   # strided
+    with pytest.raises(ValueError):
+        sk.scan_into(x, g[:3])                                     # too small for n_chars = 4
+    pl = hs.Pipeline(batch_bytes=1 << 20)
+    with pytest.raises(TypeError):
+        pl.scan_host(sk, x, x.cpu(), x.cpu())                      # device tensor as host input
+    with pytest.raises(ValueError):
+        pl.scan_host(sk, x.cpu(), np.empty((3, 32, 3, 4), np.float32), x.cpu())
+    sk.scan_into(x, g)                                             # and the good call still works
+    torch.cuda.synchronize()
+    assert torch.equal(g, x)                                       # zero locals: roots stay zero
+    pl.close()
