@@ -16,6 +16,27 @@
 #ifndef HS_PROF_HOOKS
 #define HS_PROF_HOOKS 0   // 1: the HS_DEBUG_PROF phase profile (tools/prof_*.py build it); its checks cost ~3 %
 #endif
+// HS_DEBUG_BOUNDS=1 (a debug build, tests/test_gpu_bounds.py): every shared-memory
+// slot index and TMA byte count is checked against its buffer; a violation traps.
+// compute-sanitizer is closed on this pool, so this build stands in for memcheck.
+#ifndef HS_DEBUG_BOUNDS
+#define HS_DEBUG_BOUNDS 0
+#endif
+#if HS_DEBUG_BOUNDS
+#include <cstdio>
+#define HS_BOUND(cond)                                                                       \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("hs bounds violated: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define HS_BOUND(cond) \
+    do {               \
+    } while (0)
+#endif
 #ifndef HS_LBS_U
 #define HS_LBS_U 2
 #endif
@@ -115,6 +136,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             const int64_t c0 = (g - ld.base) * ld.C;
             const int64_t nc = min((int64_t)ld.C, ld.n_chars - c0);
             const uint32_t bytes = (uint32_t)(nc * ld.J * 48);
+            HS_BOUND(nc > 0 && c0 >= 0 && (int64_t)bytes <= tile_f * 4);
             mbar_expect_tx(&full[stage], bytes);
             const char* src = reinterpret_cast<const char*>(ld.local + c0 * ld.J * 12);
             char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
@@ -153,6 +175,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             const int64_t c0 = (g - st.base) * st.C;
             const int64_t nc = min((int64_t)st.C, st.n_chars - c0);
             const uint32_t bytes = (uint32_t)(nc * st.J * 48);
+            HS_BOUND(nc > 0 && c0 >= 0 && (int64_t)bytes <= tile_f * 4);
             {
                 char* gp = reinterpret_cast<char*>(st.gout + c0 * st.J * 12);
                 const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
@@ -214,7 +237,10 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             for (int s2 = 0; s2 < K; ++s2) {
                 const int src = (int)(int16_t)(m[s2] >> 32);
                 const int ibu = (int)((m[s2] >> 16) & 0xffff);
-                if (src != kSrcNone) ldg3(S.ib + (int64_t)ibu * 12, ibr[s2]);
+                if (src != kSrcNone) {
+                    HS_BOUND(ibu >= 0 && ibu < S.J);
+                    ldg3(S.ib + (int64_t)ibu * 12, ibr[s2]);
+                }
             }
         }
         // phase-2 tables: identical for every tile of the segment, staged per CTA (the
@@ -292,6 +318,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         const int src = (int)(int16_t)(m[s] >> 32);
                         const int own = (int)(int16_t)(m[s] >> 48);
                         float l[12];
+                        HS_BOUND(off >= 0 && (off + 1) * 12 <= tile_f);
                         ld3(L + off * 12, l);
                         if (src == kSrcPrev) {
                             float tmp[12];
@@ -302,6 +329,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
 #pragma unroll
                             for (int e = 0; e < 12; ++e) acc[e] = l[e];
                         }
+                        HS_BOUND(own < a.p_floats / 12);
                         if (own >= 0) st3(P + own * 12, acc);
                     }
                 }
@@ -336,6 +364,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         const int own = (int)(int16_t)(m[s] >> 48);
                         if (own >= 0) {
                             float x[12], y[12];
+                            HS_BOUND(own < a.p_floats / 12);
                             ld3(P + own * 12, x);
                             compose(excl, x, y);
                             st3(P + own * 12, y);
@@ -361,6 +390,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                                   self = slot + ((w >> 15) & 1) * SEGV(nslots, S2_g),
                                   link = (int)(w >> 16);
                         float x[12], y[12], z[12];
+                        HS_BOUND(link >= 0 && link < a.p_floats / 12 && self < a.p_floats / 12 &&
+                                 dst < a.p_floats / 12);
                         ld3(P + link * 12, x);
                         ld3(P + self * 12, y);
                         compose(x, y, z);
@@ -377,6 +408,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         if (e < e1) {
                             const uint32_t w = s_rounds[e];
                             float x[12], y[12];
+                            HS_BOUND((int)(w >> 16) < a.p_floats / 12 && (int)(w & 0x3fff) < a.p_floats / 12);
                             ld3(P + (int)(w >> 16) * 12, x);
                             ld3(P + (int)(w & 0x3fff) * 12, y);
                             compose(x, y, z[q]);
@@ -404,6 +436,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                     if (src == kSrcNone) continue;
                     const int off = (int)(m[s] & 0xffff);
                     float l[12];
+                    HS_BOUND(off >= 0 && (off + 1) * 12 <= tile_f);
                     ld3(L + off * 12, l);
                     if (RUNS) {
                         // the parent's global pose as the left operand, then ONE compose
@@ -422,6 +455,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         } else if (src == kSrcRun) {
                             if (run_anchor >= 0) {
                                 float pa[12];
+                                HS_BOUND(run_anchor < a.p_floats / 12);
                                 ld3(P + run_anchor * 12, pa);
                                 compose(pa, excl, left);
                             } else {
@@ -429,6 +463,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                                 for (int e = 0; e < 12; ++e) left[e] = excl[e];
                             }
                         } else {
+                            HS_BOUND(src >= 0 && src < a.p_floats / 12);
                             ld3(P + src * 12, left);
                         }
                         compose(left, l, acc);
@@ -442,6 +477,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                         for (int e = 0; e < 12; ++e) acc[e] = l[e];
                     } else {
                         float pa[12];
+                        HS_BOUND(src >= 0 && src < a.p_floats / 12);
                         ld3(P + src * 12, pa);
                         compose(pa, l, acc);
                     }
@@ -486,6 +522,8 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
 #pragma unroll
                         for (int u = 0; u < kLbsU; ++u) {
                             const int v = v0 + u * NC;
+                            HS_BOUND((cl + 1) * Jn * 12 <= tile_f && js[u][0] < Jn * 12 && js[u][1] < Jn * 12 &&
+                                     js[u][2] < Jn * 12 && js[u][3] < Jn * 12);
                             if (v < V) lbs_vertex(Sc, pa[u], pb[u], js[u], vout + ((int64_t)cl * V + v) * 3);
                         }
                     }
