@@ -9,6 +9,27 @@
 #include <algorithm>
 #include <cstdint>
 
+// HS_DEBUG_BOUNDS=1 (a debug build, tests/test_gpu_bounds.py): every shared-memory
+// slot index and TMA byte count is checked against its buffer; a violation traps.
+// compute-sanitizer is closed on this pool, so this build stands in for memcheck.
+#ifndef HS_DEBUG_BOUNDS
+#define HS_DEBUG_BOUNDS 0
+#endif
+#if HS_DEBUG_BOUNDS
+#include <cstdio>
+#define HS_BOUND(cond)                                                                       \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("hs bounds violated: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define HS_BOUND(cond) \
+    do {               \
+    } while (0)
+#endif
 #ifndef HS_S1_E
 #define HS_S1_E 1      // Stage-1 elements per thread per pass
 #endif

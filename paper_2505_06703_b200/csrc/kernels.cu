@@ -16,27 +16,6 @@
 #ifndef HS_PROF_HOOKS
 #define HS_PROF_HOOKS 0   // 1: the HS_DEBUG_PROF phase profile (tools/prof_*.py build it); its checks cost ~3 %
 #endif
-// HS_DEBUG_BOUNDS=1 (a debug build, tests/test_gpu_bounds.py): every shared-memory
-// slot index and TMA byte count is checked against its buffer; a violation traps.
-// compute-sanitizer is closed on this pool, so this build stands in for memcheck.
-#ifndef HS_DEBUG_BOUNDS
-#define HS_DEBUG_BOUNDS 0
-#endif
-#if HS_DEBUG_BOUNDS
-#include <cstdio>
-#define HS_BOUND(cond)                                                                       \
-    do {                                                                                      \
-        if (!(cond)) {                                                                        \
-            printf("hs bounds violated: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__, \
-                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
-            __trap();                                                                         \
-        }                                                                                     \
-    } while (0)
-#else
-#define HS_BOUND(cond) \
-    do {               \
-    } while (0)
-#endif
 #ifndef HS_LBS_U
 #define HS_LBS_U 2
 #endif

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
             const int64_t wbase = e0 + q * 256 + (threadIdx.x & ~31);   // the warp's first element
             if (wbase >= n) break;                                      // warp-uniform
             const bool ok = wbase + lane < n;
+            HS_BOUND(!ok || (cl >= 0 && cl < nc && jj >= 0 && jj < J));
             const int j[1] = {ok ? jj : 0};
             const int4* dp[1] = {sd + (ok ? cl : 0) * nl};
             const bool valid[1] = {ok};
@@ -264,6 +265,8 @@ __global__ void __launch_bounds__(256) lbs_kernel(const float* __restrict__ S, i
             int js[4];
             mesh_joints(__ldg(mesh_j + v), js);
             const float4 pb = __ldg(mesh_b + v);
+            HS_BOUND(js[0] < J * 12 && js[1] < J * 12 && js[2] < J * 12 && js[3] < J * 12 &&
+                     __float_as_int(pb.w) >= 0 && __float_as_int(pb.w) < V);
             lbs_vertex(pal, __ldg(mesh_a + v), pb, js, vs + (int64_t)__float_as_int(pb.w) * 3);
         }
         __syncthreads();
