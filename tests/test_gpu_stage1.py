@@ -226,3 +226,28 @@ def test_workspace_trim_releases_the_pool():
     torch.cuda.synchronize()
     assert torch.equal(g1, g2) and torch.equal(s1, s2)
     assert hs.workspace_trim() == 0
+
+
+def test_c5_full_size_stage1_sampled():
+    """Stage 1 + scan + bind at C5's full size in bench.py --stage1's configuration (8
+    clips of 31 keys per type, 2 layers, two-pass placement): sampled characters
+    against the fp64 oracle, within the Stage-1 bound of each skeleton's depth."""
+    for name, n, seed, type_, ib_seed in hsgen.CONFIGS[5]:
+        par = hsgen.skeleton(name)
+        J = len(par)
+        ib = hsgen.inv_bind(ib_seed, J)
+        keys = hsgen.clips(100 + type_, J, 8, 31, type_=type_)
+        lay = hsgen.layers(seed, n, 2, 8, 1.5, type_=type_)
+        sk = hs.Skeleton(par, ib)
+        cs = hs.ClipSet(sk, keys, 30.0, 1)
+        g, s = hs.animate(sk, cs, lay)
+        torch.cuda.synchronize()
+        idx = np.unique(np.r_[0, np.linspace(0, n - 1, 10).astype(np.int64), n - 1])
+        G, S = oracle.animate(par, keys, 30.0, 1, lay[idx], ib)
+        tol = stage1_tol(levels(par))
+        eg = float(np.abs(g[idx].cpu().numpy() - G).max())
+        es = float(np.abs(s[idx].cpu().numpy() - S).max())
+        print(f"{name} x {n}: Stage-1 sampled max err {max(eg, es):.3e} (bound {tol:.1e})")
+        assert eg <= tol and es <= tol
+        del g, s
+        torch.cuda.empty_cache()
