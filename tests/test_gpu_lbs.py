@@ -200,3 +200,29 @@ def test_animate_skin_one_call_matches_two_calls():
         assert torch.equal(g, g2) and torch.equal(s, s2)
         G, S = oracle.animate(par, keys, 30.0, 1, lay, ib)
         assert np.abs(v.cpu().numpy() - oracle.skin_vertices(S, *mesh)).max() <= TOL_VERTS
+
+
+def test_c5_full_size_lbs_sampled():
+    """Scan + bind + LBS of a 1000-vertex mesh at C5's full size in bench.py
+    --skin-mesh 1000's configuration (AUTO placement per type): sampled characters'
+    vertices against the oracle's LBS of its own fp64 skin poses."""
+    for name, n, seed, type_, ib_seed in hsgen.CONFIGS[5]:
+        par = hsgen.skeleton(name)
+        J = len(par)
+        ib = hsgen.inv_bind(ib_seed, J)
+        sk = hs.Skeleton(par, ib)
+        mesh_np = hsgen.mesh(200 + type_, par, 1000, type_=type_)
+        m = hs.Mesh(sk, *mesh_np)
+        x = torch.empty((n, J, 3, 4), device="cuda")
+        assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
+                                                     torch.cuda.current_stream().cuda_stream) == 0
+        g, s, v = hs.scan_skin(sk, m, x, skin=True)
+        torch.cuda.synchronize()
+        idx = np.unique(np.r_[0, np.linspace(0, n - 1, 8).astype(np.int64), n - 1])
+        host = x[idx].cpu().numpy()
+        G, S = oracle.scan(par, host, ib)
+        err = float(np.abs(v[idx].cpu().numpy() - oracle.skin_vertices(S, *mesh_np)).max())
+        print(f"{name} x {n}: vertices sampled max err {err:.3e}")
+        assert err <= TOL_VERTS
+        del x, g, s, v
+        torch.cuda.empty_cache()
