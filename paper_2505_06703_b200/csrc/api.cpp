@@ -63,6 +63,7 @@ struct hs_skeleton {
     int smem_optin = 0;
     hs::SplitProgram sp;
     hs_skeleton* sub = nullptr;    // anchor skeleton of the split path
+    hs_skeleton* small = nullptr;  // the same chunk program in smaller tiles, for small crowds
     int split_levels = 0;
     // device tables
     float* d_ib = nullptr;
@@ -113,6 +114,7 @@ namespace {
 void free_skeleton(hs_skeleton* sk) {
     if (!sk) return;
     free_skeleton(sk->sub);
+    free_skeleton(sk->small);
     cudaFree(sk->d_ib);
     cudaFree(sk->d_parents);
     cudaFree(sk->d_lift);
@@ -254,6 +256,25 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
             (e = hs::prepare_chunked(sk->K, sk->smem)) != cudaSuccess) {
             free_skeleton(sk);
             return cuda_fail(e, "chunked program");
+        }
+        // Small crowds leave SMs idle with multi-character tiles (C1: 1,000 x hum32 is
+        // 46 tiles of 22): a second program with the same chunks in tiles of
+        // max(2n, 256) joints, used per call when the default tiles would not cover
+        // the SMs (6.65 -> 5.24 us).  Same chunking and K, so every
+        // character's arithmetic is identical: results do not depend on which runs.
+        if (depth == 0 && sk->tp.C >= 4 && !o.tile_joints && sk->chunking != hs::CHUNK_RUNS) {
+            hs_create_opts so = o;
+            so.chunk = sk->K;
+            so.chunking = sk->chunking + 1;
+            so.tile_joints = std::max(2 * n, 256);
+            hs_skeleton* small = nullptr;
+            if (create_impl(parents, n, inv_bind, so, &small, depth + 1) == HS_OK) {
+                if (small->chunked && small->tp.C >= 2 && small->tp.C < sk->tp.C && small->K == sk->K &&
+                    small->chunking == sk->chunking)
+                    sk->small = small;
+                else
+                    free_skeleton(small);
+            }
         }
     } else {
         sk->sp = hs::build_split_program(P, sk->K);
@@ -413,6 +434,8 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
     switch (algo) {
         case HS_ALGO_CHUNKED: {
             if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "skeleton does not fit the single-CTA path");
+            if (!layers && tile_ctas == 0 && sk->small && (n_chars + sk->tp.C - 1) / sk->tp.C < hs::sm_count())
+                return scan_impl(sk->small, local, n_chars, gout, sout, st, algo, max_rounds, tile_ctas);
             hs::ChunkedArgs a{};
             const ChunkItem item{sk, local, n_chars, gout, sout};
             chunked_layout(&item, 1, sk->stages, sk->sbufs, a);

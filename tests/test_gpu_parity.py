@@ -446,3 +446,20 @@ def test_c5_full_size_sampled_parity():
         torch.cuda.empty_cache()
     print(f"C5 sampled max err {worst:.3e}")
     assert worst <= TOL
+
+
+@pytest.mark.parametrize("name", ["hum32", "hum64", "chain256"])
+def test_small_crowd_program_is_bitwise_the_default(name):
+    """Small crowds run a second program with smaller tiles (more CTAs busy); it keeps
+    every character's chunks, so a character's result does not depend on the crowd it
+    is scanned in: 1,000 / 37 / 1 characters alone equal the same characters inside a
+    20,000-character crowd, bit for bit."""
+    par = hsgen.skeleton(name)
+    J = len(par)
+    sk = hs.Skeleton(par, hsgen.inv_bind(61, J))
+    x = torch.from_numpy(hsgen.local_poses(62, J, 20_000)).cuda()
+    g_big, s_big = sk.scan(x)
+    for lo, n in ((0, 1000), (4321, 37), (19_999, 1)):
+        g, s = sk.scan(x[lo:lo + n].contiguous())
+        assert torch.equal(g, g_big[lo:lo + n]) and torch.equal(s, s_big[lo:lo + n])
+    torch.cuda.synchronize()

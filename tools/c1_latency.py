@@ -17,7 +17,7 @@ for n in (1000, 100, 10000):
     x = torch.from_numpy(hsgen.local_poses(1, J, n)).cuda()
     g, s = torch.empty_like(x), torch.empty_like(x)
     res = {}
-    for tj in (64, 128, 256, 512, 1024):
+    for tj in (0, 64, 128, 256, 512, 1024):   # 0 = the default (small-crowd program per call)
         sk = hs.Skeleton(par, hsgen.inv_bind(1, J), tile_joints=tj)
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
