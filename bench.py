@@ -305,10 +305,11 @@ def run_ours(args):
     # auto: one batch launch only when every type's crowd is small (under ~32 tiles per
     # SM, where per-launch fill/drain and tails dominate; profiles/r01f_next3_sweep.json);
     # C5's crowds are thousands of tiles per SM, where per-type launches measured 3%
-    # faster (the multi-segment kernel's program switch costs registers)
+    # faster (the multi-segment kernel's program switch costs registers); a single type
+    # runs hs_scan, whose small-crowd program keeps every SM busy
     small = all(-(-w["n"] // max(1, w["sk"].query("tile_chars"))) < 32 * 148 for w in work)
     batch = args.launch == "batch" or (
-        args.launch == "auto" and small and not args.stage1 and not args.skin_mesh and args.algo == "auto"
+        args.launch == "auto" and small and len(work) > 1 and not args.stage1 and not args.skin_mesh and args.algo == "auto"
         and args.tile_ctas == 0 and len({w["sk"].query("chunk") for w in work}) == 1
         and all(w["sk"].query("path") == 1 for w in work))
     # launches per step: one hs_scan_batch over every type, or one call per type
