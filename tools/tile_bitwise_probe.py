@@ -1,3 +1,6 @@
+#!/usr/bin/env python
+"""Tuning aid: is a character's result independent of the tile size (characters per
+CTA tile)?  Bitwise comparison of hs_scan across tile_joints, per C5 skeleton."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np, hsgen
