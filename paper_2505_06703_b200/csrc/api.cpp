@@ -617,6 +617,17 @@ hs_status hs_scan_batch(const hs_batch_item* items, int32_t n_items, void* cuda_
         segs[n++] = ChunkItem{sk, it.local, it.n_chars, it.global_out, it.skin_out};
     }
     if (n == 0) return HS_OK;
+    // small crowds: when the default tiles of all items together would leave SMs idle,
+    // the small-tile twins (same chunks, bitwise the same results) take their place
+    int64_t tiles = 0;
+    for (int i = 0; i < n; ++i) tiles += (segs[i].n_chars + segs[i].sk->tp.C - 1) / segs[i].sk->tp.C;
+    if (tiles < hs::sm_count())
+        for (int i = 0; i < n; ++i)
+            if (const hs_skeleton* s = segs[i].sk->small) {
+                segs[i].sk = s;
+                stages = std::min(stages, s->stages);
+                sbufs = std::min(sbufs, s->sbufs);
+            }
     hs::ChunkedArgs a{};
     for (;;) {   // the common layout of the largest tile / anchor set / program
         chunked_layout(segs, n, stages, sbufs, a);
