@@ -749,15 +749,18 @@ hs_status hs_scan_skin_ex(const hs_skeleton* sk, const hs_mesh* mesh, const floa
     }
     if (mode == HS_SKIN_FUSED) {
         if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "the fused LBS epilogue needs a single-CTA skeleton");
+        // small crowds: the small-tile twin (same chunks and vertices, more CTAs busy)
+        const hs_skeleton* ps =
+            sk->small && (n_chars + sk->tp.C - 1) / sk->tp.C < hs::sm_count() ? sk->small : sk;
         hs::ChunkedArgs a{};
-        const ChunkItem item{sk, local, n_chars, global_out, skin_out};
-        chunked_layout(&item, 1, sk->stages, sk->sbufs, a);
+        const ChunkItem item{ps, local, n_chars, global_out, skin_out};
+        chunked_layout(&item, 1, ps->stages, ps->sbufs, a);
         a.mesh_a = mesh->d_a;
         a.mesh_b = mesh->d_b;
         a.mesh_j = mesh->d_j;
         a.verts = verts_out;
         a.n_verts = mesh->n_verts;
-        return run_chunked(a, sk->K, st);
+        return run_chunked(a, ps->K, st);
     }
     // two-pass: the scan writes S (to skin_out, or to a pooled workspace in
     // batches when the caller does not want S), then lbs_kernel skins from it
