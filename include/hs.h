@@ -323,7 +323,9 @@ typedef enum {
     HS_Q_CHUNKING = 17,      /* chunk construction in use (1 consecutive, 2 heavy-path pieces)  */
     HS_Q_TILE_SLOTS = 18,    /* plan only: P slots of the one-character tile program            */
     HS_Q_TILE_ROUNDS_ENTRIES = 19, /* plan only: phase-2 descriptors of that program           */
-    HS_Q_TILE_R2 = 20        /* plan only: its pointer-jumping rounds                           */
+    HS_Q_TILE_R2 = 20,       /* plan only: its pointer-jumping rounds                           */
+    HS_Q_SMALL_TILE_CHARS = 21 /* characters per tile of the small-crowd twin program (0 = none):
+                                  hs_scan runs it when the default tiles would not cover the SMs */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);

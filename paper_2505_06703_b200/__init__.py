@@ -38,7 +38,7 @@ QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "til
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
          "stages": 11, "device": 12, "split_levels": 13,
          "pbufs": 15, "sbufs": 16, "chunking": 17, "tile_slots": 18, "tile_rounds_entries": 19,
-         "tile_r2": 20}
+         "tile_r2": 20, "small_tile_chars": 21}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
           "anchor_link": 6, "chunk_lists": 7, "tile_meta": 8, "tile_p1len": 9,

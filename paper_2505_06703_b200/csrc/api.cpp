@@ -958,6 +958,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_PATH: *v = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT; break;
         case HS_Q_CHUNK: *v = sk->K; break;
         case HS_Q_TILE_CHARS: *v = sk->chunked ? sk->tp.C : 0; break;
+        case HS_Q_SMALL_TILE_CHARS: *v = sk->small ? sk->small->tp.C : 0; break;
         case HS_Q_ANCHORS: *v = sk->chunked ? sk->tp.nslots : sk->sp.nslots; break;
         case HS_Q_ANCHOR_ROUNDS: *v = sk->chunked ? sk->tp.R2 : (sk->sub ? sk->sub->plan.R : 0); break;
         case HS_Q_IDENTITY_ORDER: *v = sk->plan.identity ? 1 : 0; break;

@@ -457,6 +457,7 @@ def test_small_crowd_program_is_bitwise_the_default(name):
     par = hsgen.skeleton(name)
     J = len(par)
     sk = hs.Skeleton(par, hsgen.inv_bind(61, J))
+    assert 2 <= sk.query("small_tile_chars") < sk.query("tile_chars")
     x = torch.from_numpy(hsgen.local_poses(62, J, 20_000)).cuda()
     g_big, s_big = sk.scan(x)
     for lo, n in ((0, 1000), (4321, 37), (19_999, 1)):
