@@ -459,10 +459,15 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "parity": check,
     }
+    failed = check is not None and not check["pass"]
+    if failed:   # a wrong answer is not a benchmark result: no value, non-zero exit
+        line["value_if_correct"] = line["value"]
+        line["value"] = None
+        line["error"] = "sampled parity against the oracle failed (see parity)"
     emit(line, args)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 1 if failed else 0
 
 
 def sampled_parity(work, rank, per_type=24):

@@ -260,9 +260,13 @@ hs_status hs_clipset_destroy(hs_clipset* cs);
 
 /* One animation layer of one character (16 bytes). */
 typedef struct {
-    int32_t clip;      /* clip index in the clip set                                  */
+    int32_t clip;      /* clip index in the clip set; values outside [0, n_clips) are
+                          clamped to the nearest valid clip on the device (no error:
+                          layers are device data and are not validated per call)   */
     float time;        /* seconds                                                     */
-    float weight;      /* blend weight (> 0 for at least one layer)                   */
+    float weight;      /* blend weight; the weights of a character must have a
+                          positive sum (SPEC.md WeightSumZero): a sum <= 0 is not
+                          detected on the device and yields non-finite poses        */
     int32_t reserved;  /* ignored                                                     */
 } hs_layer;
 

@@ -390,15 +390,13 @@ void chunked_layout(const ChunkItem* items, int n, int stages, int sbufs, hs::Ch
     a.smem_bytes = 128 + (int64_t)(stages + sbufs) * max_f * 48 + (int64_t)p_floats * 4 + tables;
     a.threads = ((max_t + 31) / 32) * 32 + 32;
     a.has_runs = runs ? 1 : 0;
-    a.bulk_piece = 4096;   // 4 KB TMA bulk copies (measured: 4 KB 10.63, 8 KB 10.67, whole tile 10.83 ms on C5)
-    static const char* bp = std::getenv("HS_BULK_PIECE");   // tuning aid, read once
-    if (bp) a.bulk_piece = std::atoi(bp) & ~15;
+    a.bulk_piece = HS_BULK_PIECE;   // compile-time (kernels.cuh); tuning builds pass -DHS_BULK_PIECE=...
 }
 
 // Launch one chunked program (with the HS_DEBUG_PROF phase profile when set).
 hs_status run_chunked(hs::ChunkedArgs& a, int K, cudaStream_t st) {
     a.prof = nullptr;
-    if (std::getenv("HS_DEBUG_PROF")) {   // debug aid: per-phase cycle split, synchronising
+    if (HS_PROF_HOOKS && std::getenv("HS_DEBUG_PROF")) {   // profiling builds only: per-phase cycle split, synchronising
         cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
         cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
     }

@@ -176,17 +176,30 @@ __device__ __forceinline__ void key_index(float t, int n_keys, float fps, float 
     a = frac;
 }
 
-// MUFU approximations (rel. error ~2^-22): a unit quaternion's norm and the weight
-// sum are far from denormal, so the IEEE fix-up paths of rsqrtf / '/' buy nothing.
+// Normalisation of the blended quaternion and of the weight sum.  HS_S1_NORM = 0:
+// MUFU approximations (rsqrt.approx / rcp.approx, rel. error up to ~2^-22);
+// 1: correctly rounded (__frsqrt_rn / __frcp_rn), the product build (DESIGN.md §3:
+// Stage-1 error budget, measured per variant).
+#ifndef HS_S1_NORM
+#define HS_S1_NORM 1
+#endif
 __device__ __forceinline__ float rsqrt_fast(float x) {
+#if HS_S1_NORM == 0
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#else
+    return __frsqrt_rn(x);
+#endif
 }
 __device__ __forceinline__ float rcp_fast(float x) {
+#if HS_S1_NORM == 0
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#else
+    return __frcp_rn(x);
+#endif
 }
 
 // Layer descriptor of one (character, layer) of a tile, written by the producer

@@ -13,9 +13,6 @@
 
 #include "device_util.cuh"
 
-#ifndef HS_PROF_HOOKS
-#define HS_PROF_HOOKS 0   // 1: the HS_DEBUG_PROF phase profile (tools/prof_*.py build it); its checks cost ~3 %
-#endif
 #ifndef HS_LBS_U
 #define HS_LBS_U 2
 #endif
@@ -405,7 +402,12 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
 
             // phase 3: final fold, G in place, S into the S buffer
             float* S = SB + sb * tile_f;
-            if (SKIN && it >= NSS) mbar_wait(&sfree[sb], sphase);
+            // The S buffer's previous use must have been read out by the producer's bulk
+            // store.  sphase tracks the parity of use it / NSS - 1, which is only right if
+            // every use is awaited: a multi-segment launch can mix segments with and
+            // without skin output, so it waits on every tile (the producer arrives on
+            // sfree after every tile, skin or not).
+            if ((SKIN || MULTI) && it >= NSS) mbar_wait(&sfree[sb], sphase);
             prof_mark(3);
             {
                 float acc[12];

@@ -34,7 +34,7 @@ constexpr int kStage1Unroll = HS_S1K_UNROLL;
 
 template <int NLT>
 __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ ChunkedArgs a, int64_t c0,
-                                                     int64_t n_chars, float* __restrict__ local) {
+                                                     int64_t n_chars, float* __restrict__ local, int per) {
     extern __shared__ int4 sd[];   // layer descriptors of the block's characters
     __shared__ __align__(128) float stg[(HS_S1K_TMA_STORE ? 2 : 1) * 256 * 12];   // warps' local poses before the store
 #if HS_S1K_TMA_STORE
@@ -44,10 +44,10 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
     const int lane = threadIdx.x & 31;
     const int64_t n = n_chars * J;
     const int4* lay = reinterpret_cast<const int4*>(a.layers);
-    constexpr int kTile = 256 * kStage1PerThread;   // elements per block iteration
+    const int kTile = 256 * per;   // elements per block iteration (per <= kStage1PerThread)
     for (int64_t e0 = (int64_t)blockIdx.x * kTile; e0 < n; e0 += (int64_t)gridDim.x * kTile) {
         const int64_t cfirst = e0 / J;
-        const int nc = (int)((min(n, e0 + kTile) - 1) / J - cfirst + 1);
+        const int nc = (int)((min(n, e0 + (int64_t)kTile) - 1) / J - cfirst + 1);
         __syncthreads();   // the previous block-tile's readers are done
         for (int i = threadIdx.x; i < nc * nl; i += blockDim.x)
             sd[i] = layer_desc(a, __ldg(lay + (c0 + cfirst) * nl + i));
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
         int cl = rel / J, jj = rel - cl * J;
         const int sc = 256 / J, sj = 256 - sc * J;
 #pragma unroll kStage1Unroll
-        for (int q = 0; q < kStage1PerThread; ++q) {
+        for (int q = 0; q < per; ++q) {
             const int64_t wbase = e0 + q * 256 + (threadIdx.x & ~31);   // the warp's first element
             if (wbase >= n) break;                                      // warp-uniform
             const bool ok = wbase + lane < n;
@@ -484,20 +484,31 @@ cudaError_t raise_smem_once(const void* fn, int bytes, std::atomic<uint64_t>& do
 
 cudaError_t launch_stage1(const ChunkedArgs& a, int64_t c0, int64_t n_chars, float* local, cudaStream_t st) {
     const int64_t n = n_chars * a.seg[0].J;
-    int64_t blocks = (n + 256 * kStage1PerThread - 1) / (256 * kStage1PerThread);
+    // elements per thread between descriptor refreshes: fewer when the block-tile's
+    // layer descriptors would not fit shared memory beside the static staging buffer
+    // (one-joint skeletons with many layers: 2048 characters x 8 layers x 16 B)
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
+    const size_t stat = (HS_S1K_TMA_STORE ? 2 : 1) * 256 * 12 * sizeof(float);
+    int per = kStage1PerThread;
+    auto smem_of = [&](int q) { return (size_t)(256 * q / a.seg[0].J + 2) * a.n_layers * sizeof(int4); };
+    while (per > 1 && smem_of(per) + stat > (size_t)optin) --per;
+    const size_t smem = smem_of(per);
+    if (smem + stat > (size_t)optin) return cudaErrorInvalidValue;
+    int64_t blocks = (n + 256 * per - 1) / (256 * per);
     const int64_t cap = (int64_t)sm_count() * HS_S1K_CTAS_PER_SM;   // grid-stride CTAs of 256 per SM
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ChunkedArgs args = a;
-    void* params[] = {&args, &c0, &n_chars, &local};
-    const size_t smem = (size_t)(256 * kStage1PerThread / a.seg[0].J + 2) * a.n_layers * sizeof(int4);
+    void* params[] = {&args, &c0, &n_chars, &local, &per};
     // one, two and three layers (the common blends) get the unrolled layer loop
     const void* fn = !HS_S1K_SPECIALISE ? reinterpret_cast<const void*>(&stage1_kernel<0>)
                      : a.n_layers == 1   ? reinterpret_cast<const void*>(&stage1_kernel<1>)
                      : a.n_layers == 2 ? reinterpret_cast<const void*>(&stage1_kernel<2>)
                      : a.n_layers == 3 ? reinterpret_cast<const void*>(&stage1_kernel<3>)
                                        : reinterpret_cast<const void*>(&stage1_kernel<0>);
-    if (smem > 48 * 1024) {
+    if (smem + stat > 48 * 1024) {   // static + dynamic above the default 48 KB: opt in
         const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }

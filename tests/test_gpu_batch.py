@@ -122,3 +122,31 @@ def test_batch_errors():
         hs.scan_batch([(sk5, x, x, None)])                  # output aliases input
     assert ei.value.status == hs.HS_ERR_INVALID_ARG
     hs.scan_batch([])                                       # nothing to do
+
+
+def test_mixed_skin_batch_single_s_buffer():
+    """items [skin, no skin, skin] with one S buffer, sized so every CTA gets
+    exactly one tile of each item.  The consumer must await the S buffer on every tile
+    (not only on skin tiles), else the third item's S can overwrite the first item's S
+    while its bulk store still reads it.  Every item equals its own hs_scan bit for bit."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    par = hsgen.skeleton("hum64")
+    ib = hsgen.inv_bind(71, 64)
+    sk = hs.Skeleton(par, ib, stages=3, sbufs=1)
+    assert sk.query("sbufs") == 1
+    per_tile = sk.query("tile_chars")
+    items, want = [], []
+    for i, skin in enumerate((True, False, True)):
+        n = per_tile * sms
+        x = torch.from_numpy(hsgen.local_poses(72 + i, 64, n)).cuda()
+        g = torch.full_like(x, float("nan"))
+        s = torch.full_like(x, float("nan")) if skin else None
+        items.append((sk, x, g, s))
+        want.append(sk.scan(x, skin=skin))
+    for _ in range(3):   # repeated: the race is timing dependent
+        hs.scan_batch(items)
+        torch.cuda.synchronize()
+        for (_, _, g, s), (g2, s2) in zip(items, want):
+            assert torch.equal(g, g2)
+            if s is not None:
+                assert torch.equal(s, s2)

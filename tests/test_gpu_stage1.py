@@ -251,3 +251,17 @@ def test_c5_full_size_stage1_sampled():
         assert eg <= tol and es <= tol
         del g, s
         torch.cuda.empty_cache()
+
+
+def test_one_joint_eight_layers_two_pass():
+    """a one-joint skeleton with 8 layers puts 2048 characters x 8 layer
+    descriptors (256 KB) in one block-tile of the streaming kernel; the launcher shrinks
+    the block-tile to fit shared memory.  G = L (a root), against the fp64 oracle."""
+    par = np.array([-1], np.int32)
+    keys = hsgen.clips(81, 1, 4, 9)
+    lay = hsgen.layers(82, 5000, 8, 4, 1.3)
+    g, s = run(par, keys, 8.0, 1, lay, mode="two_pass")
+    G, S = oracle.animate(par, keys, 8.0, 1, lay)
+    e = max(float(np.abs(g - G).max()), float(np.abs(s - S).max()))
+    print(f"one joint, 8 layers: max err {e:.2e}")
+    assert e <= 4e-6
