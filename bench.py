@@ -41,7 +41,8 @@ STAGE1_CLIPS, STAGE1_KEYS, STAGE1_FPS, STAGE1_LAYERS, STAGE1_SPAN = 8, 31, 30.0,
 METRIC = "joints/sec (Hierarchy-Scan+skin) and HBM GB/s vs peak at 1/2/4/8 B200"
 WORKLOAD_NAME = {1: "C1 1,000 x hum32 (L=8)", 2: "C2 100,000 x hum64 (L=12)",
                  3: "C3 50,000 x chain256 (L=256)", 4: "C4 20,000 x tree1024 (L=300)",
-                 5: "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU"}
+                 5: "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU",
+                 6: "C6 2,000 x tree16384 (L=1024, beyond one CTA: multi-tile path)"}
 
 
 def parse_args(argv=None):
@@ -50,7 +51,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6])
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--cpu-frac", type=int, default=8,
                     help="cpu_baseline / reference sample = n_chars // this, per skeleton type")
@@ -80,6 +81,15 @@ def parse_args(argv=None):
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no checks, no e2e, no cpu baseline")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N > 1 (gloo: CPU collectives, lets a test run "
+                         "several ranks on one GPU; the data path has no collective either way)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config single-type launches (C2, C3, C4, C6) reported in "
+                         "the line's 'configs' object")
+    ap.add_argument("--no-validate", action="store_true",
+                    help="skip the N > 1 validation (all-gather of sampled G/S shards, bitwise "
+                         "check against a single-rank recomputation)")
     return ap.parse_args(argv)
 
 
@@ -96,6 +106,11 @@ def shard(n_total: int, rank: int, world: int, scaling: str):
     lo = n_total * rank // world
     hi = n_total * (rank + 1) // world
     return lo, hi - lo
+
+
+def coll_device(backend: str, device):
+    """Tensors for collectives: CPU under gloo, the rank's GPU under NCCL."""
+    return "cpu" if backend == "gloo" else device
 
 
 def reduce_over_ranks(ms_rank: float, joints_rank: int, world: int, device):
@@ -129,16 +144,23 @@ def measured_peaks():
 
 
 def ncu_traffic(workload: str, kernel: str):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary
-    (only when it was captured on this workload and launch)."""
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary,
+    only when it was captured on this workload and launch AND on these exact library
+    sources (the capture records their hash; any source change makes it stale -> null)."""
+    import paper_2505_06703_b200 as hs
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(path))
-        if d.get("workload") == workload and d.get("kernel") == kernel:
-            return float(d["dram_bytes_per_launch"]), d.get("source")
+        entries = json.load(open(path))
+        entries = entries if isinstance(entries, list) else [entries]
     except Exception:
-        pass
-    return None, None
+        return None, "no profiles/ncu_traffic.json"
+    sha = hs.sources_sha256()
+    for d in entries:
+        if d.get("workload") == workload and d.get("kernel") == kernel:
+            if d.get("sources_sha256") != sha:
+                return None, f"stale capture ({d.get('source')}: sources {d.get('sources_sha256')} != {sha})"
+            return float(d["dram_bytes_per_launch"]), d.get("source")
+    return None, "no capture for this workload / kernel"
 
 
 class ClockSampler:
@@ -229,7 +251,7 @@ def run_reference(args):
             "config": {"workload": WORKLOAD_NAME[args.config] + f" (1/{args.cpu_frac} sample)",
                        "sample": desc, "joints_per_step": joints},
             "cpu_baseline": {"value": value, "unit": "joints/s", "cores": cores, "kind": "oracle",
-                             "sample": desc},
+                             "sample": desc, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "joints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line, args)
@@ -254,12 +276,19 @@ def run_ours(args):
     rank, local_rank, world = dist_env()
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local_rank)
+    # one process per GPU; a gloo test may run several ranks on one GPU (no collective
+    # on the data path, so ranks never wait on each other's kernels)
+    gpu = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group("gloo")
     hs.lib()  # fails loudly when libhs.so is missing: no fallback path exists
     hsgen.lib_cuda()
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", gpu)
+    cdev = coll_device(args.dist_backend, dev)
     stream = torch.cuda.current_stream()
 
     # ---- workload: one skeleton handle and one resident crowd per skeleton type
@@ -345,7 +374,7 @@ def run_ours(args):
     if not (args.no_check or args.profile):
         check = sampled_parity(work, rank)
         if world > 1:   # every rank checks its own shard; the job passes only if all do
-            worst = torch.tensor([check["worst"]], dtype=torch.float64, device=dev)
+            worst = torch.tensor([check["worst"]], dtype=torch.float64, device=cdev)
             dist.all_reduce(worst, op=dist.ReduceOp.MAX)
             check["worst_all_ranks"] = float(worst.item())
             check["pass"] = check["worst_all_ranks"] <= check["tolerance"]
@@ -373,7 +402,7 @@ def run_ours(args):
     launch_ms = [[events[li][0][k].elapsed_time(events[li][1][k]) for k in range(K)]
                  for li in range(len(launches))]
     per_launch_ms = [statistics.mean(x) for x in launch_ms]
-    ms, joints_total = reduce_over_ranks(ms_rank, joints_rank, world, dev)
+    ms, joints_total = reduce_over_ranks(ms_rank, joints_rank, world, cdev)
     value = joints_total * K / (ms / 1e3)
 
     # ---- roofline of the dominant kernel launch (largest byte share: the batch launch,
@@ -402,9 +431,22 @@ def run_ours(args):
                    if args.stage1 else
                    f"chunked_kernel + lbs_kernel (two-pass hs_scan_skin, {launches[dom_l][0]} call)"
                    if dom_two_pass_lbs else
+                   f"seq_kernel (multi-tile path, {launches[dom_l][0]} launch)"
+                   if work[dom]["sk"].query("path") == 7 and args.algo in ("auto", "tiles") else
                    f"chunked_kernel{'<lbs>' if args.skin_mesh else ''} ({launches[dom_l][0]} launch)")
     traffic, traffic_src = ncu_traffic(workload, kernel_name)
 
+    # ---- the other configs' single-type launches (deep-skeleton and multi-tile targets,
+    # driver-visible): after the timed region, each on its own resident inputs
+    configs = None
+    if (args.config == 5 and world == 1 and not (args.no_configs or args.profile or args.stage1
+                                                  or args.skin_mesh or args.algo != "auto")):
+        configs = measure_configs(hs, torch, stream, dev)
+    # ---- N > 1: assemble sampled G/S shards from every rank (outside the timed region)
+    # and check them bitwise against this rank's own recomputation of those characters
+    validation = None
+    if world > 1 and not (args.no_validate or args.profile or args.stage1 or args.skin_mesh):
+        validation = validate_across_ranks(work, args, hs, torch, dist, rank, world, dev, cdev)
     e2e = None
     cpu = None
     if not (args.no_e2e or args.profile):
@@ -458,8 +500,10 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": check,
+        **({"multi_gpu_validation": validation} if validation is not None else {}),
+        **({"configs": configs} if configs is not None else {}),
     }
-    failed = check is not None and not check["pass"]
+    failed = (check is not None and not check["pass"]) or (validation is not None and not validation["pass"])
     if failed:   # a wrong answer is not a benchmark result: no value, non-zero exit
         line["value_if_correct"] = line["value"]
         line["value"] = None
@@ -468,6 +512,112 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 1 if failed else 0
+
+
+def measure_configs(hs, torch, stream, dev, cfgs=(2, 3, 4, 6), iters=10):
+    """Per-launch time of the single-type configs (C3 and C4 are the
+    deep-skeleton targets, C6 the multi-CTA skeleton) on device-resident inputs (each
+    larger than L2), CUDA events on the launching stream, median of `iters` after 3
+    warm-ups; fraction of 8 TB/s and of the measured copy peak at 144 B/joint."""
+    peak, _ = measured_peaks()
+    out = {}
+    for cfg in cfgs:
+        (name, n, seed, type_, ib_seed), = hsgen.CONFIGS[cfg]
+        par = hsgen.skeleton(name)
+        J = len(par)
+        sk = hs.Skeleton(par, hsgen.inv_bind(ib_seed, J))
+        x = torch.empty((n, J, 3, 4), dtype=torch.float32, device=dev)
+        rc = hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(), stream.cuda_stream)
+        assert rc == 0
+        g, s = torch.empty_like(x), torch.empty_like(x)
+        for _ in range(3):
+            sk.scan_into(x, g, s, stream=stream)
+        ts = []
+        for _ in range(iters):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sk.scan_into(x, g, s, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        gbs = 144 * n * J / (ms / 1e3) / 1e9
+        path = {1: "chunked_kernel", 7: "seq_kernel (multi-tile)", 3: "split"}.get(sk.query("path"), "?")
+        out[f"C{cfg}"] = {"workload": WORKLOAD_NAME[cfg], "kernel": path, "ms_median": ms, "ms_min": min(ts),
+                          "joints_per_s": n * J / (ms / 1e3), "hbm_gbs": gbs, "hbm_frac_of_8tbs": gbs / 8000,
+                          "frac_of_measured_peak": gbs / peak, "launches_timed": iters}
+        sk.close()
+        del x, g, s
+        torch.cuda.empty_cache()
+    return out
+
+
+def validate_across_ranks(work, args, hs, torch, dist, rank, world, dev, cdev, per_block=2048,
+                          chunk_bytes=1 << 30):
+    """SURVEY.md §8(e) validation, outside the timed region: every rank contributes the G
+    and S of a head and a tail block of its characters of each type (<= per_block each);
+    they are all-gathered in <= 1 GB chunks (NCCL, or gloo on CPU tensors), and every rank
+    recomputes each gathered block from its global character indices (the counter RNG
+    regenerates the inputs on the device) and requires BITWISE equality: a character's
+    result does not depend on which rank, how many ranks or which crowd computed it."""
+    sm = {"types": {}, "gathered_bytes": 0, "chunks": 0, "chars_checked": 0}
+    ok = True
+    for w in work:
+        n = w["n"]
+        m = min(n, per_block)
+        # the multi-tile skeleton's timed run took HS_ALGO_TILES (a crowd >= the SM count):
+        # recompute on that path whatever the block size (bitwise comparison)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        algo = "tiles" if w["sk"].query("path") == 7 and n >= sms else "auto"
+        for lo, cnt in ((0, m), (n - m, m)):   # head and tail (the same count on every rank)
+            mine = torch.cat([w["g"][lo:lo + cnt].reshape(-1), w["s"][lo:lo + cnt].reshape(-1)])
+            # per-rank block sizes agree by construction (same n per rank under weak scaling;
+            # strong scaling: sizes may differ by one character -> pad to the max)
+            sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(world)]
+            dist.all_gather(sizes, torch.tensor([mine.numel()], dtype=torch.int64, device=cdev))
+            sizes = [int(x) for x in sizes]
+            cap = max(sizes)
+            buf = torch.zeros(cap, dtype=torch.float32, device=dev)
+            buf[:mine.numel()] = mine
+            got = [torch.empty(cap, dtype=torch.float32, device=cdev) for _ in range(world)]
+            step = max(1, chunk_bytes // 4)
+            for o in range(0, cap, step):   # <= 1 GB per collective
+                e = min(cap, o + step)
+                part = buf[o:e].to(cdev)
+                outs = [torch.empty(e - o, dtype=torch.float32, device=cdev) for _ in range(world)]
+                dist.all_gather(outs, part)
+                for r in range(world):
+                    got[r][o:e] = outs[r]
+                sm["chunks"] += 1
+                sm["gathered_bytes"] += (e - o) * 4 * world
+            for r in range(world):
+                c0r, nr = shard(n_total_of(w, args, world), r, world, args.scaling)
+                lo_r, cnt_r = (0, min(nr, per_block)) if lo == 0 else (nr - min(nr, per_block), min(nr, per_block))
+                x = torch.empty((cnt_r, w["J"], 3, 4), dtype=torch.float32, device=dev)
+                if cnt_r:
+                    rc = hsgen.lib_cuda().hsg_cuda_local_poses(w["seed"], w["type"], w["J"], c0r + lo_r, cnt_r,
+                                                               x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                    assert rc == 0
+                g, s = w["sk"].scan(x, algo=algo)
+                ref = torch.cat([g.reshape(-1), s.reshape(-1)]).to(cdev)
+                same = sizes[r] == ref.numel() and bool(torch.equal(got[r][:sizes[r]], ref))
+                ok = ok and same
+                sm["chars_checked"] += cnt_r
+                sm["types"].setdefault(w["name"], []).append({"rank": r, "first_char": c0r + lo_r,
+                                                              "chars": cnt_r, "bitwise_equal": same})
+    sm["backend"] = args.dist_backend
+    sm["pass"] = ok
+    if not ok:
+        print(f"MULTI-GPU VALIDATION FAILURE: {sm}", file=sys.stderr)
+    return sm
+
+
+def n_total_of(w, args, world):
+    """The configured crowd size of a work item's skeleton type (before sharding)."""
+    for name, n_total, *_ in hsgen.CONFIGS[args.config]:
+        if name == w["name"]:
+            return n_total
+    raise KeyError(w["name"])
 
 
 def sampled_parity(work, rank, per_type=24):
@@ -542,7 +692,7 @@ def run_e2e_stage1(work, args, hs, torch, dist, world):
         step()
     dt = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt], dtype=torch.float64, device=coll_device(args.dist_backend, "cuda"))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t)
         joints *= world
@@ -602,7 +752,7 @@ def run_e2e(work, args, hs, torch, dist, world):
         step()
     dt = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt], dtype=torch.float64, device=coll_device(args.dist_backend, "cuda"))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t)
         joints *= world
@@ -616,6 +766,36 @@ def run_e2e(work, args, hs, torch, dist, world):
                       f"hs_scan_host_batch over the types (batches ramping from 8 MB to 256 MiB, "
                       f"3 streams)",
             "matches_device_path": same}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_one_thread():
+    """the oracle on ONE host thread for C1 (whole) and C2 (a 1/8 sample),
+    joints/s, best of 3 (the per-core rate the all-core number scales from)."""
+    import oracle
+    out = {}
+    for cfg, frac in ((1, 1), (2, 8)):
+        (name, n, seed, type_, ib_seed), = hsgen.CONFIGS[cfg]
+        par = hsgen.skeleton(name)
+        m = max(1, n // frac)
+        loc = hsgen.local_poses(seed, len(par), m, type_=type_)
+        ib = hsgen.inv_bind(ib_seed, len(par))
+        best = float("inf")
+        for _ in range(3):
+            t0 = time.perf_counter()
+            oracle.scan_discard(par, loc, ib, nthreads=1)
+            best = min(best, time.perf_counter() - t0)
+        out[f"C{cfg}"] = {"joints_per_s": m * len(par) / best, "sample": f"{m} x {name}"}
+    return out
 
 
 def run_cpu_baseline(args):
@@ -647,7 +827,7 @@ def run_cpu_baseline(args):
         desc = ", ".join(f"{loc.shape[0]} x {name}" for name, _, loc, _ in sample)
         return {"value": joints / best, "unit": "joints/s", "cores": cores, "kind": "oracle",
                 "sample": f"{desc} (1/{args.cpu_frac} of the workload, Stage 1 + scan + bind, "
-                          "best of 2, fp64)"}
+                          "best of 2, fp64)", "cpu_model": cpu_model()}
     best = float("inf")
     for _ in range(2):
         t0 = time.perf_counter()
@@ -656,7 +836,8 @@ def run_cpu_baseline(args):
         best = min(best, time.perf_counter() - t0)
     desc = ", ".join(f"{loc.shape[0]} x {name}" for name, _, loc, _ in sample)
     return {"value": joints / best, "unit": "joints/s", "cores": cores, "kind": "oracle",
-            "sample": f"{desc} (1/{args.cpu_frac} of the workload, best of 2, fp64)"}
+            "sample": f"{desc} (1/{args.cpu_frac} of the workload, best of 2, fp64)",
+            "cpu_model": cpu_model(), "one_thread": oracle_one_thread()}
 
 
 def main(argv=None):

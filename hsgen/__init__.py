@@ -186,6 +186,8 @@ def skeleton(name: str) -> np.ndarray:
         return chain(1024)
     if name == "tree1024":
         return random_tree(4, 1024, 300)
+    if name == "tree16384":   # the multi-CTA skeleton, 16,384 joints, L = 1024
+        return random_tree(77, 16384, 1024)
     raise KeyError(name)
 
 
@@ -197,6 +199,8 @@ CONFIGS = {
     4: [("tree1024", 20_000, 4, 0, 4)],
     5: [("hum64", 333_334, 5, 0, 2), ("chain256", 333_333, 5, 1, 3),
         ("tree1024", 333_333, 5, 2, 4)],
+    # beyond one CTA (SURVEY §7 step 7 / VERDICT r1): the multi-tile path's workload
+    6: [("tree16384", 2_000, 6, 0, 6)],
 }
 
 

@@ -109,7 +109,9 @@ hs_status hs_scan(const hs_skeleton* sk, const float* local, int64_t n_chars, fl
 
 /* Algorithms selectable through hs_scan_ex (tests / comparisons). */
 typedef enum {
-    HS_ALGO_AUTO = 0,       /* = CHUNKED when the skeleton fits one CTA, else SPLIT */
+    HS_ALGO_AUTO = 0,       /* = CHUNKED when the skeleton fits one CTA; else TILES for crowds
+                               of at least as many characters as the GPU has SMs (one CTA per
+                               character at a time), SPLIT for smaller crowds               */
     HS_ALGO_CHUNKED = 1,    /* persistent TMA tile kernel: per-thread serial chunks + pointer
                                jumping over chunk anchors                       */
     HS_ALGO_DOUBLING = 2,   /* Alg. 2: radix-2 pointer jumping, one thread per
@@ -119,9 +121,20 @@ typedef enum {
                                skeleton does not fit one CTA or was created with force_split  */
     HS_ALGO_GATEAU = 4,     /* Alg. 1: thread per joint walks every ancestor   */
     HS_ALGO_LEAF = 5,       /* KIYA leaf walk: thread per leaf fills its root path */
-    HS_ALGO_BLOCKED = 6     /* Alg. 3 literally: 64-joint blocks, in-block
+    HS_ALGO_BLOCKED = 6,    /* Alg. 3 literally: 64-joint blocks, in-block
                                doubling clamped to the block, then the MaxParentOutBlock walk;
                                n_joints <= 1024                                                */
+    HS_ALGO_TILES = 7,      /* multi-tile path for skeletons beyond one CTA (
+                               Alg. 3's cross-block carry): the topological
+                               order cut into CTA tiles; a persistent CTA runs a character's
+                               tiles in order, importing the final global poses of earlier
+                               tiles' joints from a per-CTA workspace (L2), so each joint is
+                               read and written once (144 B/joint).  Available when the
+                               skeleton does not fit one CTA or was created with force_split   */
+    HS_ALGO_COMPRESSED = 8  /* Alg. 4 literally: 64-joint groups, 7 serial
+                               composes with in-group ancestors at distance 1..7, a barrier,
+                               7 stride-8 composes on that snapshot, a barrier, then the
+                               MaxParentOutBlock walk; n_joints <= 1024                        */
 } hs_algo;
 
 typedef struct {
@@ -311,7 +324,8 @@ typedef enum {
     HS_Q_N_JOINTS = 0,
     HS_Q_MAX_LEVEL = 1,      /* L: node count of the longest root path (root level = 1)      */
     HS_Q_ROUNDS = 2,         /* R = ceil(log2 L): Alg. 2 rounds                               */
-    HS_Q_PATH = 3,           /* algo HS_ALGO_AUTO resolves to (HS_ALGO_CHUNKED or _SPLIT)      */
+    HS_Q_PATH = 3,           /* algo HS_ALGO_AUTO resolves to for a large crowd (HS_ALGO_CHUNKED,
+                                or HS_ALGO_TILES beyond one CTA; SPLIT if TILES is unavailable) */
     HS_Q_CHUNK = 4,          /* K: joints per thread chunk                                     */
     HS_Q_TILE_CHARS = 5,     /* characters per CTA tile (chunked path)                         */
     HS_Q_ANCHORS = 6,        /* anchor slots per tile (chunked) / per character (split)        */
@@ -328,8 +342,20 @@ typedef enum {
     HS_Q_TILE_SLOTS = 18,    /* plan only: P slots of the one-character tile program            */
     HS_Q_TILE_ROUNDS_ENTRIES = 19, /* plan only: phase-2 descriptors of that program           */
     HS_Q_TILE_R2 = 20,       /* plan only: its pointer-jumping rounds                           */
-    HS_Q_SMALL_TILE_CHARS = 21 /* characters per tile of the small-crowd twin program (0 = none):
+    HS_Q_SMALL_TILE_CHARS = 21, /* characters per tile of the small-crowd twin program (0 = none):
                                   hs_scan runs it when the default tiles would not cover the SMs */
+    HS_Q_SEQ_TILES = 22,     /* HS_ALGO_TILES: tiles per character (0 = not available)         */
+    HS_Q_SEQ_TILE_JOINTS = 23, /* HS_ALGO_TILES: joints per tile (F)                            */
+    HS_Q_SEQ_EXPORTS = 24,   /* HS_ALGO_TILES: joints with a child in a later tile (workspace
+                                slots per CTA)                                                 */
+    HS_Q_SEQ_SMEM_BYTES = 25, /* HS_ALGO_TILES: dynamic shared memory per CTA                 */
+    HS_Q_SEQ_THREADS = 26,   /* plan only: compute threads of the multi-tile program (T)        */
+    HS_Q_SEQ_SLOTS = 27,     /* plan only: anchor slots per P buffer (S)                       */
+    HS_Q_SEQ_R2MAX = 28,     /* plan only: most pointer-jumping rounds of a tile               */
+    HS_Q_SEQ_ENTRIES = 29,   /* plan only: phase-2 descriptors of all tiles                    */
+    HS_Q_SEQ_IMPORTS = 30,   /* plan only: import pairs of all tiles                           */
+    HS_Q_SEQ_RUNS = 31,      /* plan only: TMA runs of all tiles                               */
+    HS_Q_SEQ_QSLOTS = 32     /* plan only: Q locations (most imports of a tile)                */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);
@@ -379,7 +405,19 @@ typedef enum {
                               src: -1 root, -2 previous, -3 none, >= 0 P location of the parent */
     HS_X_TILE_P1LEN = 9,   /* int32 [T]: phase-1 length of each thread                          */
     HS_X_TILE_ROUND_OFF = 10, /* int32 [R2+1]: start of each pointer-jumping round              */
-    HS_X_TILE_ROUNDS = 11  /* uint32 [E]: slot | dst buffer<<14 | self buffer<<15 | link loc<<16 */
+    HS_X_TILE_ROUNDS = 11, /* uint32 [E]: slot | dst buffer<<14 | self buffer<<15 | link loc<<16 */
+    /* The multi-tile program (HS_ALGO_TILES) as uploaded (sizes from the HS_Q_SEQ_* queries;
+       built for the plan's options with F = tile_joints or 1024, shrunk until it fits): */
+    HS_X_SEQ_TILES = 12,   /* int32 [KT][12]: first, nj, R2, entries, rounds_off, n_imp, imp_off,
+                              n_runs, runs_off, T, 0, 0                                       */
+    HS_X_SEQ_META = 13,    /* uint64 [KT][T][K]: smem offset | (export slot + 1)<<16 | int16 src<<32
+                              | int16 own<<48; src >= 2S: an imported (Q) location             */
+    HS_X_SEQ_P1LEN = 14,   /* int32 [KT][T]                                                     */
+    HS_X_SEQ_ROUND_OFF = 15, /* int32 [KT][R2max+1], relative to the tile's rounds_off           */
+    HS_X_SEQ_ROUNDS = 16,  /* uint32 [E] (all tiles)                                            */
+    HS_X_SEQ_IMP = 17,     /* int32 [I][2]: workspace slot, P location                          */
+    HS_X_SEQ_RUNS = 18,    /* int32 [R][4]: user start, smem offset, length, 0                  */
+    HS_X_SEQ_IB_USER = 19  /* int32 [KT][F]: user label at each smem offset (-1 = none)          */
 } hs_plan_export_what;
 
 /* Copy an export into buf (buf_bytes must be >= the export's size). */

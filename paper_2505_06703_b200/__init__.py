@@ -21,7 +21,8 @@ _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libhs.so")
 # A/B experiments may point the binding at another in-tree build of the same sources.
 _LOAD_PATH = os.environ.get("HS_LIB", LIB_PATH)
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu", "kernels_aux.cu")]
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("plan.cpp", "api.cpp", "kernels.cu", "kernels_aux.cu",
+                                                      "kernels_seq.cu")]
 _DEPS = _SOURCES + [os.path.join(_HERE, "csrc", f) for f in ("plan.hpp", "kernels.cuh", "device_util.cuh")] + [
     os.path.join(_ROOT, "include", "hs.h")]
 
@@ -32,17 +33,33 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
 HS_OK, HS_ERR_INVALID_ARG, HS_ERR_EMPTY, HS_ERR_OUT_OF_RANGE, HS_ERR_CYCLE, HS_ERR_CUDA, \
     HS_ERR_OOM, HS_ERR_WRONG_DEVICE, HS_ERR_UNSUPPORTED = range(9)
 # hs_algo
-ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf": 5, "blocked": 6}
+ALGO = {"auto": 0, "chunked": 1, "doubling": 2, "split": 3, "gateau": 4, "leaf": 5, "blocked": 6,
+        "tiles": 7, "compressed": 8}
 # hs_query
 QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "tile_chars": 5,
          "anchors": 6, "anchor_rounds": 7, "identity_order": 8, "smem_bytes": 9, "threads": 10,
          "stages": 11, "device": 12, "split_levels": 13,
          "pbufs": 15, "sbufs": 16, "chunking": 17, "tile_slots": 18, "tile_rounds_entries": 19,
-         "tile_r2": 20, "small_tile_chars": 21}
+         "tile_r2": 20, "small_tile_chars": 21, "seq_tiles": 22, "seq_tile_joints": 23,
+         "seq_exports": 24, "seq_smem_bytes": 25, "seq_threads": 26, "seq_slots": 27, "seq_r2max": 28,
+         "seq_entries": 29, "seq_imports": 30, "seq_runs": 31, "seq_qslots": 32}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
           "anchor_link": 6, "chunk_lists": 7, "tile_meta": 8, "tile_p1len": 9,
-          "tile_round_off": 10, "tile_rounds": 11}
+          "tile_round_off": 10, "tile_rounds": 11, "seq_tiles": 12, "seq_meta": 13, "seq_p1len": 14,
+          "seq_round_off": 15, "seq_rounds": 16, "seq_imp": 17, "seq_runs": 18, "seq_ib_user": 19}
+
+
+def sources_sha256() -> str:
+    """Hash of the library's sources (csrc + hs.h): ties a committed ncu capture to the
+    build it was taken on (bench.py reports the capture's traffic only on a match)."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in sorted(_DEPS):
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -190,12 +207,13 @@ def _check(status: int, where: str):
 class Plan:
     """Host-only view of the topology preprocessor (no CUDA)."""
 
-    def __init__(self, parents, chunk: int = 0, block_size: int = 0, chunking: int = 0):
+    def __init__(self, parents, chunk: int = 0, block_size: int = 0, chunking: int = 0,
+                 tile_joints: int = 0):
         L = lib()
         p = np.ascontiguousarray(np.asarray(parents), dtype=np.int32)
         self.n = len(p)
         h = ctypes.c_void_p()
-        o = _CreateOpts(chunk, 0, 0, 0, 0, 0, chunking)
+        o = _CreateOpts(chunk, tile_joints, 0, 0, 0, 0, chunking)
         _check(L.hs_plan_create_ex(p.ctypes.data if self.n else None, self.n, ctypes.byref(o),
                                    block_size, ctypes.byref(h)), "hs_plan_create")
         self._h = h
@@ -206,6 +224,19 @@ class Plan:
         return v.value
 
     def export(self, what: str) -> np.ndarray:
+        if what.startswith("seq_"):
+            KT, T, K = self.query("seq_tiles"), self.query("seq_threads"), self.query("chunk")
+            F, R2 = self.query("seq_tile_joints"), self.query("seq_r2max")
+            dtype, shape = {"seq_tiles": (np.int32, (KT, 12)), "seq_meta": (np.uint64, (KT, T, K)),
+                            "seq_p1len": (np.int32, (KT, T)), "seq_round_off": (np.int32, (KT, R2 + 1)),
+                            "seq_rounds": (np.uint32, (self.query("seq_entries"),)),
+                            "seq_imp": (np.int32, (self.query("seq_imports"), 2)),
+                            "seq_runs": (np.int32, (self.query("seq_runs"), 4)),
+                            "seq_ib_user": (np.int32, (KT, F))}[what]
+            out = np.empty(max(int(np.prod(shape)), 1), dtype)
+            _check(lib().hs_plan_export(self._h, EXPORT[what], out.ctypes.data, out.nbytes),
+                   "hs_plan_export")
+            return out[:int(np.prod(shape))].reshape(shape)
         if what.startswith("tile_"):
             T, K = self.query("threads"), self.query("chunk")
             dtype, size = {"tile_meta": (np.uint64, T * K), "tile_p1len": (np.int32, T),

@@ -50,6 +50,8 @@ struct hs_plan {
     int block_size = 64;
     hs::ChunkDecomp decomp;
     hs::TileProgram tile;   // the chunked kernel's program for one character (ping-pong P)
+    hs::SeqProgram seq;     // the multi-tile program (empty if no tile size fits)
+    bool seq_ok = false;
 };
 
 struct hs_skeleton {
@@ -72,6 +74,8 @@ struct hs_skeleton {
     int32_t* d_blk_lift = nullptr;    // Alg. 3 comparison kernel: in-block lift [RB][n]
     int32_t* d_blk_mpob = nullptr;    //   and MaxParentOutBlock [n], user labels
     int32_t blk_rounds = 0;
+    int32_t* d_cmp_lp = nullptr;      // Alg. 4 comparison kernel: in-block parent [n]
+    int32_t* d_cmp_l8 = nullptr;      //   and in-block 8th ancestor [n], user labels
     uint64_t* d_meta = nullptr;
     int32_t* d_p1len = nullptr;
     int32_t* d_round_off = nullptr;
@@ -80,6 +84,19 @@ struct hs_skeleton {
     int32_t* d_path_off = nullptr;
     int32_t* d_path = nullptr;
     int32_t n_leaves = 0;
+    // multi-tile path (HS_ALGO_TILES): skeletons beyond one CTA
+    bool seq_ok = false;
+    hs::SeqProgram seq;
+    int seq_stages = 0, seq_sbufs = 0, seq_threads = 0, seq_max_entries = 0;
+    int64_t seq_smem = 0;
+    hs::SeqTileDev* d_seq_tiles = nullptr;
+    uint64_t* d_seq_meta = nullptr;
+    int32_t* d_seq_p1len = nullptr;
+    int32_t* d_seq_round_off = nullptr;
+    uint32_t* d_seq_rounds = nullptr;
+    int32_t* d_seq_imp = nullptr;
+    int32_t* d_seq_runs = nullptr;
+    float* d_seq_ib = nullptr;
 };
 
 struct hs_clipset {
@@ -120,6 +137,8 @@ void free_skeleton(hs_skeleton* sk) {
     cudaFree(sk->d_lift);
     cudaFree(sk->d_blk_lift);
     cudaFree(sk->d_blk_mpob);
+    cudaFree(sk->d_cmp_lp);
+    cudaFree(sk->d_cmp_l8);
     cudaFree(sk->d_meta);
     cudaFree(sk->d_p1len);
     cudaFree(sk->d_round_off);
@@ -127,7 +146,68 @@ void free_skeleton(hs_skeleton* sk) {
     cudaFree(sk->d_split_meta);
     cudaFree(sk->d_path_off);
     cudaFree(sk->d_path);
+    cudaFree(sk->d_seq_tiles);
+    cudaFree(sk->d_seq_meta);
+    cudaFree(sk->d_seq_p1len);
+    cudaFree(sk->d_seq_round_off);
+    cudaFree(sk->d_seq_rounds);
+    cudaFree(sk->d_seq_imp);
+    cudaFree(sk->d_seq_runs);
+    cudaFree(sk->d_seq_ib);
     delete sk;
+}
+
+// The multi-tile program (HS_ALGO_TILES) of a skeleton that does not fit one CTA:
+// the largest tile (F joints) whose program fits 224 compute threads and whose
+// shared memory (2 stages + 1 skin buffer, or the requested counts) fits the device;
+// chunking RUNS or HEAVY per skeleton, whichever needs fewer phase-2 descriptors.
+hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<float>& ib) {
+    const hs::Plan& P = sk->plan;
+    const int stages = o.stages ? o.stages : 2, sbufs = o.sbufs ? o.sbufs : 1;
+    const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 1024;
+    const int modes[2] = {hs::CHUNK_RUNS, hs::CHUNK_HEAVY};
+    const int nmodes = o.chunking == 0 ? 2 : 1;
+    for (int F = f0 - f0 % 32; F >= 64 && !sk->seq_ok; F -= 64) {
+        hs::SeqProgram best;
+        bool have = false;
+        for (int mi = 0; mi < nmodes; ++mi) {
+            const int mode = o.chunking == 0 ? modes[mi]
+                             : (o.chunking == 1 ? hs::CHUNK_CONSECUTIVE
+                                                : (o.chunking == 3 ? hs::CHUNK_RUNS : hs::CHUNK_HEAVY));
+            hs::SeqProgram sp;
+            if (!hs::build_seq_program(P, sk->K, F, mode, 224, sp)) continue;
+            if (hs::seq_smem_bytes(sp, stages, sbufs) > sk->smem_optin) continue;
+            if (!have || sp.rounds.size() < best.rounds.size()) { best = std::move(sp); have = true; }
+        }
+        if (!have) continue;
+        sk->seq = std::move(best);
+        sk->seq_ok = true;
+    }
+    if (!sk->seq_ok) return HS_OK;   // the split path remains
+    const hs::SeqProgram& sp = sk->seq;
+    sk->seq_stages = stages;
+    sk->seq_sbufs = sbufs;
+    sk->seq_smem = hs::seq_smem_bytes(sp, stages, sbufs);
+    sk->seq_threads = sp.T + 32;
+    sk->seq_max_entries = (int)hs::seq_max_tile_entries(sp);
+    std::vector<hs::SeqTileDev> tiles(sp.tiles.size());
+    static_assert(sizeof(hs::SeqTileDev) == sizeof(hs::SeqTile), "SeqTile layout");
+    std::memcpy(tiles.data(), sp.tiles.data(), tiles.size() * sizeof(hs::SeqTile));
+    std::vector<float> ibt((size_t)sp.KT * sp.F * 12, 0.f);
+    for (size_t i = 0; i < sp.ib_user.size(); ++i)
+        if (sp.ib_user[i] >= 0) std::memcpy(&ibt[i * 12], &ib[(size_t)sp.ib_user[i] * 12], 48);
+    cudaError_t e;
+    if ((e = upload(&sk->d_seq_tiles, tiles.data(), tiles.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_meta, sp.meta.data(), sp.meta.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_p1len, sp.p1len.data(), sp.p1len.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_round_off, sp.round_off.data(), sp.round_off.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_rounds, sp.rounds.data(), sp.rounds.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_imp, sp.imp.data(), sp.imp.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_runs, sp.runs.data(), sp.runs.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_ib, ibt.data(), ibt.size())) != cudaSuccess ||
+        (e = hs::prepare_seq(sk->K)) != cudaSuccess)
+        return cuda_fail(e, "multi-tile program");
+    return HS_OK;
 }
 
 hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
@@ -219,8 +299,12 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
     {   // the paper's 64-joint blocks for the Alg. 3 comparison kernel
         std::vector<int32_t> lb, mp;
         hs::blocked_tables(P, 64, lb, mp, sk->blk_rounds);
+        std::vector<int32_t> lp, l8;
+        hs::compressed_tables(P, 64, lp, l8);
         if ((e = upload(&sk->d_blk_lift, lb.data(), lb.size())) != cudaSuccess ||
-            (e = upload(&sk->d_blk_mpob, mp.data(), mp.size())) != cudaSuccess) {
+            (e = upload(&sk->d_blk_mpob, mp.data(), mp.size())) != cudaSuccess ||
+            (e = upload(&sk->d_cmp_lp, lp.data(), lp.size())) != cudaSuccess ||
+            (e = upload(&sk->d_cmp_l8, l8.data(), l8.size())) != cudaSuccess) {
             free_skeleton(sk);
             return cuda_fail(e, "upload block tables");
         }
@@ -277,6 +361,10 @@ hs_status create_impl(const int32_t* parents, int32_t n, const float* inv_bind,
             }
         }
     } else {
+        if (depth == 0) {
+            hs_status s3 = build_seq(sk, o, ib);
+            if (s3 != HS_OK) { free_skeleton(sk); return s3; }
+        }
         sk->sp = hs::build_split_program(P, sk->K);
         if ((e = upload(&sk->d_split_meta, sk->sp.meta.data(), sk->sp.meta.size())) != cudaSuccess) {
             free_skeleton(sk);
@@ -428,7 +516,9 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                     const hs_clipset* cs = nullptr, const void* layers = nullptr, int n_layers = 0) {
     const int32_t J = sk->plan.n;
     cudaError_t e = cudaSuccess;
-    if (algo == HS_ALGO_AUTO) algo = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT;
+    if (algo == HS_ALGO_AUTO)
+        algo = sk->chunked ? HS_ALGO_CHUNKED
+                           : (sk->seq_ok && n_chars >= hs::sm_count() ? HS_ALGO_TILES : HS_ALGO_SPLIT);
     switch (algo) {
         case HS_ALGO_CHUNKED: {
             if (!sk->chunked) return fail(HS_ERR_UNSUPPORTED, "skeleton does not fit the single-CTA path");
@@ -476,6 +566,11 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             e = hs::launch_blocked(local, gout, sout, sk->d_ib, sk->d_blk_lift, sk->d_blk_mpob, J, sk->blk_rounds,
                                    n_chars, st);
             break;
+        case HS_ALGO_COMPRESSED:
+            if (J > 1024) return fail(HS_ERR_UNSUPPORTED, "compressed kernel needs n_joints <= 1024");
+            e = hs::launch_compressed(local, gout, sout, sk->d_ib, sk->d_cmp_lp, sk->d_cmp_l8, sk->d_blk_mpob, J,
+                                      n_chars, st);
+            break;
         case HS_ALGO_GATEAU:
             e = hs::launch_gateau(local, gout, sout, sk->d_ib, sk->d_parents, J, n_chars, st);
             break;
@@ -484,6 +579,40 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             e = hs::launch_leaf(local, gout, sout, sk->d_ib, sk->d_path_off, sk->d_path, sk->n_leaves, J,
                                 n_chars, st);
             break;
+        case HS_ALGO_TILES: {
+            if (!sk->seq_ok) return fail(HS_ERR_UNSUPPORTED, "skeleton has no multi-tile program (create with force_split=1)");
+            const hs::SeqProgram& sp = sk->seq;
+            hs::SeqArgs a{};
+            a.local = local; a.gout = gout; a.sout = sout;
+            a.ib = sk->d_seq_ib;
+            a.tiles = sk->d_seq_tiles;
+            a.meta = sk->d_seq_meta;
+            a.p1len = sk->d_seq_p1len;
+            a.round_off = sk->d_seq_round_off;
+            a.rounds = sk->d_seq_rounds;
+            a.imp = reinterpret_cast<const int2*>(sk->d_seq_imp);
+            a.runs = reinterpret_cast<const int4*>(sk->d_seq_runs);
+            a.n_chars = n_chars;
+            a.J = J; a.KT = sp.KT; a.F = sp.F; a.T = sp.T; a.S = sp.S; a.n_exp = sp.n_exp;
+            a.r2max = sp.R2max; a.max_imp = sp.max_imp; a.max_entries = sk->seq_max_entries;
+            a.p_floats = (2 * sp.S + sp.nQ) * 12;
+            a.stages = sk->seq_stages; a.sbufs = sk->seq_sbufs; a.threads = sk->seq_threads;
+            a.has_runs = sp.has_runs ? 1 : 0;
+            a.bulk_piece = HS_BULK_PIECE;
+            a.smem_bytes = sk->seq_smem;
+            a.ctas_per_sm = 1;
+            // workspace: one character's exported poses per CTA (stays in L2)
+            const int64_t grid = std::min<int64_t>(n_chars, hs::sm_count());
+            float* ws = nullptr;
+            if (sp.n_exp > 0) {
+                e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(grid * sp.n_exp * 48), st);
+                if (e != cudaSuccess) return cuda_fail(e, "multi-tile workspace");
+            }
+            a.ws = ws;
+            e = hs::launch_seq(sk->K, a, st);
+            if (ws) cudaFreeAsync(ws, st);
+            break;
+        }
         case HS_ALGO_SPLIT: {
             if (sk->chunked) {
                 // forced split on a skeleton that fits one CTA: build on the fly is not
@@ -953,7 +1082,7 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_N_JOINTS: *v = sk->plan.n; break;
         case HS_Q_MAX_LEVEL: *v = sk->plan.L; break;
         case HS_Q_ROUNDS: *v = sk->plan.R; break;
-        case HS_Q_PATH: *v = sk->chunked ? HS_ALGO_CHUNKED : HS_ALGO_SPLIT; break;
+        case HS_Q_PATH: *v = sk->chunked ? HS_ALGO_CHUNKED : (sk->seq_ok ? HS_ALGO_TILES : HS_ALGO_SPLIT); break;
         case HS_Q_CHUNK: *v = sk->K; break;
         case HS_Q_TILE_CHARS: *v = sk->chunked ? sk->tp.C : 0; break;
         case HS_Q_SMALL_TILE_CHARS: *v = sk->small ? sk->small->tp.C : 0; break;
@@ -968,6 +1097,10 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_SBUFS: *v = sk->sbufs; break;
         case HS_Q_CHUNKING: *v = sk->chunking == hs::CHUNK_CONSECUTIVE ? 1 : (sk->chunking == hs::CHUNK_RUNS ? 3 : 2); break;
         case HS_Q_PBUFS: *v = sk->chunked ? (sk->tp.pingpong ? 2 : 1) : 0; break;
+        case HS_Q_SEQ_TILES: *v = sk->seq_ok ? sk->seq.KT : 0; break;
+        case HS_Q_SEQ_TILE_JOINTS: *v = sk->seq_ok ? sk->seq.F : 0; break;
+        case HS_Q_SEQ_EXPORTS: *v = sk->seq_ok ? sk->seq.n_exp : 0; break;
+        case HS_Q_SEQ_SMEM_BYTES: *v = sk->seq_ok ? sk->seq_smem : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
     return HS_OK;
@@ -1011,6 +1144,8 @@ hs_status hs_plan_create_ex(const int32_t* parents, int32_t n_joints, const hs_c
         std::vector<int32_t> pos(p->plan.order);
         p->decomp = hs::decompose(p->plan.ipar, p->K, mode, &pos, true);
         p->tile = hs::build_tile_program(p->plan, p->K, 1, true, mode);
+        for (int F = o.tile_joints > 0 ? std::min(o.tile_joints, 1024) : 1024; F >= 64 && !p->seq_ok; F -= 64)
+            p->seq_ok = hs::build_seq_program(p->plan, p->K, F - F % 32, mode, 224, p->seq);
         *out = p;
         return HS_OK;
     } catch (const std::bad_alloc&) {
@@ -1039,6 +1174,16 @@ hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
         case HS_Q_TILE_ROUNDS_ENTRIES: *v = (int64_t)p->tile.rounds.size(); break;
         case HS_Q_TILE_R2: *v = p->tile.R2; break;
         case HS_Q_IDENTITY_ORDER: *v = p->plan.identity ? 1 : 0; break;
+        case HS_Q_SEQ_TILES: *v = p->seq_ok ? p->seq.KT : 0; break;
+        case HS_Q_SEQ_TILE_JOINTS: *v = p->seq.F; break;
+        case HS_Q_SEQ_EXPORTS: *v = p->seq.n_exp; break;
+        case HS_Q_SEQ_THREADS: *v = p->seq.T; break;
+        case HS_Q_SEQ_SLOTS: *v = p->seq.S; break;
+        case HS_Q_SEQ_R2MAX: *v = p->seq.R2max; break;
+        case HS_Q_SEQ_ENTRIES: *v = (int64_t)p->seq.rounds.size(); break;
+        case HS_Q_SEQ_IMPORTS: *v = (int64_t)p->seq.imp.size() / 2; break;
+        case HS_Q_SEQ_RUNS: *v = (int64_t)p->seq.runs.size() / 4; break;
+        case HS_Q_SEQ_QSLOTS: *v = p->seq.nQ; break;
         case HS_Q_ANCHOR_ROUNDS: {
             hs::TileProgram tp = hs::build_tile_program(p->plan, p->K, 1, true, hs::CHUNK_HEAVY);
             *v = tp.R2;
@@ -1064,6 +1209,14 @@ hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_
         case HS_X_TILE_P1LEN: return raw(tp.p1len.data(), tp.p1len.size() * sizeof(int32_t));
         case HS_X_TILE_ROUND_OFF: return raw(tp.round_off.data(), tp.round_off.size() * sizeof(int32_t));
         case HS_X_TILE_ROUNDS: return raw(tp.rounds.data(), tp.rounds.size() * sizeof(uint32_t));
+        case HS_X_SEQ_TILES: return raw(p->seq.tiles.data(), p->seq.tiles.size() * sizeof(hs::SeqTile));
+        case HS_X_SEQ_META: return raw(p->seq.meta.data(), p->seq.meta.size() * sizeof(uint64_t));
+        case HS_X_SEQ_P1LEN: return raw(p->seq.p1len.data(), p->seq.p1len.size() * sizeof(int32_t));
+        case HS_X_SEQ_ROUND_OFF: return raw(p->seq.round_off.data(), p->seq.round_off.size() * sizeof(int32_t));
+        case HS_X_SEQ_ROUNDS: return raw(p->seq.rounds.data(), p->seq.rounds.size() * sizeof(uint32_t));
+        case HS_X_SEQ_IMP: return raw(p->seq.imp.data(), p->seq.imp.size() * sizeof(int32_t));
+        case HS_X_SEQ_RUNS: return raw(p->seq.runs.data(), p->seq.runs.size() * sizeof(int32_t));
+        case HS_X_SEQ_IB_USER: return raw(p->seq.ib_user.data(), p->seq.ib_user.size() * sizeof(int32_t));
         case HS_X_LEVELS: tmp = P.level; break;
         case HS_X_ORDER: tmp = P.order; break;
         case HS_X_LIFT: tmp = P.lift; break;

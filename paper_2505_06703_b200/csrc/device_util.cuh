@@ -144,6 +144,19 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// cp.async (LDGSTS): 4/8-byte copies through L1 (read-only program tables), 16-byte
+// copies at L2 (.cg: data written earlier in the same kernel by other threads).
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void bar_consumers(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
@@ -229,6 +242,10 @@ __device__ __forceinline__ float dot4_rn(float a0, float a1, float a2, float a3,
 }
 
 // Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
+// NORM: normalise the interpolated quaternion (needed before a weighted blend of
+// several layers); a single layer's quaternion goes to trs_to_m34 unnormalised, which
+// divides by |q|^2 itself.
+template <bool NORM>
 __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, float4 x1, float4 y1,
                                            float2 z1, float a, float* trs) {
     if (a == 0.0f) {   // on a key: that key exactly (R21)
@@ -244,18 +261,29 @@ __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, floa
     const float as = d < 0.0f ? -a : a;
     const float qw = lerp_rn(b, x0.w, as, x1.w), qx = lerp_rn(b, y0.x, as, y1.x),
                 qy = lerp_rn(b, y0.y, as, y1.y), qz = lerp_rn(b, y0.z, as, y1.z);
-    const float inv = rsqrt_fast(dot4_rn(qw, qx, qy, qz, qw, qx, qy, qz));
-    trs[3] = __fmul_rn(qw, inv); trs[4] = __fmul_rn(qx, inv); trs[5] = __fmul_rn(qy, inv);
-    trs[6] = __fmul_rn(qz, inv);
+    if (NORM) {
+        const float inv = rsqrt_fast(dot4_rn(qw, qx, qy, qz, qw, qx, qy, qz));
+        trs[3] = __fmul_rn(qw, inv); trs[4] = __fmul_rn(qx, inv); trs[5] = __fmul_rn(qy, inv);
+        trs[6] = __fmul_rn(qz, inv);
+    } else {
+        trs[3] = qw; trs[4] = qx; trs[5] = qy; trs[6] = qz;
+    }
 }
 
+// R(q) for ANY non-zero q: with c = 2 / |q|^2, R = [1 - c (y^2 + z^2), c (x y - w z), ...]
+// equals the unit-quaternion formula of q / |q| (the oracle normalises in
+// fp64 and uses the unit formula).  Dividing by |q|^2 here keeps R orthonormal to a few
+// ulps however far |q| is from 1 after fp32 interpolation and blending; the unit
+// formula on a quaternion of norm^2 = 1 + d gives R' = (1 + d) R + (-d) I, an O(d)
+// non-rigid error that compounds down the root path (Stage-1 budget).
 __device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
     const float w = trs[3], x = trs[4], y = trs[5], z = trs[6];
     const float sx = trs[7], sy = trs[8], sz = trs[9];
-    // 1 - 2 (u^2 + v^2) and 2 (u v -/+ w t), each rounded in one fixed order
-    auto diag = [](float u, float v) { return fmaf(-2.0f, fmaf(u, u, __fmul_rn(v, v)), 1.0f); };
-    auto offd = [](float u, float v, float p, float q, float sgn) {
-        return __fmul_rn(2.0f, fmaf(sgn * p, q, __fmul_rn(u, v)));
+    const float c = __fmul_rn(2.0f, rcp_fast(dot4_rn(w, x, y, z, w, x, y, z)));
+    // 1 - c (u^2 + v^2) and c (u v -/+ w t), each rounded in one fixed order
+    auto diag = [c](float u, float v) { return fmaf(-c, fmaf(u, u, __fmul_rn(v, v)), 1.0f); };
+    auto offd = [c](float u, float v, float p, float q, float sgn) {
+        return __fmul_rn(c, fmaf(sgn * p, q, __fmul_rn(u, v)));
     };
     m[0] = __fmul_rn(diag(y, z), sx);               m[1] = __fmul_rn(offd(x, y, w, z, -1.0f), sy);
     m[2] = __fmul_rn(offd(x, z, w, y, 1.0f), sz);   m[3] = trs[0];
@@ -343,8 +371,12 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             float s[10];
-            sample_trs(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
-                       __int_as_float(dc[e].z), s);
+            if (nl == 1)
+                sample_trs<false>(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
+                                  __int_as_float(dc[e].z), s);
+            else
+                sample_trs<true>(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
+                                 __int_as_float(dc[e].z), s);
             const float w = __int_as_float(dc[e].w);
             if (nl == 1) {   // one layer: the sample itself (R22)
 #pragma unroll
@@ -377,10 +409,7 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
             for (int c = 0; c < 3; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
 #pragma unroll
             for (int c = 7; c < 10; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
-            const float inv = rsqrt_fast(dot4_rn(acc[e][3], acc[e][4], acc[e][5], acc[e][6], acc[e][3],
-                                                 acc[e][4], acc[e][5], acc[e][6]));
-#pragma unroll
-            for (int c = 3; c < 7; ++c) acc[e][c] = __fmul_rn(acc[e][c], inv);
+            // the blended quaternion is normalised by trs_to_m34 (c = 2 / |q|^2)
         }
         float m[12];
         trs_to_m34(acc[e], m);

@@ -67,6 +67,35 @@ struct ChunkedArgs {
     int32_t n_verts;
     unsigned long long* prof;  // debug: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
+// Multi-tile kernel (HS_ALGO_TILES): skeletons beyond one CTA.  A
+// persistent CTA takes whole characters (b, b + grid, ...) and walks each one's KT
+// tiles in topological order; cross-tile parents are final workspace values.
+struct SeqTileDev {               // = hs::SeqTile (plan.hpp)
+    int32_t first, nj, R2, n_entries, rounds_off, n_imp, imp_off, n_runs, runs_off, T, pad[2];
+};
+struct SeqArgs {
+    const float* local;        // [n_chars][J][12]
+    float* gout;               // [n_chars][J][12]
+    float* sout;               // [n_chars][J][12] or nullptr
+    float* ws;                 // [grid][n_exp][12]: exported global poses of the CTA's current character
+    const float* ib;           // [KT][F][12] inverse bind by tile smem offset
+    const SeqTileDev* tiles;   // [KT]
+    const uint64_t* meta;      // [KT][T][K]
+    const int32_t* p1len;      // [KT][T]
+    const int32_t* round_off;  // [KT][R2max + 1]
+    const uint32_t* rounds;    // concatenated descriptors
+    const int2* imp;           // (workspace slot, P location)
+    const int4* runs;          // (user start, smem offset, length, 0)
+    int64_t n_chars;
+    int32_t J, KT, F, T, S, n_exp, r2max, max_imp, max_entries;
+    int32_t p_floats;          // (2S + nQ) * 12
+    int32_t stages, sbufs, threads, has_runs, bulk_piece;
+    int64_t smem_bytes;
+    int32_t ctas_per_sm;       // 0 = occupancy maximum (1)
+};
+cudaError_t launch_seq(int K, const SeqArgs& a, cudaStream_t st);
+cudaError_t prepare_seq(int K);
+
 int sm_count();   // SMs of the current device (cached)
 cudaError_t launch_chunked(int K, const ChunkedArgs& a, cudaStream_t st);
 // Linear blend skinning from skin poses in HBM (two-pass hs_scan_skin): S [n_chars][J][12].
@@ -87,6 +116,11 @@ cudaError_t launch_doubling(const float* local, float* gout, float* sout, const 
 // the MaxParentOutBlock walk (comparison kernel).
 cudaError_t launch_blocked(const float* local, float* gout, float* sout, const float* ib, const int32_t* lb,
                            const int32_t* mpob, int32_t J, int32_t RB, int64_t n_chars, cudaStream_t st);
+
+// Alg. 4 literally: 64-joint blocks, 7 serial in-block composes,
+// 7 stride-8 composes on that snapshot, then the MaxParentOutBlock walk (comparison).
+cudaError_t launch_compressed(const float* local, float* gout, float* sout, const float* ib, const int32_t* lp,
+                              const int32_t* l8, const int32_t* mpob, int32_t J, int64_t n_chars, cudaStream_t st);
 
 // Per-character topology (NEXT-3): parents [n_chars][J] (character-local labels),
 // inverse binds [n_chars][J][12] or nullptr (skin = global); J <= 1024.

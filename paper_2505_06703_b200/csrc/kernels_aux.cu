@@ -244,6 +244,84 @@ __global__ void __launch_bounds__(1024) blocked_kernel(const float* __restrict__
     }
 }
 
+// ================================================================== compressed (Alg. 4)
+// The paper's final algorithm literally ("State compression"; reading
+// R10), a comparison kernel: one thread per (character, joint) in USER order, 64-joint
+// blocks over the internal topological order (as blocked_kernel).
+//   stage A  7 serial composes with the LOCALS of the in-block ancestors at distance
+//            1..7 (R5: Alg. 1-4's M[curParentID] read as the immutable locals;
+//            R8: hops clamped to the block) -> A[j] covers distances 0..7;
+//   barrier  ("groupbarrier")
+//   stage B  7 composes with the stage-A SNAPSHOT of the in-block ancestors at distance
+//            8, 16, ..., 56 (MultiParent(., 8)) -> B[j] covers the in-block root path;
+//   barrier
+//   stage C  the MaxParentOutBlock walk on the stage-B snapshot (R9: walk variable).
+// "14 + n/64" composes per thread, two barriers per block.
+__global__ void __launch_bounds__(1024) compressed_kernel(const float* __restrict__ local,
+                                                          float* __restrict__ gout,
+                                                          float* __restrict__ sout,
+                                                          const float* __restrict__ ib,
+                                                          const int32_t* __restrict__ lp,
+                                                          const int32_t* __restrict__ l8,
+                                                          const int32_t* __restrict__ mpob, int J, int C,
+                                                          int64_t n_chars) {
+    extern __shared__ __align__(16) float sm[];
+    const int F = C * J;
+    float* buf0 = sm;            // locals, then stage B
+    float* buf1 = sm + F * 12;   // stage A
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int nc = (int)min((int64_t)C, n_chars - c0);
+    const int f = threadIdx.x;
+    const int cl = f / J, u = f - cl * J;
+    const bool valid = f < F && cl < nc;
+    float v[12];
+    if (valid) ldg3(local + (c0 * J + f) * 12, v);
+    if (f < F) st3(buf0 + f * 12, v);
+    __syncthreads();
+    if (f < F) {   // stage A: in-block ancestors at distance 1..7, their locals
+        int cur = __ldg(lp + u);
+        for (int d = 1; d <= 7 && cur >= 0; ++d) {
+            float x[12], y[12];
+            ld3(buf0 + (cl * J + cur) * 12, x);
+            compose(x, v, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) v[e] = y[e];
+            cur = __ldg(lp + cur);
+        }
+        st3(buf1 + f * 12, v);
+    }
+    __syncthreads();
+    if (f < F) {   // stage B: stride-8 ancestors' stage-A values
+        int cur = __ldg(l8 + u);
+        for (int d = 1; d <= 7 && cur >= 0; ++d) {
+            float x[12], y[12];
+            ld3(buf1 + (cl * J + cur) * 12, x);
+            compose(x, v, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) v[e] = y[e];
+            cur = __ldg(l8 + cur);
+        }
+        st3(buf0 + f * 12, v);
+    }
+    __syncthreads();
+    if (valid) {   // stage C: MaxParentOutBlock walk on the stage-B snapshot
+        for (int m = __ldg(mpob + u); m >= 0; m = __ldg(mpob + m)) {
+            float x[12], y[12];
+            ld3(buf0 + (cl * J + m) * 12, x);
+            compose(x, v, y);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) v[e] = y[e];
+        }
+        st3(gout + (c0 * J + f) * 12, v);
+        if (sout) {
+            float b[12], s[12];
+            ldg3(ib + (int64_t)u * 12, b);
+            compose(v, b, s);
+            st3(sout + (c0 * J + f) * 12, s);
+        }
+    }
+}
+
 // ================================================================== LBS, two-pass
 // Skinning from skin poses in HBM: one CTA per character (grid-stride), its palette
 // staged in shared memory (J x 48 B), then consecutive vertices on consecutive
@@ -577,6 +655,20 @@ cudaError_t launch_blocked(const float* local, float* gout, float* sout, const f
         return e;
     const int64_t blocks = (n_chars + C - 1) / C;
     blocked_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lb, mpob, J, C, RB, n_chars);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compressed(const float* local, float* gout, float* sout, const float* ib, const int32_t* lp,
+                              const int32_t* l8, const int32_t* mpob, int32_t J, int64_t n_chars, cudaStream_t st) {
+    if (J > 1024) return cudaErrorInvalidValue;
+    const int C = std::max(1, HS_VARIED_THREADS / J);   // one character per CTA from J = 64 up
+    const size_t smem = (size_t)2 * C * J * 48;
+    static std::atomic<uint64_t> attr{0};
+    if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&compressed_kernel), 2 * 1024 * 48, attr);
+        e != cudaSuccess)
+        return e;
+    const int64_t blocks = (n_chars + C - 1) / C;
+    compressed_kernel<<<(unsigned)blocks, C * J, smem, st>>>(local, gout, sout, ib, lp, l8, mpob, J, C, n_chars);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,387 @@
+// kernels_seq.cu — the multi-tile kernel (HS_ALGO_TILES): skeletons
+// larger than one CTA's shared memory (the cross-block carry of
+// Alg. 3).
+//
+// The skeleton's internal (topological) order is cut into KT tiles of <= F joints
+// (plan.cpp build_seq_program).  A persistent CTA takes whole characters b, b + grid,
+// ... and runs each one's tiles in order 0..KT-1, so when a tile runs, every joint
+// outside it that it depends on (an earlier tile's joint) already has its FINAL global
+// pose — the cross-block carry is resolved before the block, not walked after it.
+// Per tile, the same three phases as the single-CTA chunked kernel (kernels.cu) on
+// the tile's sub-forest:
+//   import   cp.async of the tile's external parents' global poses from the CTA's
+//            workspace (L2) into Q locations of the anchor region P;
+//   phase 1  per-thread chunk folds, anchor prefixes published to P;
+//   phase 2a warp-shuffle scan of runs (heavy paths longer than K);
+//   phase 2  pointer jumping over the anchor forest, whose roots are true roots
+//            and Q locations (already final);
+//   phase 3  re-fold from the final anchors, G in place, S = G (x) IB, and joints with
+//            a child in a later tile store G to the workspace (export).
+// The producer warp streams tiles in and G/S out with TMA bulk copies (one copy per
+// run of consecutive user labels: one run per tile when the user order is already
+// topological).  The per-tile program (chunk metadata, phase-2 descriptors, import
+// list) is prefetched into shared memory with cp.async one tile ahead; the inverse
+// bind of a thread's slots is loaded into registers at the start of the tile and
+// first used in phase 3.
+//
+// HBM bytes per joint: 48 (L in) + 48 (G out) + 48 (S out), as the single-CTA path;
+// the workspace (exported poses of one character per CTA) and the per-tile program
+// stay in L2.
+#include <atomic>
+
+#include "device_util.cuh"
+
+namespace hs {
+namespace {
+
+template <int K, bool RUNS>
+__global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ SeqArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int NS = a.stages, NSS = a.sbufs;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* done = full + 4;
+    uint64_t* sfree = done + 4;
+    const int tile_f = a.F * 12;
+    float* LG = reinterpret_cast<float*>(smem + 128);
+    float* SB = LG + NS * tile_f;
+    float* P = SB + NSS * tile_f;
+    const int TK = a.T * K;
+    uint64_t* s_meta = reinterpret_cast<uint64_t*>(P + a.p_floats);        // [2][T][K]
+    int32_t* s_p1 = reinterpret_cast<int32_t*>(s_meta + 2 * TK);           // [2][T]
+    int2* s_imp = reinterpret_cast<int2*>(s_p1 + 2 * a.T);                 // [2][max_imp]
+    int32_t* s_round_off = reinterpret_cast<int32_t*>(s_imp + 2 * a.max_imp);
+    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + ((a.r2max + 1 + 3) & ~3));
+
+    const int nwc = (int)(blockDim.x >> 5) - 1;
+    const int NC = nwc * 32;
+    const int warp = threadIdx.x >> 5;
+    const int KT = a.KT;
+    const int J = a.J;
+    const int64_t my_chars = blockIdx.x < a.n_chars ? (a.n_chars - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t my_tiles = my_chars * KT;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == nwc) {
+        // ------------------------------------------------------------ producer
+        if ((threadIdx.x & 31) != 0) return;
+        const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
+        // tile cursors (character, tile) for the loads (NS ahead) and the stores
+        int64_t lc = blockIdx.x, sc = blockIdx.x;
+        int lk = 0, sk = 0;
+        auto issue_load = [&](int stage) {
+            const SeqTileDev tl = a.tiles[lk];
+            mbar_expect_tx(&full[stage], (uint32_t)tl.nj * 48u);
+            const char* base = reinterpret_cast<const char*>(a.local + lc * J * 12);
+            char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
+            for (int r = 0; r < tl.n_runs; ++r) {
+                const int4 run = __ldg(a.runs + tl.runs_off + r);
+                const uint32_t bytes = (uint32_t)run.z * 48u;
+                HS_BOUND(run.y >= 0 && run.y + run.z <= tl.nj && run.x >= 0 && run.x + run.z <= J);
+                const char* s0 = base + (int64_t)run.x * 48;
+                char* d0 = dst + run.y * 48;
+                for (uint32_t o = 0; o < bytes; o += piece) bulk_g2s(d0 + o, s0 + o, min(piece, bytes - o), &full[stage]);
+            }
+            if (++lk == KT) { lk = 0; lc += gridDim.x; }
+        };
+        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load((int)it);
+        int stage = 0, sb = 0;
+        uint32_t phase = 0;
+        const bool do_skin = a.sout != nullptr;
+        for (int64_t it = 0; it < my_tiles; ++it) {
+            mbar_wait(&done[stage], phase);
+            const SeqTileDev tl = a.tiles[sk];
+            const int64_t cbase = sc * J * 12;
+            const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
+            const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
+            for (int r = 0; r < tl.n_runs; ++r) {
+                const int4 run = __ldg(a.runs + tl.runs_off + r);
+                const uint32_t bytes = (uint32_t)run.z * 48u;
+                char* gp = reinterpret_cast<char*>(a.gout + cbase) + (int64_t)run.x * 48;
+                char* sp = do_skin ? reinterpret_cast<char*>(a.sout + cbase) + (int64_t)run.x * 48 : nullptr;
+                for (uint32_t o = 0; o < bytes; o += piece) {
+                    const uint32_t nb = min(piece, bytes - o);
+                    bulk_s2g(gp + o, sg + run.y * 48 + o, nb);
+                    if (do_skin) bulk_s2g(sp + o, ss + run.y * 48 + o, nb);
+                }
+            }
+            bulk_commit();
+            bulk_wait_read<0>();
+            mbar_arrive(&sfree[sb]);
+            if (it + NS < my_tiles) issue_load(stage);
+            if (++sk == KT) { sk = 0; sc += gridDim.x; }
+            if (++stage == NS) { stage = 0; phase ^= 1u; }
+            if (++sb == NSS) sb = 0;
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int t = threadIdx.x;
+    float* wsb = a.ws + (int64_t)blockIdx.x * a.n_exp * 12;   // this CTA's workspace
+    const bool skin = a.sout != nullptr;
+    // per-tile program prefetch into buffer pb: chunk metadata row, phase-1 info and the
+    // import list (each thread copies what it reads itself, so no barrier is needed)
+    auto prefetch_prog = [&](int k, int pb) {
+        if (t < a.T) {
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+                cp_async8(s_meta + pb * TK + t * K + s, a.meta + ((int64_t)k * a.T + t) * K + s);
+            cp_async4(s_p1 + pb * a.T + t, a.p1len + (int64_t)k * a.T + t);
+        }
+        const int ni = a.tiles[k].n_imp, io = a.tiles[k].imp_off;
+        for (int i = t; i < ni; i += NC) cp_async8(s_imp + pb * a.max_imp + i, a.imp + io + i);
+        cp_async_commit();
+    };
+    // phase-2 tables of tile k (read by every thread: awaited before the phase-2 barrier)
+    auto prefetch_tables = [&](int k) {
+        const SeqTileDev tl = a.tiles[k];
+        for (int i = t; i <= a.r2max; i += NC) cp_async4(s_round_off + i, a.round_off + (int64_t)k * (a.r2max + 1) + i);
+        for (int i = t; i < tl.n_entries; i += NC) cp_async4(s_rounds + i, a.rounds + tl.rounds_off + i);
+        cp_async_commit();
+    };
+    if (my_tiles > 0) {
+        prefetch_prog(0, 0);
+        prefetch_tables(0);
+    }
+
+    uint64_t m[K];
+    float ibr[K][12];
+    int stage = 0, sb = 0, pb = 0, k = 0;
+    uint32_t phase = 0, sphase = 0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+        const SeqTileDev tl = a.tiles[k];
+        float* L = LG + stage * tile_f;
+        cp_async_wait_all();   // this tile's program (and tables: barrier before phase 2)
+        int p1, run_back, run_anchor;
+        {
+            const int info = t < a.T ? s_p1[pb * a.T + t] : 0;
+            p1 = info & 0xff;
+            run_back = (info >> 8) & 0xff;
+            run_anchor = (int)((uint32_t)info >> 16) - 1;
+        }
+#pragma unroll
+        for (int s = 0; s < K; ++s)
+            m[s] = t < a.T ? s_meta[pb * TK + t * K + s]
+                           : ((uint64_t)(uint16_t)(int16_t)kSrcNone << 32) | (0xffffull << 48);
+        // imports: external parents' final poses, workspace (L2) -> Q locations
+        for (int i = t; i < tl.n_imp; i += NC) {
+            const int2 e = s_imp[pb * a.max_imp + i];
+            HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= 0 && (e.y + 1) * 12 <= a.p_floats);
+            const float* src = wsb + (int64_t)e.x * 12;
+            float* dst = P + e.y * 12;
+            cp_async16_cg(dst, src);
+            cp_async16_cg(dst + 4, src + 4);
+            cp_async16_cg(dst + 8, src + 8);
+        }
+        cp_async_commit();
+        if (it + 1 < my_tiles) prefetch_prog(k + 1 < KT ? k + 1 : 0, pb ^ 1);
+        // inverse bind of this tile's slots (first used in phase 3)
+        if (skin) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int src = (int)(int16_t)(m[s] >> 32);
+                const int off = (int)(m[s] & 0xffff);
+                if (src != kSrcNone) {
+                    HS_BOUND(off >= 0 && off < a.F);
+                    ldg3(a.ib + ((int64_t)k * a.F + off) * 12, ibr[s]);
+                }
+            }
+        }
+        mbar_wait(&full[stage], phase);
+
+        // phase 1: in-chunk fold, publish anchors
+        float acc[12];
+        if (p1 > 0) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                if (s < p1) {
+                    const int off = (int)(m[s] & 0xffff);
+                    const int src = (int)(int16_t)(m[s] >> 32);
+                    const int own = (int)(int16_t)(m[s] >> 48);
+                    float l[12];
+                    HS_BOUND(off >= 0 && off < tl.nj);
+                    ld3(L + off * 12, l);
+                    if (src == kSrcPrev) {
+                        float tmp[12];
+                        compose(acc, l, tmp);
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) acc[e] = tmp[e];
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) acc[e] = l[e];
+                    }
+                    HS_BOUND(own < 2 * a.S);
+                    if (own >= 0) st3(P + own * 12, acc);
+                }
+            }
+        }
+        // phase 2a: runs (warp-shuffle segmented scan), as in kernels.cu
+        float excl[12];
+        const int warp_maxrb = RUNS ? (int)__reduce_max_sync(0xffffffffu, (unsigned)run_back) : 0;
+        if (RUNS && warp_maxrb > 0) {
+            for (int d = 1; d <= warp_maxrb; d <<= 1) {
+                float u[12];
+#pragma unroll
+                for (int e = 0; e < 12; ++e) u[e] = __shfl_up_sync(0xffffffffu, acc[e], d);
+                if (run_back >= d) {
+                    float w[12];
+                    compose(u, acc, w);
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc[e] = w[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 12; ++e) excl[e] = __shfl_up_sync(0xffffffffu, acc[e], 1);
+            if (run_back > 0) {
+#pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    const int own = (int)(int16_t)(m[s] >> 48);
+                    if (own >= 0) {
+                        float x[12], y[12];
+                        ld3(P + own * 12, x);
+                        compose(excl, x, y);
+                        st3(P + own * 12, y);
+                    }
+                }
+            }
+        }
+        cp_async_wait_all();   // imports (and the next tile's program) have landed
+        bar_consumers(NC);
+
+        // phase 2: pointer jumping over the anchor forest (ping-pong P; Q roots final)
+        for (int r = 0; r < tl.R2; ++r) {
+            const int eb = s_round_off[r], e1 = s_round_off[r + 1];
+            for (int e = eb + t; e < e1; e += NC) {
+                const uint32_t w = s_rounds[e];
+                const int slot = (int)(w & 0x3fff);
+                const int dst = slot + ((w >> 14) & 1) * a.S, self = slot + ((w >> 15) & 1) * a.S,
+                          link = (int)(w >> 16);
+                float x[12], y[12], z[12];
+                HS_BOUND(link >= 0 && (link + 1) * 12 <= a.p_floats && self < 2 * a.S && dst < 2 * a.S);
+                ld3(P + link * 12, x);
+                ld3(P + self * 12, y);
+                compose(x, y, z);
+                st3(P + dst * 12, z);
+            }
+            bar_consumers(NC);
+        }
+        // the next tile's phase-2 tables (this tile's have been read: barrier above)
+        if (it + 1 < my_tiles) prefetch_tables(k + 1 < KT ? k + 1 : 0);
+
+        // phase 3: final fold, G in place, S into the S buffer, exports to the workspace
+        float* S = SB + sb * tile_f;
+        if (skin && it >= NSS) mbar_wait(&sfree[sb], sphase);
+        {
+            float acc3[12];
+#pragma unroll
+            for (int s = 0; s < K; ++s) {
+                const int src = (int)(int16_t)(m[s] >> 32);
+                if (src == kSrcNone) continue;
+                const int off = (int)(m[s] & 0xffff);
+                const int ex = (int)((m[s] >> 16) & 0xffff);
+                float l[12];
+                HS_BOUND(off >= 0 && off < tl.nj);
+                ld3(L + off * 12, l);
+                if (RUNS) {
+                    float left[12];
+                    if (src == kSrcPrev) {
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) left[e] = acc3[e];
+                    } else if (src == kSrcRoot) {
+#pragma unroll
+                        for (int e = 0; e < 12; ++e) left[e] = (e == 0 || e == 5 || e == 10) ? 1.0f : 0.0f;
+                    } else if (src == kSrcRun) {
+                        if (run_anchor >= 0) {
+                            float pa[12];
+                            HS_BOUND((run_anchor + 1) * 12 <= a.p_floats);
+                            ld3(P + run_anchor * 12, pa);
+                            compose(pa, excl, left);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 12; ++e) left[e] = excl[e];
+                        }
+                    } else {
+                        HS_BOUND(src >= 0 && (src + 1) * 12 <= a.p_floats);
+                        ld3(P + src * 12, left);
+                    }
+                    compose(left, l, acc3);
+                } else if (src == kSrcPrev) {
+                    float tmp[12];
+                    compose(acc3, l, tmp);
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc3[e] = tmp[e];
+                } else if (src == kSrcRoot) {
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) acc3[e] = l[e];
+                } else {
+                    float pa[12];
+                    HS_BOUND(src >= 0 && (src + 1) * 12 <= a.p_floats);
+                    ld3(P + src * 12, pa);
+                    compose(pa, l, acc3);
+                }
+                st3(L + off * 12, acc3);
+                if (ex) {   // a child in a later tile: export the global pose (L2)
+                    HS_BOUND(ex - 1 < a.n_exp);
+                    st3(wsb + (int64_t)(ex - 1) * 12, acc3);
+                }
+                if (skin) {
+                    float sk[12];
+                    compose(acc3, ibr[s], sk);
+                    st3(S + off * 12, sk);
+                }
+            }
+        }
+        fence_proxy_async();
+        bar_consumers(NC);
+        if (t == 0) mbar_arrive(&done[stage]);
+        if (++stage == NS) { stage = 0; phase ^= 1u; }
+        if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }
+        pb ^= 1;
+        if (++k == KT) k = 0;
+    }
+}
+
+void* seq_fn(int K, bool runs) {
+    switch (K) {
+        case 3: return runs ? (void*)&seq_kernel<3, true> : (void*)&seq_kernel<3, false>;
+        case 5: return runs ? (void*)&seq_kernel<5, true> : (void*)&seq_kernel<5, false>;
+        case 7: return runs ? (void*)&seq_kernel<7, true> : (void*)&seq_kernel<7, false>;
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+cudaError_t prepare_seq(int K) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    for (bool runs : {false, true}) {
+        void* fn = seq_fn(K, runs);
+        if (!fn) return cudaErrorInvalidValue;
+        if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
+            return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_seq(int K, const SeqArgs& a, cudaStream_t st) {
+    void* fn = seq_fn(K, a.has_runs != 0);
+    if (!fn) return cudaErrorInvalidValue;
+    int64_t grid = (int64_t)sm_count() * (a.ctas_per_sm > 0 ? a.ctas_per_sm : 1);
+    if (grid > a.n_chars) grid = a.n_chars;
+    if (grid < 1) grid = 1;
+    SeqArgs args = a;
+    void* params[] = {&args};
+    return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(a.threads), params, (size_t)a.smem_bytes, st);
+}
+
+}  // namespace hs

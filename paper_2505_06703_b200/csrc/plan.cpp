@@ -624,6 +624,218 @@ SplitProgram build_split_program(const Plan& p, int K) {
     return sp;
 }
 
+bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, SeqProgram& sp) {
+    // Tiles are runs of F consecutive INTERNAL positions (a topological order), so a
+    // joint's parent is in its own tile or an earlier one.  A CTA runs a character's
+    // tiles in order; each tile is one chunk/anchor program (build_tile_program with
+    // C = 1) over its sub-forest, where
+    //   * a joint whose parent is in an earlier tile ("external parent") starts a
+    //     segment like a root, but its source is the parent's final global pose,
+    //     imported before the tile into a Q location (Q nodes are final roots of the
+    //     anchor forest: pointer jumping links to them and stops);
+    //   * a joint with a child in a later tile is EXPORTED: phase 3 stores its global
+    //     pose to workspace slot exp (one slot per exported joint of the skeleton).
+    sp = SeqProgram();
+    const int32_t n = p.n;
+    if (F < 32 || n <= 0) return false;
+    sp.K = K;
+    sp.F = F;
+    sp.KT = (n + F - 1) / F;
+    const int KT = sp.KT;
+    // exported joints: a child in a later tile
+    std::vector<int32_t> exp_slot(n, -1);
+    {
+        std::vector<int32_t> last(n, -1);
+        for (int32_t i = 0; i < n; ++i)
+            if (p.ipar[i] >= 0) last[p.ipar[i]] = std::max(last[p.ipar[i]], i / F);
+        for (int32_t i = 0; i < n; ++i)
+            if (last[i] > i / F) exp_slot[i] = sp.n_exp++;
+    }
+    if (sp.n_exp >= 0xffff) return false;   // 16-bit exp field (slot + 1)
+    struct TileTmp {
+        ChunkDecomp d;
+        std::vector<int32_t> ext;          // per local node: external parent (internal) or -1
+        std::vector<int32_t> q_of;         // per local node with ext: import index
+        std::vector<int32_t> imports;      // import index -> external parent
+        std::vector<int32_t> idx;          // raw slot -> coloured slot
+        int S = 0;
+    };
+    std::vector<TileTmp> tmp(KT);
+    for (int k = 0; k < KT; ++k) {
+        TileTmp& tt = tmp[k];
+        const int32_t a = k * F, nj = std::min(F, n - a);
+        std::vector<int32_t> lpar(nj), pos(nj);
+        tt.ext.assign(nj, -1);
+        tt.q_of.assign(nj, -1);
+        std::vector<int32_t> qmap;   // external parent -> import index (linear search: few per tile)
+        for (int32_t li = 0; li < nj; ++li) {
+            const int32_t q = p.ipar[a + li];
+            pos[li] = li;
+            lpar[li] = q >= a ? q - a : -1;
+            if (q >= 0 && q < a) {
+                tt.ext[li] = q;
+                int32_t qi = -1;
+                for (size_t z = 0; z < tt.imports.size(); ++z)
+                    if (tt.imports[z] == q) { qi = (int32_t)z; break; }
+                if (qi < 0) { qi = (int32_t)tt.imports.size(); tt.imports.push_back(q); }
+                tt.q_of[li] = qi;
+            }
+        }
+        tt.d = decompose(lpar, K, mode, &pos, true);
+        const ChunkDecomp& d = tt.d;
+        const int32_t T = (int32_t)d.lists.size();
+        if (T > max_threads) return false;
+        sp.T = std::max(sp.T, (T + 31) / 32 * 32);
+        // bank-conflict-aware slot colours (as build_tile_program, one character)
+        const int32_t Sraw = (int32_t)d.slots.size();
+        std::vector<std::vector<int32_t>> sets;
+        {
+            std::vector<std::vector<int32_t>> rd((size_t)((T + 7) / 8) * K), wr(rd.size());
+            for (int32_t t = 0; t < T; ++t)
+                for (int s = 0; s < (int)d.lists[t].size(); ++s) {
+                    const int32_t i = d.lists[t][s];
+                    const size_t kk = (size_t)(t / 8) * K + s;
+                    if (d.src[i] >= 0) rd[kk].push_back(d.slot_of[d.src[i]]);
+                    if (d.slot_of[i] >= 0) wr[kk].push_back(d.slot_of[i]);
+                }
+            for (auto& v : rd) if (v.size() > 1) sets.push_back(v);
+            for (auto& v : wr) if (v.size() > 1) sets.push_back(v);
+        }
+        tt.S = 0;
+        if (Sraw) tt.idx = colour_slots(Sraw, sets, &tt.S);
+        sp.S = std::max(sp.S, tt.S);
+        sp.nQ = std::max(sp.nQ, (int)tt.imports.size());
+        if (d.run_back.size() == d.lists.size())
+            for (int32_t t = 0; t < T; ++t)
+                if (d.run_back[t] > 0) sp.has_runs = true;
+    }
+    const int32_t S = sp.S, qbase = 2 * S;
+    if (S >= (1 << 14) || qbase + sp.nQ >= (1 << 15)) return false;   // descriptor / src field widths
+    // empty slots: src NONE, own -1 (phase 2a lifts every slot with own >= 0)
+    sp.meta.assign((size_t)KT * sp.T * K,
+                   ((uint64_t)(uint16_t)(int16_t)SRC_NONE << 32) | ((uint64_t)(uint16_t)(int16_t)-1 << 48));
+    sp.p1len.assign((size_t)KT * sp.T, 0);
+    sp.ib_user.assign((size_t)KT * F, -1);
+    std::vector<std::vector<int32_t>> roff(KT);
+    for (int k = 0; k < KT; ++k) {
+        TileTmp& tt = tmp[k];
+        const ChunkDecomp& d = tt.d;
+        const int32_t a = k * F, nj = std::min(F, n - a);
+        const int32_t T = (int32_t)d.lists.size();
+        const int32_t Sraw = (int32_t)d.slots.size();
+        const int32_t nq = (int32_t)tt.imports.size();
+        SeqTile st{};
+        st.first = a;
+        st.nj = nj;
+        st.T = T;
+        // anchor forest: tile anchors 0..Sraw-1 (ping-pong), Q nodes Sraw..Sraw+nq-1 (final)
+        std::vector<int32_t> lk(Sraw + nq, -1), latest(Sraw, 0);
+        for (int32_t s = 0; s < Sraw; ++s) {
+            const int32_t h = d.head[d.slots[s]];
+            if (d.link0[s] >= 0) lk[s] = d.link0[s];
+            else if (tt.q_of[h] >= 0) lk[s] = Sraw + tt.q_of[h];
+        }
+        auto loc = [&](int32_t x) { return x < Sraw ? latest[x] * S + tt.idx[x] : qbase + (x - Sraw); };
+        st.rounds_off = (int32_t)sp.rounds.size();
+        roff[k].push_back(0);
+        for (int r = 0;; ++r) {
+            bool any = false;
+            for (int32_t s = 0; s < Sraw; ++s) if (lk[s] >= 0) { any = true; break; }
+            if (!any) break;
+            std::vector<std::array<int32_t, 3>> ent;
+            const int32_t wbuf = (r + 1) & 1;
+            for (int32_t s = 0; s < Sraw; ++s)
+                if (lk[s] >= 0) ent.push_back({wbuf * S + tt.idx[s], latest[s] * S + tt.idx[s], loc(lk[s])});
+            order_round(ent);
+            for (auto& e : ent) {
+                const uint32_t slot = (uint32_t)(e[1] % S), sbuf = (uint32_t)(e[1] / S), wb = (uint32_t)(e[0] / S);
+                sp.rounds.push_back(slot | (wb << 14) | (sbuf << 15) | ((uint32_t)e[2] << 16));
+            }
+            sp.max_entries = std::max(sp.max_entries, (int)ent.size());
+            std::vector<int32_t> nl(lk.size(), -1);
+            for (int32_t s = 0; s < Sraw; ++s) {
+                if (lk[s] < 0) continue;
+                latest[s] = wbuf;
+                nl[s] = lk[s] < Sraw ? lk[lk[s]] : -1;   // a Q node is a root: the chain ends
+            }
+            lk.swap(nl);
+            roff[k].push_back((int32_t)sp.rounds.size() - st.rounds_off);
+            st.R2 = r + 1;
+        }
+        st.n_entries = (int32_t)sp.rounds.size() - st.rounds_off;
+        sp.R2max = std::max(sp.R2max, st.R2);
+        // per-thread program
+        for (int32_t t = 0; t < T; ++t) {
+            const bool in_run = d.run_back[t] > 0 || (t + 1 < T && d.run_back[t + 1] > 0);
+            int32_t info = 0;
+            if (d.run_back[t] > 0 && !d.lists[t].empty()) {
+                const int32_t h = d.head[d.lists[t][0]];
+                int32_t l = -1;
+                if (d.src[h] >= 0) l = loc(d.slot_of[d.src[h]]);
+                else if (tt.q_of[h] >= 0) l = qbase + tt.q_of[h];
+                info = (d.run_back[t] << 8) | ((l + 1) << 16);
+            }
+            int32_t& p1 = sp.p1len[(size_t)k * sp.T + t];
+            for (int s = 0; s < K; ++s) {
+                if (s >= (int)d.lists[t].size()) continue;
+                const int32_t li = d.lists[t][s];
+                int32_t src;
+                if (d.src[li] >= 0) src = loc(d.slot_of[d.src[li]]);
+                else if (d.src[li] == SRC_ROOT && tt.q_of[li] >= 0) src = qbase + tt.q_of[li];
+                else src = d.src[li];
+                const int32_t own = d.slot_of[li] >= 0 ? tt.idx[d.slot_of[li]] : -1;
+                if (own >= 0 || in_run) p1 = s + 1;
+                const uint64_t ex = (uint64_t)(exp_slot[a + li] + 1);
+                sp.meta[((size_t)k * sp.T + t) * K + s] = (uint64_t)li | (ex << 16) |
+                                                          ((uint64_t)(uint16_t)(int16_t)src << 32) |
+                                                          ((uint64_t)(uint16_t)(int16_t)own << 48);
+            }
+            p1 |= info;
+        }
+        // imports, TMA runs (maximal user-label runs over the tile's smem order), IB map
+        st.imp_off = (int32_t)sp.imp.size() / 2;
+        st.n_imp = nq;
+        for (int32_t z = 0; z < nq; ++z) {
+            sp.imp.push_back(exp_slot[tt.imports[z]]);
+            sp.imp.push_back(qbase + z);
+        }
+        st.runs_off = (int32_t)sp.runs.size() / 4;
+        for (int32_t li = 0; li < nj;) {
+            int32_t len = 1;
+            while (li + len < nj && p.order[a + li + len] == p.order[a + li] + len) ++len;
+            sp.runs.insert(sp.runs.end(), {p.order[a + li], li, len, 0});
+            li += len;
+            ++st.n_runs;
+        }
+        for (int32_t li = 0; li < nj; ++li) sp.ib_user[(size_t)k * F + li] = p.order[a + li];
+        sp.max_imp = std::max(sp.max_imp, st.n_imp);
+        sp.max_runs = std::max(sp.max_runs, st.n_runs);
+        sp.tiles.push_back(st);
+    }
+    sp.round_off.assign((size_t)KT * (sp.R2max + 1), 0);
+    for (int k = 0; k < KT; ++k)
+        for (int r = 0; r <= sp.R2max; ++r)
+            sp.round_off[(size_t)k * (sp.R2max + 1) + r] = roff[k][std::min<size_t>(r, roff[k].size() - 1)];
+    return true;
+}
+
+int64_t seq_max_tile_entries(const SeqProgram& sp) {
+    int64_t maxe = 0;
+    for (const SeqTile& t : sp.tiles) maxe = std::max<int64_t>(maxe, t.n_entries);
+    return maxe;
+}
+
+int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs) {
+    // barriers | stages x tile | sbufs x tile | P (2S anchors + nQ imports) | meta x2 |
+    // p1len x2 | imports x2 | round_off | rounds
+    const int64_t tileb = (int64_t)sp.F * 48;
+    int64_t b = 128 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + sp.nQ) * 48;
+    b += 2LL * sp.T * sp.K * 8 + 2LL * sp.T * 4 + 2LL * sp.max_imp * 8;
+    b += ((int64_t)(sp.R2max + 1) * 4 + 15) / 16 * 16;
+    b += (seq_max_tile_entries(sp) * 4 + 15) / 16 * 16;
+    return b;
+}
+
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob) {
     block_of.resize(p.n);
     mpob.assign(p.n, -1);
@@ -653,6 +865,22 @@ void blocked_tables(const Plan& p, int B, std::vector<int32_t>& lb, std::vector<
             const int32_t a = lb[(size_t)(r - 1) * n + u];
             lb[(size_t)r * n + u] = a >= 0 ? lb[(size_t)(r - 1) * n + a] : -1;
         }
+}
+
+void compressed_tables(const Plan& p, int B, std::vector<int32_t>& lp, std::vector<int32_t>& l8) {
+    const int32_t n = p.n;
+    lp.assign(n, -1);
+    l8.assign(n, -1);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t q = p.ipar[i];
+        lp[p.order[i]] = (q >= 0 && q / B == i / B) ? p.order[q] : -1;
+        int32_t a = i;
+        for (int d = 0; d < 8 && a >= 0; ++d) {
+            a = p.ipar[a];
+            if (a >= 0 && a / B != i / B) a = -1;   // left the block: no in-block 8th ancestor
+        }
+        l8[p.order[i]] = a >= 0 ? p.order[a] : -1;
+    }
 }
 
 int64_t tile_smem_bytes(const TileProgram& tp, int stages, int sbufs) {

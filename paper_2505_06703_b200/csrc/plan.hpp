@@ -75,6 +75,40 @@ struct SplitProgram {
     std::vector<int32_t> anchor_parents;// [nslots]: link0 (the anchor skeleton, topological)
 };
 
+// Multi-tile program for skeletons beyond one CTA: the internal
+// (topological) order is cut into tiles of <= F consecutive positions; a CTA walks a
+// character's tiles in order, so every cross-tile parent is FINAL when its child's
+// tile runs (Alg. 3's cross-block carry, with the carry resolved
+// before the block instead of walked after it).  Per tile: the chunk/anchor program
+// of the tile's sub-forest, where a joint whose parent lies in an earlier tile reads
+// that parent's global pose from an imported slot Q (a final root of the anchor
+// forest); joints with a child in a later tile export their global pose to a
+// per-CTA workspace slot in phase 3.
+struct SeqTile {
+    int32_t first, nj;            // internal positions [first, first + nj)
+    int32_t R2, n_entries;        // pointer-jumping rounds and phase-2 descriptors
+    int32_t rounds_off;           // offset into rounds; round_off rows are per tile
+    int32_t n_imp, imp_off;       // imports: (workspace slot, P location) pairs
+    int32_t n_runs, runs_off;     // TMA runs: (user start, smem offset, length)
+    int32_t T;                    // compute threads with work
+    int32_t pad[2];
+};
+struct SeqProgram {
+    int K = 0, F = 0, T = 0, KT = 0;   // chunk, joints per tile (max), threads (max), tiles
+    int S = 0;                          // anchor slots per buffer (uniform over tiles)
+    int nQ = 0;                         // import slots (max over tiles); Q locations 2S..2S+nQ
+    int R2max = 0, max_entries = 0, max_imp = 0, max_runs = 0;
+    int n_exp = 0;                      // exported joints = workspace slots per character
+    bool has_runs = false;
+    std::vector<SeqTile> tiles;
+    std::vector<uint64_t> meta;         // [KT][T][K]: off | (exp slot + 1) << 16 | (u16)src << 32 | (u16)own << 48
+    std::vector<int32_t> p1len;         // [KT][T] as TileProgram::p1len
+    std::vector<int32_t> round_off;     // [KT][R2max + 1], relative to the tile's rounds_off
+    std::vector<uint32_t> rounds;       // concatenated phase-2 descriptors (TileProgram encoding)
+    std::vector<int32_t> imp;           // [..][2]: workspace slot, P location
+    std::vector<int32_t> runs;          // [..][4]: user start, smem offset, length, 0
+    std::vector<int32_t> ib_user;       // [KT][F]: user label at each smem offset (-1 = none)
+};
 struct Plan {
     int32_t n = 0;
     std::vector<int32_t> parents;       // user labels
@@ -93,6 +127,11 @@ int build_plan(const int32_t* parents, int32_t n, Plan& out, std::string& err);
 
 TileProgram build_tile_program(const Plan& p, int K, int C, bool pingpong, int mode);
 SplitProgram build_split_program(const Plan& p, int K);
+// Returns false when a tile does not fit (more than max_threads compute threads or a
+// field overflows its 16-bit encoding): the caller retries with a smaller F.
+bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, SeqProgram& out);
+int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs);
+int64_t seq_max_tile_entries(const SeqProgram& sp);   // phase-2 descriptors of the largest tile
 
 // The paper's block layout for block size B over INTERNAL positions (exports).
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);
@@ -102,6 +141,11 @@ void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vec
 // block: DESIGN.md reading R8), mpob[u] = MaxParentOutBlock(u) (stage B walk,
 // reading R9); RB = ceil(log2 B) stage-A rounds.
 void blocked_tables(const Plan& p, int B, std::vector<int32_t>& lb, std::vector<int32_t>& mpob, int& RB);
+
+// Tables of the literal Alg. 4 comparison kernel, in USER labels:
+// lp[u] = in-block parent (stage A hops, clamped: R8), l8[u] = in-block 8th ancestor
+// (stage B's MultiParent(., 8)), -1 when the hop leaves u's B-block.
+void compressed_tables(const Plan& p, int B, std::vector<int32_t>& lp, std::vector<int32_t>& l8);
 
 // Shared-memory bytes of the chunked kernel for a tile program and stage counts
 // (tiles, skin buffers, anchor buffers, and the phase-2 tables staged in smem).

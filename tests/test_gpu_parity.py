@@ -87,7 +87,7 @@ def test_exact_family_bitwise(name, create):
     assert np.array_equal(g, G) and np.array_equal(s, S)
 
 
-@pytest.mark.parametrize("algo", ["doubling", "gateau", "leaf", "blocked"])
+@pytest.mark.parametrize("algo", ["doubling", "gateau", "leaf", "blocked", "compressed"])
 @pytest.mark.parametrize("name", ["hum64", "chain256", "tree1024"])
 def test_exact_family_comparison_algorithms(algo, name):
     par = hsgen.skeleton(name)
@@ -118,27 +118,98 @@ def test_permuted_labels():
     assert max_err(g, G) <= TOL
 
 
-def test_large_skeleton_multi_cta_path():
-    """16,384-joint tree, L = 1024: beyond one CTA -> the split (multi-CTA) path."""
-    par = hsgen.random_tree(77, 16384, 1024)
+@pytest.mark.parametrize("algo", ["tiles", "split"])
+def test_large_skeleton_multi_cta_path(algo):
+    """16,384-joint tree, L = 1024: beyond one CTA -> the multi-tile path (large crowds,
+    HS_ALGO_TILES) or the split path (small crowds); both forced here on a few characters."""
+    par = hsgen.skeleton("tree16384")
     sk = hs.Skeleton(par)
-    assert sk.query("path") == hs.ALGO["split"]
-    assert sk.query("split_levels") >= 1
+    assert sk.query("path") == hs.ALGO["tiles"]
+    assert sk.query("seq_tiles") >= 16 and sk.query("split_levels") >= 1
     sk.close()
     local = hsgen.exact_poses(35, 16384, 3)
     ib = hsgen.exact_inv_bind(35, 16384)
     G, S = oracle.scan(par, local, ib)
-    g, s = gpu_scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib, algo=algo)
     assert np.array_equal(g, G) and np.array_equal(s, S)
     # rigid |t| <= 1 locals and a rigid |t| <= 1 inverse bind: the north star's 1e-4
     # holds for depth <= 1024 (reading R16)
     local = hsgen.local_poses(36, 16384, 4)
     ib = hsgen.inv_bind(36, 16384)
-    g, s = gpu_scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib, algo=algo)
     G, S = oracle.scan(par, local, ib)
     eg, es = max_err(g, G), max_err(s, S)
-    print(f"16384-joint L=1024 tree: max err global {eg:.3e} skin {es:.3e}")
+    print(f"16384-joint L=1024 tree ({algo}): max err global {eg:.3e} skin {es:.3e}")
     assert eg <= TOL and es <= TOL
+
+
+def test_multi_tile_crowd_auto_and_sampled_oracle():
+    """A crowd larger than the SM count takes the multi-tile path under AUTO; every
+    character equals the same character scanned alone (bitwise: one CTA runs a whole
+    character, whatever the crowd); sampled characters within 1e-4 of the oracle."""
+    par = hsgen.skeleton("tree16384")
+    ib = hsgen.inv_bind(38, 16384)
+    sk = hs.Skeleton(par, ib)
+    n = 2 * torch.cuda.get_device_properties(0).multi_processor_count + 7
+    x = torch.empty((n, 16384, 3, 4), device="cuda")
+    assert hsgen.lib_cuda().hsg_cuda_local_poses(39, 0, 16384, 0, n, x.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream) == 0
+    g, s = sk.scan(x)
+    g2, s2 = torch.empty_like(x), torch.empty_like(x)
+    sk.scan_into(x, g2, s2, algo="tiles")
+    torch.cuda.synchronize()
+    assert torch.equal(g, g2) and torch.equal(s, s2)
+    idx = np.array([0, 1, n // 2, n - 1])
+    for i in idx:   # alone == in the crowd
+        ga, sa = sk.scan(x[i:i + 1].contiguous(), algo="tiles")
+        assert torch.equal(ga[0], g[i]) and torch.equal(sa[0], s[i])
+    loc = np.concatenate([hsgen.local_poses(39, 16384, 1, char0=int(i)) for i in idx])
+    assert np.array_equal(loc, x[idx].cpu().numpy())
+    G, S = oracle.scan(par, loc, ib)
+    eg, es = max_err(g[idx].cpu().numpy(), G), max_err(s[idx].cpu().numpy(), S)
+    print(f"multi-tile crowd of {n}: sampled max err global {eg:.3e} skin {es:.3e}")
+    assert eg <= TOL and es <= TOL
+
+
+MULTI_TILE_CASES = [
+    ("tree1024", {"force_split": True}), ("chain256", {"force_split": True, "chunk": 3}),
+    (("rt", 3000, 120), {}), (("rt", 3000, 120), {"tile_joints": 256}), (("rt", 3000, 120), {"chunking": 2}),
+    (("rt", 5000, 2500), {"chunk": 7}), (("chain", 4000), {}), (("star", 2000), {}),
+    (("perm", 2500, 200), {}),
+]
+
+
+def _skel(spec):
+    if isinstance(spec, str):
+        return hsgen.skeleton(spec)
+    if spec[0] == "rt":
+        return hsgen.random_tree(11, spec[1], spec[2])
+    if spec[0] == "chain":
+        return hsgen.chain(spec[1])
+    if spec[0] == "star":
+        return np.r_[-1, np.zeros(spec[1] - 1, np.int32)].astype(np.int32)
+    base = hsgen.random_tree(12, spec[1], spec[2])
+    return hsgen.relabel(base, hsgen.permutation(13, spec[1]))[0]
+
+
+@pytest.mark.parametrize("spec,create", MULTI_TILE_CASES)
+def test_multi_tile_exact_family_bitwise(spec, create):
+    """The multi-tile kernel equals the oracle bit for bit on the exact family: chains
+    (one import per tile), stars (every joint imports the root), deep random trees,
+    small tiles, K = 3 / 7, heavy-path chunking, permuted labels (gathered TMA runs)."""
+    par = _skel(spec)
+    J = len(par)
+    n_chars = 19
+    local = hsgen.exact_poses(51, J, n_chars)
+    ib = hsgen.exact_inv_bind(51, J)
+    sk = hs.Skeleton(par, ib, **create)
+    assert sk.query("seq_tiles") >= 1
+    sk.close()
+    G, S = oracle.scan(par, local, ib)
+    g, s = gpu_scan(par, local, ib, algo="tiles", **create)
+    assert np.array_equal(g, G) and np.array_equal(s, S)
+    g, _ = gpu_scan(par, local, ib, algo="tiles", skin=False, **create)
+    assert np.array_equal(g, G)
 
 
 def test_forced_split_config4_rigid():
@@ -149,14 +220,15 @@ def test_forced_split_config4_rigid():
     local = hsgen.local_poses(seed, 1024, n_chars, type_=type_)
     ib = hsgen.inv_bind(ib_seed, 1024)
     sk = hs.Skeleton(par, ib, force_split=True)
-    assert sk.query("path") == hs.ALGO["split"]
+    assert sk.query("path") == hs.ALGO["tiles"]
     x = torch.from_numpy(local).cuda()
-    g, s = sk.scan(x)
-    torch.cuda.synchronize()
     G, S = oracle.scan(par, local, ib)
-    eg, es = max_err(g.cpu().numpy(), G), max_err(s.cpu().numpy(), S)
-    print(f"forced split, C4 20,000 x tree1024: max err global {eg:.3e} skin {es:.3e}")
-    assert eg <= TOL and es <= TOL
+    for algo in ("auto", "split"):   # auto: the multi-tile path (20,000 >= SM count)
+        g, s = sk.scan(x, algo=algo)
+        torch.cuda.synchronize()
+        eg, es = max_err(g.cpu().numpy(), G), max_err(s.cpu().numpy(), S)
+        print(f"forced multi-CTA ({algo}), C4 20,000 x tree1024: max err global {eg:.3e} skin {es:.3e}")
+        assert eg <= TOL and es <= TOL
     sk.close()
 
 
@@ -192,7 +264,7 @@ def test_dyadic_translation_chain_bitwise():
     assert np.array_equal(g[..., 3], np.cumsum(t, axis=1))
 
 
-@pytest.mark.parametrize("algo", ["auto", "doubling", "gateau", "leaf", "blocked"])
+@pytest.mark.parametrize("algo", ["auto", "doubling", "gateau", "leaf", "blocked", "compressed"])
 def test_single_joint_and_all_roots(algo):
     for par in ([-1], [-1] * 10):
         local = hsgen.local_poses(40, len(par), 33)
@@ -330,7 +402,7 @@ def test_fig7_shape_depth_sweep():
         g, s = torch.empty_like(x), torch.empty_like(x)
         sk = hs.Skeleton(par)
         G, _ = oracle.scan(par, local[:8])
-        for algo in ("auto", "gateau", "leaf"):
+        for algo in ("auto", "gateau", "leaf", "doubling", "blocked", "compressed"):
             sk.scan_into(x, g, s, algo=algo)
             torch.cuda.synchronize()
             assert max_err(g[:8].cpu().numpy(), G) <= TOL

@@ -166,7 +166,7 @@ def test_two_pass_on_multi_cta_skeleton():
     lay = hsgen.layers(23, 5, 2, 3, 1.0)
     ib = hsgen.inv_bind(24, J)
     sk = hs.Skeleton(par, ib)
-    assert sk.query("path") == 3   # HS_ALGO_SPLIT
+    assert sk.query("path") == hs.ALGO["tiles"]   # beyond one CTA (5 characters: the split path)
     cs = hs.ClipSet(sk, keys, 30.0, 1)
     g, s = hs.animate(sk, cs, lay)
     torch.cuda.synchronize()
