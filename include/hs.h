@@ -410,12 +410,15 @@ typedef enum {
        built for the plan's options with F = tile_joints or 1024, shrunk until it fits): */
     HS_X_SEQ_TILES = 12,   /* int32 [KT][12]: first, nj, R2, entries, rounds_off, n_imp, imp_off,
                               n_runs, runs_off, T, 0, 0                                       */
-    HS_X_SEQ_META = 13,    /* uint64 [KT][T][K]: smem offset | (export slot + 1)<<16 | int16 src<<32
-                              | int16 own<<48; src >= 2S: an imported (Q) location             */
+    HS_X_SEQ_META = 13,    /* uint64 [KT][T][K]: smem offset (10 bits) | (src + 8)<<10 (13) |
+                              (own + 1)<<23 (13) | (workspace export slot + 1)<<36 (16) |
+                              (next tile's Q index + 1)<<52 (12); src >= 2S: a Q location
+                              (2S + (k & 1) nQ + index)                                        */
     HS_X_SEQ_P1LEN = 14,   /* int32 [KT][T]                                                     */
     HS_X_SEQ_ROUND_OFF = 15, /* int32 [KT][R2max+1], relative to the tile's rounds_off           */
     HS_X_SEQ_ROUNDS = 16,  /* uint32 [E] (all tiles)                                            */
-    HS_X_SEQ_IMP = 17,     /* int32 [I][2]: workspace slot, P location                          */
+    HS_X_SEQ_IMP = 17,     /* int32 [I][2]: workspace slot, Q location (parents two or more
+                              tiles back; a parent in the previous tile is forwarded)           */
     HS_X_SEQ_RUNS = 18,    /* int32 [R][4]: user start, smem offset, length, 0                  */
     HS_X_SEQ_IB_USER = 19  /* int32 [KT][F]: user label at each smem offset (-1 = none)          */
 } hs_plan_export_what;

@@ -593,9 +593,9 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.imp = reinterpret_cast<const int2*>(sk->d_seq_imp);
             a.runs = reinterpret_cast<const int4*>(sk->d_seq_runs);
             a.n_chars = n_chars;
-            a.J = J; a.KT = sp.KT; a.F = sp.F; a.T = sp.T; a.S = sp.S; a.n_exp = sp.n_exp;
+            a.J = J; a.KT = sp.KT; a.F = sp.F; a.T = sp.T; a.S = sp.S; a.nQ = sp.nQ; a.n_exp = sp.n_exp;
             a.r2max = sp.R2max; a.max_imp = sp.max_imp; a.max_entries = sk->seq_max_entries;
-            a.p_floats = (2 * sp.S + sp.nQ) * 12;
+            a.p_floats = (2 * sp.S + 2 * sp.nQ) * 12;
             a.stages = sk->seq_stages; a.sbufs = sk->seq_sbufs; a.threads = sk->seq_threads;
             a.has_runs = sp.has_runs ? 1 : 0;
             a.bulk_piece = HS_BULK_PIECE;
@@ -609,8 +609,25 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 if (e != cudaSuccess) return cuda_fail(e, "multi-tile workspace");
             }
             a.ws = ws;
+            a.prof = nullptr;
+            if (HS_PROF_HOOKS && std::getenv("HS_DEBUG_PROF")) {   // profiling builds only (synchronising)
+                cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
+                cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
+            }
             e = hs::launch_seq(sk->K, a, st);
             if (ws) cudaFreeAsync(ws, st);
+            if (a.prof) {
+                unsigned long long h[10];
+                cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                const double nt = h[9] ? (double)h[9] : 1.0;
+                std::fprintf(stderr,
+                             "[hs prof seq] tiles=%llu cycles/tile: wait_prev %.0f issue %.0f wait_full %.0f "
+                             "phase1 %.0f bar %.0f phase2 %.0f wait_ib %.0f phase3 %.0f final_bar %.0f\n",
+                             h[9], h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt,
+                             h[7] / nt, h[8] / nt);
+                cudaFree(a.prof);
+            }
             break;
         }
         case HS_ALGO_SPLIT: {

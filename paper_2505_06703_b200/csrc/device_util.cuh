@@ -43,6 +43,15 @@ namespace {
 
 enum : int { kSrcRoot = -1, kSrcPrev = -2, kSrcNone = -3, kSrcRun = -4 };
 
+// Multi-tile program slot word (plan.cpp build_seq_program): smem offset (10 bits),
+// src + 8 (13), own + 1 (13), workspace export slot + 1 (16), next-tile Q forward + 1 (12).
+constexpr uint64_t kSeqMetaNone = (uint64_t)(kSrcNone + 8) << 10;   // src none, own -1, no export
+__device__ __forceinline__ int seq_off(uint64_t m) { return (int)(m & 0x3ff); }
+__device__ __forceinline__ int seq_src(uint64_t m) { return (int)((m >> 10) & 0x1fff) - 8; }
+__device__ __forceinline__ int seq_own(uint64_t m) { return (int)((m >> 23) & 0x1fff) - 1; }
+__device__ __forceinline__ int seq_ex(uint64_t m) { return (int)((m >> 36) & 0xffff); }
+__device__ __forceinline__ int seq_fwd(uint64_t m) { return (int)((m >> 52) & 0xfff); }
+
 // ------------------------------------------------------------------ 3x4 algebra
 struct M34 {
     float v[12];
@@ -144,6 +153,45 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// L2 cache policies (createpolicy): streaming data that is touched once (tiles in, G and S
+// out) is marked evict_first, so data that is re-read within the kernel (the multi-tile
+// path's workspace of exported poses, the per-skeleton tables) stays in L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st3_hint(float* p, const float* v, uint64_t pol) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + 4 * k),
+                     "f"(v[4 * k]), "f"(v[4 * k + 1]), "f"(v[4 * k + 2]), "f"(v[4 * k + 3]), "l"(pol)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg_hint(void* sdst, const void* gsrc, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
+                 "l"(pol)
+                 : "memory");
+}
+
 // cp.async (LDGSTS): 4/8-byte copies through L1 (read-only program tables), 16-byte
 // copies at L2 (.cg: data written earlier in the same kernel by other threads).
 __device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
@@ -229,16 +277,38 @@ __device__ __forceinline__ int4 layer_desc(const ChunkedArgs& a, int4 L) {
     return make_int4(row, fr != 0.0f ? Jp * 10 : 0, __float_as_int(fr), L.z);
 }
 
-// Every product and sum below is an explicit __fmul_rn / __fadd_rn / fmaf: the
+// Every product and sum below is an explicit mul_rn / add_rn / fma_rn: the
 // compiler's FMA contraction otherwise depends on the surrounding code (an unrolled
 // layer loop contracts differently from a rolled one), and the fused and two-pass
 // placements must produce the same local poses bit for bit.
-__device__ __forceinline__ float lerp_rn(float b, float x0, float a, float x1) {
-    return fmaf(a, x1, __fmul_rn(b, x0));
+// The Stage-1 arithmetic type s1r: fp32 (HS_S1_F64 = 0) or fp64 (1: sampling, blending
+// and TRS in double, the 3x4 rounded once to fp32; DESIGN.md §3 Stage-1 budget).
+#ifndef HS_S1_F64
+#define HS_S1_F64 1
+#endif
+#if HS_S1_F64
+typedef double s1r;
+#else
+typedef float s1r;
+#endif
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float rsqrt_rn(float x) { return rsqrt_fast(x); }
+__device__ __forceinline__ double rsqrt_rn(double x) { return __drcp_rn(__dsqrt_rn(x)); }
+__device__ __forceinline__ float rcp_rn(float x) { return rcp_fast(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+
+__device__ __forceinline__ s1r lerp_rn(s1r b, s1r x0, s1r a, s1r x1) {
+    return fma_rn(a, x1, mul_rn(b, x0));
 }
-__device__ __forceinline__ float dot4_rn(float a0, float a1, float a2, float a3, float b0, float b1, float b2,
-                                         float b3) {
-    return fmaf(a3, b3, fmaf(a2, b2, fmaf(a1, b1, __fmul_rn(a0, b0))));
+__device__ __forceinline__ s1r dot4_rn(s1r a0, s1r a1, s1r a2, s1r a3, s1r b0, s1r b1, s1r b2, s1r b3) {
+    return fma_rn(a3, b3, fma_rn(a2, b2, fma_rn(a1, b1, mul_rn(a0, b0))));
 }
 
 // Sample (keys x0..z0 at k0, x1..z1 at k0 + 1): trs = t(3), q(w,x,y,z)(4), s(3).
@@ -247,24 +317,24 @@ __device__ __forceinline__ float dot4_rn(float a0, float a1, float a2, float a3,
 // divides by |q|^2 itself.
 template <bool NORM>
 __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, float4 x1, float4 y1,
-                                           float2 z1, float a, float* trs) {
-    if (a == 0.0f) {   // on a key: that key exactly (R21)
+                                           float2 z1, float af, s1r* trs) {
+    if (af == 0.0f) {   // on a key: that key exactly (R21)
         trs[0] = x0.x; trs[1] = x0.y; trs[2] = x0.z; trs[3] = x0.w;
         trs[4] = y0.x; trs[5] = y0.y; trs[6] = y0.z;
         trs[7] = y0.w; trs[8] = z0.x; trs[9] = z0.y;
         return;
     }
-    const float b = __fsub_rn(1.0f, a);
+    const s1r a = af, b = sub_rn((s1r)1, a);
     trs[0] = lerp_rn(b, x0.x, a, x1.x); trs[1] = lerp_rn(b, x0.y, a, x1.y); trs[2] = lerp_rn(b, x0.z, a, x1.z);
     trs[7] = lerp_rn(b, y0.w, a, y1.w); trs[8] = lerp_rn(b, z0.x, a, z1.x); trs[9] = lerp_rn(b, z0.y, a, z1.y);
-    const float d = dot4_rn(x0.w, y0.x, y0.y, y0.z, x1.w, y1.x, y1.y, y1.z);
-    const float as = d < 0.0f ? -a : a;
-    const float qw = lerp_rn(b, x0.w, as, x1.w), qx = lerp_rn(b, y0.x, as, y1.x),
-                qy = lerp_rn(b, y0.y, as, y1.y), qz = lerp_rn(b, y0.z, as, y1.z);
+    const s1r d = dot4_rn(x0.w, y0.x, y0.y, y0.z, x1.w, y1.x, y1.y, y1.z);
+    const s1r as = d < (s1r)0 ? -a : a;
+    const s1r qw = lerp_rn(b, x0.w, as, x1.w), qx = lerp_rn(b, y0.x, as, y1.x),
+              qy = lerp_rn(b, y0.y, as, y1.y), qz = lerp_rn(b, y0.z, as, y1.z);
     if (NORM) {
-        const float inv = rsqrt_fast(dot4_rn(qw, qx, qy, qz, qw, qx, qy, qz));
-        trs[3] = __fmul_rn(qw, inv); trs[4] = __fmul_rn(qx, inv); trs[5] = __fmul_rn(qy, inv);
-        trs[6] = __fmul_rn(qz, inv);
+        const s1r inv = rsqrt_rn(dot4_rn(qw, qx, qy, qz, qw, qx, qy, qz));
+        trs[3] = mul_rn(qw, inv); trs[4] = mul_rn(qx, inv); trs[5] = mul_rn(qy, inv);
+        trs[6] = mul_rn(qz, inv);
     } else {
         trs[3] = qw; trs[4] = qx; trs[5] = qy; trs[6] = qz;
     }
@@ -276,21 +346,21 @@ __device__ __forceinline__ void sample_trs(float4 x0, float4 y0, float2 z0, floa
 // ulps however far |q| is from 1 after fp32 interpolation and blending; the unit
 // formula on a quaternion of norm^2 = 1 + d gives R' = (1 + d) R + (-d) I, an O(d)
 // non-rigid error that compounds down the root path (Stage-1 budget).
-__device__ __forceinline__ void trs_to_m34(const float* trs, float* m) {
-    const float w = trs[3], x = trs[4], y = trs[5], z = trs[6];
-    const float sx = trs[7], sy = trs[8], sz = trs[9];
-    const float c = __fmul_rn(2.0f, rcp_fast(dot4_rn(w, x, y, z, w, x, y, z)));
+__device__ __forceinline__ void trs_to_m34(const s1r* trs, float* m) {
+    const s1r w = trs[3], x = trs[4], y = trs[5], z = trs[6];
+    const s1r sx = trs[7], sy = trs[8], sz = trs[9];
+    const s1r c = mul_rn((s1r)2, rcp_rn(dot4_rn(w, x, y, z, w, x, y, z)));
     // 1 - c (u^2 + v^2) and c (u v -/+ w t), each rounded in one fixed order
-    auto diag = [c](float u, float v) { return fmaf(-c, fmaf(u, u, __fmul_rn(v, v)), 1.0f); };
-    auto offd = [c](float u, float v, float p, float q, float sgn) {
-        return __fmul_rn(c, fmaf(sgn * p, q, __fmul_rn(u, v)));
+    auto diag = [c](s1r u, s1r v) { return fma_rn(-c, fma_rn(u, u, mul_rn(v, v)), (s1r)1); };
+    auto offd = [c](s1r u, s1r v, s1r p, s1r q, s1r sgn) {
+        return mul_rn(c, fma_rn(sgn * p, q, mul_rn(u, v)));
     };
-    m[0] = __fmul_rn(diag(y, z), sx);               m[1] = __fmul_rn(offd(x, y, w, z, -1.0f), sy);
-    m[2] = __fmul_rn(offd(x, z, w, y, 1.0f), sz);   m[3] = trs[0];
-    m[4] = __fmul_rn(offd(x, y, w, z, 1.0f), sx);   m[5] = __fmul_rn(diag(x, z), sy);
-    m[6] = __fmul_rn(offd(y, z, w, x, -1.0f), sz);  m[7] = trs[1];
-    m[8] = __fmul_rn(offd(x, z, w, y, -1.0f), sx);  m[9] = __fmul_rn(offd(y, z, w, x, 1.0f), sy);
-    m[10] = __fmul_rn(diag(x, y), sz);              m[11] = trs[2];
+    m[0] = (float)mul_rn(diag(y, z), sx);                  m[1] = (float)mul_rn(offd(x, y, w, z, -1), sy);
+    m[2] = (float)mul_rn(offd(x, z, w, y, 1), sz);         m[3] = (float)trs[0];
+    m[4] = (float)mul_rn(offd(x, y, w, z, 1), sx);         m[5] = (float)mul_rn(diag(x, z), sy);
+    m[6] = (float)mul_rn(offd(y, z, w, x, -1), sz);        m[7] = (float)trs[1];
+    m[8] = (float)mul_rn(offd(x, z, w, y, -1), sx);        m[9] = (float)mul_rn(offd(y, z, w, x, 1), sy);
+    m[10] = (float)mul_rn(diag(x, y), sz);                 m[11] = (float)trs[2];
 }
 
 // Local poses of E tile elements at once (E independent (character, joint) pairs,
@@ -326,7 +396,7 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
                                              const int* j, const bool* valid, int nl_rt, int Jp, float* L,
                                              const int* off) {
     const int nl = NLT > 0 ? NLT : nl_rt;
-    float acc[E][10], q0[E][4], wsum[E];
+    s1r acc[E][10], q0[E][4], wsum[E];
     KeyPair kp[E];
     int4 d[E];
     constexpr int kPre = NLT > 0 ? NLT : 1;
@@ -370,14 +440,14 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            float s[10];
+            s1r s[10];
             if (nl == 1)
                 sample_trs<false>(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
                                   __int_as_float(dc[e].z), s);
             else
                 sample_trs<true>(cur[e].x0, cur[e].y0, cur[e].z0, cur[e].x1, cur[e].y1, cur[e].z1,
                                  __int_as_float(dc[e].z), s);
-            const float w = __int_as_float(dc[e].w);
+            const s1r w = __int_as_float(dc[e].w);
             if (nl == 1) {   // one layer: the sample itself (R22)
 #pragma unroll
                 for (int c = 0; c < 10; ++c) acc[e][c] = s[c];
@@ -385,18 +455,18 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
 #pragma unroll
                 for (int c = 0; c < 4; ++c) q0[e][c] = s[3 + c];
 #pragma unroll
-                for (int c = 0; c < 10; ++c) acc[e][c] = __fmul_rn(w, s[c]);
+                for (int c = 0; c < 10; ++c) acc[e][c] = mul_rn(w, s[c]);
                 wsum[e] = w;
             } else {
-                const float dq = dot4_rn(s[3], s[4], s[5], s[6], q0[e][0], q0[e][1], q0[e][2], q0[e][3]);
-                const float ws = dq < 0.0f ? -w : w;
+                const s1r dq = dot4_rn(s[3], s[4], s[5], s[6], q0[e][0], q0[e][1], q0[e][2], q0[e][3]);
+                const s1r ws = dq < (s1r)0 ? -w : w;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) acc[e][c] = fmaf(w, s[c], acc[e][c]);
+                for (int c = 0; c < 3; ++c) acc[e][c] = fma_rn(w, s[c], acc[e][c]);
 #pragma unroll
-                for (int c = 3; c < 7; ++c) acc[e][c] = fmaf(ws, s[c], acc[e][c]);
+                for (int c = 3; c < 7; ++c) acc[e][c] = fma_rn(ws, s[c], acc[e][c]);
 #pragma unroll
-                for (int c = 7; c < 10; ++c) acc[e][c] = fmaf(w, s[c], acc[e][c]);
-                wsum[e] = __fadd_rn(wsum[e], w);
+                for (int c = 7; c < 10; ++c) acc[e][c] = fma_rn(w, s[c], acc[e][c]);
+                wsum[e] = add_rn(wsum[e], w);
             }
         }
     }
@@ -404,11 +474,11 @@ __device__ __forceinline__ void stage1_elems(const float* __restrict__ keys, con
     for (int e = 0; e < E; ++e) {
         if (!valid[e]) continue;
         if (nl > 1) {
-            const float iw = rcp_fast(wsum[e]);
+            const s1r iw = rcp_rn(wsum[e]);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
+            for (int c = 0; c < 3; ++c) acc[e][c] = mul_rn(acc[e][c], iw);
 #pragma unroll
-            for (int c = 7; c < 10; ++c) acc[e][c] = __fmul_rn(acc[e][c], iw);
+            for (int c = 7; c < 10; ++c) acc[e][c] = mul_rn(acc[e][c], iw);
             // the blended quaternion is normalised by trs_to_m34 (c = 2 / |q|^2)
         }
         float m[12];

@@ -87,11 +87,12 @@ struct SeqArgs {
     const int2* imp;           // (workspace slot, P location)
     const int4* runs;          // (user start, smem offset, length, 0)
     int64_t n_chars;
-    int32_t J, KT, F, T, S, n_exp, r2max, max_imp, max_entries;
-    int32_t p_floats;          // (2S + nQ) * 12
+    int32_t J, KT, F, T, S, nQ, n_exp, r2max, max_imp, max_entries;
+    int32_t p_floats;          // (2S + 2 nQ) * 12: anchors (ping-pong) and two Q buffers
     int32_t stages, sbufs, threads, has_runs, bulk_piece;
     int64_t smem_bytes;
     int32_t ctas_per_sm;       // 0 = occupancy maximum (1)
+    unsigned long long* prof;  // profiling builds: per-phase clock64 sums of consumer thread 0 (or nullptr)
 };
 cudaError_t launch_seq(int K, const SeqArgs& a, cudaStream_t st);
 cudaError_t prepare_seq(int K);

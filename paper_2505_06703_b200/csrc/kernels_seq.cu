@@ -40,17 +40,19 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     const int NS = a.stages, NSS = a.sbufs;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* done = full + 4;
-    uint64_t* sfree = done + 4;
+    uint64_t* ibfull = done + 4;   // S buffer holds the tile's inverse binds (TMA), S computed in place
     const int tile_f = a.F * 12;
     float* LG = reinterpret_cast<float*>(smem + 128);
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
     const int TK = a.T * K;
+    const int IMPW = (a.max_imp + 1) & ~1;                                  // import-list slots (even)
+    const int TABW = ((a.r2max + 1 + 3) & ~3) + ((a.max_entries + 3) & ~3); // one table buffer (ints)
     uint64_t* s_meta = reinterpret_cast<uint64_t*>(P + a.p_floats);        // [2][T][K]
     int32_t* s_p1 = reinterpret_cast<int32_t*>(s_meta + 2 * TK);           // [2][T]
-    int2* s_imp = reinterpret_cast<int2*>(s_p1 + 2 * a.T);                 // [2][max_imp]
-    int32_t* s_round_off = reinterpret_cast<int32_t*>(s_imp + 2 * a.max_imp);
-    uint32_t* s_rounds = reinterpret_cast<uint32_t*>(s_round_off + ((a.r2max + 1 + 3) & ~3));
+    int2* s_imp = reinterpret_cast<int2*>(s_p1 + 2 * a.T);                 // [2][IMPW]
+    int32_t* s_tab = reinterpret_cast<int32_t*>(s_imp + 2 * IMPW);         // [2][round_off | rounds]
+    SeqTileDev* s_tiles = reinterpret_cast<SeqTileDev*>(s_tab + 2 * TABW); // [KT]
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
@@ -60,9 +62,11 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     const int64_t my_chars = blockIdx.x < a.n_chars ? (a.n_chars - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int64_t my_tiles = my_chars * KT;
 
+    for (int i = threadIdx.x; i < KT * (int)(sizeof(SeqTileDev) / 4); i += blockDim.x)
+        reinterpret_cast<int32_t*>(s_tiles)[i] = __ldg(reinterpret_cast<const int32_t*>(a.tiles) + i);
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
-        for (int s = 0; s < NSS; ++s) mbar_init(&sfree[s], 1);
+        for (int s = 0; s < NSS; ++s) mbar_init(&ibfull[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -71,11 +75,12 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         // ------------------------------------------------------------ producer
         if ((threadIdx.x & 31) != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
+        const uint64_t stream_pol = policy_evict_first(), keep_pol = policy_evict_last();
         // tile cursors (character, tile) for the loads (NS ahead) and the stores
         int64_t lc = blockIdx.x, sc = blockIdx.x;
         int lk = 0, sk = 0;
         auto issue_load = [&](int stage) {
-            const SeqTileDev tl = a.tiles[lk];
+            const SeqTileDev tl = s_tiles[lk];
             mbar_expect_tx(&full[stage], (uint32_t)tl.nj * 48u);
             const char* base = reinterpret_cast<const char*>(a.local + lc * J * 12);
             char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
@@ -85,17 +90,33 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 HS_BOUND(run.y >= 0 && run.y + run.z <= tl.nj && run.x >= 0 && run.x + run.z <= J);
                 const char* s0 = base + (int64_t)run.x * 48;
                 char* d0 = dst + run.y * 48;
-                for (uint32_t o = 0; o < bytes; o += piece) bulk_g2s(d0 + o, s0 + o, min(piece, bytes - o), &full[stage]);
+                for (uint32_t o = 0; o < bytes; o += piece)
+                    bulk_g2s_hint(d0 + o, s0 + o, min(piece, bytes - o), &full[stage], stream_pol);
             }
             if (++lk == KT) { lk = 0; lc += gridDim.x; }
         };
         for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load((int)it);
+        const bool do_skin = a.sout != nullptr;
+        // inverse binds of a tile, by smem offset, into its S buffer (phase 3 computes
+        // S = G (x) IB in place: each slot is read and then written by one thread)
+        int ibk = 0;
+        auto issue_ib = [&](int buf) {
+            const SeqTileDev tl = s_tiles[ibk];
+            const uint32_t bytes = (uint32_t)tl.nj * 48u;
+            mbar_expect_tx(&ibfull[buf], bytes);
+            const char* src = reinterpret_cast<const char*>(a.ib + (int64_t)ibk * a.F * 12);
+            char* dst = reinterpret_cast<char*>(SB + buf * tile_f);
+            for (uint32_t o = 0; o < bytes; o += piece)
+                bulk_g2s_hint(dst + o, src + o, min(piece, bytes - o), &ibfull[buf], keep_pol);
+            if (++ibk == KT) ibk = 0;
+        };
+        if (do_skin)
+            for (int64_t it = 0; it < my_tiles && it < NSS; ++it) issue_ib((int)it);
         int stage = 0, sb = 0;
         uint32_t phase = 0;
-        const bool do_skin = a.sout != nullptr;
         for (int64_t it = 0; it < my_tiles; ++it) {
             mbar_wait(&done[stage], phase);
-            const SeqTileDev tl = a.tiles[sk];
+            const SeqTileDev tl = s_tiles[sk];
             const int64_t cbase = sc * J * 12;
             const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
             const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
@@ -106,13 +127,13 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 char* sp = do_skin ? reinterpret_cast<char*>(a.sout + cbase) + (int64_t)run.x * 48 : nullptr;
                 for (uint32_t o = 0; o < bytes; o += piece) {
                     const uint32_t nb = min(piece, bytes - o);
-                    bulk_s2g(gp + o, sg + run.y * 48 + o, nb);
-                    if (do_skin) bulk_s2g(sp + o, ss + run.y * 48 + o, nb);
+                    bulk_s2g_hint(gp + o, sg + run.y * 48 + o, nb, stream_pol);
+                    if (do_skin) bulk_s2g_hint(sp + o, ss + run.y * 48 + o, nb, stream_pol);
                 }
             }
             bulk_commit();
             bulk_wait_read<0>();
-            mbar_arrive(&sfree[sb]);
+            if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
             if (it + NS < my_tiles) issue_load(stage);
             if (++sk == KT) { sk = 0; sc += gridDim.x; }
             if (++stage == NS) { stage = 0; phase ^= 1u; }
@@ -123,42 +144,63 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     }
 
     // ---------------------------------------------------------------- consumers
+    // Everything a tile needs is requested one tile ahead with cp.async and awaited at
+    // the top of the tile: its program (chunk metadata, phase-1 info; ring by tile
+    // counter parity), its phase-2 tables (ring), and its Q values: parents from tiles
+    // <= k - 2 are imported from the workspace (L2) at the top of tile k - 1 (the lists
+    // are prefetched two tiles ahead), parents from tile k - 1 are forwarded into Q by
+    // the threads that compute them in phase 3 of tile k - 1.  Q buffers alternate with
+    // the tile index k (the plan bakes the locations in).
     const int t = threadIdx.x;
     float* wsb = a.ws + (int64_t)blockIdx.x * a.n_exp * 12;   // this CTA's workspace
     const bool skin = a.sout != nullptr;
-    // per-tile program prefetch into buffer pb: chunk metadata row, phase-1 info and the
-    // import list (each thread copies what it reads itself, so no barrier is needed)
-    auto prefetch_prog = [&](int k, int pb) {
+    const uint64_t ws_pol = policy_evict_last();   // the workspace is re-read by later tiles
+    auto prefetch_prog = [&](int k, int buf) {      // meta row + phase-1 info of tile k
         if (t < a.T) {
 #pragma unroll
             for (int s = 0; s < K; ++s)
-                cp_async8(s_meta + pb * TK + t * K + s, a.meta + ((int64_t)k * a.T + t) * K + s);
-            cp_async4(s_p1 + pb * a.T + t, a.p1len + (int64_t)k * a.T + t);
+                cp_async8(s_meta + buf * TK + t * K + s, a.meta + ((int64_t)k * a.T + t) * K + s);
+            cp_async4(s_p1 + buf * a.T + t, a.p1len + (int64_t)k * a.T + t);
         }
-        const int ni = a.tiles[k].n_imp, io = a.tiles[k].imp_off;
-        for (int i = t; i < ni; i += NC) cp_async8(s_imp + pb * a.max_imp + i, a.imp + io + i);
-        cp_async_commit();
     };
-    // phase-2 tables of tile k (read by every thread: awaited before the phase-2 barrier)
-    auto prefetch_tables = [&](int k) {
-        const SeqTileDev tl = a.tiles[k];
-        for (int i = t; i <= a.r2max; i += NC) cp_async4(s_round_off + i, a.round_off + (int64_t)k * (a.r2max + 1) + i);
-        for (int i = t; i < tl.n_entries; i += NC) cp_async4(s_rounds + i, a.rounds + tl.rounds_off + i);
-        cp_async_commit();
+    auto prefetch_list = [&](int k, int buf) {      // tile k's workspace imports
+        const int ni = s_tiles[k].n_imp, io = s_tiles[k].imp_off;
+        for (int i = t; i < ni; i += NC) cp_async8(s_imp + buf * IMPW + i, a.imp + io + i);
+    };
+    auto prefetch_tables = [&](int k, int buf) {    // phase-2 tables of tile k
+        int32_t* ro = s_tab + buf * TABW;
+        uint32_t* rd = reinterpret_cast<uint32_t*>(ro + ((a.r2max + 1 + 3) & ~3));
+        const int ne = s_tiles[k].n_entries, eo = s_tiles[k].rounds_off;
+        for (int i = t; i <= a.r2max; i += NC) cp_async4(ro + i, a.round_off + (int64_t)k * (a.r2max + 1) + i);
+        for (int i = t; i < ne; i += NC) cp_async4(rd + i, a.rounds + eo + i);
     };
     if (my_tiles > 0) {
         prefetch_prog(0, 0);
-        prefetch_tables(0);
+        prefetch_tables(0, 0);
+        if (my_tiles > 1) prefetch_list(1 % KT, 1);
+        cp_async_commit();
     }
+    const int qb0 = 2 * a.S, nQ = a.nQ;
 
+    // profiling builds (HS_PROF_HOOKS): consumer thread 0's cycles per phase, summed
+    long long prof_last = 0;
+    auto prof_mark = [&](int slot) {
+        if (HS_PROF_HOOKS && a.prof && t == 0) {
+            const long long now = clock64();
+            if (slot >= 0) atomicAdd(a.prof + slot, (unsigned long long)(now - prof_last));
+            prof_last = now;
+        }
+    };
     uint64_t m[K];
-    float ibr[K][12];
     int stage = 0, sb = 0, pb = 0, k = 0;
     uint32_t phase = 0, sphase = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
-        const SeqTileDev tl = a.tiles[k];
+        const SeqTileDev tl = s_tiles[k];
+        const int kn = k + 1 < KT ? k + 1 : 0, kn2 = kn + 1 < KT ? kn + 1 : 0;
         float* L = LG + stage * tile_f;
-        cp_async_wait_all();   // this tile's program (and tables: barrier before phase 2)
+        prof_mark(-1);
+        cp_async_wait_all();   // requested during the previous tile (tables, Q: the phase-2 barrier)
+        prof_mark(0);
         int p1, run_back, run_anchor;
         {
             const int info = t < a.T ? s_p1[pb * a.T + t] : 0;
@@ -167,34 +209,28 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             run_anchor = (int)((uint32_t)info >> 16) - 1;
         }
 #pragma unroll
-        for (int s = 0; s < K; ++s)
-            m[s] = t < a.T ? s_meta[pb * TK + t * K + s]
-                           : ((uint64_t)(uint16_t)(int16_t)kSrcNone << 32) | (0xffffull << 48);
-        // imports: external parents' final poses, workspace (L2) -> Q locations
-        for (int i = t; i < tl.n_imp; i += NC) {
-            const int2 e = s_imp[pb * a.max_imp + i];
-            HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= 0 && (e.y + 1) * 12 <= a.p_floats);
-            const float* src = wsb + (int64_t)e.x * 12;
-            float* dst = P + e.y * 12;
-            cp_async16_cg(dst, src);
-            cp_async16_cg(dst + 4, src + 4);
-            cp_async16_cg(dst + 8, src + 8);
-        }
-        cp_async_commit();
-        if (it + 1 < my_tiles) prefetch_prog(k + 1 < KT ? k + 1 : 0, pb ^ 1);
-        // inverse bind of this tile's slots (first used in phase 3)
-        if (skin) {
-#pragma unroll
-            for (int s = 0; s < K; ++s) {
-                const int src = (int)(int16_t)(m[s] >> 32);
-                const int off = (int)(m[s] & 0xffff);
-                if (src != kSrcNone) {
-                    HS_BOUND(off >= 0 && off < a.F);
-                    ldg3(a.ib + ((int64_t)k * a.F + off) * 12, ibr[s]);
-                }
+        for (int s = 0; s < K; ++s) m[s] = t < a.T ? s_meta[pb * TK + t * K + s] : kSeqMetaNone;
+        if (it + 1 < my_tiles) {
+            // the next tile's workspace imports into its Q buffer (its parents in tiles
+            // <= k - 1 are final: their exports preceded this tile's start)
+            const int ni = s_tiles[kn].n_imp;
+            for (int i = t; i < ni; i += NC) {
+                const int2 e = s_imp[(pb ^ 1) * IMPW + i];
+                HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= qb0 && (e.y + 1) * 12 <= a.p_floats);
+                const float* src = wsb + (int64_t)e.x * 12;
+                float* dst = P + e.y * 12;
+                cp_async16_cg_hint(dst, src, ws_pol);
+                cp_async16_cg_hint(dst + 4, src + 4, ws_pol);
+                cp_async16_cg_hint(dst + 8, src + 8, ws_pol);
             }
+            prefetch_prog(kn, pb ^ 1);
+            prefetch_tables(kn, pb ^ 1);
+            if (it + 2 < my_tiles) prefetch_list(kn2, pb);
+            cp_async_commit();
         }
+        prof_mark(1);
         mbar_wait(&full[stage], phase);
+        prof_mark(2);
 
         // phase 1: in-chunk fold, publish anchors
         float acc[12];
@@ -202,9 +238,9 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
 #pragma unroll
             for (int s = 0; s < K; ++s) {
                 if (s < p1) {
-                    const int off = (int)(m[s] & 0xffff);
-                    const int src = (int)(int16_t)(m[s] >> 32);
-                    const int own = (int)(int16_t)(m[s] >> 48);
+                    const int off = seq_off(m[s]);
+                    const int src = seq_src(m[s]);
+                    const int own = seq_own(m[s]);
                     float l[12];
                     HS_BOUND(off >= 0 && off < tl.nj);
                     ld3(L + off * 12, l);
@@ -242,7 +278,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             if (run_back > 0) {
 #pragma unroll
                 for (int s = 0; s < K; ++s) {
-                    const int own = (int)(int16_t)(m[s] >> 48);
+                    const int own = seq_own(m[s]);
                     if (own >= 0) {
                         float x[12], y[12];
                         ld3(P + own * 12, x);
@@ -252,10 +288,13 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 }
             }
         }
-        cp_async_wait_all();   // imports (and the next tile's program) have landed
-        bar_consumers(NC);
+        prof_mark(3);
+        bar_consumers(NC);   // anchors published; this tile's Q and tables visible to all
+        prof_mark(4);
 
         // phase 2: pointer jumping over the anchor forest (ping-pong P; Q roots final)
+        const int32_t* s_round_off = s_tab + pb * TABW;
+        const uint32_t* s_rounds = reinterpret_cast<const uint32_t*>(s_round_off + ((a.r2max + 1 + 3) & ~3));
         for (int r = 0; r < tl.R2; ++r) {
             const int eb = s_round_off[r], e1 = s_round_off[r + 1];
             for (int e = eb + t; e < e1; e += NC) {
@@ -272,20 +311,20 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             }
             bar_consumers(NC);
         }
-        // the next tile's phase-2 tables (this tile's have been read: barrier above)
-        if (it + 1 < my_tiles) prefetch_tables(k + 1 < KT ? k + 1 : 0);
 
         // phase 3: final fold, G in place, S into the S buffer, exports to the workspace
         float* S = SB + sb * tile_f;
-        if (skin && it >= NSS) mbar_wait(&sfree[sb], sphase);
+        prof_mark(5);
+        if (skin) mbar_wait(&ibfull[sb], sphase);   // this tile's inverse binds are in S
+        prof_mark(6);
         {
             float acc3[12];
 #pragma unroll
             for (int s = 0; s < K; ++s) {
-                const int src = (int)(int16_t)(m[s] >> 32);
+                const int src = seq_src(m[s]);
                 if (src == kSrcNone) continue;
-                const int off = (int)(m[s] & 0xffff);
-                const int ex = (int)((m[s] >> 16) & 0xffff);
+                const int off = seq_off(m[s]);
+                const int ex = seq_ex(m[s]), fw = seq_fwd(m[s]);
                 float l[12];
                 HS_BOUND(off >= 0 && off < tl.nj);
                 ld3(L + off * 12, l);
@@ -327,22 +366,30 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                     compose(pa, l, acc3);
                 }
                 st3(L + off * 12, acc3);
-                if (ex) {   // a child in a later tile: export the global pose (L2)
+                if (ex) {   // a child in tile k + 2 or later: export the global pose (L2)
                     HS_BOUND(ex - 1 < a.n_exp);
-                    st3(wsb + (int64_t)(ex - 1) * 12, acc3);
+                    st3_hint(wsb + (int64_t)(ex - 1) * 12, acc3, ws_pol);
+                }
+                if (fw) {   // a child in tile k + 1: forward into that tile's Q buffer
+                    HS_BOUND(fw - 1 < nQ);
+                    st3(P + (qb0 + ((k + 1) & 1) * nQ + fw - 1) * 12, acc3);
                 }
                 if (skin) {
-                    float sk[12];
-                    compose(acc3, ibr[s], sk);
+                    float sk[12], ibv[12];
+                    ld3(S + off * 12, ibv);
+                    compose(acc3, ibv, sk);
                     st3(S + off * 12, sk);
                 }
             }
         }
+        prof_mark(7);
         fence_proxy_async();
         bar_consumers(NC);
+        prof_mark(8);
+        if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 9, 1ull);
         if (t == 0) mbar_arrive(&done[stage]);
         if (++stage == NS) { stage = 0; phase ^= 1u; }
-        if (++sb == NSS) { sb = 0; if (it + 1 >= 2 * NSS) sphase ^= 1u; }
+        if (++sb == NSS) { sb = 0; sphase ^= 1u; }   // parity of use it / NSS of buffer sb
         pb ^= 1;
         if (++k == KT) k = 0;
     }

@@ -630,11 +630,15 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     // tiles in order; each tile is one chunk/anchor program (build_tile_program with
     // C = 1) over its sub-forest, where
     //   * a joint whose parent is in an earlier tile ("external parent") starts a
-    //     segment like a root, but its source is the parent's final global pose,
-    //     imported before the tile into a Q location (Q nodes are final roots of the
-    //     anchor forest: pointer jumping links to them and stops);
-    //   * a joint with a child in a later tile is EXPORTED: phase 3 stores its global
-    //     pose to workspace slot exp (one slot per exported joint of the skeleton).
+    //     segment like a root, but its source is the parent's final global pose in a
+    //     Q location (Q nodes are final roots of the anchor forest: pointer jumping
+    //     links to them and stops);
+    //   * the Q values of tile j are delivered one tile ahead: a parent in tile j - 1 is
+    //     FORWARDED by the thread that computes it in phase 3 of tile j - 1 (a shared-
+    //     memory store into tile j's Q buffer); a parent in tile <= j - 2 was stored to
+    //     a workspace slot in its own tile's phase 3 and is IMPORTED by cp.async at the
+    //     start of tile j - 1.  Two Q buffers alternate with the tile index.
+    //   * workspace slots are reused once their last import has been issued.
     sp = SeqProgram();
     const int32_t n = p.n;
     if (F < 32 || n <= 0) return false;
@@ -642,21 +646,18 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     sp.F = F;
     sp.KT = (n + F - 1) / F;
     const int KT = sp.KT;
-    // exported joints: a child in a later tile
-    std::vector<int32_t> exp_slot(n, -1);
-    {
-        std::vector<int32_t> last(n, -1);
-        for (int32_t i = 0; i < n; ++i)
-            if (p.ipar[i] >= 0) last[p.ipar[i]] = std::max(last[p.ipar[i]], i / F);
-        for (int32_t i = 0; i < n; ++i)
-            if (last[i] > i / F) exp_slot[i] = sp.n_exp++;
+    // consumers: for every joint, the tiles (after its own) holding a child
+    std::vector<int32_t> last_ws_use(n, -1);   // last consumer tile >= own + 2 (-1: none)
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t q = p.ipar[i];
+        if (q < 0) continue;
+        const int32_t tq = q / F, ti = i / F;
+        if (ti >= tq + 2) last_ws_use[q] = std::max(last_ws_use[q], ti);
     }
-    if (sp.n_exp >= 0xffff) return false;   // 16-bit exp field (slot + 1)
     struct TileTmp {
         ChunkDecomp d;
-        std::vector<int32_t> ext;          // per local node: external parent (internal) or -1
-        std::vector<int32_t> q_of;         // per local node with ext: import index
-        std::vector<int32_t> imports;      // import index -> external parent
+        std::vector<int32_t> q_of;         // per local node with an external parent: Q index
+        std::vector<int32_t> imports;      // Q index -> external parent (internal position)
         std::vector<int32_t> idx;          // raw slot -> coloured slot
         int S = 0;
     };
@@ -665,20 +666,15 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         TileTmp& tt = tmp[k];
         const int32_t a = k * F, nj = std::min(F, n - a);
         std::vector<int32_t> lpar(nj), pos(nj);
-        tt.ext.assign(nj, -1);
         tt.q_of.assign(nj, -1);
-        std::vector<int32_t> qmap;   // external parent -> import index (linear search: few per tile)
+        std::vector<int32_t> qmap(a, -1);   // external parent -> Q index
         for (int32_t li = 0; li < nj; ++li) {
             const int32_t q = p.ipar[a + li];
             pos[li] = li;
             lpar[li] = q >= a ? q - a : -1;
             if (q >= 0 && q < a) {
-                tt.ext[li] = q;
-                int32_t qi = -1;
-                for (size_t z = 0; z < tt.imports.size(); ++z)
-                    if (tt.imports[z] == q) { qi = (int32_t)z; break; }
-                if (qi < 0) { qi = (int32_t)tt.imports.size(); tt.imports.push_back(q); }
-                tt.q_of[li] = qi;
+                if (qmap[q] < 0) { qmap[q] = (int32_t)tt.imports.size(); tt.imports.push_back(q); }
+                tt.q_of[li] = qmap[q];
             }
         }
         tt.d = decompose(lpar, K, mode, &pos, true);
@@ -709,11 +705,40 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
             for (int32_t t = 0; t < T; ++t)
                 if (d.run_back[t] > 0) sp.has_runs = true;
     }
-    const int32_t S = sp.S, qbase = 2 * S;
-    if (S >= (1 << 14) || qbase + sp.nQ >= (1 << 15)) return false;   // descriptor / src field widths
-    // empty slots: src NONE, own -1 (phase 2a lifts every slot with own >= 0)
-    sp.meta.assign((size_t)KT * sp.T * K,
-                   ((uint64_t)(uint16_t)(int16_t)SRC_NONE << 32) | ((uint64_t)(uint16_t)(int16_t)-1 << 48));
+    const int32_t S = sp.S, nQ = sp.nQ;
+    auto qloc = [&](int k, int32_t z) { return 2 * S + (k & 1) * nQ + z; };
+    if (S >= (1 << 12) || 2 * S + 2 * nQ >= (1 << 12) - 8 || F > 1024) return false;   // meta field widths
+    // workspace slots: joint q (tile tq) needs one iff a child sits in a tile >= tq + 2;
+    // the slot is free again for exports of tiles >= its last consumer (whose import
+    // was issued at the start of the tile before, and awaited at the start of that tile)
+    std::vector<int32_t> ws_slot(n, -1);
+    {
+        std::vector<std::pair<int32_t, int32_t>> busy;   // (free from tile, slot)
+        std::vector<int32_t> freel;
+        for (int k = 0; k < KT; ++k) {
+            for (size_t b = 0; b < busy.size();)
+                if (busy[b].first <= k) { freel.push_back(busy[b].second); busy[b] = busy.back(); busy.pop_back(); }
+                else ++b;
+            std::sort(freel.begin(), freel.end(), std::greater<int32_t>());
+            const int32_t a = k * F, nj = std::min(F, n - a);
+            for (int32_t li = 0; li < nj; ++li) {
+                const int32_t i = a + li;
+                if (last_ws_use[i] < 0) continue;
+                int32_t sl;
+                if (!freel.empty()) { sl = freel.back(); freel.pop_back(); }
+                else sl = sp.n_exp++;
+                ws_slot[i] = sl;
+                busy.push_back({last_ws_use[i], sl});
+            }
+        }
+    }
+    if (sp.n_exp >= (1 << 16) - 1) return false;
+    // encoded meta (seq_meta_* in kernels.cuh): off 10 | src + 8 13 | own + 1 13 | ex 16 | fwd 12
+    auto enc = [](int32_t off, int32_t src, int32_t own, int32_t ex, int32_t fwd) {
+        return (uint64_t)off | ((uint64_t)(src + 8) << 10) | ((uint64_t)(own + 1) << 23) | ((uint64_t)ex << 36) |
+               ((uint64_t)fwd << 52);
+    };
+    sp.meta.assign((size_t)KT * sp.T * K, enc(0, SRC_NONE, -1, 0, 0));
     sp.p1len.assign((size_t)KT * sp.T, 0);
     sp.ib_user.assign((size_t)KT * F, -1);
     std::vector<std::vector<int32_t>> roff(KT);
@@ -724,6 +749,13 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         const int32_t T = (int32_t)d.lists.size();
         const int32_t Sraw = (int32_t)d.slots.size();
         const int32_t nq = (int32_t)tt.imports.size();
+        // the next tile's Q index of each of this tile's joints it imports (forwarding)
+        std::vector<int32_t> fwd_of(nj, -1);
+        if (k + 1 < KT)
+            for (size_t z = 0; z < tmp[k + 1].imports.size(); ++z) {
+                const int32_t q = tmp[k + 1].imports[z];
+                if (q >= a) fwd_of[q - a] = (int32_t)z;
+            }
         SeqTile st{};
         st.first = a;
         st.nj = nj;
@@ -735,7 +767,7 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
             if (d.link0[s] >= 0) lk[s] = d.link0[s];
             else if (tt.q_of[h] >= 0) lk[s] = Sraw + tt.q_of[h];
         }
-        auto loc = [&](int32_t x) { return x < Sraw ? latest[x] * S + tt.idx[x] : qbase + (x - Sraw); };
+        auto loc = [&](int32_t x) { return x < Sraw ? latest[x] * S + tt.idx[x] : qloc(k, x - Sraw); };
         st.rounds_off = (int32_t)sp.rounds.size();
         roff[k].push_back(0);
         for (int r = 0;; ++r) {
@@ -772,7 +804,7 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
                 const int32_t h = d.head[d.lists[t][0]];
                 int32_t l = -1;
                 if (d.src[h] >= 0) l = loc(d.slot_of[d.src[h]]);
-                else if (tt.q_of[h] >= 0) l = qbase + tt.q_of[h];
+                else if (tt.q_of[h] >= 0) l = qloc(k, tt.q_of[h]);
                 info = (d.run_back[t] << 8) | ((l + 1) << 16);
             }
             int32_t& p1 = sp.p1len[(size_t)k * sp.T + t];
@@ -781,23 +813,25 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
                 const int32_t li = d.lists[t][s];
                 int32_t src;
                 if (d.src[li] >= 0) src = loc(d.slot_of[d.src[li]]);
-                else if (d.src[li] == SRC_ROOT && tt.q_of[li] >= 0) src = qbase + tt.q_of[li];
+                else if (d.src[li] == SRC_ROOT && tt.q_of[li] >= 0) src = qloc(k, tt.q_of[li]);
                 else src = d.src[li];
                 const int32_t own = d.slot_of[li] >= 0 ? tt.idx[d.slot_of[li]] : -1;
                 if (own >= 0 || in_run) p1 = s + 1;
-                const uint64_t ex = (uint64_t)(exp_slot[a + li] + 1);
-                sp.meta[((size_t)k * sp.T + t) * K + s] = (uint64_t)li | (ex << 16) |
-                                                          ((uint64_t)(uint16_t)(int16_t)src << 32) |
-                                                          ((uint64_t)(uint16_t)(int16_t)own << 48);
+                const int32_t ex = ws_slot[a + li] + 1;
+                const int32_t fw = fwd_of[li] + 1;
+                sp.meta[((size_t)k * sp.T + t) * K + s] = enc(li, src, own, ex, fw);
             }
             p1 |= info;
         }
-        // imports, TMA runs (maximal user-label runs over the tile's smem order), IB map
+        // imports from the workspace (parents in tiles <= k - 2; tile k - 1 forwards),
+        // TMA runs (maximal user-label runs over the tile's smem order), IB map
         st.imp_off = (int32_t)sp.imp.size() / 2;
-        st.n_imp = nq;
         for (int32_t z = 0; z < nq; ++z) {
-            sp.imp.push_back(exp_slot[tt.imports[z]]);
-            sp.imp.push_back(qbase + z);
+            const int32_t q = tt.imports[z];
+            if (q / F >= k - 1) continue;   // forwarded by the previous tile
+            sp.imp.push_back(ws_slot[q]);
+            sp.imp.push_back(qloc(k, z));
+            ++st.n_imp;
         }
         st.runs_off = (int32_t)sp.runs.size() / 4;
         for (int32_t li = 0; li < nj;) {
@@ -826,13 +860,13 @@ int64_t seq_max_tile_entries(const SeqProgram& sp) {
 }
 
 int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs) {
-    // barriers | stages x tile | sbufs x tile | P (2S anchors + nQ imports) | meta x2 |
-    // p1len x2 | imports x2 | round_off | rounds
+    // barriers | stages x tile | sbufs x tile | P (2S anchors + 2 x nQ Q buffers) |
+    // meta x2 | p1len x2 | import lists x2 | (round_off | rounds) x2 | tile descriptors
     const int64_t tileb = (int64_t)sp.F * 48;
-    int64_t b = 128 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + sp.nQ) * 48;
-    b += 2LL * sp.T * sp.K * 8 + 2LL * sp.T * 4 + 2LL * sp.max_imp * 8;
-    b += ((int64_t)(sp.R2max + 1) * 4 + 15) / 16 * 16;
-    b += (seq_max_tile_entries(sp) * 4 + 15) / 16 * 16;
+    int64_t b = 128 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + 2 * sp.nQ) * 48;
+    b += 2LL * sp.T * sp.K * 8 + 2LL * sp.T * 4 + 2LL * ((sp.max_imp + 1) / 2 * 2) * 8;
+    b += 2 * (((int64_t)(sp.R2max + 1) + 3) / 4 * 16 + (seq_max_tile_entries(sp) + 3) / 4 * 16);
+    b += (int64_t)sp.KT * (int64_t)sizeof(SeqTile);
     return b;
 }
 

@@ -96,12 +96,13 @@ struct SeqTile {
 struct SeqProgram {
     int K = 0, F = 0, T = 0, KT = 0;   // chunk, joints per tile (max), threads (max), tiles
     int S = 0;                          // anchor slots per buffer (uniform over tiles)
-    int nQ = 0;                         // import slots (max over tiles); Q locations 2S..2S+nQ
+    int nQ = 0;                         // Q slots per buffer (max imports of a tile); tile k's Q
+                                        // buffer is 2S + (k & 1) nQ .. + nQ
     int R2max = 0, max_entries = 0, max_imp = 0, max_runs = 0;
-    int n_exp = 0;                      // exported joints = workspace slots per character
+    int n_exp = 0;                      // workspace slots per character (reused once free)
     bool has_runs = false;
     std::vector<SeqTile> tiles;
-    std::vector<uint64_t> meta;         // [KT][T][K]: off | (exp slot + 1) << 16 | (u16)src << 32 | (u16)own << 48
+    std::vector<uint64_t> meta;         // [KT][T][K]: off 10 | src + 8 13 | own + 1 13 | ws slot + 1 16 | fwd + 1 12
     std::vector<int32_t> p1len;         // [KT][T] as TileProgram::p1len
     std::vector<int32_t> round_off;     // [KT][R2max + 1], relative to the tile's rounds_off
     std::vector<uint32_t> rounds;       // concatenated phase-2 descriptors (TileProgram encoding)

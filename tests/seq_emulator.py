@@ -2,10 +2,12 @@
 
 Replays the exported multi-tile program (``Plan.export("seq_*")``: the tables
 ``hs_skeleton_create`` uploads for HS_ALGO_TILES) for one character, tile by tile in
-the kernel's order, in fp64 on 4x4 homogeneous matrices: import of external parents
-from the workspace into Q locations, phase 1 chunk folds publishing anchors, phase 2a
-run scans, phase 2 pointer jumping (ping-pong locations as encoded, Q locations
-final), phase 3 re-folds with exports to the workspace and the bind epilogue.  On the
+the kernel's order, in fp64 on 4x4 homogeneous matrices: at the top of tile k the
+NEXT tile's workspace imports land in its Q buffer (so a reused workspace slot must not
+have been overwritten yet), then phase 1 chunk folds publishing anchors, phase 2a run
+scans, phase 2 pointer jumping (ping-pong locations as encoded, Q locations final),
+phase 3 re-folds with exports to the workspace, forwards into the next tile's Q buffer
+and the bind epilogue.  On the
 exact-arithmetic family every association order gives the same bits, so a bitwise
 match with the oracle pins the encoding (tiles, runs, imports, exports, locations).
 """
@@ -17,14 +19,10 @@ from tests.tile_emulator import SRC_NONE, SRC_PREV, SRC_ROOT, SRC_RUN, _h
 
 
 def decode(w):
+    """Slot word: off 10 | src + 8 13 | own + 1 13 | export slot + 1 16 | forward + 1 12."""
     w = int(w)
-    off = w & 0xFFFF
-    exp = (w >> 16) & 0xFFFF
-    src = (w >> 32) & 0xFFFF
-    own = (w >> 48) & 0xFFFF
-    src = src - 0x10000 if src >= 0x8000 else src
-    own = own - 0x10000 if own >= 0x8000 else own
-    return off, exp, src, own
+    return (w & 0x3FF, (w >> 36) & 0xFFFF, ((w >> 10) & 0x1FFF) - 8, ((w >> 23) & 0x1FFF) - 1,
+            (w >> 52) & 0xFFF)
 
 
 def run(plan, local, inv_bind=None):
@@ -38,6 +36,7 @@ def run(plan, local, inv_bind=None):
     runs = plan.export("seq_runs")
     ib_user = plan.export("seq_ib_user")
     S = plan.query("seq_slots")
+    nQ = plan.query("seq_qslots")
     KT, T, K = meta.shape
     J = local.shape[0]
     IB = np.asarray(inv_bind, np.float64) if inv_bind is not None else \
@@ -45,6 +44,7 @@ def run(plan, local, inv_bind=None):
     G = [None] * J
     SK = [None] * J
     ws = {}
+    P = {}
     covered = np.zeros(J, int)
     for k in range(KT):
         first, nj, R2, n_ent, r_off, n_imp, imp_off, n_runs, runs_off, Tk = tiles[k][:10]
@@ -60,11 +60,18 @@ def run(plan, local, inv_bind=None):
                 covered[u0 + z] += 1
         assert all(x is not None for x in Lt), "a smem slot of the tile is not loaded"
         assert list(ib_user[k][:nj]) == user_of
-        P = {}
-        for z in range(n_imp):
-            slot, loc = imp[imp_off + z]
-            assert loc >= 2 * S and slot in ws, "import of a value not exported before"
-            P[int(loc)] = ws[int(slot)]
+        for loc in [x for x in P if x < 2 * S]:
+            del P[loc]                                   # anchors are per tile; Q buffers persist
+        nb = 2 * S + ((k + 1) & 1) * nQ
+        for loc in [x for x in P if nb <= x < nb + nQ]:
+            del P[loc]                                   # the next tile's Q buffer starts empty
+        if k + 1 < KT:   # top of tile k: the next tile's workspace imports into its Q buffer
+            t1 = tiles[k + 1]
+            for z in range(t1[5]):
+                slot, loc = imp[t1[6] + z]
+                assert 2 * S + ((k + 1) & 1) * nQ <= loc < 2 * S + ((k + 1) & 1) * nQ + nQ
+                assert slot in ws, "import of a value not exported before"
+                P[int(loc)] = ws[int(slot)]
         dec = [[decode(meta[k, t, s]) for s in range(K)] for t in range(T)]
         info = [int(x) for x in p1len[k]]
         p1 = [x & 0xFF for x in info]
@@ -73,7 +80,7 @@ def run(plan, local, inv_bind=None):
         accs = [None] * T
         for t in range(T):      # phase 1
             for s in range(p1[t]):
-                off, ex, src, own = dec[t][s]
+                off, ex, src, own, fw = dec[t][s]
                 accs[t] = accs[t] @ Lt[off] if src == SRC_PREV else Lt[off].copy()
                 if own >= 0:
                     assert own < 2 * S
@@ -112,7 +119,7 @@ def run(plan, local, inv_bind=None):
         for t in range(T):      # phase 3
             acc = None
             for s in range(K):
-                off, ex, src, own = dec[t][s]
+                off, ex, src, own, fw = dec[t][s]
                 if src == SRC_NONE:
                     continue
                 if src == SRC_PREV:
@@ -129,5 +136,8 @@ def run(plan, local, inv_bind=None):
                 SK[u] = (acc @ _h(IB[u]))[:3]
                 if ex:
                     ws[ex - 1] = acc.copy()
+                if fw:
+                    assert k + 1 < KT and fw - 1 < nQ
+                    P[2 * S + ((k + 1) & 1) * nQ + fw - 1] = acc.copy()
     assert (covered == 1).all(), "every joint is loaded exactly once"
     return np.stack(G), np.stack(SK)

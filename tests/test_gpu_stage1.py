@@ -19,11 +19,12 @@ TOL = 1e-4
 
 
 def stage1_tol(L):
-    """End-to-end bound with Stage 1 in fp32: the north-star 1e-4 for the
-    scan on identical inputs, plus the fp32 rounding of each computed local pose
-    (~2^-23 relative on R and t) carried down the root path with a lever arm that grows
-    with depth: 4e-9 * L^2 (L = levels; |t| <= 1 per joint)."""
-    return max(TOL, 4e-9 * L * L)
+    """End-to-end bound with Stage 1: the north-star 1e-4 at every depth.
+    Stage 1 computes each local pose in fp64 and rounds it once to fp32 (the measured
+    budget, tests/test_gpu_stage1_budget.py: fp32 Stage-1 arithmetic put 4e-7 rotation
+    errors into every local pose, 1.5e-4 after 256 levels; correctly rounded locals carry
+    5e-6), so the scan's own bound applies unchanged."""
+    return TOL
 
 
 def levels(par):
@@ -75,7 +76,9 @@ def test_stage1_local_poses(n_layers):
     _, _, Lo = oracle.animate(par, keys, 16.0, 1, lay, return_local=True)
     e = float(np.abs(g - Lo).max())
     print(f"stage-1 locals, {n_layers} layers: max err {e:.2e}")
-    assert e <= 2e-6
+    # fp64 arithmetic rounded once: within half an fp32 ulp of the oracle's locals
+    # (|entries| <= 1.25: ulp 2^-23 at most), up to the fp64 rounding itself
+    assert e <= 2 ** -24 * 1.25 * (1 + 1e-9)
 
 
 def test_animate_key_times_bitwise_on_exact_keys():
@@ -104,7 +107,9 @@ def test_animate_scaled_shallow_skeleton():
     lay = hsgen.layers(12, 50, 3, 3, 0.7)
     g, s = run(par, keys, 10.0, 1, lay)
     G, S = oracle.animate(par, keys, 10.0, 1, lay)
-    assert float(np.abs(g - G).max()) <= stage1_tol(8) * 4   # scales up to 1.25 per level
+    e = max(float(np.abs(g - G).max()), float(np.abs(s - S).max()))
+    print(f"hum32 with scales 0.8-1.25: max err {e:.2e} (max |G| {np.abs(G).max():.1f})")
+    assert e <= TOL
 
 
 def test_animate_equals_scan_of_oracle_locals_chunk_variants():
@@ -264,4 +269,4 @@ def test_one_joint_eight_layers_two_pass():
     G, S = oracle.animate(par, keys, 8.0, 1, lay)
     e = max(float(np.abs(g - G).max()), float(np.abs(s - S).max()))
     print(f"one joint, 8 layers: max err {e:.2e}")
-    assert e <= 4e-6
+    assert e <= 2 ** -24 * (1 + 1e-9)

@@ -63,12 +63,21 @@ def test_stage1_error_budget(name, type_, ib_seed, n):
     e_local = float(np.abs(Lg - Lo).max())
     G_gl, _ = oracle.scan(par, Lg.astype(np.float32), ib)
     e_prop = float(np.abs(G_gl - G_o).max())
+    # which part of the local error carries down the path: only the translation column
+    # of the GPU locals (rotation blocks exact), or only the rotation blocks
+    Lt = Lo.copy()
+    Lt[..., 3] = Lg[..., 3]
+    LR = Lg.copy()
+    LR[..., 3] = Lo[..., 3]
+    e_prop_t = float(np.abs(oracle.scan(par, Lt, ib)[0] - G_o).max())
+    e_prop_R = float(np.abs(oracle.scan(par, LR, ib)[0] - G_o).max())
     G_g, S_g = _animate(par, keys, lay, ib)
     e_scan = float(np.abs(G_g - G_gl).max())
     e_total = max(float(np.abs(G_g - G_o).max()), float(np.abs(S_g - S_o).max()))
     rec = {"skeleton": name, "chars": n, "e_repr": e_repr, "e_local": e_local,
            "orth_gpu_locals": _orth_defect(Lg), "orth_rounded_locals": _orth_defect(Lf.astype(np.float64)),
-           "e_prop": e_prop, "e_scan": e_scan, "e_total": e_total}
+           "e_prop": e_prop, "e_prop_t_only": e_prop_t, "e_prop_R_only": e_prop_R, "e_scan": e_scan,
+           "e_total": e_total}
     print("stage1-budget " + json.dumps(rec))
     # the pieces are consistent (triangle inequality) and the total meets the bound
     assert float(np.abs(G_g - G_o).max()) <= e_prop + e_scan + 1e-12
