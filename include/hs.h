@@ -355,7 +355,9 @@ typedef enum {
     HS_Q_SEQ_ENTRIES = 29,   /* plan only: phase-2 descriptors of all tiles                    */
     HS_Q_SEQ_IMPORTS = 30,   /* plan only: import pairs of all tiles                           */
     HS_Q_SEQ_RUNS = 31,      /* plan only: TMA runs of all tiles                               */
-    HS_Q_SEQ_QSLOTS = 32     /* plan only: Q locations (most imports of a tile)                */
+    HS_Q_SEQ_QSLOTS = 32,    /* plan only: Q locations (most imports of a tile)                */
+    HS_Q_SEQ_CHUNK = 33,     /* HS_ALGO_TILES: chunk K of the multi-tile program                */
+    HS_Q_SEQ_SBUFS = 34      /* HS_ALGO_TILES: skin / inverse-bind buffers                      */
 } hs_query;
 
 hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* value);
@@ -415,10 +417,11 @@ typedef enum {
                               (next tile's Q index + 1)<<52 (12); src >= 2S: a Q location
                               (2S + (k & 1) nQ + index)                                        */
     HS_X_SEQ_P1LEN = 14,   /* int32 [KT][T]                                                     */
-    HS_X_SEQ_ROUND_OFF = 15, /* int32 [KT][R2max+1], relative to the tile's rounds_off           */
-    HS_X_SEQ_ROUNDS = 16,  /* uint32 [E] (all tiles)                                            */
+    HS_X_SEQ_ROUND_OFF = 15, /* int32 [KT][R2max+1 rounded up to 4], relative to rounds_off      */
+    HS_X_SEQ_ROUNDS = 16,  /* uint32 [E] (all tiles; each tile's records padded to 4)           */
     HS_X_SEQ_IMP = 17,     /* int32 [I][2]: workspace slot, Q location (parents two or more
-                              tiles back; a parent in the previous tile is forwarded)           */
+                              tiles back; a parent in the previous tile is forwarded); each
+                              tile's pairs padded to an even count                              */
     HS_X_SEQ_RUNS = 18,    /* int32 [R][4]: user start, smem offset, length, 0                  */
     HS_X_SEQ_IB_USER = 19  /* int32 [KT][F]: user label at each smem offset (-1 = none)          */
 } hs_plan_export_what;

@@ -42,7 +42,8 @@ QUERY = {"n_joints": 0, "max_level": 1, "rounds": 2, "path": 3, "chunk": 4, "til
          "pbufs": 15, "sbufs": 16, "chunking": 17, "tile_slots": 18, "tile_rounds_entries": 19,
          "tile_r2": 20, "small_tile_chars": 21, "seq_tiles": 22, "seq_tile_joints": 23,
          "seq_exports": 24, "seq_smem_bytes": 25, "seq_threads": 26, "seq_slots": 27, "seq_r2max": 28,
-         "seq_entries": 29, "seq_imports": 30, "seq_runs": 31, "seq_qslots": 32}
+         "seq_entries": 29, "seq_imports": 30, "seq_runs": 31, "seq_qslots": 32, "seq_chunk": 33,
+         "seq_sbufs": 34}
 # hs_plan_export_what
 EXPORT = {"levels": 0, "order": 1, "lift": 2, "block_of": 3, "mpob": 4, "chunk_src": 5,
           "anchor_link": 6, "chunk_lists": 7, "tile_meta": 8, "tile_p1len": 9,
@@ -228,7 +229,7 @@ class Plan:
             KT, T, K = self.query("seq_tiles"), self.query("seq_threads"), self.query("chunk")
             F, R2 = self.query("seq_tile_joints"), self.query("seq_r2max")
             dtype, shape = {"seq_tiles": (np.int32, (KT, 12)), "seq_meta": (np.uint64, (KT, T, K)),
-                            "seq_p1len": (np.int32, (KT, T)), "seq_round_off": (np.int32, (KT, R2 + 1)),
+                            "seq_p1len": (np.int32, (KT, T)), "seq_round_off": (np.int32, (KT, (R2 + 4) // 4 * 4)),
                             "seq_rounds": (np.uint32, (self.query("seq_entries"),)),
                             "seq_imp": (np.int32, (self.query("seq_imports"), 2)),
                             "seq_runs": (np.int32, (self.query("seq_runs"), 4)),

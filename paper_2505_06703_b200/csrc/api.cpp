@@ -87,7 +87,7 @@ struct hs_skeleton {
     // multi-tile path (HS_ALGO_TILES): skeletons beyond one CTA
     bool seq_ok = false;
     hs::SeqProgram seq;
-    int seq_stages = 0, seq_sbufs = 0, seq_threads = 0, seq_max_entries = 0;
+    int seq_stages = 0, seq_sbufs = 0, seq_threads = 0, seq_max_entries = 0, seq_K = 3;
     int64_t seq_smem = 0;
     hs::SeqTileDev* d_seq_tiles = nullptr;
     uint64_t* d_seq_meta = nullptr;
@@ -157,37 +157,45 @@ void free_skeleton(hs_skeleton* sk) {
     delete sk;
 }
 
-// The multi-tile program (HS_ALGO_TILES) of a skeleton that does not fit one CTA:
-// the largest tile (F joints) whose program fits 224 compute threads and whose
-// shared memory (2 stages + 1 skin buffer, or the requested counts) fits the device;
-// chunking RUNS or HEAVY per skeleton, whichever needs fewer phase-2 descriptors.
+// The multi-tile program (HS_ALGO_TILES) of a skeleton that does not fit one CTA.
+// Defaults measured on C6 (2,000 x tree16384; tools/tune_tiles.py): chunk K = 3, two
+// skin buffers (the next tile's inverse binds load during this tile), 576-joint tiles;
+// the largest tile up to the target whose program fits 224 compute threads and whose
+// shared memory fits the device; chunking RUNS or HEAVY, whichever needs fewer phase-2
+// descriptors.  Explicit options override each choice.
 hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<float>& ib) {
     const hs::Plan& P = sk->plan;
-    const int stages = o.stages ? o.stages : 2, sbufs = o.sbufs ? o.sbufs : 1;
-    const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 1024;
+    const int K = o.chunk ? o.chunk : 3;
+    const int stages = o.stages ? o.stages : 2;
+    const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 576;
     const int modes[2] = {hs::CHUNK_RUNS, hs::CHUNK_HEAVY};
     const int nmodes = o.chunking == 0 ? 2 : 1;
-    for (int F = f0 - f0 % 32; F >= 64 && !sk->seq_ok; F -= 64) {
-        hs::SeqProgram best;
-        bool have = false;
-        for (int mi = 0; mi < nmodes; ++mi) {
-            const int mode = o.chunking == 0 ? modes[mi]
-                             : (o.chunking == 1 ? hs::CHUNK_CONSECUTIVE
-                                                : (o.chunking == 3 ? hs::CHUNK_RUNS : hs::CHUNK_HEAVY));
-            hs::SeqProgram sp;
-            if (!hs::build_seq_program(P, sk->K, F, mode, 224, sp)) continue;
-            if (hs::seq_smem_bytes(sp, stages, sbufs) > sk->smem_optin) continue;
-            if (!have || sp.rounds.size() < best.rounds.size()) { best = std::move(sp); have = true; }
+    const int sb_cand[2] = {o.sbufs ? o.sbufs : 2, o.sbufs ? o.sbufs : 1};
+    for (int sbufs : sb_cand) {
+        for (int F = f0 - f0 % 32; F >= 64 && !sk->seq_ok; F -= 32) {
+            hs::SeqProgram best;
+            bool have = false;
+            for (int mi = 0; mi < nmodes; ++mi) {
+                const int mode = o.chunking == 0 ? modes[mi]
+                                 : (o.chunking == 1 ? hs::CHUNK_CONSECUTIVE
+                                                    : (o.chunking == 3 ? hs::CHUNK_RUNS : hs::CHUNK_HEAVY));
+                hs::SeqProgram sp;
+                if (!hs::build_seq_program(P, K, F, mode, 224, sp)) continue;
+                if (hs::seq_smem_bytes(sp, stages, sbufs) > sk->smem_optin) continue;
+                if (!have || sp.rounds.size() < best.rounds.size()) { best = std::move(sp); have = true; }
+            }
+            if (!have) continue;
+            sk->seq = std::move(best);
+            sk->seq_ok = true;
+            sk->seq_sbufs = sbufs;
         }
-        if (!have) continue;
-        sk->seq = std::move(best);
-        sk->seq_ok = true;
+        if (sk->seq_ok) break;
     }
     if (!sk->seq_ok) return HS_OK;   // the split path remains
     const hs::SeqProgram& sp = sk->seq;
     sk->seq_stages = stages;
-    sk->seq_sbufs = sbufs;
-    sk->seq_smem = hs::seq_smem_bytes(sp, stages, sbufs);
+    sk->seq_K = K;
+    sk->seq_smem = hs::seq_smem_bytes(sp, stages, sk->seq_sbufs);
     sk->seq_threads = sp.T + 32;
     sk->seq_max_entries = (int)hs::seq_max_tile_entries(sp);
     std::vector<hs::SeqTileDev> tiles(sp.tiles.size());
@@ -205,7 +213,7 @@ hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<
         (e = upload(&sk->d_seq_imp, sp.imp.data(), sp.imp.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_runs, sp.runs.data(), sp.runs.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_ib, ibt.data(), ibt.size())) != cudaSuccess ||
-        (e = hs::prepare_seq(sk->K)) != cudaSuccess)
+        (e = hs::prepare_seq(K)) != cudaSuccess)
         return cuda_fail(e, "multi-tile program");
     return HS_OK;
 }
@@ -431,6 +439,7 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
 }
 
 static_assert(HS_MAX_BATCH <= hs::kMaxSegs, "one kernel segment per batch item");
+static_assert(hs::kSeqImportsPerThread == hs::kSeqImpPerThread, "multi-tile import staging width");
 
 struct ChunkItem {
     const hs_skeleton* sk;
@@ -596,13 +605,20 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.J = J; a.KT = sp.KT; a.F = sp.F; a.T = sp.T; a.S = sp.S; a.nQ = sp.nQ; a.n_exp = sp.n_exp;
             a.r2max = sp.R2max; a.max_imp = sp.max_imp; a.max_entries = sk->seq_max_entries;
             a.p_floats = (2 * sp.S + 2 * sp.nQ) * 12;
+            a.r2p = (sp.R2max + 1 + 3) & ~3;
+            a.entp = 0;
+            a.impp = 0;
+            for (const hs::SeqTile& tl : sp.tiles) {
+                a.entp = std::max(a.entp, (tl.n_entries + 3) & ~3);
+                a.impp = std::max(a.impp, (tl.n_imp + 1) & ~1);
+            }
             a.stages = sk->seq_stages; a.sbufs = sk->seq_sbufs; a.threads = sk->seq_threads;
             a.has_runs = sp.has_runs ? 1 : 0;
             a.bulk_piece = HS_BULK_PIECE;
             a.smem_bytes = sk->seq_smem;
-            a.ctas_per_sm = 1;
+            a.ctas_per_sm = tile_ctas > 0 ? tile_ctas : 1;
             // workspace: one character's exported poses per CTA (stays in L2)
-            const int64_t grid = std::min<int64_t>(n_chars, hs::sm_count());
+            const int64_t grid = std::min<int64_t>(n_chars, (int64_t)hs::sm_count() * a.ctas_per_sm);
             float* ws = nullptr;
             if (sp.n_exp > 0) {
                 e = ws_alloc(reinterpret_cast<void**>(&ws), (size_t)(grid * sp.n_exp * 48), st);
@@ -614,7 +630,7 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
                 cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
                 cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
             }
-            e = hs::launch_seq(sk->K, a, st);
+            e = hs::launch_seq(sk->seq_K, a, st);
             if (ws) cudaFreeAsync(ws, st);
             if (a.prof) {
                 unsigned long long h[10];
@@ -1118,6 +1134,8 @@ hs_status hs_skeleton_query(const hs_skeleton* sk, int32_t what, int64_t* v) {
         case HS_Q_SEQ_TILE_JOINTS: *v = sk->seq_ok ? sk->seq.F : 0; break;
         case HS_Q_SEQ_EXPORTS: *v = sk->seq_ok ? sk->seq.n_exp : 0; break;
         case HS_Q_SEQ_SMEM_BYTES: *v = sk->seq_ok ? sk->seq_smem : 0; break;
+        case HS_Q_SEQ_CHUNK: *v = sk->seq_ok ? sk->seq_K : 0; break;
+        case HS_Q_SEQ_SBUFS: *v = sk->seq_ok ? sk->seq_sbufs : 0; break;
         default: return fail(HS_ERR_INVALID_ARG, "unknown query");
     }
     return HS_OK;

@@ -70,6 +70,9 @@ struct ChunkedArgs {
 // Multi-tile kernel (HS_ALGO_TILES): skeletons beyond one CTA.  A
 // persistent CTA takes whole characters (b, b + grid, ...) and walks each one's KT
 // tiles in topological order; cross-tile parents are final workspace values.
+// Multi-tile workspace imports staged in registers: at most this many 16-byte pieces per
+// compute thread per tile (3 x imports <= kSeqImpPerThread x threads; the plan checks).
+constexpr int kSeqImpPerThread = 16;
 struct SeqTileDev {               // = hs::SeqTile (plan.hpp)
     int32_t first, nj, R2, n_entries, rounds_off, n_imp, imp_off, n_runs, runs_off, T, pad[2];
 };
@@ -88,6 +91,7 @@ struct SeqArgs {
     const int4* runs;          // (user start, smem offset, length, 0)
     int64_t n_chars;
     int32_t J, KT, F, T, S, nQ, n_exp, r2max, max_imp, max_entries;
+    int32_t r2p, entp, impp;   // program record widths: round_off row, phase-2 entries, import pairs (padded)
     int32_t p_floats;          // (2S + 2 nQ) * 12: anchors (ping-pong) and two Q buffers
     int32_t stages, sbufs, threads, has_runs, bulk_piece;
     int64_t smem_bytes;

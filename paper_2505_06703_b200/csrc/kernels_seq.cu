@@ -41,18 +41,26 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* done = full + 4;
     uint64_t* ibfull = done + 4;   // S buffer holds the tile's inverse binds (TMA), S computed in place
+    uint64_t* progfull = ibfull + 4;   // [3]: a tile program has landed (TMA by the producer)
     const int tile_f = a.F * 12;
     float* LG = reinterpret_cast<float*>(smem + 128);
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
+    // three program buffers (tile counter mod 3), each: meta [T][K] | p1 [T] | round_off
+    // [r2p] | rounds [entp] | import list [impp] (16-byte multiples, TMA destinations)
     const int TK = a.T * K;
-    const int IMPW = (a.max_imp + 1) & ~1;                                  // import-list slots (even)
-    const int TABW = ((a.r2max + 1 + 3) & ~3) + ((a.max_entries + 3) & ~3); // one table buffer (ints)
-    uint64_t* s_meta = reinterpret_cast<uint64_t*>(P + a.p_floats);        // [2][T][K]
-    int32_t* s_p1 = reinterpret_cast<int32_t*>(s_meta + 2 * TK);           // [2][T]
-    int2* s_imp = reinterpret_cast<int2*>(s_p1 + 2 * a.T);                 // [2][IMPW]
-    int32_t* s_tab = reinterpret_cast<int32_t*>(s_imp + 2 * IMPW);         // [2][round_off | rounds]
-    SeqTileDev* s_tiles = reinterpret_cast<SeqTileDev*>(s_tab + 2 * TABW); // [KT]
+    const int PROGW = TK * 2 + a.T + a.r2p + a.entp + 2 * a.impp;           // 4-byte words
+    int32_t* s_prog = reinterpret_cast<int32_t*>(P + a.p_floats);
+    SeqTileDev* s_tiles = reinterpret_cast<SeqTileDev*>(s_prog + 3 * PROGW); // [KT]
+    auto prog_meta = [&](int b) { return reinterpret_cast<const uint64_t*>(s_prog + b * PROGW); };
+    auto prog_p1 = [&](int b) { return s_prog + b * PROGW + 2 * TK; };
+    auto prog_roff = [&](int b) { return s_prog + b * PROGW + 2 * TK + a.T; };
+    auto prog_rounds = [&](int b) {
+        return reinterpret_cast<const uint32_t*>(s_prog + b * PROGW + 2 * TK + a.T + a.r2p);
+    };
+    auto prog_imp = [&](int b) {
+        return reinterpret_cast<const int2*>(s_prog + b * PROGW + 2 * TK + a.T + a.r2p + a.entp);
+    };
 
     const int nwc = (int)(blockDim.x >> 5) - 1;
     const int NC = nwc * 32;
@@ -67,13 +75,15 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
         for (int s = 0; s < NSS; ++s) mbar_init(&ibfull[s], 1);
+        for (int s = 0; s < 3; ++s) mbar_init(&progfull[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
 
     if (warp == nwc) {
         // ------------------------------------------------------------ producer
-        if ((threadIdx.x & 31) != 0) return;
+        // lane 0 streams tiles, programs and inverse binds
+        const int lane = threadIdx.x & 31;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
         const uint64_t stream_pol = policy_evict_first(), keep_pol = policy_evict_last();
         // tile cursors (character, tile) for the loads (NS ahead) and the stores
@@ -95,7 +105,23 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             }
             if (++lk == KT) { lk = 0; lc += gridDim.x; }
         };
-        for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load((int)it);
+        // tile programs: counter c's tile into program buffer c % 3, three tiles ahead (so a
+        // tile's import list is in place when the tile before it stages the imports)
+        int pk = 0;
+        auto issue_prog = [&](int buf) {
+            const SeqTileDev tl = s_tiles[pk];
+            const uint32_t b_meta = (uint32_t)TK * 8u, b_p1 = (uint32_t)a.T * 4u, b_ro = (uint32_t)a.r2p * 4u;
+            const uint32_t b_rd = (uint32_t)((tl.n_entries + 3) & ~3) * 4u, b_imp = (uint32_t)((tl.n_imp + 1) & ~1) * 8u;
+            mbar_expect_tx(&progfull[buf], b_meta + b_p1 + b_ro + b_rd + b_imp);
+            int32_t* d = s_prog + buf * PROGW;
+            bulk_g2s(d, a.meta + (int64_t)pk * TK, b_meta, &progfull[buf]);
+            bulk_g2s(d + 2 * TK, a.p1len + (int64_t)pk * a.T, b_p1, &progfull[buf]);
+            bulk_g2s(d + 2 * TK + a.T, a.round_off + (int64_t)pk * a.r2p, b_ro, &progfull[buf]);
+            if (b_rd) bulk_g2s(d + 2 * TK + a.T + a.r2p, a.rounds + tl.rounds_off, b_rd, &progfull[buf]);
+            if (b_imp)
+                bulk_g2s(d + 2 * TK + a.T + a.r2p + a.entp, a.imp + tl.imp_off, b_imp, &progfull[buf]);
+            if (++pk == KT) pk = 0;
+        };
         const bool do_skin = a.sout != nullptr;
         // inverse binds of a tile, by smem offset, into its S buffer (phase 3 computes
         // S = G (x) IB in place: each slot is read and then written by one thread)
@@ -110,78 +136,60 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 bulk_g2s_hint(dst + o, src + o, min(piece, bytes - o), &ibfull[buf], keep_pol);
             if (++ibk == KT) ibk = 0;
         };
-        if (do_skin)
-            for (int64_t it = 0; it < my_tiles && it < NSS; ++it) issue_ib((int)it);
-        int stage = 0, sb = 0;
+        if (lane == 0) {
+            for (int64_t it = 0; it < my_tiles && it < 3; ++it) issue_prog((int)it);
+            for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load((int)it);
+            if (do_skin)
+                for (int64_t it = 0; it < my_tiles && it < NSS; ++it) issue_ib((int)it);
+        }
+        int stage = 0, sb = 0, pbuf = 0;
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
             mbar_wait(&done[stage], phase);
-            const SeqTileDev tl = s_tiles[sk];
-            const int64_t cbase = sc * J * 12;
-            const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
-            const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
-            for (int r = 0; r < tl.n_runs; ++r) {
-                const int4 run = __ldg(a.runs + tl.runs_off + r);
-                const uint32_t bytes = (uint32_t)run.z * 48u;
-                char* gp = reinterpret_cast<char*>(a.gout + cbase) + (int64_t)run.x * 48;
-                char* sp = do_skin ? reinterpret_cast<char*>(a.sout + cbase) + (int64_t)run.x * 48 : nullptr;
-                for (uint32_t o = 0; o < bytes; o += piece) {
-                    const uint32_t nb = min(piece, bytes - o);
-                    bulk_s2g_hint(gp + o, sg + run.y * 48 + o, nb, stream_pol);
-                    if (do_skin) bulk_s2g_hint(sp + o, ss + run.y * 48 + o, nb, stream_pol);
+            if (lane == 0 && it + 3 < my_tiles) issue_prog(pbuf);   // tile it no longer reads its program
+            if (++pbuf == 3) pbuf = 0;
+            if (lane == 0) {
+                const SeqTileDev tl = s_tiles[sk];
+                const int64_t cbase = sc * J * 12;
+                const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
+                const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
+                for (int r = 0; r < tl.n_runs; ++r) {
+                    const int4 run = __ldg(a.runs + tl.runs_off + r);
+                    const uint32_t bytes = (uint32_t)run.z * 48u;
+                    char* gp = reinterpret_cast<char*>(a.gout + cbase) + (int64_t)run.x * 48;
+                    char* sp = do_skin ? reinterpret_cast<char*>(a.sout + cbase) + (int64_t)run.x * 48 : nullptr;
+                    for (uint32_t o = 0; o < bytes; o += piece) {
+                        const uint32_t nb = min(piece, bytes - o);
+                        bulk_s2g_hint(gp + o, sg + run.y * 48 + o, nb, stream_pol);
+                        if (do_skin) bulk_s2g_hint(sp + o, ss + run.y * 48 + o, nb, stream_pol);
+                    }
                 }
+                bulk_commit();
+                bulk_wait_read<0>();
+                if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
+                if (it + NS < my_tiles) issue_load(stage);
             }
-            bulk_commit();
-            bulk_wait_read<0>();
-            if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
-            if (it + NS < my_tiles) issue_load(stage);
             if (++sk == KT) { sk = 0; sc += gridDim.x; }
             if (++stage == NS) { stage = 0; phase ^= 1u; }
             if (++sb == NSS) sb = 0;
         }
-        bulk_wait_all();
+        if (lane == 0) bulk_wait_all();
         return;
     }
 
     // ---------------------------------------------------------------- consumers
-    // Everything a tile needs is requested one tile ahead with cp.async and awaited at
-    // the top of the tile: its program (chunk metadata, phase-1 info; ring by tile
-    // counter parity), its phase-2 tables (ring), and its Q values: parents from tiles
-    // <= k - 2 are imported from the workspace (L2) at the top of tile k - 1 (the lists
-    // are prefetched two tiles ahead), parents from tile k - 1 are forwarded into Q by
-    // the threads that compute them in phase 3 of tile k - 1.  Q buffers alternate with
-    // the tile index k (the plan bakes the locations in).
+    // A tile's program (chunk metadata, phase-1 info, phase-2 tables, the import list)
+    // arrives by TMA two tiles ahead (program buffer = tile counter parity).  Its Q
+    // values arrive one tile ahead: parents from tiles <= k - 2 are imported from the
+    // workspace (L2) by cp.async issued between phase 2 and phase 3 of tile k - 1 and
+    // awaited at the top of tile k; parents from tile k - 1 are forwarded into Q by the
+    // threads that compute them in phase 3 of tile k - 1.  Q buffers alternate with the
+    // tile index k (the plan bakes the locations in).
     const int t = threadIdx.x;
     float* wsb = a.ws + (int64_t)blockIdx.x * a.n_exp * 12;   // this CTA's workspace
     const bool skin = a.sout != nullptr;
     const uint64_t ws_pol = policy_evict_last();   // the workspace is re-read by later tiles
-    auto prefetch_prog = [&](int k, int buf) {      // meta row + phase-1 info of tile k
-        if (t < a.T) {
-#pragma unroll
-            for (int s = 0; s < K; ++s)
-                cp_async8(s_meta + buf * TK + t * K + s, a.meta + ((int64_t)k * a.T + t) * K + s);
-            cp_async4(s_p1 + buf * a.T + t, a.p1len + (int64_t)k * a.T + t);
-        }
-    };
-    auto prefetch_list = [&](int k, int buf) {      // tile k's workspace imports
-        const int ni = s_tiles[k].n_imp, io = s_tiles[k].imp_off;
-        for (int i = t; i < ni; i += NC) cp_async8(s_imp + buf * IMPW + i, a.imp + io + i);
-    };
-    auto prefetch_tables = [&](int k, int buf) {    // phase-2 tables of tile k
-        int32_t* ro = s_tab + buf * TABW;
-        uint32_t* rd = reinterpret_cast<uint32_t*>(ro + ((a.r2max + 1 + 3) & ~3));
-        const int ne = s_tiles[k].n_entries, eo = s_tiles[k].rounds_off;
-        for (int i = t; i <= a.r2max; i += NC) cp_async4(ro + i, a.round_off + (int64_t)k * (a.r2max + 1) + i);
-        for (int i = t; i < ne; i += NC) cp_async4(rd + i, a.rounds + eo + i);
-    };
-    if (my_tiles > 0) {
-        prefetch_prog(0, 0);
-        prefetch_tables(0, 0);
-        if (my_tiles > 1) prefetch_list(1 % KT, 1);
-        cp_async_commit();
-    }
     const int qb0 = 2 * a.S, nQ = a.nQ;
-
     // profiling builds (HS_PROF_HOOKS): consumer thread 0's cycles per phase, summed
     long long prof_last = 0;
     auto prof_mark = [&](int slot) {
@@ -192,42 +200,23 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         }
     };
     uint64_t m[K];
-    int stage = 0, sb = 0, pb = 0, k = 0;
-    uint32_t phase = 0, sphase = 0;
+    int stage = 0, sb = 0, pb = 0, k = 0;     // pb: program buffer (tile counter mod 3)
+    uint32_t phase = 0, sphase = 0, pphase = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
         const SeqTileDev tl = s_tiles[k];
-        const int kn = k + 1 < KT ? k + 1 : 0, kn2 = kn + 1 < KT ? kn + 1 : 0;
         float* L = LG + stage * tile_f;
         prof_mark(-1);
-        cp_async_wait_all();   // requested during the previous tile (tables, Q: the phase-2 barrier)
+        mbar_wait(&progfull[pb], pphase);
         prof_mark(0);
         int p1, run_back, run_anchor;
         {
-            const int info = t < a.T ? s_p1[pb * a.T + t] : 0;
+            const int info = t < a.T ? prog_p1(pb)[t] : 0;
             p1 = info & 0xff;
             run_back = (info >> 8) & 0xff;
             run_anchor = (int)((uint32_t)info >> 16) - 1;
         }
 #pragma unroll
-        for (int s = 0; s < K; ++s) m[s] = t < a.T ? s_meta[pb * TK + t * K + s] : kSeqMetaNone;
-        if (it + 1 < my_tiles) {
-            // the next tile's workspace imports into its Q buffer (its parents in tiles
-            // <= k - 1 are final: their exports preceded this tile's start)
-            const int ni = s_tiles[kn].n_imp;
-            for (int i = t; i < ni; i += NC) {
-                const int2 e = s_imp[(pb ^ 1) * IMPW + i];
-                HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= qb0 && (e.y + 1) * 12 <= a.p_floats);
-                const float* src = wsb + (int64_t)e.x * 12;
-                float* dst = P + e.y * 12;
-                cp_async16_cg_hint(dst, src, ws_pol);
-                cp_async16_cg_hint(dst + 4, src + 4, ws_pol);
-                cp_async16_cg_hint(dst + 8, src + 8, ws_pol);
-            }
-            prefetch_prog(kn, pb ^ 1);
-            prefetch_tables(kn, pb ^ 1);
-            if (it + 2 < my_tiles) prefetch_list(kn2, pb);
-            cp_async_commit();
-        }
+        for (int s = 0; s < K; ++s) m[s] = t < a.T ? prog_meta(pb)[t * K + s] : kSeqMetaNone;
         prof_mark(1);
         mbar_wait(&full[stage], phase);
         prof_mark(2);
@@ -293,8 +282,8 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         prof_mark(4);
 
         // phase 2: pointer jumping over the anchor forest (ping-pong P; Q roots final)
-        const int32_t* s_round_off = s_tab + pb * TABW;
-        const uint32_t* s_rounds = reinterpret_cast<const uint32_t*>(s_round_off + ((a.r2max + 1 + 3) & ~3));
+        const int32_t* s_round_off = prog_roff(pb);
+        const uint32_t* s_rounds = prog_rounds(pb);
         for (int r = 0; r < tl.R2; ++r) {
             const int eb = s_round_off[r], e1 = s_round_off[r + 1];
             for (int e = eb + t; e < e1; e += NC) {
@@ -312,6 +301,27 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             bar_consumers(NC);
         }
 
+        // the next tile's workspace imports (parents in tiles <= k - 1: final), loaded
+        // into registers now, stored into its Q buffer after phase 3 (the loads complete
+        // under phase 3); three consecutive lanes per 48-byte row
+        float4 impv[kSeqImpPerThread];
+        int nimp3 = 0;
+        const int pbn = pb == 2 ? 0 : pb + 1;   // the next tile's program buffer
+        const int2* lst = prog_imp(pbn);
+        if (it + 1 < my_tiles) {
+            mbar_wait(&progfull[pbn], pb == 2 ? pphase ^ 1u : pphase);
+            nimp3 = 3 * s_tiles[k + 1 < KT ? k + 1 : 0].n_imp;
+#pragma unroll
+            for (int u = 0; u < kSeqImpPerThread; ++u) {
+                const int q = t + u * NC;
+                if (q < nimp3) {
+                    const int i = q / 3, c = q - 3 * i;
+                    const int2 e = lst[i];
+                    HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= qb0 && (e.y + 1) * 12 <= a.p_floats);
+                    impv[u] = ldg4_hint(wsb + (int64_t)e.x * 12 + 4 * c, ws_pol);
+                }
+            }
+        }
         // phase 3: final fold, G in place, S into the S buffer, exports to the workspace
         float* S = SB + sb * tile_f;
         prof_mark(5);
@@ -328,6 +338,8 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 float l[12];
                 HS_BOUND(off >= 0 && off < tl.nj);
                 ld3(L + off * 12, l);
+                float ibv[12];   // loaded with L: the stores below could alias it for the compiler
+                if (skin) ld3(S + off * 12, ibv);
                 if (RUNS) {
                     float left[12];
                     if (src == kSrcPrev) {
@@ -375,22 +387,29 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                     st3(P + (qb0 + ((k + 1) & 1) * nQ + fw - 1) * 12, acc3);
                 }
                 if (skin) {
-                    float sk[12], ibv[12];
-                    ld3(S + off * 12, ibv);
+                    float sk[12];
                     compose(acc3, ibv, sk);
                     st3(S + off * 12, sk);
                 }
             }
         }
+#pragma unroll
+        for (int u = 0; u < kSeqImpPerThread; ++u) {
+            const int q = t + u * NC;
+            if (q < nimp3) {
+                const int i = q / 3, c = q - 3 * i;
+                *reinterpret_cast<float4*>(P + lst[i].y * 12 + 4 * c) = impv[u];
+            }
+        }
         prof_mark(7);
-        fence_proxy_async();
+        fence_proxy_async();   // smem G/S for the bulk stores
         bar_consumers(NC);
         prof_mark(8);
         if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 9, 1ull);
         if (t == 0) mbar_arrive(&done[stage]);
         if (++stage == NS) { stage = 0; phase ^= 1u; }
         if (++sb == NSS) { sb = 0; sphase ^= 1u; }   // parity of use it / NSS of buffer sb
-        pb ^= 1;
+        if (++pb == 3) { pb = 0; pphase ^= 1u; }     // program buffer use (it / 3) parity
         if (++k == KT) k = 0;
     }
 }

@@ -708,29 +708,19 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     const int32_t S = sp.S, nQ = sp.nQ;
     auto qloc = [&](int k, int32_t z) { return 2 * S + (k & 1) * nQ + z; };
     if (S >= (1 << 12) || 2 * S + 2 * nQ >= (1 << 12) - 8 || F > 1024) return false;   // meta field widths
-    // workspace slots: joint q (tile tq) needs one iff a child sits in a tile >= tq + 2;
-    // the slot is free again for exports of tiles >= its last consumer (whose import
-    // was issued at the start of the tile before, and awaited at the start of that tile)
+    // workspace slots: joint q (tile tq) needs one iff a child sits in a tile >= tq + 2.
+    // Numbered in the order phase 3 stores them (tile, chunk slot, thread), so the
+    // exporting lanes of one warp store to consecutive rows (coalesced stores); no reuse.
     std::vector<int32_t> ws_slot(n, -1);
-    {
-        std::vector<std::pair<int32_t, int32_t>> busy;   // (free from tile, slot)
-        std::vector<int32_t> freel;
-        for (int k = 0; k < KT; ++k) {
-            for (size_t b = 0; b < busy.size();)
-                if (busy[b].first <= k) { freel.push_back(busy[b].second); busy[b] = busy.back(); busy.pop_back(); }
-                else ++b;
-            std::sort(freel.begin(), freel.end(), std::greater<int32_t>());
-            const int32_t a = k * F, nj = std::min(F, n - a);
-            for (int32_t li = 0; li < nj; ++li) {
-                const int32_t i = a + li;
-                if (last_ws_use[i] < 0) continue;
-                int32_t sl;
-                if (!freel.empty()) { sl = freel.back(); freel.pop_back(); }
-                else sl = sp.n_exp++;
-                ws_slot[i] = sl;
-                busy.push_back({last_ws_use[i], sl});
-            }
-        }
+    for (int k = 0; k < KT; ++k) {
+        const ChunkDecomp& d = tmp[k].d;
+        const int32_t a = k * F;
+        for (int s = 0; s < K; ++s)
+            for (size_t t = 0; t < d.lists.size(); ++t)
+                if (s < (int)d.lists[t].size()) {
+                    const int32_t i = a + d.lists[t][s];
+                    if (last_ws_use[i] >= 0) ws_slot[i] = sp.n_exp++;
+                }
     }
     if (sp.n_exp >= (1 << 16) - 1) return false;
     // encoded meta (seq_meta_* in kernels.cuh): off 10 | src + 8 13 | own + 1 13 | ex 16 | fwd 12
@@ -795,6 +785,7 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
             st.R2 = r + 1;
         }
         st.n_entries = (int32_t)sp.rounds.size() - st.rounds_off;
+        while (sp.rounds.size() % 4) sp.rounds.push_back(0);   // 16-byte tile records (TMA)
         sp.R2max = std::max(sp.R2max, st.R2);
         // per-thread program
         for (int32_t t = 0; t < T; ++t) {
@@ -833,6 +824,7 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
             sp.imp.push_back(qloc(k, z));
             ++st.n_imp;
         }
+        while (sp.imp.size() % 4) sp.imp.push_back(0);         // 16-byte tile records (TMA)
         st.runs_off = (int32_t)sp.runs.size() / 4;
         for (int32_t li = 0; li < nj;) {
             int32_t len = 1;
@@ -843,13 +835,15 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         }
         for (int32_t li = 0; li < nj; ++li) sp.ib_user[(size_t)k * F + li] = p.order[a + li];
         sp.max_imp = std::max(sp.max_imp, st.n_imp);
+        if (3 * st.n_imp > kSeqImportsPerThread * sp.T) return false;   // register-staged imports
         sp.max_runs = std::max(sp.max_runs, st.n_runs);
         sp.tiles.push_back(st);
     }
-    sp.round_off.assign((size_t)KT * (sp.R2max + 1), 0);
+    const int R2P = (sp.R2max + 1 + 3) & ~3;   // round_off rows padded to 16 bytes (TMA)
+    sp.round_off.assign((size_t)KT * R2P, 0);
     for (int k = 0; k < KT; ++k)
-        for (int r = 0; r <= sp.R2max; ++r)
-            sp.round_off[(size_t)k * (sp.R2max + 1) + r] = roff[k][std::min<size_t>(r, roff[k].size() - 1)];
+        for (int r = 0; r < R2P; ++r)
+            sp.round_off[(size_t)k * R2P + r] = roff[k][std::min<size_t>(r, roff[k].size() - 1)];
     return true;
 }
 
@@ -861,13 +855,21 @@ int64_t seq_max_tile_entries(const SeqProgram& sp) {
 
 int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs) {
     // barriers | stages x tile | sbufs x tile | P (2S anchors + 2 x nQ Q buffers) |
-    // meta x2 | p1len x2 | import lists x2 | (round_off | rounds) x2 | tile descriptors
+    // 2 program buffers (meta | p1 | round_off | rounds | import list) | tile descriptors
     const int64_t tileb = (int64_t)sp.F * 48;
     int64_t b = 128 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + 2 * sp.nQ) * 48;
-    b += 2LL * sp.T * sp.K * 8 + 2LL * sp.T * 4 + 2LL * ((sp.max_imp + 1) / 2 * 2) * 8;
-    b += 2 * (((int64_t)(sp.R2max + 1) + 3) / 4 * 16 + (seq_max_tile_entries(sp) + 3) / 4 * 16);
+    b += 3 * 4 * seq_prog_words(sp);   // three program buffers
     b += (int64_t)sp.KT * (int64_t)sizeof(SeqTile);
     return b;
+}
+
+int64_t seq_prog_words(const SeqProgram& sp) {
+    int64_t entp = 0, impp = 0;
+    for (const SeqTile& t : sp.tiles) {
+        entp = std::max<int64_t>(entp, (t.n_entries + 3) & ~3);
+        impp = std::max<int64_t>(impp, (t.n_imp + 1) & ~1);
+    }
+    return 2LL * sp.T * sp.K + sp.T + ((sp.R2max + 1 + 3) & ~3) + entp + 2 * impp;
 }
 
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob) {

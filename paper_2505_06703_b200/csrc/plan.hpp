@@ -84,6 +84,7 @@ struct SplitProgram {
 // that parent's global pose from an imported slot Q (a final root of the anchor
 // forest); joints with a child in a later tile export their global pose to a
 // per-CTA workspace slot in phase 3.
+constexpr int kSeqImportsPerThread = 16;   // = kernels.cuh kSeqImpPerThread (16-byte pieces)
 struct SeqTile {
     int32_t first, nj;            // internal positions [first, first + nj)
     int32_t R2, n_entries;        // pointer-jumping rounds and phase-2 descriptors
@@ -104,9 +105,10 @@ struct SeqProgram {
     std::vector<SeqTile> tiles;
     std::vector<uint64_t> meta;         // [KT][T][K]: off 10 | src + 8 13 | own + 1 13 | ws slot + 1 16 | fwd + 1 12
     std::vector<int32_t> p1len;         // [KT][T] as TileProgram::p1len
-    std::vector<int32_t> round_off;     // [KT][R2max + 1], relative to the tile's rounds_off
-    std::vector<uint32_t> rounds;       // concatenated phase-2 descriptors (TileProgram encoding)
-    std::vector<int32_t> imp;           // [..][2]: workspace slot, P location
+    // per-tile records are 16-byte aligned and sized (the producer warp loads them by TMA)
+    std::vector<int32_t> round_off;     // [KT][R2max + 1 rounded up to 4], relative to rounds_off
+    std::vector<uint32_t> rounds;       // per tile, padded to 4: phase-2 descriptors (TileProgram encoding)
+    std::vector<int32_t> imp;           // per tile, padded to 2 pairs: (workspace slot, Q location)
     std::vector<int32_t> runs;          // [..][4]: user start, smem offset, length, 0
     std::vector<int32_t> ib_user;       // [KT][F]: user label at each smem offset (-1 = none)
 };
@@ -133,6 +135,7 @@ SplitProgram build_split_program(const Plan& p, int K);
 bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, SeqProgram& out);
 int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs);
 int64_t seq_max_tile_entries(const SeqProgram& sp);   // phase-2 descriptors of the largest tile
+int64_t seq_prog_words(const SeqProgram& sp);         // 4-byte words of one program buffer
 
 // The paper's block layout for block size B over INTERNAL positions (exports).
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob);

@@ -19,24 +19,26 @@ assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream) == 0
 g, s = torch.empty_like(x), torch.empty_like(x)
 ref = None
-for kw in [{}, {"tile_joints": 640}, {"tile_joints": 512}, {"tile_joints": 384}, {"chunking": 2},
-           {"chunking": 3}, {"chunk": 3}, {"chunk": 7}, {"stages": 3, "tile_joints": 512}]:
+for kw in [{}, {"tile_joints": 640}, {"tile_joints": 512}, {"tile_joints": 448}, {"tile_joints": 384},
+           {"chunk": 5}, {"sbufs": 1}, {"stages": 3, "tile_joints": 448}]:
+    kw = dict(kw)
+    ctas = kw.pop("ctas", 0)
     try:
         sk = hs.Skeleton(par, hsgen.inv_bind(ib_seed, J), force_split=True, **kw)
     except hs.HSError as e:
         print(kw, "create failed", e)
         continue
     for _ in range(2):
-        sk.scan_into(x, g, s, algo="tiles")
+        sk.scan_into(x, g, s, algo="tiles", tile_ctas=ctas)
     ts = []
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        sk.scan_into(x, g, s, algo="tiles")
+        sk.scan_into(x, g, s, algo="tiles", tile_ctas=ctas)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
-    print(kw, "F", sk.query("seq_tile_joints"), "KT", sk.query("seq_tiles"), "smem", sk.query("seq_smem_bytes"),
+    print(kw, "ctas/SM", ctas or 1, "K", sk.query("seq_chunk"), "sbufs", sk.query("seq_sbufs"), "F", sk.query("seq_tile_joints"), "KT", sk.query("seq_tiles"), "smem", sk.query("seq_smem_bytes"),
           f"{ms:.4f} ms {144 * n * J / ms / 1e6:.0f} GB/s", flush=True)
     sk.close()
