@@ -87,7 +87,7 @@ struct hs_skeleton {
     // multi-tile path (HS_ALGO_TILES): skeletons beyond one CTA
     bool seq_ok = false;
     hs::SeqProgram seq;
-    int seq_stages = 0, seq_sbufs = 0, seq_threads = 0, seq_max_entries = 0, seq_K = 3;
+    int seq_stages = 0, seq_sbufs = 0, seq_threads = 0, seq_max_entries = 0, seq_K = 3, seq_helpers = 1;
     int64_t seq_smem = 0;
     hs::SeqTileDev* d_seq_tiles = nullptr;
     uint64_t* d_seq_meta = nullptr;
@@ -158,15 +158,16 @@ void free_skeleton(hs_skeleton* sk) {
 }
 
 // The multi-tile program (HS_ALGO_TILES) of a skeleton that does not fit one CTA.
-// Defaults measured on C6 (2,000 x tree16384; tools/tune_tiles.py): chunk K = 3, two
-// skin buffers (the next tile's inverse binds load during this tile), 576-joint tiles;
+// Defaults measured on C6 (2,000 x tree16384; tools/tune_tiles.py): chunk K = 3, three
+// load stages, two skin buffers (the next tile's inverse binds load during this tile),
+// 512-joint tiles;
 // the largest tile up to the target whose program fits 224 compute threads and whose
 // shared memory fits the device; chunking RUNS or HEAVY, whichever needs fewer phase-2
 // descriptors.  Explicit options override each choice.
 hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<float>& ib) {
     const hs::Plan& P = sk->plan;
     const int K = o.chunk ? o.chunk : 3;
-    const int stages = o.stages ? o.stages : 2;
+    const int stages = o.stages ? o.stages : 3;
     const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 576;
     const int modes[2] = {hs::CHUNK_RUNS, hs::CHUNK_HEAVY};
     const int nmodes = o.chunking == 0 ? 2 : 1;
@@ -180,7 +181,7 @@ hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<
                                  : (o.chunking == 1 ? hs::CHUNK_CONSECUTIVE
                                                     : (o.chunking == 3 ? hs::CHUNK_RUNS : hs::CHUNK_HEAVY));
                 hs::SeqProgram sp;
-                if (!hs::build_seq_program(P, K, F, mode, 224, sp)) continue;
+                if (!hs::build_seq_program(P, K, F, mode, 224, sp)) continue;   // + the producer warp
                 if (hs::seq_smem_bytes(sp, stages, sbufs) > sk->smem_optin) continue;
                 if (!have || sp.rounds.size() < best.rounds.size()) { best = std::move(sp); have = true; }
             }
@@ -196,7 +197,7 @@ hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<
     sk->seq_stages = stages;
     sk->seq_K = K;
     sk->seq_smem = hs::seq_smem_bytes(sp, stages, sk->seq_sbufs);
-    sk->seq_threads = sp.T + 32;
+    sk->seq_threads = sp.T + 32;   // consumers and the TMA producer warp
     sk->seq_max_entries = (int)hs::seq_max_tile_entries(sp);
     std::vector<hs::SeqTileDev> tiles(sp.tiles.size());
     static_assert(sizeof(hs::SeqTileDev) == sizeof(hs::SeqTile), "SeqTile layout");
@@ -210,7 +211,7 @@ hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<
         (e = upload(&sk->d_seq_p1len, sp.p1len.data(), sp.p1len.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_round_off, sp.round_off.data(), sp.round_off.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_rounds, sp.rounds.data(), sp.rounds.size())) != cudaSuccess ||
-        (e = upload(&sk->d_seq_imp, sp.imp.data(), sp.imp.size())) != cudaSuccess ||
+        (e = upload(&sk->d_seq_imp, sp.exl.data(), sp.exl.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_runs, sp.runs.data(), sp.runs.size())) != cudaSuccess ||
         (e = upload(&sk->d_seq_ib, ibt.data(), ibt.size())) != cudaSuccess ||
         (e = hs::prepare_seq(K)) != cudaSuccess)
@@ -439,7 +440,7 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
 }
 
 static_assert(HS_MAX_BATCH <= hs::kMaxSegs, "one kernel segment per batch item");
-static_assert(hs::kSeqImportsPerThread == hs::kSeqImpPerThread, "multi-tile import staging width");
+static_assert(hs::kSeqInboxPiecesPerThread == hs::kSeqInboxPieces, "multi-tile inbox staging width");
 
 struct ChunkItem {
     const hs_skeleton* sk;
@@ -599,19 +600,16 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.p1len = sk->d_seq_p1len;
             a.round_off = sk->d_seq_round_off;
             a.rounds = sk->d_seq_rounds;
-            a.imp = reinterpret_cast<const int2*>(sk->d_seq_imp);
+            a.exl = reinterpret_cast<const int2*>(sk->d_seq_imp);
             a.runs = reinterpret_cast<const int4*>(sk->d_seq_runs);
             a.n_chars = n_chars;
             a.J = J; a.KT = sp.KT; a.F = sp.F; a.T = sp.T; a.S = sp.S; a.nQ = sp.nQ; a.n_exp = sp.n_exp;
             a.r2max = sp.R2max; a.max_imp = sp.max_imp; a.max_entries = sk->seq_max_entries;
             a.p_floats = (2 * sp.S + 2 * sp.nQ) * 12;
             a.r2p = (sp.R2max + 1 + 3) & ~3;
+            a.max_exl = sp.max_exl;
             a.entp = 0;
-            a.impp = 0;
-            for (const hs::SeqTile& tl : sp.tiles) {
-                a.entp = std::max(a.entp, (tl.n_entries + 3) & ~3);
-                a.impp = std::max(a.impp, (tl.n_imp + 1) & ~1);
-            }
+            for (const hs::SeqTile& tl : sp.tiles) a.entp = std::max(a.entp, (tl.n_entries + 3) & ~3);
             a.stages = sk->seq_stages; a.sbufs = sk->seq_sbufs; a.threads = sk->seq_threads;
             a.has_runs = sp.has_runs ? 1 : 0;
             a.bulk_piece = HS_BULK_PIECE;
@@ -627,21 +625,22 @@ hs_status scan_impl(const hs_skeleton* sk, const float* local, int64_t n_chars, 
             a.ws = ws;
             a.prof = nullptr;
             if (HS_PROF_HOOKS && std::getenv("HS_DEBUG_PROF")) {   // profiling builds only (synchronising)
-                cudaMalloc(reinterpret_cast<void**>(&a.prof), 10 * sizeof(unsigned long long));
-                cudaMemsetAsync(a.prof, 0, 10 * sizeof(unsigned long long), st);
+                cudaMalloc(reinterpret_cast<void**>(&a.prof), 12 * sizeof(unsigned long long));
+                cudaMemsetAsync(a.prof, 0, 12 * sizeof(unsigned long long), st);
             }
             e = hs::launch_seq(sk->seq_K, a, st);
             if (ws) cudaFreeAsync(ws, st);
             if (a.prof) {
-                unsigned long long h[10];
+                unsigned long long h[12];
                 cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);
                 const double nt = h[9] ? (double)h[9] : 1.0;
                 std::fprintf(stderr,
-                             "[hs prof seq] tiles=%llu cycles/tile: wait_prev %.0f issue %.0f wait_full %.0f "
-                             "phase1 %.0f bar %.0f phase2 %.0f wait_ib %.0f phase3 %.0f final_bar %.0f\n",
-                             h[9], h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt,
-                             h[7] / nt, h[8] / nt);
+                             "[hs prof seq] tiles=%llu cycles/tile: wait_prog %.0f read_prog %.0f wait_full %.0f "
+                             "phase1 %.0f bar %.0f phase2 %.0f (mark) %.0f wait_ib %.0f phase3 %.0f "
+                             "final_bar %.0f exports %.0f\n",
+                             h[9], h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[10] / nt, h[5] / nt,
+                             h[6] / nt, h[7] / nt, h[8] / nt, h[11] / nt);
                 cudaFree(a.prof);
             }
             break;
@@ -1216,7 +1215,7 @@ hs_status hs_plan_query(const hs_plan* p, int32_t what, int64_t* v) {
         case HS_Q_SEQ_SLOTS: *v = p->seq.S; break;
         case HS_Q_SEQ_R2MAX: *v = p->seq.R2max; break;
         case HS_Q_SEQ_ENTRIES: *v = (int64_t)p->seq.rounds.size(); break;
-        case HS_Q_SEQ_IMPORTS: *v = (int64_t)p->seq.imp.size() / 2; break;
+        case HS_Q_SEQ_IMPORTS: *v = (int64_t)p->seq.exl.size() / 2; break;
         case HS_Q_SEQ_RUNS: *v = (int64_t)p->seq.runs.size() / 4; break;
         case HS_Q_SEQ_QSLOTS: *v = p->seq.nQ; break;
         case HS_Q_ANCHOR_ROUNDS: {
@@ -1249,7 +1248,7 @@ hs_status hs_plan_export(const hs_plan* p, int32_t what, void* buf, int64_t buf_
         case HS_X_SEQ_P1LEN: return raw(p->seq.p1len.data(), p->seq.p1len.size() * sizeof(int32_t));
         case HS_X_SEQ_ROUND_OFF: return raw(p->seq.round_off.data(), p->seq.round_off.size() * sizeof(int32_t));
         case HS_X_SEQ_ROUNDS: return raw(p->seq.rounds.data(), p->seq.rounds.size() * sizeof(uint32_t));
-        case HS_X_SEQ_IMP: return raw(p->seq.imp.data(), p->seq.imp.size() * sizeof(int32_t));
+        case HS_X_SEQ_IMP: return raw(p->seq.exl.data(), p->seq.exl.size() * sizeof(int32_t));
         case HS_X_SEQ_RUNS: return raw(p->seq.runs.data(), p->seq.runs.size() * sizeof(int32_t));
         case HS_X_SEQ_IB_USER: return raw(p->seq.ib_user.data(), p->seq.ib_user.size() * sizeof(int32_t));
         case HS_X_LEVELS: tmp = P.level; break;

@@ -152,6 +152,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 // generic-proxy writes (shared AND global) ordered before later async-proxy (TMA) accesses
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -187,6 +190,11 @@ __device__ __forceinline__ void st3_hint(float* p, const float* v, uint64_t pol)
         asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + 4 * k),
                      "f"(v[4 * k]), "f"(v[4 * k + 1]), "f"(v[4 * k + 2]), "f"(v[4 * k + 3]), "l"(pol)
                      : "memory");
+}
+__device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
 }
 __device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
     float4 v;

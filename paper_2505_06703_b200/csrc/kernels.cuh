@@ -70,28 +70,32 @@ struct ChunkedArgs {
 // Multi-tile kernel (HS_ALGO_TILES): skeletons beyond one CTA.  A
 // persistent CTA takes whole characters (b, b + grid, ...) and walks each one's KT
 // tiles in topological order; cross-tile parents are final workspace values.
-// Multi-tile workspace imports staged in registers: at most this many 16-byte pieces per
-// compute thread per tile (3 x imports <= kSeqImpPerThread x threads; the plan checks).
-constexpr int kSeqImpPerThread = 16;
+// Multi-tile kernel: barrier header bytes, and the helper warp's inbox loads in flight
+// per lane (16-byte pieces)
+constexpr int kSeqHeaderBytes = 256;
+// inbox staging by the consumers: at most this many 16-byte pieces per thread
+// (3 x inbox rows <= kSeqInboxPieces x threads; the plan checks)
+constexpr int kSeqInboxPieces = 12;
 struct SeqTileDev {               // = hs::SeqTile (plan.hpp)
-    int32_t first, nj, R2, n_entries, rounds_off, n_imp, imp_off, n_runs, runs_off, T, pad[2];
+    int32_t n_early, nj, R2, n_entries, rounds_off, n_imp, imp_off, n_runs, runs_off, T, n_exl, exl_off;
 };
 struct SeqArgs {
     const float* local;        // [n_chars][J][12]
     float* gout;               // [n_chars][J][12]
     float* sout;               // [n_chars][J][12] or nullptr
-    float* ws;                 // [grid][n_exp][12]: exported global poses of the CTA's current character
+    float* ws;                 // [grid][n_exp][12]: the inboxes of the CTA's current character
     const float* ib;           // [KT][F][12] inverse bind by tile smem offset
     const SeqTileDev* tiles;   // [KT]
     const uint64_t* meta;      // [KT][T][K]
     const int32_t* p1len;      // [KT][T]
     const int32_t* round_off;  // [KT][R2max + 1]
     const uint32_t* rounds;    // concatenated descriptors
-    const int2* imp;           // (workspace slot, P location)
+    const int2* exl;           // export lists: (smem offset in the tile, workspace row)
     const int4* runs;          // (user start, smem offset, length, 0)
     int64_t n_chars;
     int32_t J, KT, F, T, S, nQ, n_exp, r2max, max_imp, max_entries;
-    int32_t r2p, entp, impp;   // program record widths: round_off row, phase-2 entries, import pairs (padded)
+    int32_t r2p, entp;         // program record widths: round_off row, phase-2 entries (padded to 4)
+    int32_t max_exl;           // export-list buffer (pairs, even)
     int32_t p_floats;          // (2S + 2 nQ) * 12: anchors (ping-pong) and two Q buffers
     int32_t stages, sbufs, threads, has_runs, bulk_piece;
     int64_t smem_bytes;

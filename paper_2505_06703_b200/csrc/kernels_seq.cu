@@ -42,27 +42,26 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     uint64_t* done = full + 4;
     uint64_t* ibfull = done + 4;   // S buffer holds the tile's inverse binds (TMA), S computed in place
     uint64_t* progfull = ibfull + 4;   // [3]: a tile program has landed (TMA by the producer)
+    uint64_t* exlfull = progfull + 3;  // [1]: the export list of the current tile has landed
     const int tile_f = a.F * 12;
-    float* LG = reinterpret_cast<float*>(smem + 128);
+    float* LG = reinterpret_cast<float*>(smem + kSeqHeaderBytes);
     float* SB = LG + NS * tile_f;
     float* P = SB + NSS * tile_f;
     // three program buffers (tile counter mod 3), each: meta [T][K] | p1 [T] | round_off
-    // [r2p] | rounds [entp] | import list [impp] (16-byte multiples, TMA destinations)
+    // [r2p] | rounds [entp] (16-byte multiples, TMA destinations)
     const int TK = a.T * K;
-    const int PROGW = TK * 2 + a.T + a.r2p + a.entp + 2 * a.impp;           // 4-byte words
+    const int PROGW = TK * 2 + a.T + a.r2p + a.entp;                        // 4-byte words
     int32_t* s_prog = reinterpret_cast<int32_t*>(P + a.p_floats);
-    SeqTileDev* s_tiles = reinterpret_cast<SeqTileDev*>(s_prog + 3 * PROGW); // [KT]
+    int2* s_exl = reinterpret_cast<int2*>(s_prog + 3 * PROGW);              // [max_exl]
+    SeqTileDev* s_tiles = reinterpret_cast<SeqTileDev*>(s_exl + a.max_exl);  // [KT]
     auto prog_meta = [&](int b) { return reinterpret_cast<const uint64_t*>(s_prog + b * PROGW); };
     auto prog_p1 = [&](int b) { return s_prog + b * PROGW + 2 * TK; };
     auto prog_roff = [&](int b) { return s_prog + b * PROGW + 2 * TK + a.T; };
     auto prog_rounds = [&](int b) {
         return reinterpret_cast<const uint32_t*>(s_prog + b * PROGW + 2 * TK + a.T + a.r2p);
     };
-    auto prog_imp = [&](int b) {
-        return reinterpret_cast<const int2*>(s_prog + b * PROGW + 2 * TK + a.T + a.r2p + a.entp);
-    };
 
-    const int nwc = (int)(blockDim.x >> 5) - 1;
+    const int nwc = (int)(blockDim.x >> 5) - 1;   // consumer warps; then the TMA producer warp
     const int NC = nwc * 32;
     const int warp = threadIdx.x >> 5;
     const int KT = a.KT;
@@ -73,17 +72,19 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
     for (int i = threadIdx.x; i < KT * (int)(sizeof(SeqTileDev) / 4); i += blockDim.x)
         reinterpret_cast<int32_t*>(s_tiles)[i] = __ldg(reinterpret_cast<const int32_t*>(a.tiles) + i);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+        // done: every consumer thread arrives after its share of the tile's exports
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], NC); }
         for (int s = 0; s < NSS; ++s) mbar_init(&ibfull[s], 1);
         for (int s = 0; s < 3; ++s) mbar_init(&progfull[s], 1);
+        mbar_init(exlfull, 1);
         fence_mbar_init();
     }
     __syncthreads();
 
     if (warp == nwc) {
         // ------------------------------------------------------------ producer
-        // lane 0 streams tiles, programs and inverse binds
-        const int lane = threadIdx.x & 31;
+        // lane 0 streams tiles, programs, inverse binds and export lists
+        if ((threadIdx.x & 31) != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
         const uint64_t stream_pol = policy_evict_first(), keep_pol = policy_evict_last();
         // tile cursors (character, tile) for the loads (NS ahead) and the stores
@@ -111,15 +112,13 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         auto issue_prog = [&](int buf) {
             const SeqTileDev tl = s_tiles[pk];
             const uint32_t b_meta = (uint32_t)TK * 8u, b_p1 = (uint32_t)a.T * 4u, b_ro = (uint32_t)a.r2p * 4u;
-            const uint32_t b_rd = (uint32_t)((tl.n_entries + 3) & ~3) * 4u, b_imp = (uint32_t)((tl.n_imp + 1) & ~1) * 8u;
-            mbar_expect_tx(&progfull[buf], b_meta + b_p1 + b_ro + b_rd + b_imp);
+            const uint32_t b_rd = (uint32_t)((tl.n_entries + 3) & ~3) * 4u;
+            mbar_expect_tx(&progfull[buf], b_meta + b_p1 + b_ro + b_rd);
             int32_t* d = s_prog + buf * PROGW;
             bulk_g2s(d, a.meta + (int64_t)pk * TK, b_meta, &progfull[buf]);
             bulk_g2s(d + 2 * TK, a.p1len + (int64_t)pk * a.T, b_p1, &progfull[buf]);
             bulk_g2s(d + 2 * TK + a.T, a.round_off + (int64_t)pk * a.r2p, b_ro, &progfull[buf]);
             if (b_rd) bulk_g2s(d + 2 * TK + a.T + a.r2p, a.rounds + tl.rounds_off, b_rd, &progfull[buf]);
-            if (b_imp)
-                bulk_g2s(d + 2 * TK + a.T + a.r2p + a.entp, a.imp + tl.imp_off, b_imp, &progfull[buf]);
             if (++pk == KT) pk = 0;
         };
         const bool do_skin = a.sout != nullptr;
@@ -136,7 +135,15 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 bulk_g2s_hint(dst + o, src + o, min(piece, bytes - o), &ibfull[buf], keep_pol);
             if (++ibk == KT) ibk = 0;
         };
-        if (lane == 0) {
+        // the export list of a tile into the (single) export-list buffer
+        auto issue_exl = [&](int j) {
+            const SeqTileDev tl = s_tiles[j];
+            const uint32_t bytes = (uint32_t)((tl.n_exl + 1) & ~1) * 8u;
+            mbar_expect_tx(exlfull, bytes);
+            if (bytes) bulk_g2s(s_exl, a.exl + tl.exl_off, bytes, exlfull);
+        };
+        {
+            if (my_tiles > 0) issue_exl(0);
             for (int64_t it = 0; it < my_tiles && it < 3; ++it) issue_prog((int)it);
             for (int64_t it = 0; it < my_tiles && it < NS; ++it) issue_load((int)it);
             if (do_skin)
@@ -146,10 +153,10 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
             mbar_wait(&done[stage], phase);
-            if (lane == 0 && it + 3 < my_tiles) issue_prog(pbuf);   // tile it no longer reads its program
+            const SeqTileDev tl = s_tiles[sk];
+            if (it + 3 < my_tiles) issue_prog(pbuf);   // tile it no longer reads its program
             if (++pbuf == 3) pbuf = 0;
-            if (lane == 0) {
-                const SeqTileDev tl = s_tiles[sk];
+            {
                 const int64_t cbase = sc * J * 12;
                 const char* sg = reinterpret_cast<const char*>(LG + stage * tile_f);
                 const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
@@ -165,6 +172,9 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                     }
                 }
                 bulk_commit();
+            }
+            {
+                if (it + 1 < my_tiles) issue_exl(sk + 1 < KT ? sk + 1 : 0);   // the list buffer is free
                 bulk_wait_read<0>();
                 if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
                 if (it + NS < my_tiles) issue_load(stage);
@@ -173,22 +183,24 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             if (++stage == NS) { stage = 0; phase ^= 1u; }
             if (++sb == NSS) sb = 0;
         }
-        if (lane == 0) bulk_wait_all();
+        bulk_wait_all();
         return;
     }
 
     // ---------------------------------------------------------------- consumers
-    // A tile's program (chunk metadata, phase-1 info, phase-2 tables, the import list)
-    // arrives by TMA two tiles ahead (program buffer = tile counter parity).  Its Q
-    // values arrive one tile ahead: parents from tiles <= k - 2 are imported from the
-    // workspace (L2) by cp.async issued between phase 2 and phase 3 of tile k - 1 and
-    // awaited at the top of tile k; parents from tile k - 1 are forwarded into Q by the
-    // threads that compute them in phase 3 of tile k - 1.  Q buffers alternate with the
-    // tile index k (the plan bakes the locations in).
+    // A tile's program (chunk metadata, phase-1 info, phase-2 tables) and its export
+    // list arrive by TMA ahead of it.  Its Q values: parents in tile k - 1 are
+    // forwarded into Q by the threads that compute them in phase 3 of tile k - 1;
+    // parents in tiles <= k - 2 form the tile's inbox, staged during tile k - 1 through
+    // registers (coalesced 16-byte loads): the rows exported by tiles <= k - 3 at the
+    // top of tile k - 1, the rows exported by tile k - 2 after its phase-2 barrier.
+    // After phase 3 each tile stores its exports (the joints tiles two or more later
+    // read) into their inboxes.  Q buffers alternate with the tile index k (the plan
+    // bakes the locations in).
     const int t = threadIdx.x;
-    float* wsb = a.ws + (int64_t)blockIdx.x * a.n_exp * 12;   // this CTA's workspace
     const bool skin = a.sout != nullptr;
-    const uint64_t ws_pol = policy_evict_last();   // the workspace is re-read by later tiles
+    float* wsb = a.ws + (int64_t)blockIdx.x * a.n_exp * 12;   // this CTA's workspace (inboxes)
+    const uint64_t ws_pol = policy_evict_last();
     const int qb0 = 2 * a.S, nQ = a.nQ;
     // profiling builds (HS_PROF_HOOKS): consumer thread 0's cycles per phase, summed
     long long prof_last = 0;
@@ -217,6 +229,23 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         }
 #pragma unroll
         for (int s = 0; s < K; ++s) m[s] = t < a.T ? prog_meta(pb)[t * K + s] : kSeqMetaNone;
+        // the next tile's inbox: the rows exported by tiles <= k - 2 (before the barriers
+        // of tile k - 1) now, the rest after this tile's phase-2 barrier
+        float4 inb[kSeqInboxPieces];
+        int nin3 = 0, ine3 = 0, inq = 0;
+        const float* insrc = wsb;
+        if (it + 1 < my_tiles) {
+            const SeqTileDev tn = s_tiles[k + 1 < KT ? k + 1 : 0];
+            nin3 = 3 * tn.n_imp;
+            ine3 = 3 * tn.n_early;
+            inq = (qb0 + ((k + 1) & 1) * nQ) * 12;
+            insrc = wsb + (int64_t)tn.imp_off * 12;
+#pragma unroll
+            for (int u = 0; u < kSeqInboxPieces; ++u) {
+                const int q = t + u * NC;
+                if (q < ine3) inb[u] = ldg4_hint(insrc + 4 * q, ws_pol);
+            }
+        }
         prof_mark(1);
         mbar_wait(&full[stage], phase);
         prof_mark(2);
@@ -301,25 +330,14 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             bar_consumers(NC);
         }
 
-        // the next tile's workspace imports (parents in tiles <= k - 1: final), loaded
-        // into registers now, stored into its Q buffer after phase 3 (the loads complete
-        // under phase 3); three consecutive lanes per 48-byte row
-        float4 impv[kSeqImpPerThread];
-        int nimp3 = 0;
-        const int pbn = pb == 2 ? 0 : pb + 1;   // the next tile's program buffer
-        const int2* lst = prog_imp(pbn);
-        if (it + 1 < my_tiles) {
-            mbar_wait(&progfull[pbn], pb == 2 ? pphase ^ 1u : pphase);
-            nimp3 = 3 * s_tiles[k + 1 < KT ? k + 1 : 0].n_imp;
+        prof_mark(10);
+        // the rest of the next tile's inbox: rows exported by the previous tile (its
+        // exports preceded this tile's phase-2 barrier)
+        if (ine3 < nin3) {
 #pragma unroll
-            for (int u = 0; u < kSeqImpPerThread; ++u) {
+            for (int u = 0; u < kSeqInboxPieces; ++u) {
                 const int q = t + u * NC;
-                if (q < nimp3) {
-                    const int i = q / 3, c = q - 3 * i;
-                    const int2 e = lst[i];
-                    HS_BOUND(e.x >= 0 && e.x < a.n_exp && e.y >= qb0 && (e.y + 1) * 12 <= a.p_floats);
-                    impv[u] = ldg4_hint(wsb + (int64_t)e.x * 12 + 4 * c, ws_pol);
-                }
+                if (q >= ine3 && q < nin3) inb[u] = ldg4_hint(insrc + 4 * q, ws_pol);
             }
         }
         // phase 3: final fold, G in place, S into the S buffer, exports to the workspace
@@ -334,7 +352,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 const int src = seq_src(m[s]);
                 if (src == kSrcNone) continue;
                 const int off = seq_off(m[s]);
-                const int ex = seq_ex(m[s]), fw = seq_fwd(m[s]);
+                const int fw = seq_fwd(m[s]);
                 float l[12];
                 HS_BOUND(off >= 0 && off < tl.nj);
                 ld3(L + off * 12, l);
@@ -378,10 +396,6 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                     compose(pa, l, acc3);
                 }
                 st3(L + off * 12, acc3);
-                if (ex) {   // a child in tile k + 2 or later: export the global pose (L2)
-                    HS_BOUND(ex - 1 < a.n_exp);
-                    st3_hint(wsb + (int64_t)(ex - 1) * 12, acc3, ws_pol);
-                }
                 if (fw) {   // a child in tile k + 1: forward into that tile's Q buffer
                     HS_BOUND(fw - 1 < nQ);
                     st3(P + (qb0 + ((k + 1) & 1) * nQ + fw - 1) * 12, acc3);
@@ -394,22 +408,37 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             }
         }
 #pragma unroll
-        for (int u = 0; u < kSeqImpPerThread; ++u) {
+        for (int u = 0; u < kSeqInboxPieces; ++u) {
             const int q = t + u * NC;
-            if (q < nimp3) {
-                const int i = q / 3, c = q - 3 * i;
-                *reinterpret_cast<float4*>(P + lst[i].y * 12 + 4 * c) = impv[u];
-            }
+            if (q < nin3) *reinterpret_cast<float4*>(P + inq + 4 * q) = inb[u];
         }
         prof_mark(7);
         fence_proxy_async();   // smem G/S for the bulk stores
-        bar_consumers(NC);
+        bar_consumers(NC);     // the whole tile's G is in shared memory
         prof_mark(8);
         if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 9, 1ull);
-        if (t == 0) mbar_arrive(&done[stage]);
+        // exports: the tile's joints that later tiles read (two or more tiles on) into
+        // their inboxes; consecutive threads store consecutive 16-byte pieces of each
+        // contiguous inbox range (coalesced)
+        {
+            const int n3 = 3 * tl.n_exl;
+            if (n3) {
+                mbar_wait(exlfull, (uint32_t)(it & 1));
+                for (int q = t; q < n3; q += NC) {
+                    const int e = q / 3, c = q - 3 * e;
+                    const int2 x = s_exl[e];
+                    HS_BOUND(x.x >= 0 && x.x < tl.nj && x.y >= 0 && x.y < a.n_exp);
+                    st4_hint(wsb + (int64_t)x.y * 12 + 4 * c, *reinterpret_cast<const float4*>(L + x.x * 12 + 4 * c),
+                             ws_pol);
+                }
+            }
+        }
+        prof_mark(11);
+        mbar_arrive(&done[stage]);   // every consumer thread (count NC): its exports read the stage
         if (++stage == NS) { stage = 0; phase ^= 1u; }
         if (++sb == NSS) { sb = 0; sphase ^= 1u; }   // parity of use it / NSS of buffer sb
         if (++pb == 3) { pb = 0; pphase ^= 1u; }     // program buffer use (it / 3) parity
+
         if (++k == KT) k = 0;
     }
 }

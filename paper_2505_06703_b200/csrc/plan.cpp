@@ -633,12 +633,14 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     //     segment like a root, but its source is the parent's final global pose in a
     //     Q location (Q nodes are final roots of the anchor forest: pointer jumping
     //     links to them and stops);
-    //   * the Q values of tile j are delivered one tile ahead: a parent in tile j - 1 is
-    //     FORWARDED by the thread that computes it in phase 3 of tile j - 1 (a shared-
-    //     memory store into tile j's Q buffer); a parent in tile <= j - 2 was stored to
-    //     a workspace slot in its own tile's phase 3 and is IMPORTED by cp.async at the
-    //     start of tile j - 1.  Two Q buffers alternate with the tile index.
-    //   * workspace slots are reused once their last import has been issued.
+    //   * the Q values of tile j: a parent in tile j - 1 is FORWARDED by the thread that
+    //     computes it in phase 3 of tile j - 1 (a shared-memory store into tile j's Q
+    //     buffer); the parents in tiles <= j - 2 form tile j's INBOX, a contiguous
+    //     workspace range ordered by source tile: each source tile i writes its share
+    //     (a contiguous sub-range) once it is done (the producer warp, coalesced stores
+    //     from the finished tile in shared memory), and the inbox reaches tile j's Q
+    //     buffer in ONE bulk copy issued when tile j - 2 is done.  Two Q buffers
+    //     alternate with the tile index; inbox entries come first in Q.
     sp = SeqProgram();
     const int32_t n = p.n;
     if (F < 32 || n <= 0) return false;
@@ -646,20 +648,14 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     sp.F = F;
     sp.KT = (n + F - 1) / F;
     const int KT = sp.KT;
-    // consumers: for every joint, the tiles (after its own) holding a child
-    std::vector<int32_t> last_ws_use(n, -1);   // last consumer tile >= own + 2 (-1: none)
-    for (int32_t i = 0; i < n; ++i) {
-        const int32_t q = p.ipar[i];
-        if (q < 0) continue;
-        const int32_t tq = q / F, ti = i / F;
-        if (ti >= tq + 2) last_ws_use[q] = std::max(last_ws_use[q], ti);
-    }
     struct TileTmp {
         ChunkDecomp d;
         std::vector<int32_t> q_of;         // per local node with an external parent: Q index
         std::vector<int32_t> imports;      // Q index -> external parent (internal position)
         std::vector<int32_t> idx;          // raw slot -> coloured slot
         int S = 0;
+        int32_t n_inbox = 0;               // imports[0 .. n_inbox): the workspace inbox
+        int32_t inbox_base = 0;            // first workspace row of the inbox
     };
     std::vector<TileTmp> tmp(KT);
     for (int k = 0; k < KT; ++k) {
@@ -676,6 +672,28 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
                 if (qmap[q] < 0) { qmap[q] = (int32_t)tt.imports.size(); tt.imports.push_back(q); }
                 tt.q_of[li] = qmap[q];
             }
+        }
+        // Q order: the inbox (parents in tiles <= k - 2, by source position: grouped by
+        // source tile), then the forwarded parents (tile k - 1)
+        {
+            std::vector<int32_t> order_q(tt.imports.size());
+            for (size_t z = 0; z < order_q.size(); ++z) order_q[z] = (int32_t)z;
+            std::stable_sort(order_q.begin(), order_q.end(), [&](int32_t x, int32_t y) {
+                const bool fx = tt.imports[x] / F >= k - 1, fy = tt.imports[y] / F >= k - 1;
+                if (fx != fy) return !fx;
+                return tt.imports[x] < tt.imports[y];
+            });
+            std::vector<int32_t> newidx(order_q.size()), imp2(order_q.size());
+            for (size_t z = 0; z < order_q.size(); ++z) {
+                newidx[order_q[z]] = (int32_t)z;
+                imp2[z] = tt.imports[order_q[z]];
+            }
+            tt.imports.swap(imp2);
+            for (auto& q : tt.q_of)
+                if (q >= 0) q = newidx[q];
+            tt.n_inbox = 0;
+            for (int32_t q : tt.imports)
+                if (q / F < k - 1) ++tt.n_inbox;
         }
         tt.d = decompose(lpar, K, mode, &pos, true);
         const ChunkDecomp& d = tt.d;
@@ -708,21 +726,12 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
     const int32_t S = sp.S, nQ = sp.nQ;
     auto qloc = [&](int k, int32_t z) { return 2 * S + (k & 1) * nQ + z; };
     if (S >= (1 << 12) || 2 * S + 2 * nQ >= (1 << 12) - 8 || F > 1024) return false;   // meta field widths
-    // workspace slots: joint q (tile tq) needs one iff a child sits in a tile >= tq + 2.
-    // Numbered in the order phase 3 stores them (tile, chunk slot, thread), so the
-    // exporting lanes of one warp store to consecutive rows (coalesced stores); no reuse.
-    std::vector<int32_t> ws_slot(n, -1);
+    // workspace: the inboxes of all tiles, back to back (rows of 48 B per CTA)
     for (int k = 0; k < KT; ++k) {
-        const ChunkDecomp& d = tmp[k].d;
-        const int32_t a = k * F;
-        for (int s = 0; s < K; ++s)
-            for (size_t t = 0; t < d.lists.size(); ++t)
-                if (s < (int)d.lists[t].size()) {
-                    const int32_t i = a + d.lists[t][s];
-                    if (last_ws_use[i] >= 0) ws_slot[i] = sp.n_exp++;
-                }
+        tmp[k].inbox_base = sp.n_exp;
+        sp.n_exp += tmp[k].n_inbox;
     }
-    if (sp.n_exp >= (1 << 16) - 1) return false;
+    if (sp.n_exp >= (1 << 24)) return false;
     // encoded meta (seq_meta_* in kernels.cuh): off 10 | src + 8 13 | own + 1 13 | ex 16 | fwd 12
     auto enc = [](int32_t off, int32_t src, int32_t own, int32_t ex, int32_t fwd) {
         return (uint64_t)off | ((uint64_t)(src + 8) << 10) | ((uint64_t)(own + 1) << 23) | ((uint64_t)ex << 36) |
@@ -742,12 +751,12 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         // the next tile's Q index of each of this tile's joints it imports (forwarding)
         std::vector<int32_t> fwd_of(nj, -1);
         if (k + 1 < KT)
-            for (size_t z = 0; z < tmp[k + 1].imports.size(); ++z) {
+            for (size_t z = (size_t)tmp[k + 1].n_inbox; z < tmp[k + 1].imports.size(); ++z) {
                 const int32_t q = tmp[k + 1].imports[z];
                 if (q >= a) fwd_of[q - a] = (int32_t)z;
             }
         SeqTile st{};
-        st.first = a;
+        st.n_early = 0;
         st.nj = nj;
         st.T = T;
         // anchor forest: tile anchors 0..Sraw-1 (ping-pong), Q nodes Sraw..Sraw+nq-1 (final)
@@ -808,23 +817,29 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
                 else src = d.src[li];
                 const int32_t own = d.slot_of[li] >= 0 ? tt.idx[d.slot_of[li]] : -1;
                 if (own >= 0 || in_run) p1 = s + 1;
-                const int32_t ex = ws_slot[a + li] + 1;
                 const int32_t fw = fwd_of[li] + 1;
-                sp.meta[((size_t)k * sp.T + t) * K + s] = enc(li, src, own, ex, fw);
+                sp.meta[((size_t)k * sp.T + t) * K + s] = enc(li, src, own, 0, fw);
             }
             p1 |= info;
         }
-        // imports from the workspace (parents in tiles <= k - 2; tile k - 1 forwards),
-        // TMA runs (maximal user-label runs over the tile's smem order), IB map
-        st.imp_off = (int32_t)sp.imp.size() / 2;
-        for (int32_t z = 0; z < nq; ++z) {
-            const int32_t q = tt.imports[z];
-            if (q / F >= k - 1) continue;   // forwarded by the previous tile
-            sp.imp.push_back(ws_slot[q]);
-            sp.imp.push_back(qloc(k, z));
-            ++st.n_imp;
-        }
-        while (sp.imp.size() % 4) sp.imp.push_back(0);         // 16-byte tile records (TMA)
+        // the inbox (workspace rows read by tile k) and the export list of tile k: for
+        // every later tile j >= k + 2, its inbox entries whose parent is in tile k (a
+        // contiguous sub-range, rows ascending): (smem offset in tile k, workspace row)
+        st.n_imp = tt.n_inbox;
+        st.imp_off = tt.inbox_base;
+        for (int32_t z = 0; z < tt.n_inbox; ++z)   // the inbox is sorted by parent: a prefix
+            if (tt.imports[z] / F <= k - 3) st.n_early = z + 1;
+        st.exl_off = (int32_t)sp.exl.size() / 2;
+        for (int j = k + 2; j < KT; ++j)
+            for (int32_t z = 0; z < tmp[j].n_inbox; ++z) {
+                const int32_t q = tmp[j].imports[z];
+                if (q / F != k) continue;
+                sp.exl.push_back(q - a);
+                sp.exl.push_back(tmp[j].inbox_base + z);
+                ++st.n_exl;
+            }
+        while (sp.exl.size() % 4) sp.exl.push_back(0);   // 16-byte tile records (TMA)
+        sp.max_exl = std::max(sp.max_exl, (st.n_exl + 1) & ~1);
         st.runs_off = (int32_t)sp.runs.size() / 4;
         for (int32_t li = 0; li < nj;) {
             int32_t len = 1;
@@ -835,7 +850,7 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         }
         for (int32_t li = 0; li < nj; ++li) sp.ib_user[(size_t)k * F + li] = p.order[a + li];
         sp.max_imp = std::max(sp.max_imp, st.n_imp);
-        if (3 * st.n_imp > kSeqImportsPerThread * sp.T) return false;   // register-staged imports
+        if (3 * st.n_imp > kSeqInboxPiecesPerThread * sp.T) return false;   // register-staged inbox
         sp.max_runs = std::max(sp.max_runs, st.n_runs);
         sp.tiles.push_back(st);
     }
@@ -857,19 +872,17 @@ int64_t seq_smem_bytes(const SeqProgram& sp, int stages, int sbufs) {
     // barriers | stages x tile | sbufs x tile | P (2S anchors + 2 x nQ Q buffers) |
     // 2 program buffers (meta | p1 | round_off | rounds | import list) | tile descriptors
     const int64_t tileb = (int64_t)sp.F * 48;
-    int64_t b = 128 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + 2 * sp.nQ) * 48;
+    int64_t b = 256 + (int64_t)(stages + sbufs) * tileb + (int64_t)(2 * sp.S + 2 * sp.nQ) * 48;   // kSeqHeaderBytes
     b += 3 * 4 * seq_prog_words(sp);   // three program buffers
+    b += (int64_t)sp.max_exl * 8;      // the export-list buffer
     b += (int64_t)sp.KT * (int64_t)sizeof(SeqTile);
     return b;
 }
 
 int64_t seq_prog_words(const SeqProgram& sp) {
-    int64_t entp = 0, impp = 0;
-    for (const SeqTile& t : sp.tiles) {
-        entp = std::max<int64_t>(entp, (t.n_entries + 3) & ~3);
-        impp = std::max<int64_t>(impp, (t.n_imp + 1) & ~1);
-    }
-    return 2LL * sp.T * sp.K + sp.T + ((sp.R2max + 1 + 3) & ~3) + entp + 2 * impp;
+    int64_t entp = 0;
+    for (const SeqTile& t : sp.tiles) entp = std::max<int64_t>(entp, (t.n_entries + 3) & ~3);
+    return 2LL * sp.T * sp.K + sp.T + ((sp.R2max + 1 + 3) & ~3) + entp;
 }
 
 void block_layout(const Plan& p, int B, std::vector<int32_t>& block_of, std::vector<int32_t>& mpob) {

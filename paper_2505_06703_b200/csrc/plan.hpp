@@ -84,15 +84,15 @@ struct SplitProgram {
 // that parent's global pose from an imported slot Q (a final root of the anchor
 // forest); joints with a child in a later tile export their global pose to a
 // per-CTA workspace slot in phase 3.
-constexpr int kSeqImportsPerThread = 16;   // = kernels.cuh kSeqImpPerThread (16-byte pieces)
+constexpr int kSeqInboxPiecesPerThread = 12;   // = kernels.cuh kSeqInboxPieces
 struct SeqTile {
-    int32_t first, nj;            // internal positions [first, first + nj)
+    int32_t n_early, nj;          // inbox rows from tiles <= k - 3 (a prefix); joints [k F, k F + nj)
     int32_t R2, n_entries;        // pointer-jumping rounds and phase-2 descriptors
     int32_t rounds_off;           // offset into rounds; round_off rows are per tile
-    int32_t n_imp, imp_off;       // imports: (workspace slot, P location) pairs
+    int32_t n_imp, imp_off;       // inbox: workspace rows [imp_off, imp_off + n_imp) -> Q 0..n_imp
     int32_t n_runs, runs_off;     // TMA runs: (user start, smem offset, length)
     int32_t T;                    // compute threads with work
-    int32_t pad[2];
+    int32_t n_exl, exl_off;       // export list: pairs [exl_off, exl_off + n_exl) of exl
 };
 struct SeqProgram {
     int K = 0, F = 0, T = 0, KT = 0;   // chunk, joints per tile (max), threads (max), tiles
@@ -100,7 +100,8 @@ struct SeqProgram {
     int nQ = 0;                         // Q slots per buffer (max imports of a tile); tile k's Q
                                         // buffer is 2S + (k & 1) nQ .. + nQ
     int R2max = 0, max_entries = 0, max_imp = 0, max_runs = 0;
-    int n_exp = 0;                      // workspace slots per character (reused once free)
+    int max_exl = 0;                    // largest export list of a tile (pairs, padded to 2)
+    int n_exp = 0;                      // workspace rows per CTA: all tiles' inboxes
     bool has_runs = false;
     std::vector<SeqTile> tiles;
     std::vector<uint64_t> meta;         // [KT][T][K]: off 10 | src + 8 13 | own + 1 13 | ws slot + 1 16 | fwd + 1 12
@@ -108,7 +109,8 @@ struct SeqProgram {
     // per-tile records are 16-byte aligned and sized (the producer warp loads them by TMA)
     std::vector<int32_t> round_off;     // [KT][R2max + 1 rounded up to 4], relative to rounds_off
     std::vector<uint32_t> rounds;       // per tile, padded to 4: phase-2 descriptors (TileProgram encoding)
-    std::vector<int32_t> imp;           // per tile, padded to 2 pairs: (workspace slot, Q location)
+    std::vector<int32_t> exl;           // export lists: (smem offset in the tile, workspace row)
+                                        // pairs, each tile's list padded to 2 pairs (TMA)
     std::vector<int32_t> runs;          // [..][4]: user start, smem offset, length, 0
     std::vector<int32_t> ib_user;       // [KT][F]: user label at each smem offset (-1 = none)
 };

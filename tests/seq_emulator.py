@@ -2,12 +2,11 @@
 
 Replays the exported multi-tile program (``Plan.export("seq_*")``: the tables
 ``hs_skeleton_create`` uploads for HS_ALGO_TILES) for one character, tile by tile in
-the kernel's order, in fp64 on 4x4 homogeneous matrices: at the top of tile k the
-NEXT tile's workspace imports land in its Q buffer (so a reused workspace slot must not
-have been overwritten yet), then phase 1 chunk folds publishing anchors, phase 2a run
-scans, phase 2 pointer jumping (ping-pong locations as encoded, Q locations final),
-phase 3 re-folds with exports to the workspace, forwards into the next tile's Q buffer
-and the bind epilogue.  On the
+the kernel's order, in fp64 on 4x4 homogeneous matrices: phase 1 chunk folds
+publishing anchors, phase 2a run scans, phase 2 pointer jumping (ping-pong locations
+as encoded, Q locations final), phase 3 re-folds with forwards into the next tile's Q
+buffer and the bind epilogue; then the tile's export list fills later tiles' inboxes
+and tile k + 2's inbox lands in its Q buffer (each inbox row must have been written).  On the
 exact-arithmetic family every association order gives the same bits, so a bitwise
 match with the oracle pins the encoding (tiles, runs, imports, exports, locations).
 """
@@ -32,7 +31,7 @@ def run(plan, local, inv_bind=None):
     p1len = plan.export("seq_p1len")
     round_off = plan.export("seq_round_off")
     rounds = plan.export("seq_rounds")
-    imp = plan.export("seq_imp")
+    exl = plan.export("seq_imp")       # export lists: (smem offset, workspace row)
     runs = plan.export("seq_runs")
     ib_user = plan.export("seq_ib_user")
     S = plan.query("seq_slots")
@@ -62,16 +61,6 @@ def run(plan, local, inv_bind=None):
         assert list(ib_user[k][:nj]) == user_of
         for loc in [x for x in P if x < 2 * S]:
             del P[loc]                                   # anchors are per tile; Q buffers persist
-        nb = 2 * S + ((k + 1) & 1) * nQ
-        for loc in [x for x in P if nb <= x < nb + nQ]:
-            del P[loc]                                   # the next tile's Q buffer starts empty
-        if k + 1 < KT:   # top of tile k: the next tile's workspace imports into its Q buffer
-            t1 = tiles[k + 1]
-            for z in range(t1[5]):
-                slot, loc = imp[t1[6] + z]
-                assert 2 * S + ((k + 1) & 1) * nQ <= loc < 2 * S + ((k + 1) & 1) * nQ + nQ
-                assert slot in ws, "import of a value not exported before"
-                P[int(loc)] = ws[int(slot)]
         dec = [[decode(meta[k, t, s]) for s in range(K)] for t in range(T)]
         info = [int(x) for x in p1len[k]]
         p1 = [x & 0xFF for x in info]
@@ -134,10 +123,31 @@ def run(plan, local, inv_bind=None):
                 u = user_of[off]
                 G[u] = acc[:3].copy()
                 SK[u] = (acc @ _h(IB[u]))[:3]
-                if ex:
-                    ws[ex - 1] = acc.copy()
+                assert ex == 0                           # exports go through the export list
                 if fw:
                     assert k + 1 < KT and fw - 1 < nQ
                     P[2 * S + ((k + 1) & 1) * nQ + fw - 1] = acc.copy()
+        # tile k done: its exports into the later inboxes, then tile k + 2's inbox lands
+        # in its Q buffer (k + 2) & 1 (the kernel's producer warp, after tile k is done)
+        Gt = {o: None for o in range(nj)}
+        for t in range(T):
+            for s_ in range(K):
+                off, ex, src, own, fw = dec[t][s_]
+                if src != SRC_NONE:
+                    Gt[off] = True
+        n_exl, exl_off = tiles[k][10], tiles[k][11]
+        for e in range(n_exl):
+            off, row = exl[exl_off + e]
+            assert Gt[int(off)], "export of a joint the tile did not compute"
+            u = user_of[int(off)]
+            ws[int(row)] = _h(G[u])
+        if k + 2 < KT:
+            nb = 2 * S + ((k + 2) & 1) * nQ
+            for loc in [x for x in P if nb <= x < nb + nQ]:
+                del P[loc]
+            n_in, base = tiles[k + 2][5], tiles[k + 2][6]
+            for z in range(n_in):
+                assert base + z in ws, "inbox row not written before it is read"
+                P[nb + z] = ws[base + z]
     assert (covered == 1).all(), "every joint is loaded exactly once"
     return np.stack(G), np.stack(SK)
