@@ -440,7 +440,8 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
 }
 
 static_assert(HS_MAX_BATCH <= hs::kMaxSegs, "one kernel segment per batch item");
-static_assert(hs::kSeqInboxPiecesPerThread == hs::kSeqInboxPieces, "multi-tile inbox staging width");
+static_assert(hs::kSeqInboxPiecesPerThread == hs::kSeqInboxPieces && hs::kSeqInboxLatePerThread == hs::kSeqInboxLate,
+              "multi-tile inbox staging width");
 
 struct ChunkItem {
     const hs_skeleton* sk;

@@ -75,7 +75,8 @@ struct ChunkedArgs {
 constexpr int kSeqHeaderBytes = 256;
 // inbox staging by the consumers: at most this many 16-byte pieces per thread
 // (3 x inbox rows <= kSeqInboxPieces x threads; the plan checks)
-constexpr int kSeqInboxPieces = 12;
+constexpr int kSeqInboxPieces = 9;   // rows from tiles <= k - 2 (loaded at the top of tile k - 1)
+constexpr int kSeqInboxLate = 4;     // rows from tile k - 1 (loaded after its phase-2 barrier)
 struct SeqTileDev {               // = hs::SeqTile (plan.hpp)
     int32_t n_early, nj, R2, n_entries, rounds_off, n_imp, imp_off, n_runs, runs_off, T, n_exl, exl_off;
 };

@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         for (int s = 0; s < K; ++s) m[s] = t < a.T ? prog_meta(pb)[t * K + s] : kSeqMetaNone;
         // the next tile's inbox: the rows exported by tiles <= k - 2 (before the barriers
         // of tile k - 1) now, the rest after this tile's phase-2 barrier
-        float4 inb[kSeqInboxPieces];
-        int nin3 = 0, ine3 = 0, inq = 0;
+        float4 inb[kSeqInboxPieces], inl[kSeqInboxLate];   // early / late pieces (distinct registers:
+        int nin3 = 0, ine3 = 0, inq = 0;                    // a late load must not wait for an early one)
         const float* insrc = wsb;
         if (it + 1 < my_tiles) {
             const SeqTileDev tn = s_tiles[k + 1 < KT ? k + 1 : 0];
@@ -335,9 +335,9 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         // exports preceded this tile's phase-2 barrier)
         if (ine3 < nin3) {
 #pragma unroll
-            for (int u = 0; u < kSeqInboxPieces; ++u) {
-                const int q = t + u * NC;
-                if (q >= ine3 && q < nin3) inb[u] = ldg4_hint(insrc + 4 * q, ws_pol);
+            for (int u = 0; u < kSeqInboxLate; ++u) {
+                const int q = ine3 + t + u * NC;
+                if (q < nin3) inl[u] = ldg4_hint(insrc + 4 * q, ws_pol);
             }
         }
         // phase 3: final fold, G in place, S into the S buffer, exports to the workspace
@@ -410,7 +410,12 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
 #pragma unroll
         for (int u = 0; u < kSeqInboxPieces; ++u) {
             const int q = t + u * NC;
-            if (q < nin3) *reinterpret_cast<float4*>(P + inq + 4 * q) = inb[u];
+            if (q < ine3) *reinterpret_cast<float4*>(P + inq + 4 * q) = inb[u];
+        }
+#pragma unroll
+        for (int u = 0; u < kSeqInboxLate; ++u) {
+            const int q = ine3 + t + u * NC;
+            if (q < nin3) *reinterpret_cast<float4*>(P + inq + 4 * q) = inl[u];
         }
         prof_mark(7);
         fence_proxy_async();   // smem G/S for the bulk stores

@@ -850,7 +850,9 @@ bool build_seq_program(const Plan& p, int K, int F, int mode, int max_threads, S
         }
         for (int32_t li = 0; li < nj; ++li) sp.ib_user[(size_t)k * F + li] = p.order[a + li];
         sp.max_imp = std::max(sp.max_imp, st.n_imp);
-        if (3 * st.n_imp > kSeqInboxPiecesPerThread * sp.T) return false;   // register-staged inbox
+        if (3 * st.n_early > kSeqInboxPiecesPerThread * sp.T ||               // register-staged inbox
+            3 * (st.n_imp - st.n_early) > kSeqInboxLatePerThread * sp.T)
+            return false;
         sp.max_runs = std::max(sp.max_runs, st.n_runs);
         sp.tiles.push_back(st);
     }

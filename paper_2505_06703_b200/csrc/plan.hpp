@@ -84,7 +84,8 @@ struct SplitProgram {
 // that parent's global pose from an imported slot Q (a final root of the anchor
 // forest); joints with a child in a later tile export their global pose to a
 // per-CTA workspace slot in phase 3.
-constexpr int kSeqInboxPiecesPerThread = 12;   // = kernels.cuh kSeqInboxPieces
+constexpr int kSeqInboxPiecesPerThread = 9;    // = kernels.cuh kSeqInboxPieces
+constexpr int kSeqInboxLatePerThread = 4;      // = kernels.cuh kSeqInboxLate
 struct SeqTile {
     int32_t n_early, nj;          // inbox rows from tiles <= k - 3 (a prefix); joints [k F, k F + nj)
     int32_t R2, n_entries;        // pointer-jumping rounds and phase-2 descriptors
