@@ -191,6 +191,10 @@ __device__ __forceinline__ void st3_hint(float* p, const float* v, uint64_t pol)
                      "f"(v[4 * k]), "f"(v[4 * k + 1]), "f"(v[4 * k + 2]), "f"(v[4 * k + 3]), "l"(pol)
                      : "memory");
 }
+// invalidate one 128-byte L2 line without writing it back (its data is dead)
+__device__ __forceinline__ void discard_l2(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w), "l"(pol)
@@ -318,9 +322,22 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float rsqrt_rn(float x) { return rsqrt_fast(x); }
-__device__ __forceinline__ double rsqrt_rn(double x) { return __drcp_rn(__dsqrt_rn(x)); }
 __device__ __forceinline__ float rcp_rn(float x) { return rcp_fast(x); }
-__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+// fp64: the MUFU approximation (rel. error < 2^-21) refined by one Newton step in fp64
+// (error ~2^-42, far below the final fp32 rounding) instead of the IEEE double sqrt /
+// reciprocal sequences, which cost several times more issue slots
+__device__ __forceinline__ double rsqrt_rn(double x) {
+    float yf;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"((float)x));
+    const double y = yf;
+    return y * fma(-0.5 * x * y, y, 1.5);
+}
+__device__ __forceinline__ double rcp_rn(double x) {
+    float yf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"((float)x));
+    const double y = yf;
+    return y * fma(-x, y, 2.0);
+}
 
 __device__ __forceinline__ s1r lerp_rn(s1r b, s1r x0, s1r a, s1r x1) {
     return fma_rn(a, x1, mul_rn(b, x0));

@@ -422,6 +422,15 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         bar_consumers(NC);     // the whole tile's G is in shared memory
         prof_mark(8);
         if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 9, 1ull);
+        // the next tile's inbox has been read by every thread (its pieces are in Q): its
+        // L2 lines are dead, so drop the ones lying wholly inside it without a write-back
+        // (the workspace would otherwise reach DRAM as dirty evictions)
+        if (nin3) {
+            const uintptr_t b0 = reinterpret_cast<uintptr_t>(insrc), b1 = b0 + (uintptr_t)nin3 * 16;
+            for (uintptr_t p = ((b0 + 127) & ~(uintptr_t)127) + (uintptr_t)t * 128; p + 128 <= b1;
+                 p += (uintptr_t)NC * 128)
+                discard_l2(reinterpret_cast<const void*>(p));
+        }
         // exports: the tile's joints that later tiles read (two or more tiles on) into
         // their inboxes; consecutive threads store consecutive 16-byte pieces of each
         // contiguous inbox range (coalesced)

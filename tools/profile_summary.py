@@ -1,22 +1,39 @@
-"""Summarise a round's ncu captures into profiles/ (launch list + full capture of the
-dominant kernel) and refresh profiles/ncu_traffic.json for bench.py's roofline."""
+"""Summarise a round's ncu captures (tools/round_artifacts.sh TAG -> gpurun_out/TAG/) into
+profiles/: the launch list of the bench command (per-launch times, step shares), the
+`--set full` summaries of the dominant launches, and profiles/ncu_traffic.json — the
+DRAM bytes per launch bench.py reports as `roofline.traffic`, each entry tagged with the
+library sources' hash the capture was taken on (bench.py reports it only on a match).
+
+    python tools/profile_summary.py TAG [SOURCES_SHA]
+
+SOURCES_SHA defaults to the current tree's `paper_2505_06703_b200.sources_sha256()`:
+pass the hash the bench printed for the captured build when the tree changed since."""
 from __future__ import annotations
 
 import csv
 import json
+import os
 import subprocess
 import sys
 
-LAUNCH_ROLES = ["gen hum64", "gen chain256", "gen tree1024", "scan hum64 (check step)",
-                "scan chain256 (check step)", "scan tree1024 (check step)", "scan hum64 (timed step)",
-                "scan chain256 (timed step)", "scan tree1024 (timed step)"]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 UNITS = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
+        "launch__shared_mem_per_block_dynamic", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smsp__inst_executed.sum",
+        "sm__cycles_elapsed.avg.per_second"]
 
 
 def launches(csv_path, out_path, tag):
-    rows = list(csv.reader(open(csv_path)))
-    hdr, recs = None, []
-    for r in rows:
+    recs, hdr = [], None
+    for r in csv.reader(open(csv_path)):
         if r and r[0] == "ID":
             hdr = r
             continue
@@ -25,104 +42,72 @@ def launches(csv_path, out_path, tag):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 recs.append((int(d["ID"]), d["Kernel Name"],
                              float(d["Metric Value"].replace(",", "")) * UNITS[d["Metric Unit"]]))
+    ours = [x for x in recs if "hs::" in x[1] or "chunked_kernel" in x[1] or "seq_kernel" in x[1]]
     with open(out_path, "w") as f:
-        f.write(f"# Launch list ({tag}): ncu --metrics gpu__time_duration.sum --clock-control none\n")
-        f.write("#   python bench.py --profile --steps 1 --warmup 0   (config C5, 1 GPU)\n")
-        f.write("# Cold-cache, serialised launches: compare SHARES, not absolutes.\n")
-        f.write("# id  duration_us  role  kernel\n")
-        for (i, k, us), nm in zip(recs, LAUNCH_ROLES):
-            f.write(f"{i:3d} {us:12.1f}  {nm:28s} {k}\n")
-        step = [us for (_, _, us) in recs[6:9]]
-        f.write("\n# timed step (3 chunked_kernel launches): share of step time\n")
-        for nm, us in zip(["hum64", "chain256", "tree1024"], step):
-            f.write(f"#   {nm:9s} {us:9.1f} us  {100 * us / sum(step):5.1f}%\n")
-    return recs
+        f.write(f"# Launch list ({tag}): ncu --metrics gpu__time_duration.sum --clock-control none -c 400\n")
+        f.write("#   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-configs   (C5, 1 GPU)\n")
+        f.write("# Cold-cache, serialised launches: compare SHARES of the step, not absolutes.\n")
+        f.write("# id  duration_us  kernel\n")
+        for i, k, us in recs:
+            f.write(f"{i:4d} {us:12.1f}  {k[:110]}\n")
+        step = [x for x in ours if "chunked_kernel" in x[1]][-3:]   # the last timed step: 3 launches
+        tot = sum(us for _, _, us in step)
+        f.write("\n# last timed step (3 chunked_kernel launches: hum64, chain256, tree1024): share of the step\n")
+        for (_, k, us), nm in zip(step, ["hum64", "chain256", "tree1024"]):
+            f.write(f"#   {nm:9s} {us:9.1f} us  {100 * us / tot:5.1f}%\n")
 
 
-def full_capture(rep, out_path, tag, n_joints, workload):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+def capture(rep, out_path, title, alg_bytes):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, u, v = rows[0], rows[1], rows[2]
-    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-            "launch__block_size", "launch__grid_size", "launch__shared_mem_per_block_dynamic",
-            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
-            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
-            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-            "sm__cycles_elapsed.avg.per_second"]
-    res = {}
-    for i, k in enumerate(h):
-        if k in want or ("average_warps_issue_stalled" in k and "per_issue_active" in k):
-            res[k] = (v[i], u[i])
-    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
-    rd = float(res["dram__bytes_read.sum"][0]) * scale[res["dram__bytes_read.sum"][1]]
-    wr = float(res["dram__bytes_write.sum"][0]) * scale[res["dram__bytes_write.sum"][1]]
-    alg = n_joints * 144
-    lines = [f"# {tag}: ncu --set full --clock-control none --import-source on -k regex:chunked_kernel -s 2 -c 1",
-             "#   python bench.py --profile --steps 1 --warmup 0   (the C5 tree1024 launch)",
+    res = {k: (v[h.index(k)], u[h.index(k)]) for k in KEYS if k in h}
+    rd = float(res["dram__bytes_read.sum"][0]) * SCALE[res["dram__bytes_read.sum"][1]]
+    wr = float(res["dram__bytes_write.sum"][0]) * SCALE[res["dram__bytes_write.sum"][1]]
+    lines = [f"# {title}", f"# kernel: {v[h.index('Kernel Name')] if 'Kernel Name' in h else '?'}",
              f"# DRAM traffic per launch = {rd / 1e9:.3f} GB read + {wr / 1e9:.3f} GB write = {(rd + wr) / 1e9:.3f} GB",
-             f"# algorithmic bytes (144 B/joint x {n_joints / 1e6:.2f} M joints) = {alg / 1e9:.3f} GB"
-             f"  (ratio {(rd + wr) / alg:.4f})", ""]
-    for k in want:
-        if k in res:
-            lines.append(f"{k:75s} {res[k][0]:>18s} {res[k][1]}")
+             f"# algorithmic bytes = {alg_bytes / 1e9:.3f} GB  (traffic / algorithmic = {(rd + wr) / alg_bytes:.4f})", ""]
+    lines += [f"{k:75s} {res[k][0]:>18s} {res[k][1]}" for k in KEYS if k in res]
     lines += ["", "# warp stall reasons (warps stalled per issued instruction)"]
-    stalls = sorted(((k, float(res[k][0])) for k in res if "stalled" in k), key=lambda z: -z[1])
-    lines += [f"{k:75s} {x:8.3f}" for k, x in stalls if x > 0.01]
-    open(out_path, "w").write("\n".join(lines) + "\n")
-    json.dump({"workload": workload, "kernel": "chunked_kernel (tree1024 launch)",
-               "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-               "algorithmic_bytes_per_launch": alg, "source": f"{out_path} (ncu --set full, {tag})"},
-              open("profiles/ncu_traffic.json", "w"), indent=1)
-
-
-def kernel_summary(rep, out_path, title, alg_bytes):
-    """Key counters of one captured launch (no ncu_traffic.json update)."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
-    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "lts__t_sectors_srcunit_tex_op_read.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
-            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-            "launch__shared_mem_per_block_dynamic", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smsp__inst_executed.sum"]
-    lines = [f"# {title}", f"# algorithmic HBM bytes per launch: {alg_bytes / 1e9:.3f} GB", ""]
-    for k in keys:
-        if k in h:
-            i = h.index(k)
-            lines.append(f"{k:75s} {v[i]:>18s} {u[i]}")
     stalls = sorted(((h[i], float(v[i])) for i in range(len(h))
-                     if "average_warps_issue_stalled" in h[i] and "per_issue_active" in h[i]),
-                    key=lambda z: -z[1])
-    lines += ["", "# warp stall reasons (warps stalled per issued instruction)"]
+                     if "average_warps_issue_stalled" in h[i] and "per_issue_active" in h[i]), key=lambda z: -z[1])
     lines += [f"{k:75s} {x:8.3f}" for k, x in stalls if x > 0.01]
     open(out_path, "w").write("\n".join(lines) + "\n")
-    print("\n".join(lines))
+    return rd, wr
+
+
+def main():
+    tag = sys.argv[1]
+    src = f"{ROOT}/gpurun_out/{tag}"
+    import paper_2505_06703_b200 as hs
+    sha = sys.argv[2] if len(sys.argv) > 2 else hs.sources_sha256()
+    entries = []
+    if os.path.exists(f"{src}/launches.csv"):
+        launches(f"{src}/launches.csv", f"{ROOT}/profiles/{tag}_launches.txt", tag)
+    if os.path.exists(f"{src}/prof_tree1024.ncu-rep"):
+        alg = 333_333 * 1024 * 144
+        rd, wr = capture(f"{src}/prof_tree1024.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_tree1024.txt",
+                         f"{tag}: ncu --set full, the C5 tree1024 launch (bench.py --profile)", alg)
+        entries.append({"workload": "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU",
+                        "kernel": "chunked_kernel (tree1024 launch)", "dram_bytes_per_launch": rd + wr,
+                        "dram_read": rd, "dram_write": wr, "algorithmic_bytes_per_launch": alg,
+                        "source": f"profiles/{tag}_ncu_tree1024.txt", "sources_sha256": sha})
+    if os.path.exists(f"{src}/prof_seq_c6.ncu-rep"):
+        alg = 2000 * 16384 * 144
+        rd, wr = capture(f"{src}/prof_seq_c6.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_seq_c6.txt",
+                         f"{tag}: ncu --set full, the C6 multi-tile launch (tools/tiles_one.py)", alg)
+        entries.append({"workload": "C6 2,000 x tree16384 (L=1024, beyond one CTA: multi-tile path)",
+                        "kernel": "seq_kernel (multi-tile path, tree16384 launch)", "dram_bytes_per_launch": rd + wr,
+                        "dram_read": rd, "dram_write": wr, "algorithmic_bytes_per_launch": alg,
+                        "source": f"profiles/{tag}_ncu_seq_c6.txt", "sources_sha256": sha})
+    if os.path.exists(f"{src}/prof_stage1.ncu-rep"):
+        capture(f"{src}/prof_stage1.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_stage1_streaming_kernel.txt",
+                f"{tag}: ncu --set full, stage1_kernel (two-pass hs_animate, tree1024 x 50,000, 2 layers)",
+                50_000 * (1024 * 48 + 32))
+    json.dump(entries, open(f"{ROOT}/profiles/ncu_traffic.json", "w"), indent=1)
+    for e in entries:
+        print(e["kernel"], e["dram_bytes_per_launch"] / e["algorithmic_bytes_per_launch"])
 
 
 if __name__ == "__main__":
-    tag = sys.argv[1]
-    if len(sys.argv) > 2 and sys.argv[2] == "stage1":
-        kernel_summary(f"gpurun_out/prof_stage1_{tag}.ncu-rep", f"profiles/{tag}_ncu_stage1_tree1024.txt",
-                       f"{tag}: ncu --set full, hs_animate tree1024 x 50,000 characters, 2 layers "
-                       "(tools/stage1_one.py, 3rd launch)", 50_000 * (1024 * 96 + 32))
-        sys.exit(0)
-    if len(sys.argv) > 2 and sys.argv[2] == "lbs":
-        kernel_summary(f"gpurun_out/prof_lbs_{tag}.ncu-rep", f"profiles/{tag}_ncu_lbs_tree1024.txt",
-                       f"{tag}: ncu --set full, hs_scan_skin tree1024 x 20,000 characters, 1000-vertex "
-                       "mesh (tools/lbs_one.py, 3rd launch)", 20_000 * (1024 * 144 + 1000 * 12))
-        sys.exit(0)
-    launches(f"gpurun_out/launches_{tag}.csv", f"profiles/{tag}_launches.txt", tag)
-    full_capture(f"gpurun_out/prof_tree_{tag}.ncu-rep", f"profiles/{tag}_ncu_tree1024.txt", tag,
-                 333333 * 1024, "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU")
-    print(open(f"profiles/{tag}_launches.txt").read())
-    print(open(f"profiles/{tag}_ncu_tree1024.txt").read())
+    main()
