@@ -16,6 +16,9 @@
 #ifndef HS_LBS_U
 #define HS_LBS_U 2
 #endif
+#ifndef HS_STREAM_HINTS
+#define HS_STREAM_HINTS 0   // L2 evict_first on the streaming TMA copies (A/B: tools/time_scan.py)
+#endif
 
 namespace hs {
 namespace {
@@ -100,6 +103,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
         const int lane = threadIdx.x & 31;
         if (!PRO && lane != 0) return;
         const uint32_t piece = a.bulk_piece > 0 ? (uint32_t)a.bulk_piece : 0xffffffffu;
+#if HS_STREAM_HINTS
+        const uint64_t stream_pol = policy_evict_first();   // tiles in, G and S out: touched once
+#endif
         // stage / S-buffer indices and mbarrier parities advance incrementally: no
         // 64-bit division in the loop; segment cursors for the loads (run NS tiles
         // ahead) and for the stores
@@ -116,8 +122,13 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             mbar_expect_tx(&full[stage], bytes);
             const char* src = reinterpret_cast<const char*>(ld.local + c0 * ld.J * 12);
             char* dst = reinterpret_cast<char*>(LG + stage * tile_f);
-            for (uint32_t o = 0; o < bytes; o += piece)
+            for (uint32_t o = 0; o < bytes; o += piece) {
+#if HS_STREAM_HINTS
+                bulk_g2s_hint(dst + o, src + o, min(piece, bytes - o), &full[stage], stream_pol);
+#else
                 bulk_g2s(dst + o, src + o, min(piece, bytes - o), &full[stage]);
+#endif
+            }
         };
         // Stage 1 (one segment): descriptors of tile `it`'s (character, layer) pairs
         // into desc[stage], then full[stage] tells the consumers the stage is theirs
@@ -159,8 +170,13 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 const char* ss = reinterpret_cast<const char*>(SB + sb * tile_f);
                 for (uint32_t o = 0; o < bytes; o += piece) {
                     const uint32_t nb = min(piece, bytes - o);
+#if HS_STREAM_HINTS
+                    bulk_s2g_hint(gp + o, sg + o, nb, stream_pol);
+                    if (do_skin) bulk_s2g_hint(sp + o, ss + o, nb, stream_pol);
+#else
                     bulk_s2g(gp + o, sg + o, nb);
                     if (do_skin) bulk_s2g(sp + o, ss + o, nb);
+#endif
                 }
             }
             bulk_commit();

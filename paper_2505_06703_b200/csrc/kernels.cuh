@@ -73,6 +73,7 @@ struct ChunkedArgs {
 // Multi-tile kernel: barrier header bytes, and the helper warp's inbox loads in flight
 // per lane (16-byte pieces)
 constexpr int kSeqHeaderBytes = 256;
+constexpr int kSeqExportUnroll = 4;   // export pieces in flight per thread
 // inbox staging by the consumers: at most this many 16-byte pieces per thread
 // (3 x inbox rows <= kSeqInboxPieces x threads; the plan checks)
 constexpr int kSeqInboxPieces = 9;   // rows from tiles <= k - 2 (loaded at the top of tile k - 1)

@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         for (int64_t it = 0; it < my_tiles; ++it) {
             mbar_wait(&done[stage], phase);
             const SeqTileDev tl = s_tiles[sk];
+            if (it + 1 < my_tiles) issue_exl(sk + 1 < KT ? sk + 1 : 0);   // read by tile it's exports: done
             if (it + 3 < my_tiles) issue_prog(pbuf);   // tile it no longer reads its program
             if (++pbuf == 3) pbuf = 0;
             {
@@ -174,7 +175,6 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 bulk_commit();
             }
             {
-                if (it + 1 < my_tiles) issue_exl(sk + 1 < KT ? sk + 1 : 0);   // the list buffer is free
                 bulk_wait_read<0>();
                 if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
                 if (it + NS < my_tiles) issue_load(stage);
@@ -438,12 +438,24 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             const int n3 = 3 * tl.n_exl;
             if (n3) {
                 mbar_wait(exlfull, (uint32_t)(it & 1));
-                for (int q = t; q < n3; q += NC) {
-                    const int e = q / 3, c = q - 3 * e;
-                    const int2 x = s_exl[e];
-                    HS_BOUND(x.x >= 0 && x.x < tl.nj && x.y >= 0 && x.y < a.n_exp);
-                    st4_hint(wsb + (int64_t)x.y * 12 + 4 * c, *reinterpret_cast<const float4*>(L + x.x * 12 + 4 * c),
-                             ws_pol);
+                for (int q0 = t; q0 < n3; q0 += kSeqExportUnroll * NC) {
+                    float4 v[kSeqExportUnroll];
+                    int dst[kSeqExportUnroll];
+#pragma unroll
+                    for (int u = 0; u < kSeqExportUnroll; ++u) {   // independent loads first (ILP)
+                        const int q = q0 + u * NC;
+                        dst[u] = -1;
+                        if (q < n3) {
+                            const int e = q / 3, c = q - 3 * e;
+                            const int2 x = s_exl[e];
+                            HS_BOUND(x.x >= 0 && x.x < tl.nj && x.y >= 0 && x.y < a.n_exp);
+                            v[u] = *reinterpret_cast<const float4*>(L + x.x * 12 + 4 * c);
+                            dst[u] = x.y * 12 + 4 * c;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSeqExportUnroll; ++u)
+                        if (dst[u] >= 0) st4_hint(wsb + dst[u], v[u], ws_pol);
                 }
             }
         }

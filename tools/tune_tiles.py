@@ -19,7 +19,7 @@ assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream) == 0
 g, s = torch.empty_like(x), torch.empty_like(x)
 ref = None
-for kw in [{}, {"tile_joints": 512}]:
+for kw in [{}]:
     kw = dict(kw)
     ctas = kw.pop("ctas", 0)
     try:
