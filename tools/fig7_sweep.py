@@ -47,7 +47,7 @@ def main(argv=None):
     ap.add_argument("--joints", type=int, default=300)
     ap.add_argument("--depths", default="15,30,45,60,90,120")
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_fig7_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02b_fig7_sweep.json"))
     args = ap.parse_args(argv)
 
     import torch

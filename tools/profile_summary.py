@@ -102,8 +102,9 @@ def main():
                         "source": f"profiles/{tag}_ncu_seq_c6.txt", "sources_sha256": sha})
     if os.path.exists(f"{src}/prof_stage1.ncu-rep"):
         capture(f"{src}/prof_stage1.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_stage1_streaming_kernel.txt",
-                f"{tag}: ncu --set full, stage1_kernel (two-pass hs_animate, tree1024 x 50,000, 2 layers)",
-                50_000 * (1024 * 48 + 32))
+                f"{tag}: ncu --set full, stage1_kernel (two-pass hs_animate, tree1024 x 50,000, 2 layers; "
+                "the captured launch is the 3rd workspace batch: 6,310 characters)",
+                6_310 * (1024 * 48 + 32))
     json.dump(entries, open(f"{ROOT}/profiles/ncu_traffic.json", "w"), indent=1)
     for e in entries:
         print(e["kernel"], e["dram_bytes_per_launch"] / e["algorithmic_bytes_per_launch"])
