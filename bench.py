@@ -42,7 +42,8 @@ METRIC = "joints/sec (Hierarchy-Scan+skin) and HBM GB/s vs peak at 1/2/4/8 B200"
 WORKLOAD_NAME = {1: "C1 1,000 x hum32 (L=8)", 2: "C2 100,000 x hum64 (L=12)",
                  3: "C3 50,000 x chain256 (L=256)", 4: "C4 20,000 x tree1024 (L=300)",
                  5: "C5 1,000,000 mixed hum64/chain256/tree1024 per GPU",
-                 6: "C6 2,000 x tree16384 (L=1024, beyond one CTA: multi-tile path)"}
+                 6: "C6 2,000 x tree16384 (L=1024, beyond one CTA: multi-tile path)",
+                 7: "C7 2,000 x tree16384, depth-first labels (multi-tile path)"}
 
 
 def parse_args(argv=None):
@@ -51,7 +52,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--cpu-frac", type=int, default=8,
                     help="cpu_baseline / reference sample = n_chars // this, per skeleton type")
@@ -85,7 +86,7 @@ def parse_args(argv=None):
                     help="process-group backend for N > 1 (gloo: CPU collectives, lets a test run "
                          "several ranks on one GPU; the data path has no collective either way)")
     ap.add_argument("--no-configs", action="store_true",
-                    help="skip the per-config single-type launches (C2, C3, C4, C6) reported in "
+                    help="skip the per-config single-type launches (C2, C3, C4, C6, C7) reported in "
                          "the line's 'configs' object")
     ap.add_argument("--no-validate", action="store_true",
                     help="skip the N > 1 validation (all-gather of sampled G/S shards, bitwise "
@@ -514,9 +515,10 @@ def run_ours(args):
     return 1 if failed else 0
 
 
-def measure_configs(hs, torch, stream, dev, cfgs=(2, 3, 4, 6), iters=10):
+def measure_configs(hs, torch, stream, dev, cfgs=(2, 3, 4, 6, 7), iters=10):
     """Per-launch time of the single-type configs (C3 and C4 are the
-    deep-skeleton targets, C6 the multi-CTA skeleton) on device-resident inputs (each
+    deep-skeleton targets, C6 / C7 the multi-CTA skeleton in generation / depth-first
+    label order) on device-resident inputs (each
     larger than L2), CUDA events on the launching stream, median of `iters` after 3
     warm-ups; fraction of 8 TB/s and of the measured copy peak at 144 B/joint."""
     peak, _ = measured_peaks()

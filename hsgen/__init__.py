@@ -174,6 +174,42 @@ def relabel(parents, perm):
     return new_par, inv
 
 
+def dfs_labels(parents) -> np.ndarray:
+    """The same forest relabelled in depth-first preorder, the largest child subtree
+    first (how skeleton files usually list joints); roots in their original order."""
+    par = np.asarray(parents, np.int32)
+    J = len(par)
+    children = [[] for _ in range(J)]
+    for j in range(J):
+        if par[j] >= 0:
+            children[par[j]].append(j)
+    size = np.ones(J, np.int64)
+    for j in _topo(par)[::-1]:
+        if par[j] >= 0:
+            size[par[j]] += size[j]
+    order, stack = [], [r for r in range(J) if par[r] < 0][::-1]
+    while stack:
+        v = stack.pop()
+        order.append(v)
+        stack.extend(sorted(children[v], key=lambda c: size[c]))   # largest popped first
+    return relabel(par, np.array(order, np.int32))[0]
+
+
+def _topo(par):
+    """A topological order (parents first) of a forest given as a parent array."""
+    J = len(par)
+    children = [[] for _ in range(J)]
+    for j in range(J):
+        if par[j] >= 0:
+            children[par[j]].append(j)
+    out, stack = [], [r for r in range(J) if par[r] < 0]
+    while stack:
+        v = stack.pop()
+        out.append(v)
+        stack.extend(children[v])
+    return np.array(out, np.int64)
+
+
 # --- the BASELINE.json configs (SURVEY.md §8(d)) ------------------------------
 def skeleton(name: str) -> np.ndarray:
     if name == "hum32":
@@ -188,6 +224,8 @@ def skeleton(name: str) -> np.ndarray:
         return random_tree(4, 1024, 300)
     if name == "tree16384":   # the multi-CTA skeleton, 16,384 joints, L = 1024
         return random_tree(77, 16384, 1024)
+    if name == "tree16384dfs":   # the same tree with depth-first labels (skeleton-file order)
+        return dfs_labels(random_tree(77, 16384, 1024))
     raise KeyError(name)
 
 
@@ -201,6 +239,8 @@ CONFIGS = {
         ("tree1024", 333_333, 5, 2, 4)],
     # beyond one CTA (SURVEY §7 step 7 / VERDICT r1): the multi-tile path's workload
     6: [("tree16384", 2_000, 6, 0, 6)],
+    # the same trees labelled depth-first: few cross-tile parents
+    7: [("tree16384dfs", 2_000, 7, 0, 7)],
 }
 
 

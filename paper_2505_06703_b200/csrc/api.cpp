@@ -158,17 +158,17 @@ void free_skeleton(hs_skeleton* sk) {
 }
 
 // The multi-tile program (HS_ALGO_TILES) of a skeleton that does not fit one CTA.
-// Defaults measured on C6 (2,000 x tree16384; tools/tune_tiles.py): chunk K = 3, three
-// load stages, two skin buffers (the next tile's inverse binds load during this tile),
-// 512-joint tiles;
-// the largest tile up to the target whose program fits 224 compute threads and whose
-// shared memory fits the device; chunking RUNS or HEAVY, whichever needs fewer phase-2
+// Defaults measured on C6 / C7 (2,000 x tree16384 in generation / depth-first label
+// order; tools/tune_tiles.py): chunk K = 3, three load stages, two skin buffers (the
+// next tile's inverse binds load during this tile), the largest tile up to 672 joints
+// whose program fits 224 compute threads and whose shared memory fits the device (C6's
+// many cross-tile parents need Q space: 576; C7: 672, 17 % faster than 576); chunking RUNS or HEAVY, whichever needs fewer phase-2
 // descriptors.  Explicit options override each choice.
 hs_status build_seq(hs_skeleton* sk, const hs_create_opts& o, const std::vector<float>& ib) {
     const hs::Plan& P = sk->plan;
     const int K = o.chunk ? o.chunk : 3;
     const int stages = o.stages ? o.stages : 3;
-    const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 576;
+    const int f0 = o.tile_joints ? std::min(o.tile_joints, 1024) : 672;
     const int modes[2] = {hs::CHUNK_RUNS, hs::CHUNK_HEAVY};
     const int nmodes = o.chunking == 0 ? 2 : 1;
     const int sb_cand[2] = {o.sbufs ? o.sbufs : 2, o.sbufs ? o.sbufs : 1};

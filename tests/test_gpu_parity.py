@@ -143,11 +143,13 @@ def test_large_skeleton_multi_cta_path(algo):
     assert eg <= TOL and es <= TOL
 
 
-def test_multi_tile_crowd_auto_and_sampled_oracle():
+@pytest.mark.parametrize("name", ["tree16384", "tree16384dfs"])
+def test_multi_tile_crowd_auto_and_sampled_oracle(name):
     """A crowd larger than the SM count takes the multi-tile path under AUTO; every
     character equals the same character scanned alone (bitwise: one CTA runs a whole
-    character, whatever the crowd); sampled characters within 1e-4 of the oracle."""
-    par = hsgen.skeleton("tree16384")
+    character, whatever the crowd); sampled characters within 1e-4 of the oracle.  The
+    C6 tree in generation order and depth-first (C7: larger tiles, few imports)."""
+    par = hsgen.skeleton(name)
     ib = hsgen.inv_bind(38, 16384)
     sk = hs.Skeleton(par, ib)
     n = 2 * torch.cuda.get_device_properties(0).multi_processor_count + 7
@@ -167,7 +169,8 @@ def test_multi_tile_crowd_auto_and_sampled_oracle():
     assert np.array_equal(loc, x[idx].cpu().numpy())
     G, S = oracle.scan(par, loc, ib)
     eg, es = max_err(g[idx].cpu().numpy(), G), max_err(s[idx].cpu().numpy(), S)
-    print(f"multi-tile crowd of {n}: sampled max err global {eg:.3e} skin {es:.3e}")
+    print(f"multi-tile crowd of {n} x {name} (F = {sk.query('seq_tile_joints')}): sampled max err "
+          f"global {eg:.3e} skin {es:.3e}")
     assert eg <= TOL and es <= TOL
 
 

@@ -41,6 +41,36 @@ def test_tree16384_depth1024():
     assert plan.query("seq_runs") == plan.query("seq_tiles")       # topological labels: one run per tile
 
 
+def test_dfs_labels_are_a_preorder_of_the_same_tree():
+    """hsgen.dfs_labels (the C7 workload): a relabelling of the same forest in which every
+    subtree is a contiguous label range starting at its root (depth-first preorder)."""
+    par = hsgen.random_tree(77, 4000, 300)
+    d = hsgen.dfs_labels(par)
+    J = len(d)
+    assert all(d[j] < j for j in range(J))
+    size = np.ones(J, int)
+    for j in range(J - 1, 0, -1):
+        size[d[j]] += size[j]
+    for j in range(J):   # children of j lie inside [j + 1, j + size[j])
+        kids = np.nonzero(d == j)[0]
+        assert all(j < c < j + size[j] for c in kids)
+    # the same tree: sorted child-count and depth profiles agree
+    def prof(p):
+        lev = np.zeros(len(p), int)
+        for j in range(len(p)):
+            lev[j] = 0 if p[j] < 0 else lev[p[j]] + 1
+        deg = np.bincount(p[p >= 0], minlength=len(p))
+        return sorted(lev.tolist()), sorted(deg.tolist())
+    assert prof(par) == prof(d)
+
+
+def test_tree16384_dfs_labels():
+    """C7: the bench tree in depth-first labels (K = 3, tiles of up to 672 joints)."""
+    plan = check(hsgen.skeleton("tree16384dfs"), 3, chunk=3, tile_joints=672)
+    assert plan.query("seq_qslots") < 100            # few cross-tile parents
+    assert plan.query("seq_runs") == plan.query("seq_tiles")
+
+
 @pytest.mark.parametrize("kw", [{}, {"chunking": 1}, {"chunking": 2}, {"chunk": 3}, {"chunk": 7},
                                 {"tile_joints": 256}, {"tile_joints": 96, "chunk": 3}])
 def test_variants_random_tree(kw):

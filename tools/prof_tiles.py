@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Per-phase cycle split of the multi-tile kernel (consumer thread 0, clock64) on C6
-(2,000 x tree16384): builds the HS_PROF_HOOKS=1 variant and prints hs prof lines."""
+(2,000 x tree16384): builds the HS_PROF_HOOKS=1 variant and prints hs prof lines.
+Options: --dfs (depth-first labels), create options as key=value (tile_joints=672)."""
 import os
 import sys
 
@@ -14,8 +15,11 @@ import paper_2505_06703_b200 as hs  # noqa: E402
 hs.use_library(hs.build_variant("libhs_prof.so", ["-DHS_PROF_HOOKS=1"]))
 (name, n, seed, type_, ib_seed), = hsgen.CONFIGS[6]
 par = hsgen.skeleton(name)
+if "--dfs" in sys.argv:   # the same trees with depth-first labels
+    par = hsgen.dfs_labels(par)
+kw = {k: int(v) for k, v in (x.split("=") for x in sys.argv[1:] if "=" in x)}   # e.g. tile_joints=672
 J = len(par)
-sk = hs.Skeleton(par, hsgen.inv_bind(ib_seed, J))
+sk = hs.Skeleton(par, hsgen.inv_bind(ib_seed, J), **kw)
 x = torch.empty((n, J, 3, 4), device="cuda")
 assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream) == 0

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Tuning aid: HS_ALGO_TILES on C6 (2,000 x tree16384) across tile sizes / stage counts;
-median of 7 launches after 2 warm-ups (CUDA events), GB/s at 144 B/joint."""
+median of 7 launches after 2 warm-ups (CUDA events), GB/s at 144 B/joint.  --dfs: the
+same trees with depth-first labels (few cross-tile parents)."""
 import os
 import statistics
 import sys
@@ -13,13 +14,20 @@ import paper_2505_06703_b200 as hs  # noqa: E402
 
 (name, n, seed, type_, ib_seed), = hsgen.CONFIGS[6]
 par = hsgen.skeleton(name)
+DFS = "--dfs" in sys.argv   # the same trees labelled in depth-first order (heavy child first)
+if DFS:
+    par = hsgen.dfs_labels(par)
 J = len(par)
 x = torch.empty((n, J, 3, 4), device="cuda")
 assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream) == 0
 g, s = torch.empty_like(x), torch.empty_like(x)
 ref = None
-for kw in [{}]:
+for kw in ([{}, {"tile_joints": 1024, "chunk": 5}, {"tile_joints": 1024, "chunk": 5, "stages": 2},
+            {"tile_joints": 768, "chunk": 3}, {"tile_joints": 1024, "chunk": 7}] if DFS else
+           [{}, {"tile_joints": 672, "sbufs": 1}, {"tile_joints": 672, "stages": 2},
+            {"tile_joints": 672, "stages": 2, "sbufs": 1}, {"tile_joints": 640, "sbufs": 1},
+            {"tile_joints": 608}]):
     kw = dict(kw)
     ctas = kw.pop("ctas", 0)
     try:
