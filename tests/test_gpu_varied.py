@@ -78,3 +78,37 @@ def test_varied_errors_and_no_skin():
     assert torch.equal(g, s)
     G, _ = oracle.scan([-1, 0, -1, 1], loc.cpu().numpy()[0])
     assert np.abs(g.cpu().numpy()[0] - G).max() <= 1e-5
+
+
+@pytest.mark.parametrize("J,n,deep", [(64, 10_000, False), (1024, 300, True), (300, 1000, False)])
+def test_varied_persistent_crowd_sampled(J, n, deep):
+    """Crowds of more groups than SMs: the persistent CTA streams group after group
+    (double-buffered locals, re-issued inverse binds, prefetched parents); sampled
+    characters bitwise against the oracle on the exact family.  deep: 1024-joint chains
+    (depth 1024: the longest anchor chains)."""
+    rng = np.random.default_rng(J + n)
+    base = forests(J + 3, 64, J) if not deep else np.tile(hsgen.chain(J), (64, 1))
+    if deep:
+        for c in range(64):
+            base[c], _ = hsgen.relabel(hsgen.chain(J), rng.permutation(J).astype(np.int32))
+    par = base[np.arange(n) % 64]
+    loc = hsgen.exact_poses(J + 5, J, n)
+    ibs = np.stack([hsgen.exact_inv_bind(c, J) for c in range(64)])
+    ib = ibs[np.arange(n) % 64]
+    g, s = hs.scan_varied(torch.from_numpy(np.ascontiguousarray(par)).cuda(), torch.from_numpy(loc).cuda(),
+                          torch.from_numpy(np.ascontiguousarray(ib)).cuda())
+    torch.cuda.synchronize()
+    g, s = g.cpu().numpy(), s.cpu().numpy()
+    for c in sorted(set([0, 1, n // 2, n - 2, n - 1] + rng.integers(0, n, 12).tolist())):
+        G, S = oracle.scan(par[c], loc[c], ib[c])
+        assert np.array_equal(g[c], G) and np.array_equal(s[c], S), c
+
+
+def test_varied_cycle_terminates():
+    """A cyclic parent array gives undefined values but the launch terminates."""
+    par = torch.tensor([[1, 2, 0, -1, 3] * 100], dtype=torch.int32, device="cuda")[:, :500]
+    par = par % 500
+    loc = torch.from_numpy(hsgen.local_poses(3, 500, 1)).cuda()
+    g, s = hs.scan_varied(par.contiguous(), loc)
+    torch.cuda.synchronize()
+    assert g.shape == (1, 500, 3, 4)

@@ -100,11 +100,19 @@ def main():
                         "kernel": "seq_kernel (multi-tile path, tree16384 launch)", "dram_bytes_per_launch": rd + wr,
                         "dram_read": rd, "dram_write": wr, "algorithmic_bytes_per_launch": alg,
                         "source": f"profiles/{tag}_ncu_seq_c6.txt", "sources_sha256": sha})
+    if os.path.exists(f"{src}/prof_seq_c7.ncu-rep"):
+        alg = 2000 * 16384 * 144
+        rd, wr = capture(f"{src}/prof_seq_c7.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_seq_c7.txt",
+                         f"{tag}: ncu --set full, the C7 multi-tile launch (tools/tiles_one.py --dfs)", alg)
+        entries.append({"workload": "C7 2,000 x tree16384, depth-first labels (multi-tile path)",
+                        "kernel": "seq_kernel (multi-tile path, tree16384dfs launch)", "dram_bytes_per_launch": rd + wr,
+                        "dram_read": rd, "dram_write": wr, "algorithmic_bytes_per_launch": alg,
+                        "source": f"profiles/{tag}_ncu_seq_c7.txt", "sources_sha256": sha})
     if os.path.exists(f"{src}/prof_stage1.ncu-rep"):
         capture(f"{src}/prof_stage1.ncu-rep", f"{ROOT}/profiles/{tag}_ncu_stage1_streaming_kernel.txt",
                 f"{tag}: ncu --set full, stage1_kernel (two-pass hs_animate, tree1024 x 50,000, 2 layers; "
-                "the captured launch is the 3rd workspace batch: 6,310 characters)",
-                6_310 * (1024 * 48 + 32))
+                "the captured launch is a full 1 GiB workspace batch: 21,845 characters)",
+                21_845 * (1024 * 48 + 32))
     json.dump(entries, open(f"{ROOT}/profiles/ncu_traffic.json", "w"), indent=1)
     for e in entries:
         print(e["kernel"], e["dram_bytes_per_launch"] / e["algorithmic_bytes_per_launch"])

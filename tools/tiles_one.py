@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""ncu target: three HS_ALGO_TILES launches on C6 (2,000 x tree16384, L = 1024);
+"""ncu target: three HS_ALGO_TILES launches on C6 (2,000 x tree16384, L = 1024; --dfs:
+C7, the same trees in depth-first labels);
 capture the third with  ncu -k regex:seq_kernel -s 2 -c 1 ..."""
 import os
 import sys
@@ -10,7 +11,7 @@ import torch  # noqa: E402
 import hsgen  # noqa: E402
 import paper_2505_06703_b200 as hs  # noqa: E402
 
-(name, n, seed, type_, ib_seed), = hsgen.CONFIGS[6]
+(name, n, seed, type_, ib_seed), = hsgen.CONFIGS[7 if "--dfs" in sys.argv else 6]   # --dfs: C7
 par = hsgen.skeleton(name)
 J = len(par)
 sk = hs.Skeleton(par, hsgen.inv_bind(ib_seed, J))
