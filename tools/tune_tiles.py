@@ -23,7 +23,8 @@ assert hsgen.lib_cuda().hsg_cuda_local_poses(seed, type_, J, 0, n, x.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream) == 0
 g, s = torch.empty_like(x), torch.empty_like(x)
 ref = None
-for kw in ([{}, {"tile_joints": 1024, "chunk": 5}, {"tile_joints": 1024, "chunk": 5, "stages": 2},
+QUICK = "--quick" in sys.argv   # the library defaults only
+for kw in [{}] if QUICK else ([{}, {"tile_joints": 1024, "chunk": 5}, {"tile_joints": 1024, "chunk": 5, "stages": 2},
             {"tile_joints": 768, "chunk": 3}, {"tile_joints": 1024, "chunk": 7}] if DFS else
            [{}, {"tile_joints": 672, "sbufs": 1}, {"tile_joints": 672, "stages": 2},
             {"tile_joints": 672, "stages": 2, "sbufs": 1}, {"tile_joints": 640, "sbufs": 1},
