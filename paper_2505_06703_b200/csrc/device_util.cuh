@@ -30,6 +30,21 @@
     do {               \
     } while (0)
 #endif
+// Protocol stress build (HS_DEBUG_DELAY=1, tests/test_gpu_stress.py): random sleeps of
+// up to ~4 us at the producer / consumer hand-off points of the TMA + mbarrier kernels,
+// so a missing wait, a parity slip or an early buffer reuse shows up as a wrong bit in
+// the bitwise parity suites instead of hiding behind the usual timing.  Compiled out
+// of the shipped library.
+#ifndef HS_DEBUG_DELAY
+#define HS_DEBUG_DELAY 0
+#endif
+#if HS_DEBUG_DELAY
+#define HS_DELAY(site) hs_debug_delay(site)
+#else
+#define HS_DELAY(site) \
+    do {               \
+    } while (0)
+#endif
 #ifndef HS_S1_E
 #define HS_S1_E 1      // Stage-1 elements per thread per pass
 #endif
@@ -97,6 +112,17 @@ __device__ __forceinline__ void ldg3(const float* p, float* v) {
 }
 
 // ------------------------------------------------------------------ PTX helpers
+#if HS_DEBUG_DELAY
+__device__ __forceinline__ void hs_debug_delay(unsigned site) {
+    unsigned x = (unsigned)clock() ^ (blockIdx.x * 0x9E3779B9u) ^ (threadIdx.x * 0x85EBCA6Bu) ^ (site * 0xC2B2AE35u);
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    if ((x & 3) == 0) __nanosleep((x >> 8) & 4095);
+}
+#endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
         int stage = 0, sb = 0;
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
+            HS_DELAY(1);
             mbar_wait(&done[stage], phase);
+            HS_DELAY(2);
             if (PRO && lane != 0) {   // lanes 1..31: only the descriptor fill
                 __syncwarp();
                 if (it + NS < my_tiles) fill_desc(it + NS, stage);
@@ -180,7 +182,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 }
             }
             bulk_commit();
+            HS_DELAY(3);
             bulk_wait_read<0>();                  // smem of this tile has been read out
+            HS_DELAY(4);
             mbar_arrive(&sfree[sb]);              // (also when this segment has no skin output)
             if (PRO) {   // Stage 1 computes tiles in place: the stage is free once read out
                 __syncwarp();
@@ -285,6 +289,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             const int64_t g = blockIdx.x + it * gridDim.x;
             float* L = LG + stage * tile_f;
             prof_mark(-1);
+            HS_DELAY(5);
             mbar_wait(&full[stage], phase);
             prof_mark(0);
             if (PRO) {
@@ -423,6 +428,7 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
             // every use is awaited: a multi-segment launch can mix segments with and
             // without skin output, so it waits on every tile (the producer arrives on
             // sfree after every tile, skin or not).
+            HS_DELAY(6);
             if ((SKIN || MULTI) && it >= NSS) mbar_wait(&sfree[sb], sphase);
             prof_mark(3);
             {
@@ -487,7 +493,9 @@ __global__ void __launch_bounds__(256, 1) chunked_kernel(const __grid_constant__
                 }
             }
             fence_proxy_async();
+            HS_DELAY(7);
             bar_consumers(NC);
+            HS_DELAY(8);
             if (t == 0) mbar_arrive(&done[stage]);
             if (LBS) {
                 // linear blend skinning (R24): the tile's skin palette is in

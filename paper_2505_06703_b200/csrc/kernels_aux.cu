@@ -71,11 +71,13 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
             // buffers per warp) and written by one TMA bulk store, so the LSU carries
             // only the key loads; the store of two iterations ago must have been read
             float* sbuf = stg + (it & 1) * 256 * 12;
+            HS_DELAY(21);
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
             stage1_elems<1, false, NLT>(a.keys, dp, j, valid, nl, J + (J & 1), sbuf + threadIdx.x * 12, off);
             fence_proxy_async();
             __syncwarp();
+            HS_DELAY(22);
             if (lane == 0) {
                 bulk_s2g(local + wbase * 12, sbuf + (threadIdx.x & ~31) * 12,
                          (uint32_t)(48 * min((int64_t)32, n - wbase)));

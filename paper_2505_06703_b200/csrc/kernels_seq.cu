@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         int stage = 0, sb = 0, pbuf = 0;
         uint32_t phase = 0;
         for (int64_t it = 0; it < my_tiles; ++it) {
+            HS_DELAY(11);
             mbar_wait(&done[stage], phase);
+            HS_DELAY(12);
             const SeqTileDev tl = s_tiles[sk];
             if (it + 1 < my_tiles) issue_exl(sk + 1 < KT ? sk + 1 : 0);   // read by tile it's exports: done
             if (it + 3 < my_tiles) issue_prog(pbuf);   // tile it no longer reads its program
@@ -174,8 +176,10 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
                 }
                 bulk_commit();
             }
+            HS_DELAY(13);
             {
                 bulk_wait_read<0>();
+                HS_DELAY(14);
                 if (do_skin && it + NSS < my_tiles) issue_ib(sb);   // the S buffer has been read out
                 if (it + NS < my_tiles) issue_load(stage);
             }
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         const SeqTileDev tl = s_tiles[k];
         float* L = LG + stage * tile_f;
         prof_mark(-1);
+        HS_DELAY(15);
         mbar_wait(&progfull[pb], pphase);
         prof_mark(0);
         int p1, run_back, run_anchor;
@@ -247,6 +252,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             }
         }
         prof_mark(1);
+        HS_DELAY(16);
         mbar_wait(&full[stage], phase);
         prof_mark(2);
 
@@ -419,6 +425,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         }
         prof_mark(7);
         fence_proxy_async();   // smem G/S for the bulk stores
+        HS_DELAY(17);
         bar_consumers(NC);     // the whole tile's G is in shared memory
         prof_mark(8);
         if (HS_PROF_HOOKS && a.prof && t == 0) atomicAdd(a.prof + 9, 1ull);
@@ -437,6 +444,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
         {
             const int n3 = 3 * tl.n_exl;
             if (n3) {
+                HS_DELAY(18);
                 mbar_wait(exlfull, (uint32_t)(it & 1));
                 for (int q0 = t; q0 < n3; q0 += kSeqExportUnroll * NC) {
                     float4 v[kSeqExportUnroll];
@@ -460,6 +468,7 @@ __global__ void __launch_bounds__(256, 1) seq_kernel(const __grid_constant__ Seq
             }
         }
         prof_mark(11);
+        HS_DELAY(19);
         mbar_arrive(&done[stage]);   // every consumer thread (count NC): its exports read the stage
         if (++stage == NS) { stage = 0; phase ^= 1u; }
         if (++sb == NSS) { sb = 0; sphase ^= 1u; }   // parity of use it / NSS of buffer sb
