@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
 #ifndef HS_VARIED_THREADS
 #define HS_VARIED_THREADS 64
 #endif
+#ifndef HS_VARIED_M2_ABOVE
+#define HS_VARIED_M2_ABOVE 128   // hs_scan_varied: two joints per thread above this size
+#endif
 // NEXT-3's per-character topology: every character brings its own parent array
 // (4 B/joint more input), so nothing can be planned per skeleton.  One thread per
 // (character, joint), C = max(1, 64 / J) characters per CTA — one character per CTA
@@ -119,11 +122,18 @@ __global__ void __launch_bounds__(256) stage1_kernel(const __grid_constant__ Chu
 // parent pointers (Alg. 2 with the Eq. 2 lift built on the fly): V[i] <- V[p[i]] (x)
 // V[i], p[i] <- p[p[i]] on ping-pong snapshots until no pointer is left (at most
 // ceil(log2 J) + 1 rounds, so a malformed array still terminates).
-__global__ void __launch_bounds__(1024) varied_kernel(const int32_t* __restrict__ parents,
-                                                      const float* __restrict__ local,
-                                                      const float* __restrict__ ib, int J, int C,
-                                                      int64_t n_chars, int max_rounds,
-                                                      float* __restrict__ gout, float* __restrict__ sout) {
+// M joints per thread (slots f, f + T, ... of the CTA's C characters, T = blockDim.x):
+// M = 1 up to 128 joints; M = 2 above, so a 1024-joint character runs on 512 threads
+// with at most 64 registers and two CTAs share an SM (one CTA's barrier waits overlap
+// the other's rounds; a 1024-thread CTA per SM had nothing to overlap with), and each
+// thread's two joints are independent work between barriers.  Measured
+// (tools/time_varied.py): tree1024 1.71 -> 1.42 ms, chain256 0.74 -> 0.69 ms; M = 2
+// from 32 joints or M = 4 above 128 / 512 were slower.
+template <int M>
+__global__ void __launch_bounds__(1024 / M, M == 1 ? 1 : 2)
+    varied_kernel(const int32_t* __restrict__ parents, const float* __restrict__ local,
+                  const float* __restrict__ ib, int J, int C, int64_t n_chars, int max_rounds,
+                  float* __restrict__ gout, float* __restrict__ sout) {
     extern __shared__ __align__(16) float sm[];
     const int F = C * J;
     float* v0 = sm;
@@ -132,54 +142,71 @@ __global__ void __launch_bounds__(1024) varied_kernel(const int32_t* __restrict_
     int32_t* q1 = q0 + F;
     const int64_t c0 = (int64_t)blockIdx.x * C;
     const int nc = (int)min((int64_t)C, n_chars - c0);
-    const int f = threadIdx.x;
-    const int cl = f / J;
-    const bool valid = f < F && cl < nc;
-    float v[12];
-    int p = -1;
-    if (valid) {
-        ldg3(local + (c0 * J + f) * 12, v);
-        p = __ldg(parents + c0 * J + f);
-        if (p < -1 || p >= J) p = -1;   // out of range: treated as a root (documented)
+    const int T = blockDim.x;
+    float v[M][12];
+    int p[M];
+    bool any_local = false;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int f = threadIdx.x + m * T;
+        const int cl = f / J;
+        p[m] = -1;
+        if (f < F && cl < nc) {
+            ldg3(local + (c0 * J + f) * 12, v[m]);
+            p[m] = __ldg(parents + c0 * J + f);
+            if (p[m] < -1 || p[m] >= J) p[m] = -1;   // out of range: treated as a root (documented)
+        }
+        if (f < F) { st3(v0 + f * 12, v[m]); q0[f] = p[m]; }
+        any_local |= p[m] >= 0;
     }
-    if (f < F) { st3(v0 + f * 12, v); q0[f] = p; }
     float* vc = v0;
     float* vn = v1;
     int32_t* qc = q0;
     int32_t* qn = q1;
     // one barrier per round: the OR of "a pointer is left" rides on the barrier that
     // publishes the round's snapshot
-    int any = __syncthreads_or(p >= 0);
+    int any = __syncthreads_or(any_local);
     for (int r = 0; r < max_rounds && any; ++r) {
-        if (f < F) {
-            if (p >= 0) {
-                float x[12], y[12];
-                ld3(vc + (cl * J + p) * 12, x);
-                compose(x, v, y);
+        any_local = false;
 #pragma unroll
-                for (int e = 0; e < 12; ++e) v[e] = y[e];
-                p = qc[cl * J + p];
+        for (int m = 0; m < M; ++m) {
+            const int f = threadIdx.x + m * T;
+            if (f < F) {
+                if (p[m] >= 0) {
+                    const int base = (f / J) * J;
+                    float x[12], y[12];
+                    ld3(vc + (base + p[m]) * 12, x);
+                    compose(x, v[m], y);
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) v[m][e] = y[e];
+                    p[m] = qc[base + p[m]];
+                }
+                st3(vn + f * 12, v[m]);
+                qn[f] = p[m];
+                any_local |= p[m] >= 0;
             }
-            st3(vn + f * 12, v);
-            qn[f] = p;
         }
-        any = __syncthreads_or(p >= 0);
+        any = __syncthreads_or(any_local);
         float* tv = vc; vc = vn; vn = tv;
         int32_t* tq = qc; qc = qn; qn = tq;
     }
-    if (valid) {
-        st3(gout + (c0 * J + f) * 12, v);
-        if (sout) {
-            float s[12];
-            if (ib) {
-                float b[12];
-                ldg3(ib + (c0 * J + f) * 12, b);
-                compose(v, b, s);
-            } else {
 #pragma unroll
-                for (int e = 0; e < 12; ++e) s[e] = v[e];
+    for (int m = 0; m < M; ++m) {
+        const int f = threadIdx.x + m * T;
+        if (f < F && f / J < nc) {
+            st3(gout + (c0 * J + f) * 12, v[m]);
+            if (sout) {
+                float s[12];
+                if (ib) {
+                    float b[12];
+                    ldg3(ib + (c0 * J + f) * 12, b);
+                    compose(v[m], b, s);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) s[e] = v[m][e];
+                }
+                st3(sout + (c0 * J + f) * 12, s);
             }
-            st3(sout + (c0 * J + f) * 12, s);
         }
     }
 }
@@ -636,13 +663,23 @@ cudaError_t launch_varied(const int32_t* parents, const float* local, const floa
     int rounds = 1;
     while ((1 << (rounds - 1)) < J) ++rounds;   // ceil(log2 J) + 1: enough for any forest
     const size_t smem = (size_t)C * J * (2 * 48 + 2 * 4);
-    static std::atomic<uint64_t> attr{0};
-    if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&varied_kernel),
-                                              1024 * (2 * 48 + 2 * 4), attr);
-        e != cudaSuccess)
-        return e;
+    static std::atomic<uint64_t> attr1{0}, attr2{0};
     const int64_t blocks = (n_chars + C - 1) / C;
-    varied_kernel<<<(unsigned)blocks, C * J, smem, st>>>(parents, local, ib, J, C, n_chars, rounds, gout, sout);
+    if (J <= HS_VARIED_M2_ABOVE) {
+        if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&varied_kernel<1>),
+                                                  1024 * (2 * 48 + 2 * 4), attr1);
+            e != cudaSuccess)
+            return e;
+        varied_kernel<1><<<(unsigned)blocks, C * J, smem, st>>>(parents, local, ib, J, C, n_chars, rounds, gout,
+                                                               sout);
+    } else {   // two joints per thread
+        if (const cudaError_t e = raise_smem_once(reinterpret_cast<const void*>(&varied_kernel<2>),
+                                                  1024 * (2 * 48 + 2 * 4), attr2);
+            e != cudaSuccess)
+            return e;
+        varied_kernel<2><<<(unsigned)blocks, (C * J + 1) / 2, smem, st>>>(parents, local, ib, J, C, n_chars, rounds,
+                                                                      gout, sout);
+    }
     return cudaGetLastError();
 }
 
