@@ -8,25 +8,27 @@
 // outside it that it depends on (an earlier tile's joint) already has its FINAL global
 // pose — the cross-block carry is resolved before the block, not walked after it.
 // Per tile, the same three phases as the single-CTA chunked kernel (kernels.cu) on
-// the tile's sub-forest:
-//   import   cp.async of the tile's external parents' global poses from the CTA's
-//            workspace (L2) into Q locations of the anchor region P;
+// the tile's sub-forest, whose external parents are Q locations (final roots):
 //   phase 1  per-thread chunk folds, anchor prefixes published to P;
 //   phase 2a warp-shuffle scan of runs (heavy paths longer than K);
 //   phase 2  pointer jumping over the anchor forest, whose roots are true roots
 //            and Q locations (already final);
-//   phase 3  re-fold from the final anchors, G in place, S = G (x) IB, and joints with
-//            a child in a later tile store G to the workspace (export).
-// The producer warp streams tiles in and G/S out with TMA bulk copies (one copy per
-// run of consecutive user labels: one run per tile when the user order is already
-// topological).  The per-tile program (chunk metadata, phase-2 descriptors, import
-// list) is prefetched into shared memory with cp.async one tile ahead; the inverse
-// bind of a thread's slots is loaded into registers at the start of the tile and
-// first used in phase 3.
+//   phase 3  re-fold from the final anchors, G in place, S = G (x) IB in place over
+//            the tile's inverse binds, and a joint with a child in the next tile
+//            forwards its G into that tile's Q buffer.
+// Parents two or more tiles back reach Q through the tile's inbox: after each tile the
+// compute threads store its exported joints into later tiles' inboxes (a contiguous
+// workspace range per consumer tile, coalesced, L2-resident), and during tile k - 1
+// the threads stage tile k's inbox into its Q buffer through registers.
+// The producer warp's lane 0 streams, by TMA bulk copies with mbarrier completion,
+// the tiles in (one copy per run of consecutive user labels: one run per tile when
+// the user order is already topological), G and S out, each tile's program (chunk
+// metadata, phase-1 info, phase-2 descriptors; three tiles ahead), export list and
+// inverse binds (into the tile's S buffer).  DESIGN.md §5.1e.
 //
 // HBM bytes per joint: 48 (L in) + 48 (G out) + 48 (S out), as the single-CTA path;
-// the workspace (exported poses of one character per CTA) and the per-tile program
-// stay in L2.
+// the workspace (one character's inboxes per CTA), programs and inverse binds stay
+// in L2.
 #include <atomic>
 
 #include "device_util.cuh"
